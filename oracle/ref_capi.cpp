@@ -1,0 +1,299 @@
+// C ABI over the REFERENCE implementation compiled unmodified from
+// /root/reference/proj/src (TEST INFRASTRUCTURE ONLY — oracle/_ref).
+//
+// This file is ours; it only marshals flat FP64 arrays into the reference's
+// own types and calls its public API:
+//   gvr::render / render_with_tape   (proj/src/blender.cpp:141, proj/src/grad.cpp:38)
+//   gvr::backward                    (proj/src/grad.cpp:49)
+//   gvr::ScalarLoss::value           (proj/src/grad.cpp:201)
+//   gvr::coarse_select               (proj/src/tracer.cpp:37)
+//   gvr::make_bench_scene / camera   (proj/src/bench.cpp:9-24)
+//   gvr::make_orbit_camera           (proj/src/shapes.cpp:118)
+// Per-pixel variable-length lists come back padded to k_prime (index -1).
+// Errors: return 1 for gvr::ValidationError, 2 for anything else; the message
+// is available from gvr_ref_last_error().
+#include "gvr/bench.hpp"
+#include "gvr/blender.hpp"
+#include "gvr/grad.hpp"
+#include "gvr/scene.hpp"
+#include "gvr/shapes.hpp"
+#include "gvr/tracer.hpp"
+
+#include <cstring>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+
+gvr::GaussianScene make_scene(int k, int d, double tau, const double* centers, const double* inv_cov,
+                              const double* attr) {
+    gvr::GaussianScene s;
+    s.tau = tau;
+    s.kernels.resize(k);
+    for (int i = 0; i < k; ++i) {
+        auto& g = s.kernels[i];
+        g.center = gvr::Vec3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) g.inv_cov(r, c) = inv_cov[9 * i + 3 * r + c];
+        g.attr = gvr::VecX(d);
+        for (int c = 0; c < d; ++c) g.attr[c] = attr[static_cast<size_t>(d) * i + c];
+    }
+    return s;
+}
+
+// cam[17] = R(9, row-major) T(3) focal ox oy height width
+gvr::Camera make_camera(const double* cam) {
+    gvr::Camera c;
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) c.rotation(r, k) = cam[3 * r + k];
+    c.translation = gvr::Vec3(cam[9], cam[10], cam[11]);
+    c.focal = cam[12];
+    c.ox = cam[13];
+    c.oy = cam[14];
+    c.height = static_cast<int>(cam[15]);
+    c.width = static_cast<int>(cam[16]);
+    return c;
+}
+
+void export_camera(const gvr::Camera& c, double* cam) {
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) cam[3 * r + k] = c.rotation(r, k);
+    cam[9] = c.translation.x();
+    cam[10] = c.translation.y();
+    cam[11] = c.translation.z();
+    cam[12] = c.focal;
+    cam[13] = c.ox;
+    cam[14] = c.oy;
+    cam[15] = c.height;
+    cam[16] = c.width;
+}
+
+gvr::SelectionConfig make_cfg(double eta, int k_prime, int coarse, int ds) {
+    gvr::SelectionConfig c;
+    c.eta = eta;
+    c.k_prime = k_prime;
+    c.coarse_enabled = coarse != 0;
+    c.coarse_downsample = ds;
+    return c;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const gvr::ValidationError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+void export_buffers(const gvr::RenderBuffers& b, double* image, double* alpha, double* depth) {
+    if (image) std::memcpy(image, b.image.data.data(), b.image.data.size() * sizeof(double));
+    if (alpha) std::memcpy(alpha, b.alpha.data.data(), b.alpha.data.size() * sizeof(double));
+    if (depth) std::memcpy(depth, b.depth.data.data(), b.depth.data.size() * sizeof(double));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gvr_ref_last_error() { return g_err.c_str(); }
+
+// Forward render. Outputs (nullable): image[H*W*max(D,1)], alpha[H*W], depth[H*W],
+// topk_idx[H*W*kp] (int32, -1 pad), topk_w[H*W*kp], topk_l/q/sigma[H*W*kp]
+// (the tape: selected traced kernels, ascending (l, idx)).
+int gvr_ref_render(int k, int d, double tau, const double* centers, const double* inv_cov,
+                   const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                   int ds, int threads, double* image, double* alpha, double* depth, int* topk_idx,
+                   double* topk_w, double* topk_l, double* topk_q, double* topk_sigma) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        const gvr::ForwardResult fr = gvr::render_with_tape(scene, camera, cfg, threads);
+        export_buffers(fr.buffers, image, alpha, depth);
+        const size_t p_count = static_cast<size_t>(camera.height) * camera.width;
+        for (size_t p = 0; p < p_count; ++p) {
+            const auto& ws = fr.buffers.weight_store[p];
+            const auto& tr = fr.tape.traced[p];
+            for (int s = 0; s < k_prime; ++s) {
+                const size_t o = p * k_prime + s;
+                const bool ok = s < static_cast<int>(ws.size());
+                if (topk_idx) topk_idx[o] = ok ? ws[s].first : -1;
+                if (topk_w) topk_w[o] = ok ? ws[s].second : 0.0;
+                if (topk_l) topk_l[o] = ok ? tr[s].l : 0.0;
+                if (topk_q) topk_q[o] = ok ? tr[s].q : 0.0;
+                if (topk_sigma) topk_sigma[o] = ok ? tr[s].sigma : 0.0;
+            }
+        }
+    });
+}
+
+// render_with_tape + backward for a given upstream gradient. Outputs (nullable):
+// d_center[K*3], d_inv_cov[K*9] (row-major), d_attr[K*D], d_rotation[9], d_translation[3].
+int gvr_ref_backward(int k, int d, double tau, const double* centers, const double* inv_cov,
+                     const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                     int ds, int threads, const double* d_image, const double* d_alpha,
+                     int through_transmittance, int through_density, double* d_center,
+                     double* d_inv_cov, double* d_attr, double* d_rotation, double* d_translation) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        const gvr::ForwardResult fr = gvr::render_with_tape(scene, camera, cfg, threads);
+        gvr::Image di(camera.height, camera.width, d);
+        gvr::Image da(camera.height, camera.width, 1, gvr::ChannelSemantics::Alpha);
+        if (d_image) std::memcpy(di.data.data(), d_image, di.data.size() * sizeof(double));
+        if (d_alpha) std::memcpy(da.data.data(), d_alpha, da.data.size() * sizeof(double));
+        gvr::GradFlags flags;
+        flags.through_transmittance = through_transmittance != 0;
+        flags.through_density = through_density != 0;
+        const gvr::GradientBundle g = gvr::backward(fr.tape, di, da, flags);
+        for (int i = 0; i < k; ++i) {
+            for (int c = 0; c < 3; ++c)
+                if (d_center) d_center[3 * i + c] = g.d_center[i][c];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c)
+                    if (d_inv_cov) d_inv_cov[9 * i + 3 * r + c] = g.d_inv_cov[i](r, c);
+            for (int c = 0; c < d; ++c)
+                if (d_attr) d_attr[static_cast<size_t>(d) * i + c] = g.d_attr[i][c];
+        }
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                if (d_rotation) d_rotation[3 * r + c] = g.d_rotation(r, c);
+        for (int c = 0; c < 3; ++c)
+            if (d_translation) d_translation[c] = g.d_translation[c];
+    });
+}
+
+// One full fwd+bwd step exactly as the reference's gradcheck / fit loop runs it:
+// render_with_tape -> ScalarLoss::value -> backward (proj/src/grad.cpp:38-216).
+// Used as the CPU baseline arm. Returns the loss in *loss_out.
+int gvr_ref_fwd_bwd_step(int k, int d, double tau, const double* centers, const double* inv_cov,
+                         const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                         int ds, int threads, const double* target_image, const double* target_alpha,
+                         double* loss_out, double* d_center, double* d_attr) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        const gvr::ForwardResult fr = gvr::render_with_tape(scene, camera, cfg, threads);
+        gvr::ScalarLoss loss;
+        loss.target_image = gvr::Image(camera.height, camera.width, std::max(d, 1));
+        loss.target_alpha = gvr::Image(camera.height, camera.width, 1, gvr::ChannelSemantics::Alpha);
+        std::memcpy(loss.target_image.data.data(), target_image,
+                    loss.target_image.data.size() * sizeof(double));
+        std::memcpy(loss.target_alpha.data.data(), target_alpha,
+                    loss.target_alpha.data.size() * sizeof(double));
+        gvr::Image di, da;
+        const double l = loss.value(fr.buffers, &di, &da);
+        const gvr::GradientBundle g = gvr::backward(fr.tape, di, da);
+        if (loss_out) *loss_out = l;
+        for (int i = 0; i < k; ++i) {
+            for (int c = 0; c < 3; ++c)
+                if (d_center) d_center[3 * i + c] = g.d_center[i][c];
+            for (int c = 0; c < d; ++c)
+                if (d_attr) d_attr[static_cast<size_t>(d) * i + c] = g.d_attr[i][c];
+        }
+    });
+}
+
+// Coarse map statistics and the per-kernel cell boxes actually pushed.
+// cell_box[K*4] = (cr_lo, cr_hi, cc_lo, cc_hi) in coarse-cell units, -1 if not pushed.
+int gvr_ref_coarse_boxes(int k, int d, double tau, const double* centers, const double* inv_cov,
+                         const double* attr, const double* cam, double eta, int k_prime, int ds,
+                         int* cell_box, int* dropped_behind) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, 1, ds);
+        const auto cam_scene = gvr::view_transform(scene, camera);
+        const gvr::PixelKernelMap map = gvr::coarse_select(cam_scene, camera, cfg);
+        for (int i = 0; i < 4 * k; ++i) cell_box[i] = -1;
+        for (int cr = 0; cr < map.grid_rows; ++cr) {
+            for (int cc = 0; cc < map.grid_cols; ++cc) {
+                for (int kk : map.cells[static_cast<size_t>(cr) * map.grid_cols + cc]) {
+                    int* b = cell_box + 4 * kk;
+                    if (b[0] < 0 || cr < b[0]) b[0] = cr;
+                    if (cr > b[1]) b[1] = cr;
+                    if (b[2] < 0 || cc < b[2]) b[2] = cc;
+                    if (cc > b[3]) b[3] = cc;
+                }
+            }
+        }
+        if (dropped_behind) *dropped_behind = map.dropped_behind_camera;
+    });
+}
+
+// Work counters on the same inputs (implementation independent):
+// counts[0] = C = sum_p |candidates(p)|, counts[1] = N1 = sum_p n_p, counts[2] = N2 = sum_p n_p^2.
+int gvr_ref_work_counts(int k, int d, double tau, const double* centers, const double* inv_cov,
+                        const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                        int ds, int threads, double* counts) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        const auto cam_scene = gvr::view_transform(scene, camera);
+        double c = 0.0;
+        if (coarse) {
+            const gvr::PixelKernelMap map = gvr::coarse_select(cam_scene, camera, cfg);
+            for (int i = 0; i < camera.height; ++i)
+                for (int j = 0; j < camera.width; ++j) c += map.candidates(i, j).size();
+        } else {
+            int front = 0;
+            for (const auto& kk : cam_scene.kernels) front += kk.center.z() > gvr::kBehindCameraEps;
+            c = static_cast<double>(front) * camera.height * camera.width;
+        }
+        const gvr::RenderBuffers b = gvr::render(scene, camera, cfg, threads);
+        double n1 = 0.0, n2 = 0.0;
+        for (const auto& ws : b.weight_store) {
+            n1 += ws.size();
+            n2 += static_cast<double>(ws.size()) * ws.size();
+        }
+        counts[0] = c;
+        counts[1] = n1;
+        counts[2] = n2;
+    });
+}
+
+// Synthetic benchmark inputs (proj/src/bench.cpp:9-24, proj/src/shapes.cpp:118-141).
+// Call with centers == nullptr to get the kernel count in *k_out.
+int gvr_ref_make_bench_scene(int n, int* k_out, int* d_out, double* tau_out, double* centers,
+                             double* inv_cov, double* attr) {
+    return guarded([&] {
+        const gvr::GaussianScene s = gvr::make_bench_scene(n);
+        *k_out = s.size();
+        *d_out = s.attr_dim();
+        *tau_out = s.tau;
+        if (!centers) return;
+        for (int i = 0; i < s.size(); ++i) {
+            const auto& g = s.kernels[i];
+            for (int c = 0; c < 3; ++c) centers[3 * i + c] = g.center[c];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) inv_cov[9 * i + 3 * r + c] = g.inv_cov(r, c);
+            for (int c = 0; c < s.attr_dim(); ++c) attr[static_cast<size_t>(s.attr_dim()) * i + c] = g.attr[c];
+        }
+    });
+}
+
+int gvr_ref_make_bench_camera(int size, double* cam) {
+    return guarded([&] { export_camera(gvr::make_bench_camera(size), cam); });
+}
+
+int gvr_ref_make_orbit_camera(double azimuth, double elevation, double distance, const double* target,
+                              int height, int width, double focal, double* cam) {
+    return guarded([&] {
+        export_camera(gvr::make_orbit_camera(azimuth, elevation, distance,
+                                             gvr::Vec3(target[0], target[1], target[2]), height,
+                                             width, focal),
+                      cam);
+    });
+}
+
+}  // extern "C"
