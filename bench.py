@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py — renders/s of the VoGE render path, forward + backward.
+
+Metric (BASELINE.json): "renders/sec (fwd+bwd) 512x512 K=20 100k ellipsoids at
+1/2/4/8 B200 vs CPU ref". Workload = config C2: the reference's bench cuboid
+(make_bench_scene(100000) -> 101,402 kernels, bench.cpp:9-14) seen by
+make_bench_camera(512) (bench.cpp:16-24), SelectionConfig defaults (eta 0.01,
+K' = 20, 8-px coarse cells), ScalarLoss upstream against uniform(0,1) targets.
+
+A step = render_with_tape -> ScalarLoss::value -> backward (the reference's
+gradcheck / fit inner step, grad.cpp:38-216).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched with torch.distributed.run (one process per GPU); every rank
+renders its own view of the scene (views are independent: weak scaling, no
+data-path collective; NCCL only for the barrier and the max-over-ranks time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "renders/sec (fwd+bwd) 512x512 K=20 100k ellipsoids at 1/2/4/8 B200 vs CPU ref"
+UNIT = "renders/s"
+WORKLOAD = "C2: single view 512x512, bench cuboid 101,402 ellipsoids (make_bench_scene(100000)), K'=20, eta=0.01, fwd+bwd"
+IMAGE = 512
+N_KERNELS = 100000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def inputs(rank: int):
+    """Synthetic C2 inputs; identical bytes on every arm."""
+    from paper_2205_15401_b200 import synthetic
+    from paper_2205_15401_b200.types import SelectionConfig
+
+    scene = synthetic.make_bench_scene(N_KERNELS)
+    cam = synthetic.make_bench_camera(IMAGE)
+    rng = np.random.default_rng(0)
+    target_image = rng.uniform(0.0, 1.0, (IMAGE, IMAGE, 3))
+    target_alpha = rng.uniform(0.0, 1.0, (IMAGE, IMAGE, 1))
+    return scene, cam, SelectionConfig(), target_image, target_alpha
+
+
+def cpu_info():
+    cores = os.cpu_count() or 1
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+def reference_step_fn(scene, cam, cfg, ti, ta, threads):
+    """The reference's own CPU implementation (oracle/_ref, compiled unmodified
+    from /root/reference) when present, else the C restatement (oracle port)."""
+    import oracle
+
+    if oracle.ref_available():
+        return "reference", lambda: oracle.ref_fwd_bwd_step(scene, cam, cfg, ti, ta, threads)
+    return "port", lambda: oracle.port_fwd_bwd_step(scene, cam, cfg, ti, ta, threads)
+
+
+def time_cpu(fn, warmup: int, max_steps: int, budget_s: float):
+    for _ in range(warmup):
+        fn()
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_steps and (not times or time.perf_counter() - t_all < budget_s):
+        t = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t)
+    return times
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_flops(wc, D=3):
+    """SURVEY.md §8d per-unit counts x oracle work counters (per render)."""
+    fwd = 40 * wc["C"] + 6 * wc["N2"] + (8 + 2 * D) * wc["N1"] + 300 * wc["kernels"]
+    bwd = 20 * wc["N2"] + (100 + 4 * D) * wc["N1"] + 150 * wc["kernels"]
+    return fwd, bwd
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    scene, cam, cfg, ti, ta = inputs(rank)
+    cores, model = cpu_info()
+    kind, fn = reference_step_fn(scene, cam, cfg, ti, ta, cores)
+    # each step is one full fwd+bwd render on all host cores; cap the timed
+    # steps so the run stays within a few minutes
+    times = time_cpu(fn, min(args.warmup, 1), args.steps, budget_s=120.0)
+    per = sum(times) / len(times)
+    value = 1.0 / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "threads": cores, "cpu": model},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{len(times)} full fwd+bwd renders of the C2 workload, GVR_THREADS={cores}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_15401_b200 as gvr
+    from paper_2205_15401_b200.render import _ptr
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    ctx = gvr.Context(local)
+    # one stream: torch's flushes/events and our kernels serialise on the context stream
+    stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device=dev)
+    torch.cuda.set_stream(stream)
+
+    scene, cam, cfg, ti_h, ta_h = inputs(rank)
+    H = W = IMAGE
+    K = scene.size
+
+    # ---------------- device-resident arm (value)
+    dscene = gvr.DeviceScene(ctx)
+    dscene.set_raw(K, 3, scene.tau, torch.from_numpy(scene.centers).to(dev), torch.from_numpy(scene.inv_cov).to(dev),
+                   torch.from_numpy(scene.attr).to(dev))
+    tape = gvr.Tape(ctx)
+    img = torch.empty((H, W, 3), dtype=torch.float64, device=dev)
+    alpha = torch.empty((H, W, 1), dtype=torch.float64, device=dev)
+    depth = torch.empty((H, W, 1), dtype=torch.float64, device=dev)
+    ti = torch.from_numpy(ti_h).to(dev)
+    ta = torch.from_numpy(ta_h).to(dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    g_center = torch.empty((K, 3), dtype=torch.float64, device=dev)
+    g_inv_cov = torch.empty((K, 3, 3), dtype=torch.float64, device=dev)
+    g_attr = torch.empty((K, 3), dtype=torch.float64, device=dev)
+    g_rot = torch.empty((3, 3), dtype=torch.float64, device=dev)
+    g_trans = torch.empty(3, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        gvr.render_into(ctx, dscene, cam, cfg, tape, img, alpha, depth)
+        ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(ti), _ptr(ta), 1.0, 1.0, _ptr(loss), None,
+                                          None))
+        gvr.backward_into(tape, None, None, gvr.GradFlags(), g_center, g_inv_cov, g_attr, g_rot, g_trans)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    launches0, libcalls0 = ctx.launch_count, ctx.library_call_count
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for a, b in ev:
+        flush.zero_()  # L2 flush between timed steps, outside the timed window
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = ctx.launch_count - launches0
+    libcalls = ctx.library_call_count - libcalls0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    clocks = sampler.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    max_total_ms = float(t.item())
+    value = world * args.steps / (max_total_ms / 1e3)
+    ms_per_step = max_total_ms / args.steps
+
+    # ---------------- per-stage device times (roofline of the dominant kernel)
+    ctx.enable_timing(True)
+    prof_steps = min(args.steps, 20)
+    for _ in range(prof_steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    stages = ctx.stage_times()
+    ctx.enable_timing(False)
+    wc_all = json.load(open(os.path.join(ROOT, "bench_workcounts.json")))
+    wc = wc_all["C2"]
+    fwd_flop, bwd_flop = algorithmic_flops(wc)
+    fp32_peak = ctx.pipe_peak("fp32")
+    fp64_peak = ctx.pipe_peak("fp64")
+    fwd_ms = stages["forward"][0] / max(stages["forward"][1], 1)
+    bwd_ms = stages["backward"][0] / max(stages["backward"][1], 1)
+    dominant = "forward" if fwd_ms >= bwd_ms else "backward"
+    dom_ms = fwd_ms if dominant == "forward" else bwd_ms
+    dom_flop = fwd_flop if dominant == "forward" else bwd_flop
+    achieved = dom_flop / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get(dominant)
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {
+        "bound": "fp32", "kernel": "fine_forward_kernel" if dominant == "forward" else "backward_pixels_kernel",
+        "achieved": achieved, "peak": fp32_peak / 1e12, "unit": "TFLOP/s", "frac": achieved * 1e12 / fp32_peak,
+        "traffic": traffic,
+        "peak_source": "measured in-run: FP32 FMA-chain microbenchmark (gvr_measure_pipe_peak)",
+        "fp64_peak_tflops": fp64_peak / 1e12,
+        "algorithmic_gflop_per_launch": dom_flop / 1e9,
+        "work_counts": {k: wc[k] for k in ("C", "N1", "N2", "kernels")},
+        "stage_ms_per_step": {k: v[0] / max(prof_steps, 1) for k, v in stages.items()},
+    }
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_c, h_s, h_a = pin(scene.centers), pin(scene.inv_cov), pin(scene.attr)
+        h_ti, h_ta = pin(ti_h), pin(ta_h)
+        h_img = torch.empty((H, W, 3), dtype=torch.float64).pin_memory()
+        h_alpha = torch.empty((H, W, 1), dtype=torch.float64).pin_memory()
+        h_depth = torch.empty((H, W, 1), dtype=torch.float64).pin_memory()
+        h_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+        h_gc = torch.empty((K, 3), dtype=torch.float64).pin_memory()
+        h_gs = torch.empty((K, 3, 3), dtype=torch.float64).pin_memory()
+        h_ga = torch.empty((K, 3), dtype=torch.float64).pin_memory()
+        h_gr = torch.empty((3, 3), dtype=torch.float64).pin_memory()
+        h_gt = torch.empty(3, dtype=torch.float64).pin_memory()
+        escene = gvr.DeviceScene(ctx)
+        etape = gvr.Tape(ctx)
+
+        def hp(x):
+            return x.data_ptr()
+
+        def e2e_step():
+            escene.set_raw(K, 3, scene.tau, h_c, h_s, h_a)  # H2D + device validation
+            gvr.render_into(ctx, escene, cam, cfg, etape, h_img, h_alpha, h_depth)  # D2H buffers
+            ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, etape.handle, hp(h_ti), hp(h_ta), 1.0, 1.0, hp(h_loss),
+                                              None, None))  # H2D targets, D2H loss
+            gvr.backward_into(etape, None, None, gvr.GradFlags(), h_gc, h_gs, h_ga, h_gr, h_gt)  # D2H bundle
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e_steps = max(5, min(args.steps, 30))
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e_steps)]
+        for a, b in eev:
+            flush.zero_()
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = sum(a.elapsed_time(b) for a, b in eev)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = 8 * (K * 15) + 8 * (H * W * 4)
+        d2h = 8 * (H * W * 5) + 8 * (K * 15 + 12) + 8
+        e2e = {"value": world * e_steps / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e_steps,
+               "path": "gvr_scene_set(host) -> gvr_render(host image/alpha/depth) -> gvr_scalar_loss(host targets, "
+                       "host loss) -> gvr_backward(host GradientBundle)"}
+
+    # ---------------- CPU baseline (rank 0, N = 1 only)
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores, model = cpu_info()
+        kind, fn = reference_step_fn(scene, cam, cfg, ti_h, ta_h, cores)
+        times = time_cpu(fn, 1, 3, budget_s=60.0)
+        per = sum(times) / len(times)
+        cpu_baseline = {"value": 1.0 / per, "unit": UNIT, "cores": cores, "kind": kind,
+                        "sample": f"1 warm-up + {len(times)} timed full fwd+bwd renders of the C2 workload "
+                                  f"(reference protocol, bench.cpp:65-86), GVR_THREADS={cores}, cpu: {model}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "kernels": K, "image": [H, W], "k_prime": cfg.k_prime,
+                       "views": "every rank renders the C2 view (weak scaling)",
+                       "l2": "flushed (256 MB write) between timed steps, outside the timed window",
+                       "step": "render_with_tape -> ScalarLoss (device) -> backward, inputs resident in HBM"},
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches, "library_calls": libcalls,
+            "loss": float(loss.item()),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/* gvr_cuda.h — C ABI of the B200-native VoGE render path (sm_100a).
+ *
+ * Drop-in boundary for the reference's C++ render API
+ * (namespace gvr, static library `gvr`, /root/reference/proj):
+ *
+ *   reference (proj/include/gvr/...)                           replaced by
+ *   ----------------------------------------------------------  -----------------------------
+ *   GaussianScene::validate            types.hpp:41, types.cpp:31  gvr_scene_set (validates once
+ *                                                                   per upload, on the device)
+ *   Camera::validate / SelectionConfig::validate
+ *                                      types.cpp:44, tracer.cpp:8   gvr_render (host checks,
+ *                                                                   same messages)
+ *   RenderBuffers render(scene, camera, cfg, threads)
+ *                                      blender.hpp:40-41            gvr_render(tape = context tape)
+ *   ForwardResult render_with_tape(scene, camera, cfg, threads)
+ *                                      grad.hpp:41-42               gvr_render(tape)
+ *   detail::render_core(..., traced_out, cam_scene_out)
+ *                                      blender.hpp:53-56            gvr_render + gvr_tape_traced
+ *   RenderBuffers::weight_store        blender.hpp:24               gvr_render_outputs.topk_idx/topk_w
+ *   GradientBundle backward(tape, d_image, d_alpha, flags)
+ *                                      grad.hpp:53-54               gvr_backward
+ *   double ScalarLoss::value(buf, d_image*, d_alpha*)
+ *                                      grad.hpp:68, grad.cpp:201    gvr_scalar_loss
+ *   ValidationError (std::runtime_error)
+ *                                      types.hpp:19-22              return GVR_ERR_VALIDATION +
+ *                                                                   gvr_last_error() (same text)
+ *
+ * Conventions (identical to the reference):
+ *   centers[K*3]; inv_cov[K*9] = Sigma^-1 row-major; attr[K*D]; FP64.
+ *   camera: rotation row-major, x_cam = R x_obj + T; pixel (i, j) = (row, col),
+ *   pixel centres at integers, i pairs with oy; images H*W*C, channels interleaved,
+ *   C = max(D, 1) for the image (zero channel when D == 0), 1 for alpha and depth.
+ *   Per-pixel lists ascending by (l, kernel index), padded to k_prime with -1.
+ *
+ * Memory: every pointer argument may be HOST memory (pageable or pinned) or
+ * DEVICE memory of the context's device; the library detects which with
+ * cudaPointerGetAttributes and copies on the context's stream. All work is
+ * enqueued on the context stream; calls that return host data synchronise.
+ *
+ * Errors: 0 = ok, 1 = validation (the reference throws gvr::ValidationError),
+ * 2 = runtime / CUDA. The message is returned by gvr_last_error(ctx).
+ * There is no CPU fallback: without a usable sm_100 device every call fails
+ * with GVR_ERR_RUNTIME.
+ */
+#ifndef GVR_CUDA_H
+#define GVR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GVR_OK 0
+#define GVR_ERR_VALIDATION 1
+#define GVR_ERR_RUNTIME 2
+
+typedef struct gvr_context gvr_context;
+typedef struct gvr_scene gvr_scene;
+typedef struct gvr_tape gvr_tape;
+
+/* gvr::Camera (types.hpp:46-56) */
+typedef struct {
+    double rotation[9]; /* row-major */
+    double translation[3];
+    double focal, ox, oy;
+    int32_t height, width;
+} gvr_camera;
+
+/* gvr::SelectionConfig (tracer.hpp:18-25); defaults eta 0.01, k_prime 20, coarse on, 8 */
+typedef struct {
+    double eta;
+    int32_t k_prime;
+    int32_t coarse_enabled;
+    int32_t coarse_downsample;
+} gvr_selection;
+
+/* gvr::GradFlags (grad.hpp:46-49) */
+typedef struct {
+    int32_t through_transmittance;
+    int32_t through_density;
+} gvr_grad_flags;
+
+/* Outputs of a render; every field nullable (host or device pointers). */
+typedef struct {
+    double* image;    /* H*W*max(D,1) */
+    double* alpha;    /* H*W */
+    double* depth;    /* H*W */
+    int32_t* topk_idx; /* H*W*k_prime, -1 padded        (weight_store indices) */
+    double* topk_w;    /* H*W*k_prime, 0 padded         (weight_store weights) */
+} gvr_render_outputs;
+
+/* gvr::GradientBundle (grad.hpp:13-22); every field nullable (host or device). */
+typedef struct {
+    double* d_center;      /* K*3 */
+    double* d_inv_cov;     /* K*9 row-major, exactly symmetric */
+    double* d_attr;        /* K*D */
+    double* d_rotation;    /* 9 row-major */
+    double* d_translation; /* 3 */
+} gvr_gradients;
+
+/* ---- context: device, stream, scratch arenas ---------------------------- */
+int gvr_context_create(int device, gvr_context** out);
+void gvr_context_destroy(gvr_context* ctx);
+const char* gvr_last_error(const gvr_context* ctx);
+/* Use an external cudaStream_t (NULL = the context's own stream). */
+int gvr_context_set_stream(gvr_context* ctx, void* cuda_stream);
+void* gvr_context_stream(gvr_context* ctx);
+int gvr_context_synchronize(gvr_context* ctx);
+/* Instrumentation: kernels of this library launched since creation, and
+ * device-wide CUB calls (exclusive scan, radix sort) issued. */
+int64_t gvr_context_launch_count(const gvr_context* ctx);
+int64_t gvr_context_library_call_count(const gvr_context* ctx);
+/* Per-stage device time via CUDA events around each launch (off by default).
+ * Stages: 0 project, 1 scan, 2 emit, 3 sort, 4 ranges, 5 forward, 6 loss,
+ * 7 backward, 8 object-space. Enabling resets the accumulators. */
+int gvr_context_enable_timing(gvr_context* ctx, int on);
+int gvr_context_stage_times(gvr_context* ctx, double* ms, int64_t* count, int n);
+/* Calibration for the roofline: FMA-chain peak of the FP32 (kind 0) or FP64
+ * (kind 1) pipe on this device, FLOP/s (FMA = 2). */
+int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops);
+/* Test hook: FP32 pre-filter guard band on q (default 0.02); a huge value sends
+ * every candidate through the exact FP64 trace. Results must not change. */
+int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard);
+
+/* ---- scene: device-resident, validated once per upload ------------------ */
+int gvr_scene_create(gvr_context* ctx, gvr_scene** out);
+void gvr_scene_destroy(gvr_scene* scene);
+/* Upload + validate (GaussianScene::validate, types.cpp:31-42). attr may be NULL when D == 0. */
+int gvr_scene_set(gvr_context* ctx, gvr_scene* scene, int32_t K, int32_t D, double tau,
+                  const double* centers, const double* inv_cov, const double* attr);
+int32_t gvr_scene_size(const gvr_scene* scene);
+int32_t gvr_scene_attr_dim(const gvr_scene* scene);
+
+/* ---- forward ------------------------------------------------------------- */
+int gvr_tape_create(gvr_context* ctx, gvr_tape** out);
+void gvr_tape_destroy(gvr_tape* tape);
+
+/* render_with_tape: view transform, projection + culling, 16x16 tile binning,
+ * fused trace / top-K' selection / closed-form blend. The tape records the
+ * per-pixel selection for gvr_backward and references `scene`, which must not be
+ * re-set before the backward (checked). `out` may be NULL. */
+int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
+               const gvr_selection* cfg, gvr_tape* tape, const gvr_render_outputs* out);
+
+/* Copy out the taped selection (Tape::traced, grad.hpp:32): per pixel the selected
+ * kernels ascending by (l, idx) with their FP64 (l, q, sigma); -1 / 0 padded.
+ * Any pointer may be NULL. */
+int gvr_tape_traced(gvr_context* ctx, const gvr_tape* tape, int32_t* idx, double* l, double* q,
+                    double* sigma);
+/* Shape of the taped render. */
+int gvr_tape_shape(const gvr_tape* tape, int32_t* height, int32_t* width, int32_t* k_prime,
+                   int32_t* attr_dim);
+
+/* ---- loss + backward ----------------------------------------------------- */
+/* ScalarLoss::value on the taped render (grad.cpp:201-216). targets: H*W*max(D,1)
+ * and H*W. loss_out (host or device, nullable). The upstream gradients are kept
+ * in the tape for gvr_backward(d_image = NULL) and also written to
+ * d_image_out / d_alpha_out when non-NULL. */
+int gvr_scalar_loss(gvr_context* ctx, gvr_tape* tape, const double* target_image,
+                    const double* target_alpha, double w_image, double w_alpha, double* loss_out,
+                    double* d_image_out, double* d_alpha_out);
+
+/* backward (grad.cpp:49-199). d_image: H*W*D, d_alpha: H*W; both NULL = use the
+ * upstream stored by gvr_scalar_loss. flags NULL = both paths on. */
+int gvr_backward(gvr_context* ctx, gvr_tape* tape, const double* d_image, const double* d_alpha,
+                 const gvr_grad_flags* flags, const gvr_gradients* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVR_CUDA_H */

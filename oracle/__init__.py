@@ -170,6 +170,23 @@ def port_backward(scene, cam, cfg, d_image, d_alpha, through_transmittance=True,
     return g
 
 
+def port_fwd_bwd_step(scene, cam, cfg, target_image, target_alpha, threads: int = 0):
+    """C-port fwd+bwd step (render_with_tape -> ScalarLoss -> backward); returns (loss, d_center)."""
+    lib = port_lib()
+    c, s, a = _scene_arrays(scene)
+    ti = np.ascontiguousarray(target_image, dtype=np.float64)
+    ta = np.ascontiguousarray(target_alpha, dtype=np.float64)
+    loss = ctypes.c_double(0.0)
+    dc = np.zeros((scene.size, 3))
+    camc, selc = _cam_c(cam), _sel_c(cfg)
+    rc = lib.gvro_fwd_bwd_step(scene.size, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s), _ptr(a),
+                               ctypes.byref(camc), ctypes.byref(selc), threads, _ptr(ti), _ptr(ta), ctypes.byref(loss),
+                               _ptr(dc), ctypes.cast(None, _dp))
+    if rc:
+        raise OracleError(rc, lib.gvro_last_error().decode())
+    return loss.value, dc
+
+
 def port_coarse_boxes(scene, cam, cfg):
     lib = port_lib()
     c, s, a = _scene_arrays(scene)

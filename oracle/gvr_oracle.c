@@ -725,26 +725,15 @@ static void init_bwd_part(void* part, int w, int b, int e, void* ctx) {
     p->row_end = e;
 }
 
-int gvro_backward(int K, int D, double tau, const double* centers, const double* inv_cov,
-                  const double* attr, const gvro_camera* cam, const gvro_selection* cfg, int threads,
-                  const double* d_image, const double* d_alpha, int through_transmittance,
-                  int through_density, double* d_center, double* d_inv_cov, double* d_attr,
-                  double* d_rotation, double* d_translation) {
-    const int Dc = D > 1 ? D : 1;
-    const size_t P = (size_t)cam->height * cam->width;
-    double* image = malloc(sizeof(double) * P * Dc);
-    double* alpha = malloc(sizeof(double) * P);
-    double* depth = malloc(sizeof(double) * P);
-    forward_state_t st;
-    const int rc = render_core(K, D, tau, centers, inv_cov, attr, cam, cfg, threads, image, alpha, depth, &st);
-    free(image);
-    free(alpha);
-    free(depth);
-    if (rc) return rc;
-
-    bwd_job_t job = {&st, cam, attr, d_image, d_alpha, tau, through_transmittance, through_density};
+/* backward (src/grad.cpp:49-199) on a rendered state. */
+static void backward_from_state(forward_state_t* st, int K, int D, const double* centers, const double* inv_cov,
+                                const double* attr, double tau, const gvro_camera* cam, int threads,
+                                const double* d_image, const double* d_alpha, int through_transmittance,
+                                int through_density, double* d_center, double* d_inv_cov, double* d_attr,
+                                double* d_rotation, double* d_translation) {
+    bwd_job_t job = {st, cam, attr, d_image, d_alpha, tau, through_transmittance, through_density};
     const int workers_req = resolve_threads(threads);
-    int workers = workers_req < st.H ? workers_req : st.H;
+    int workers = workers_req < st->H ? workers_req : st->H;
     if (workers < 1) workers = 1;
     bwd_part_t* parts = calloc((size_t)workers, sizeof(bwd_part_t));
     for (int w = 0; w < workers; ++w) {
@@ -752,7 +741,7 @@ int gvro_backward(int K, int D, double tau, const double* centers, const double*
         parts[w].d_inv_cov = calloc(9 * (size_t)(K > 0 ? K : 1), sizeof(double));
         parts[w].d_attr = calloc((size_t)(D > 0 ? D : 1) * (size_t)(K > 0 ? K : 1), sizeof(double));
     }
-    run_partitions(st.H, workers, backward_rows, parts, sizeof(bwd_part_t), init_bwd_part, &job);
+    run_partitions(st->H, workers, backward_rows, parts, sizeof(bwd_part_t), init_bwd_part, &job);
 
     /* fixed worker-order reduction (src/grad.cpp:176-182) */
     double* tc = calloc(3 * (size_t)(K > 0 ? K : 1), sizeof(double));
@@ -798,7 +787,66 @@ int gvro_backward(int K, int D, double tau, const double* centers, const double*
     free(tc);
     free(ts);
     free(ta);
+}
+
+int gvro_backward(int K, int D, double tau, const double* centers, const double* inv_cov,
+                  const double* attr, const gvro_camera* cam, const gvro_selection* cfg, int threads,
+                  const double* d_image, const double* d_alpha, int through_transmittance,
+                  int through_density, double* d_center, double* d_inv_cov, double* d_attr,
+                  double* d_rotation, double* d_translation) {
+    const int Dc = D > 1 ? D : 1;
+    const size_t P = (size_t)cam->height * cam->width;
+    double* image = malloc(sizeof(double) * P * Dc);
+    double* alpha = malloc(sizeof(double) * P);
+    double* depth = malloc(sizeof(double) * P);
+    forward_state_t st;
+    const int rc = render_core(K, D, tau, centers, inv_cov, attr, cam, cfg, threads, image, alpha, depth, &st);
+    free(image);
+    free(alpha);
+    free(depth);
+    if (rc) return rc;
+    backward_from_state(&st, K, D, centers, inv_cov, attr, tau, cam, threads, d_image, d_alpha, through_transmittance,
+                        through_density, d_center, d_inv_cov, d_attr, d_rotation, d_translation);
     free_state(&st);
+    return 0;
+}
+
+/* One fwd+bwd step as the reference's loss loop runs it: render_with_tape ->
+ * ScalarLoss::value (src/grad.cpp:201-216, w = 1) -> backward. D >= 1. */
+int gvro_fwd_bwd_step(int K, int D, double tau, const double* centers, const double* inv_cov,
+                      const double* attr, const gvro_camera* cam, const gvro_selection* cfg, int threads,
+                      const double* target_image, const double* target_alpha, double* loss_out,
+                      double* d_center, double* d_attr) {
+    const size_t P = (size_t)cam->height * cam->width;
+    double* image = malloc(sizeof(double) * P * (size_t)D);
+    double* alpha = malloc(sizeof(double) * P);
+    double* depth = malloc(sizeof(double) * P);
+    forward_state_t st;
+    const int rc = render_core(K, D, tau, centers, inv_cov, attr, cam, cfg, threads, image, alpha, depth, &st);
+    if (rc) {
+        free(image);
+        free(alpha);
+        free(depth);
+        return rc;
+    }
+    double loss = 0.0;
+    for (size_t i = 0; i < P * (size_t)D; ++i) {
+        const double diff = image[i] - target_image[i];
+        loss += 0.5 * diff * diff;
+        image[i] = diff; /* d_image in place */
+    }
+    for (size_t i = 0; i < P; ++i) {
+        const double diff = alpha[i] - target_alpha[i];
+        loss += 0.5 * diff * diff;
+        alpha[i] = diff;
+    }
+    if (loss_out) *loss_out = loss;
+    backward_from_state(&st, K, D, centers, inv_cov, attr, tau, cam, threads, image, alpha, 1, 1, d_center, NULL,
+                        d_attr, NULL, NULL);
+    free_state(&st);
+    free(image);
+    free(alpha);
+    free(depth);
     return 0;
 }
 

@@ -1,0 +1,31 @@
+"""B200-native VoGE render path (arXiv 2205.15401): Gaussian-ellipsoid volume
+rendering forward + backward as sm_100a CUDA kernels behind a C ABI
+(include/gvr_cuda.h), with this package as the host-side mirror of the
+reference's ``gvr::`` render API.
+"""
+from .types import (  # noqa: F401
+    Camera,
+    GaussianScene,
+    GradFlags,
+    GradientBundle,
+    RenderBuffers,
+    ScalarLoss,
+    SelectionConfig,
+    ValidationError,
+)
+from .render import (  # noqa: F401
+    Context,
+    DeviceScene,
+    ForwardResult,
+    GvrRuntimeError,
+    Tape,
+    backward,
+    backward_into,
+    default_context,
+    render,
+    render_into,
+    render_with_tape,
+    scalar_loss,
+)
+from .synthetic import make_bench_camera, make_bench_scene, make_orbit_camera  # noqa: F401
+from .scene_io import load_camera_json, load_scene_json  # noqa: F401

@@ -1,0 +1,139 @@
+"""ctypes binding of the C ABI (include/gvr_cuda.h) — no compute happens in Python.
+
+The product path is: Python/C++ caller -> libgvr_cuda.so (C ABI) -> sm_100a kernels.
+If the shared library is missing, importing the API fails loudly; there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgvr_cuda.so")
+
+GVR_OK = 0
+GVR_ERR_VALIDATION = 1
+GVR_ERR_RUNTIME = 2
+
+EXPORTED_SYMBOLS = (
+    "gvr_context_create",
+    "gvr_context_destroy",
+    "gvr_last_error",
+    "gvr_context_set_stream",
+    "gvr_context_stream",
+    "gvr_context_synchronize",
+    "gvr_context_launch_count",
+    "gvr_context_library_call_count",
+    "gvr_context_enable_timing",
+    "gvr_context_stage_times",
+    "gvr_measure_pipe_peak",
+    "gvr_context_set_prefilter_guard",
+    "gvr_scene_create",
+    "gvr_scene_destroy",
+    "gvr_scene_set",
+    "gvr_scene_size",
+    "gvr_scene_attr_dim",
+    "gvr_tape_create",
+    "gvr_tape_destroy",
+    "gvr_render",
+    "gvr_tape_traced",
+    "gvr_tape_shape",
+    "gvr_scalar_loss",
+    "gvr_backward",
+)
+
+
+class GvrCamera(ctypes.Structure):
+    _fields_ = [
+        ("rotation", ctypes.c_double * 9),
+        ("translation", ctypes.c_double * 3),
+        ("focal", ctypes.c_double),
+        ("ox", ctypes.c_double),
+        ("oy", ctypes.c_double),
+        ("height", ctypes.c_int32),
+        ("width", ctypes.c_int32),
+    ]
+
+
+class GvrSelection(ctypes.Structure):
+    _fields_ = [
+        ("eta", ctypes.c_double),
+        ("k_prime", ctypes.c_int32),
+        ("coarse_enabled", ctypes.c_int32),
+        ("coarse_downsample", ctypes.c_int32),
+    ]
+
+
+class GvrGradFlags(ctypes.Structure):
+    _fields_ = [("through_transmittance", ctypes.c_int32), ("through_density", ctypes.c_int32)]
+
+
+class GvrRenderOutputs(ctypes.Structure):
+    _fields_ = [
+        ("image", ctypes.c_void_p),
+        ("alpha", ctypes.c_void_p),
+        ("depth", ctypes.c_void_p),
+        ("topk_idx", ctypes.c_void_p),
+        ("topk_w", ctypes.c_void_p),
+    ]
+
+
+class GvrGradients(ctypes.Structure):
+    _fields_ = [
+        ("d_center", ctypes.c_void_p),
+        ("d_inv_cov", ctypes.c_void_p),
+        ("d_attr", ctypes.c_void_p),
+        ("d_rotation", ctypes.c_void_p),
+        ("d_translation", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libgvr_cuda.so; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, dp = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
+    sig = {
+        "gvr_context_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
+        "gvr_context_destroy": (None, [vp]),
+        "gvr_last_error": (ctypes.c_char_p, [vp]),
+        "gvr_context_set_stream": (ctypes.c_int, [vp, vp]),
+        "gvr_context_stream": (vp, [vp]),
+        "gvr_context_synchronize": (ctypes.c_int, [vp]),
+        "gvr_context_launch_count": (ctypes.c_int64, [vp]),
+        "gvr_context_library_call_count": (ctypes.c_int64, [vp]),
+        "gvr_context_enable_timing": (ctypes.c_int, [vp, ctypes.c_int]),
+        "gvr_context_stage_times": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
+        "gvr_measure_pipe_peak": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(dp)]),
+        "gvr_context_set_prefilter_guard": (ctypes.c_int, [vp, dp]),
+        "gvr_scene_create": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+        "gvr_scene_destroy": (None, [vp]),
+        "gvr_scene_set": (ctypes.c_int, [vp, vp, i32, i32, dp, vp, vp, vp]),
+        "gvr_scene_size": (i32, [vp]),
+        "gvr_scene_attr_dim": (i32, [vp]),
+        "gvr_tape_create": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+        "gvr_tape_destroy": (None, [vp]),
+        "gvr_render": (ctypes.c_int, [vp, vp, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection), vp,
+                                      ctypes.POINTER(GvrRenderOutputs)]),
+        "gvr_tape_traced": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
+        "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                          ctypes.POINTER(i32)]),
+        "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),
+        "gvr_backward": (ctypes.c_int, [vp, vp, vp, vp, ctypes.POINTER(GvrGradFlags), ctypes.POINTER(GvrGradients)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,137 @@
+// Shared device definitions of the B200 render path.
+//
+// Precision contract:
+//  * Everything that DECIDES (culling boxes, the eta threshold, the K' nearest by
+//    (l, index), early exit) runs on exact FP64 arithmetic that reproduces the
+//    reference's evaluation order without FMA contraction (__dmul_rn/__dadd_rn),
+//    so index sets, l, q and sigma are bit-identical to the CPU reference
+//    (proj/src/tracer.cpp:20-35, scene.cpp:5-22, tracer.cpp:37-113).
+//  * The bulk per-candidate work is an FP32 centre-relative pre-filter that
+//    only rejects candidates whose q is below ln(eta) by more than a guard band;
+//    survivors are re-traced in FP64 and decided exactly.
+//  * The O(n^2) closed-form blend and its backward run in FP32 with FP64
+//    accumulation where sums cancel (tolerance 1e-4 relative, north star).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gvrk {
+
+constexpr double kBehindCameraEps = 1e-4;  // include/gvr/tracer.hpp:28
+
+struct CameraP {
+    double R[9];
+    double T[3];
+    double focal, ox, oy;
+    int H, W;
+};
+
+struct SelP {
+    double eta, log_eta, chi;  // chi = 2 ln(1/eta) (tracer.cpp:47), log_eta (tracer.cpp:117)
+    int kp, coarse, ds;
+};
+
+// Per-kernel FP32 record for the pre-filter and the exact cell predicate (64 B).
+struct __align__(16) Rec32 {
+    float s00, s01, s02, s11;
+    float s12, s22, zf, zmin;  // zf = z / F; zmin = conservative lower bound of l
+    float ci_frac, cj_frac;
+    int ci_int, cj_int;        // screen centre (row, col) = int + frac
+    int cr_lo, cr_hi, cc_lo, cc_hi;  // coarse cells pushed (tracer.cpp:100-110)
+};
+
+// Per-kernel FP64 camera-space record for the exact trace (128 B).
+struct __align__(16) Rec64 {
+    double m[3];
+    double s[9];
+    double sm[3];  // S m (tracer.cpp:30, d^T (S m))
+    double pad;
+};
+
+// ---------------------------------------------------------------- exact FP64 (no contraction)
+
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// y = M x, acc = 0.0; acc += m_ik x_k  (oracle mat_vec / Eigen-shim product order)
+__device__ __forceinline__ void xmatvec(const double* m, const double* x, double* y) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double acc = xadd(0.0, xmul(m[3 * i], x[0]));
+        acc = xadd(acc, xmul(m[3 * i + 1], x[1]));
+        acc = xadd(acc, xmul(m[3 * i + 2], x[2]));
+        y[i] = acc;
+    }
+}
+
+__device__ __forceinline__ void xmatmul(const double* a, const double* b, double* c) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double acc = xadd(0.0, xmul(a[3 * i], b[j]));
+            acc = xadd(acc, xmul(a[3 * i + 1], b[3 + j]));
+            acc = xadd(acc, xmul(a[3 * i + 2], b[6 + j]));
+            c[3 * i + j] = acc;
+        }
+}
+
+// a0 b0 + a1 b1 + a2 b2, left to right (Eigen-shim dot: acc starts at 0.0)
+__device__ __forceinline__ double xdot(const double* a, const double* b) {
+    double acc = xadd(0.0, xmul(a[0], b[0]));
+    acc = xadd(acc, xmul(a[1], b[1]));
+    return xadd(acc, xmul(a[2], b[2]));
+}
+
+// pixel_ray (scene.cpp:19-22): normalize(((i - Oy)/F, (j - Ox)/F, 1))
+__device__ __forceinline__ void pixel_ray(const CameraP& c, int row, int col, double* d) {
+    d[0] = xdiv(xsub((double)row, c.oy), c.focal);
+    d[1] = xdiv(xsub((double)col, c.ox), c.focal);
+    d[2] = 1.0;
+    const double n = xadd(xadd(xadd(0.0, xmul(d[0], d[0])), xmul(d[1], d[1])), xmul(d[2], d[2]));
+    if (n > 0.0) {
+        const double s = __dsqrt_rn(n);
+        d[0] = xdiv(d[0], s);
+        d[1] = xdiv(d[1], s);
+        d[2] = xdiv(d[2], s);
+    }
+}
+
+struct Traced64 {
+    double l, q, a;
+};
+
+// trace_kernel (tracer.cpp:20-35), bit-exact: a = d.Sd, b = (m.Sd + d.Sm)/2,
+// l = b/a, v = m - l d, q = min(0, -v.Sv/2), sigma = 1/sqrt(a).
+__device__ __forceinline__ Traced64 trace_exact(const double* d, const Rec64& r) {
+    double sd[3], v[3], sv[3];
+    xmatvec(r.s, d, sd);
+    const double a = xdot(d, sd);
+    const double b = xmul(0.5, xadd(xdot(r.m, sd), xdot(d, r.sm)));
+    const double l = xdiv(b, a);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v[i] = xsub(r.m[i], xmul(l, d[i]));
+    xmatvec(r.s, v, sv);
+    double q = xmul(-0.5, xdot(v, sv));
+    if (q > 0.0) q = 0.0;
+    return Traced64{l, q, a};
+}
+
+__device__ __forceinline__ double sigma_of(double a) { return xdiv(1.0, __dsqrt_rn(a)); }
+
+// ---------------------------------------------------------------- FP32 closed-form pieces
+
+// Phi(x) = 0.5 erfc(-x / sqrt 2)  (blender.cpp:13-15)
+__device__ __forceinline__ float normal_cdf_f(float x) { return 0.5f * erfcf(-x * 0.70710678118654752f); }
+// phi(x) = exp(-x^2/2) / sqrt(2 pi)  (grad.cpp:16)
+__device__ __forceinline__ float normal_pdf_f(float x) { return 0.398942280401432678f * expf(-0.5f * x * x); }
+
+// (l, idx) lexicographic order of fine_select (tracer.cpp:119-122)
+__device__ __forceinline__ bool traced_less(double la, int ia, double lb, int ib) {
+    return la < lb || (la == lb && ia < ib);
+}
+
+}  // namespace gvrk

@@ -1,0 +1,939 @@
+// C ABI of the B200 render path: context / scene / tape management and the
+// launch sequence (include/gvr_cuda.h documents the contract).
+//
+//   gvr_scene_set : H2D (or D2D) FP64 upload + K0 validate  [1 sync: error code]
+//   gvr_render    : K1 project -> scan -> [1 sync: pair count] -> K2a emit ->
+//                   radix sort (tile|depth) -> K2c ranges -> K3 fused forward
+//   gvr_scalar_loss, gvr_backward : K4 per-pixel backward -> K5 object space
+#include "../../include/gvr_cuda.h"
+#include "backward.cuh"
+#include "forward.cuh"
+#include "project.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+using namespace gvrk;
+
+namespace {
+
+constexpr int kFwdTileSmall = 16;  // forward tile edge for k_prime <= 24
+constexpr int kFwdTileLarge = 8;   // forward tile edge for 24 < k_prime <= 64
+constexpr int kBwdTile = 8;
+constexpr int kMaxKPrime = 64;
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = bytes > 0 ? bytes + bytes / 4 : 256;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+bool is_device_ptr(const void* ptr) {
+    if (!ptr) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+enum Stage { ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_FORWARD, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT };
+
+struct gvr_context {
+    int device = 0;
+    // optional per-stage timing (events around each launch, summed at query time)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+    double stage_ms[ST_COUNT] = {0};
+    int64_t stage_n[ST_COUNT] = {0};
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    int64_t launches = 0;   // kernels of this library
+    int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
+    double guard = 0.02;
+    Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
+    int* h_flags = nullptr;  // pinned mirror (64 B)
+};
+
+struct gvr_scene {
+    gvr_context* ctx = nullptr;
+    int K = 0, D = 0;
+    double tau = 1.0;
+    uint64_t version = 0;
+    bool valid = false;
+    Buf centers, inv_cov, attr;
+};
+
+struct gvr_tape {
+    gvr_context* ctx = nullptr;
+    const gvr_scene* scene = nullptr;
+    uint64_t scene_version = 0;
+    bool valid = false;
+    bool has_upstream = false;
+    gvr_camera cam{};
+    gvr_selection cfg{};
+    CameraP camp{};
+    SelP selp{};
+    int K = 0, D = 0, H = 0, W = 0, tile = 16, tiles_x = 0, tiles_y = 0;
+    uint32_t pairs = 0;
+    int dropped_behind = 0;
+    // per kernel
+    Buf rec32, rec64, counts, offsets;
+    // pairs
+    Buf keys, keys_alt, vals, vals_alt, cub_tmp, ranges;
+    // per pixel
+    Buf topk, count, image, alpha, depth, topk_w;
+    Buf d_image, d_alpha;
+    // gradients
+    Buf acc, d_attr, d_center, d_inv_cov, d_rt;
+    // host copy-out staging
+    Buf stage_i, stage_w;
+};
+
+namespace {
+
+int set_err(gvr_context* ctx, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                             \
+    do {                                                                                                \
+        cudaError_t e_ = (expr);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return set_err((ctx), GVR_ERR_RUNTIME, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), \
+                           __FILE__, __LINE__, cudaGetErrorString(e_));                                 \
+    } while (0)
+
+#define LAUNCH_CHECK(ctx)                  \
+    do {                                   \
+        ++(ctx)->launches;                 \
+        CUDA_TRY((ctx), cudaGetLastError()); \
+    } while (0)
+
+// Camera::validate (types.cpp:44-63), same messages.
+int validate_camera(gvr_context* ctx, const gvr_camera* c) {
+    if (!c) return set_err(ctx, GVR_ERR_VALIDATION, "camera is null");
+    for (int i = 0; i < 9; ++i)
+        if (!std::isfinite(c->rotation[i])) return set_err(ctx, GVR_ERR_VALIDATION, "camera extrinsics have non-finite values");
+    for (int i = 0; i < 3; ++i)
+        if (!std::isfinite(c->translation[i]))
+            return set_err(ctx, GVR_ERR_VALIDATION, "camera extrinsics have non-finite values");
+    const double* r = c->rotation;
+    double worst = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += r[3 * k + i] * r[3 * k + j];
+            worst = std::fmax(worst, std::fabs(acc - (i == j ? 1.0 : 0.0)));
+        }
+    if (worst > 1e-6) return set_err(ctx, GVR_ERR_VALIDATION, "camera rotation is not orthonormal");
+    const double det = r[0] * (r[4] * r[8] - r[5] * r[7]) - r[1] * (r[3] * r[8] - r[5] * r[6]) +
+                       r[2] * (r[3] * r[7] - r[4] * r[6]);
+    if (std::fabs(det - 1.0) > 1e-6) return set_err(ctx, GVR_ERR_VALIDATION, "camera rotation determinant is not +1");
+    if (!(c->focal > 0.0) || !std::isfinite(c->focal))
+        return set_err(ctx, GVR_ERR_VALIDATION, "camera focal length must be > 0");
+    if (c->height < 1 || c->width < 1) return set_err(ctx, GVR_ERR_VALIDATION, "camera image size must be at least 1x1");
+    if (!std::isfinite(c->ox) || !std::isfinite(c->oy))
+        return set_err(ctx, GVR_ERR_VALIDATION, "camera principal point has non-finite values");
+    return GVR_OK;
+}
+
+// SelectionConfig::validate (tracer.cpp:8-18), same messages.
+int validate_cfg(gvr_context* ctx, const gvr_selection* s) {
+    if (!s) return set_err(ctx, GVR_ERR_VALIDATION, "selection config is null");
+    if (!(s->eta > 0.0 && s->eta < 1.0)) return set_err(ctx, GVR_ERR_VALIDATION, "selection eta must be in (0, 1)");
+    if (s->k_prime < 1) return set_err(ctx, GVR_ERR_VALIDATION, "selection k_prime must be >= 1");
+    if (s->coarse_downsample < 1) return set_err(ctx, GVR_ERR_VALIDATION, "coarse downsample must be >= 1");
+    if (s->k_prime > kMaxKPrime)
+        return set_err(ctx, GVR_ERR_RUNTIME, "k_prime %d exceeds the CUDA backend limit of %d", s->k_prime, kMaxKPrime);
+    return GVR_OK;
+}
+
+int copy_in(gvr_context* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return GVR_OK;
+    const cudaMemcpyKind kind = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream));
+    return GVR_OK;
+}
+
+// Returns true in *host if a D2H copy was enqueued (caller must synchronise).
+int copy_out(gvr_context* ctx, void* dst, const void* src, size_t bytes, bool* host) {
+    if (!dst || bytes == 0) return GVR_OK;
+    const bool dev = is_device_ptr(dst);
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    if (!dev) *host = true;
+    return GVR_OK;
+}
+
+cudaEvent_t take_event(gvr_context* ctx) {
+    if (!ctx->ev_pool.empty()) {
+        cudaEvent_t e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// RAII bracket: records events around the enclosed launches when timing is on.
+struct StageTimer {
+    gvr_context* ctx;
+    int stage;
+    cudaEvent_t a = nullptr, b = nullptr;
+    StageTimer(gvr_context* c, int st) : ctx(c), stage(st) {
+        if (ctx->timing) {
+            a = take_event(ctx);
+            b = take_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~StageTimer() {
+        if (a) {
+            cudaEventRecord(b, ctx->stream);
+            ctx->ev_pending.push_back({stage, {a, b}});
+        }
+    }
+};
+
+void harvest_timings(gvr_context* ctx) {
+    for (auto& pe : ctx->ev_pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pe.second.first, pe.second.second) == cudaSuccess) {
+            ctx->stage_ms[pe.first] += ms;
+            ctx->stage_n[pe.first] += 1;
+        }
+        ctx->ev_pool.push_back(pe.second.first);
+        ctx->ev_pool.push_back(pe.second.second);
+    }
+    ctx->ev_pending.clear();
+    cudaGetLastError();
+}
+
+unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+int ceil_log2(uint32_t v) {
+    int b = 0;
+    while ((1ull << b) < v) ++b;
+    return b;
+}
+
+template <int KMAX, int TILE>
+int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
+    constexpr int NT = TILE * TILE;
+    const size_t chunk = (size_t)NT * (sizeof(Rec32) + sizeof(Rec64) + sizeof(int));
+    const size_t blend = (size_t)KMAX * NT * 20;
+    const size_t smem = chunk > blend ? chunk : blend;
+    auto kern = fine_forward_kernel<KMAX, TILE>;
+    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {
+        StageTimer st(ctx, ST_FORWARD);
+        kern<<<tiles, NT, smem, ctx->stream>>>(fp);
+    }
+    LAUNCH_CHECK(ctx);
+    return GVR_OK;
+}
+
+template <int KMAX>
+int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
+    constexpr int NT = kBwdTile * kBwdTile;
+    const size_t smem = (size_t)KMAX * NT * 44;
+    auto kern = backward_pixels_kernel<KMAX, kBwdTile>;
+    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {
+        StageTimer st(ctx, ST_BACKWARD);
+        kern<<<tiles, NT, smem, ctx->stream>>>(bp);
+    }
+    LAUNCH_CHECK(ctx);
+    return GVR_OK;
+}
+
+int sync_and_check(gvr_context* ctx) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (!ctx->ev_pending.empty()) harvest_timings(ctx);
+    return GVR_OK;
+}
+
+// Calibration: a long chain of independent FMAs per thread (8 chains) on the
+// FP32 (kind 0) or FP64 (kind 1) pipe; returns achieved FLOP/s (FMA = 2).
+template <typename T>
+__global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
+    T x0 = (T)threadIdx.x, x1 = x0 + (T)1, x2 = x0 + (T)2, x3 = x0 + (T)3;
+    T x4 = x0 + (T)4, x5 = x0 + (T)5, x6 = x0 + (T)6, x7 = x0 + (T)7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = x0 * a + b; x1 = x1 * a + b; x2 = x2 * a + b; x3 = x3 * a + b;
+            x4 = x4 * a + b; x5 = x5 * a + b; x6 = x6 * a + b; x7 = x7 * a + b;
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gvr_context_create(int device, gvr_context** out) {
+    if (!out) return GVR_ERR_RUNTIME;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) {
+        cudaGetLastError();
+        return GVR_ERR_RUNTIME;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return GVR_ERR_RUNTIME;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) return GVR_ERR_RUNTIME;
+    auto* ctx = new gvr_context();
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return GVR_ERR_RUNTIME;
+    }
+    ctx->stream = ctx->own_stream;
+    if (ctx->flags.ensure(64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess) {
+        delete ctx;
+        return GVR_ERR_RUNTIME;
+    }
+    *out = ctx;
+    return GVR_OK;
+}
+
+void gvr_context_destroy(gvr_context* ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    harvest_timings(ctx);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    ctx->flags.release();
+    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* gvr_last_error(const gvr_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gvr_context_set_stream(gvr_context* ctx, void* s) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    return GVR_OK;
+}
+
+void* gvr_context_stream(gvr_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int gvr_context_synchronize(gvr_context* ctx) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    return sync_and_check(ctx);
+}
+
+int64_t gvr_context_launch_count(const gvr_context* ctx) { return ctx ? ctx->launches : 0; }
+int64_t gvr_context_library_call_count(const gvr_context* ctx) { return ctx ? ctx->lib_calls : 0; }
+
+int gvr_context_enable_timing(gvr_context* ctx, int on) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    if (int rc = sync_and_check(ctx)) return rc;
+    ctx->timing = on != 0;
+    for (int i = 0; i < ST_COUNT; ++i) {
+        ctx->stage_ms[i] = 0.0;
+        ctx->stage_n[i] = 0;
+    }
+    return GVR_OK;
+}
+
+int gvr_context_stage_times(gvr_context* ctx, double* ms, int64_t* count, int n) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    if (int rc = sync_and_check(ctx)) return rc;
+    for (int i = 0; i < n && i < ST_COUNT; ++i) {
+        if (ms) ms[i] = ctx->stage_ms[i];
+        if (count) count[i] = ctx->stage_n[i];
+    }
+    return GVR_OK;
+}
+
+int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
+    if (!ctx || !flops) return GVR_ERR_RUNTIME;
+    cudaDeviceProp prop;
+    CUDA_TRY(ctx, cudaGetDeviceProperties(&prop, ctx->device));
+    const int threads = 512, blocks = prop.multiProcessorCount * 4;
+    const int iters = kind == 0 ? 4096 : 1024;
+    void* out = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&out, sizeof(double) * threads * blocks));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, ctx->stream);
+        if (kind == 0)
+            fma_peak_kernel<float><<<blocks, threads, 0, ctx->stream>>>((float*)out, iters, 0.999f, 0.001f);
+        else
+            fma_peak_kernel<double><<<blocks, threads, 0, ctx->stream>>>((double*)out, iters, 0.999, 0.001);
+        cudaEventRecord(b, ctx->stream);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    CUDA_TRY(ctx, cudaGetLastError());
+    *flops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3);
+    return GVR_OK;
+}
+
+int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard) {
+    if (!ctx || !(guard >= 0.0)) return GVR_ERR_RUNTIME;
+    ctx->guard = guard;
+    return GVR_OK;
+}
+
+// ---------------------------------------------------------------- scene
+
+int gvr_scene_create(gvr_context* ctx, gvr_scene** out) {
+    if (!ctx || !out) return GVR_ERR_RUNTIME;
+    auto* s = new gvr_scene();
+    s->ctx = ctx;
+    *out = s;
+    return GVR_OK;
+}
+
+void gvr_scene_destroy(gvr_scene* s) {
+    if (!s) return;
+    cudaStreamSynchronize(s->ctx->stream);
+    s->centers.release();
+    s->inv_cov.release();
+    s->attr.release();
+    delete s;
+}
+
+int32_t gvr_scene_size(const gvr_scene* s) { return s ? s->K : 0; }
+int32_t gvr_scene_attr_dim(const gvr_scene* s) { return s ? s->D : 0; }
+
+int gvr_scene_set(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double tau, const double* centers,
+                  const double* inv_cov, const double* attr) {
+    if (!ctx || !s) return GVR_ERR_RUNTIME;
+    s->valid = false;
+    ++s->version;
+    if (K < 0 || D < 0) return set_err(ctx, GVR_ERR_VALIDATION, "scene sizes must be >= 0");
+    // GaussianScene::validate order: tau first, then kernels (types.cpp:31-42)
+    if (tau < 0.0 || !std::isfinite(tau)) return set_err(ctx, GVR_ERR_VALIDATION, "tau must be finite and >= 0");
+    if (K > 0 && (!centers || !inv_cov || (D > 0 && !attr)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "scene arrays must not be null");
+    CUDA_TRY(ctx, s->centers.ensure(sizeof(double) * 3 * (size_t)K));
+    CUDA_TRY(ctx, s->inv_cov.ensure(sizeof(double) * 9 * (size_t)K));
+    CUDA_TRY(ctx, s->attr.ensure(sizeof(double) * (size_t)D * K));
+    if (int rc = copy_in(ctx, s->centers.p, centers, sizeof(double) * 3 * (size_t)K)) return rc;
+    if (int rc = copy_in(ctx, s->inv_cov.p, inv_cov, sizeof(double) * 9 * (size_t)K)) return rc;
+    if (int rc = copy_in(ctx, s->attr.p, attr, sizeof(double) * (size_t)D * K)) return rc;
+    s->K = K;
+    s->D = D;
+    s->tau = tau;
+    if (K > 0) {
+        unsigned long long* first = reinterpret_cast<unsigned long long*>(ctx->flags.as<int>() + 2);
+        CUDA_TRY(ctx, cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
+        validate_scene_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(K, D, s->centers.as<double>(),
+                                                                           s->inv_cov.as<double>(),
+                                                                           s->attr.as<double>(), first);
+        LAUNCH_CHECK(ctx);
+        unsigned long long h = 0;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, first, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        if (int rc = sync_and_check(ctx)) return rc;
+        std::memcpy(&h, ctx->h_flags + 2, sizeof h);
+        if (h != ~0ull) {
+            const long long k = (long long)(h >> 2);
+            switch ((int)(h & 3)) {
+                case 1: return set_err(ctx, GVR_ERR_VALIDATION, "kernel has non-finite values (kernel %lld)", k);
+                case 2: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not symmetric (kernel %lld)", k);
+                default: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not positive-definite (kernel %lld)", k);
+            }
+        }
+    }
+    s->valid = true;
+    return GVR_OK;
+}
+
+// ---------------------------------------------------------------- tape / forward
+
+int gvr_tape_create(gvr_context* ctx, gvr_tape** out) {
+    if (!ctx || !out) return GVR_ERR_RUNTIME;
+    auto* t = new gvr_tape();
+    t->ctx = ctx;
+    *out = t;
+    return GVR_OK;
+}
+
+void gvr_tape_destroy(gvr_tape* t) {
+    if (!t) return;
+    cudaStreamSynchronize(t->ctx->stream);
+    Buf* bufs[] = {&t->rec32, &t->rec64, &t->counts, &t->offsets, &t->keys, &t->keys_alt, &t->vals,
+                   &t->vals_alt, &t->cub_tmp, &t->ranges, &t->topk, &t->count, &t->image, &t->alpha,
+                   &t->depth, &t->topk_w, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
+                   &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w};
+    for (Buf* b : bufs) b->release();
+    delete t;
+}
+
+int gvr_tape_shape(const gvr_tape* t, int32_t* h, int32_t* w, int32_t* kp, int32_t* d) {
+    if (!t || !t->valid) return GVR_ERR_RUNTIME;
+    if (h) *h = t->H;
+    if (w) *w = t->W;
+    if (kp) *kp = t->cfg.k_prime;
+    if (d) *d = t->D;
+    return GVR_OK;
+}
+
+int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera, const gvr_selection* cfg,
+               gvr_tape* tape, const gvr_render_outputs* out) {
+    if (!ctx || !scene || !tape) return GVR_ERR_RUNTIME;
+    if (tape->ctx != ctx || scene->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
+    if (!scene->valid) return set_err(ctx, GVR_ERR_VALIDATION, "scene has not been validated");
+    if (int rc = validate_camera(ctx, camera)) return rc;
+    if (int rc = validate_cfg(ctx, cfg)) return rc;
+    tape->valid = false;
+    tape->has_upstream = false;
+
+    const int K = scene->K, D = scene->D, H = camera->height, W = camera->width;
+    const int Dc = D > 1 ? D : 1;
+    const int kp = cfg->k_prime;
+    const long long P = (long long)H * W;
+    const int tile = kp <= 24 ? kFwdTileSmall : kFwdTileLarge;
+    const int tiles_x = (W + tile - 1) / tile, tiles_y = (H + tile - 1) / tile;
+    const int tiles = tiles_x * tiles_y;
+
+    tape->scene = scene;
+    tape->scene_version = scene->version;
+    tape->cam = *camera;
+    tape->cfg = *cfg;
+    tape->K = K;
+    tape->D = D;
+    tape->H = H;
+    tape->W = W;
+    tape->tile = tile;
+    tape->tiles_x = tiles_x;
+    tape->tiles_y = tiles_y;
+
+    CameraP cp;
+    std::memcpy(cp.R, camera->rotation, sizeof cp.R);
+    std::memcpy(cp.T, camera->translation, sizeof cp.T);
+    cp.focal = camera->focal;
+    cp.ox = camera->ox;
+    cp.oy = camera->oy;
+    cp.H = H;
+    cp.W = W;
+    SelP sp;
+    sp.eta = cfg->eta;
+    sp.log_eta = std::log(cfg->eta);
+    sp.chi = 2.0 * std::log(1.0 / cfg->eta);
+    sp.kp = kp;
+    sp.coarse = cfg->coarse_enabled ? 1 : 0;
+    sp.ds = cfg->coarse_downsample;
+    tape->camp = cp;
+    tape->selp = sp;
+
+    CUDA_TRY(ctx, tape->rec32.ensure(sizeof(Rec32) * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, tape->rec64.ensure(sizeof(Rec64) * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, tape->counts.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
+    CUDA_TRY(ctx, tape->offsets.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
+    CUDA_TRY(ctx, tape->ranges.ensure(sizeof(int) * 2 * (size_t)tiles));
+    CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
+    CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
+    CUDA_TRY(ctx, tape->image.ensure(sizeof(double) * (size_t)P * Dc));
+    CUDA_TRY(ctx, tape->alpha.ensure(sizeof(double) * (size_t)P));
+    CUDA_TRY(ctx, tape->depth.ensure(sizeof(double) * (size_t)P));
+    const bool want_w = out && out->topk_w;
+    if (want_w) CUDA_TRY(ctx, tape->topk_w.ensure(sizeof(double) * (size_t)P * kp));
+
+    int* dflags = ctx->flags.as<int>();
+    CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 2 * sizeof(int), ctx->stream));
+    int* ranges = tape->ranges.as<int>();
+    CUDA_TRY(ctx, cudaMemsetAsync(ranges, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
+
+    uint32_t pairs = 0;
+    if (K > 0) {
+        // K1 projection + culling
+        ProjectParams pp;
+        pp.K = K;
+        pp.centers = scene->centers.as<double>();
+        pp.inv_cov = scene->inv_cov.as<double>();
+        pp.cam = cp;
+        pp.sel = sp;
+        pp.tile = tile;
+        pp.tiles_x = tiles_x;
+        pp.tiles_y = tiles_y;
+        pp.rec32 = tape->rec32.as<Rec32>();
+        pp.rec64 = tape->rec64.as<Rec64>();
+        pp.counts = tape->counts.as<uint32_t>();
+        pp.dropped_behind = dflags;
+        {
+            StageTimer st(ctx, ST_PROJECT);
+            project_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(pp);
+        }
+        LAUNCH_CHECK(ctx);
+
+        // exclusive scan of per-kernel pair counts (counts[K] = 0 -> offsets[K] = total)
+        size_t scan_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tape->counts.as<uint32_t>(), tape->offsets.as<uint32_t>(),
+                                      K + 1, ctx->stream);
+        CUDA_TRY(ctx, tape->cub_tmp.ensure(scan_bytes));
+        {
+            StageTimer st(ctx, ST_SCAN);
+            CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(tape->cub_tmp.p, scan_bytes, tape->counts.as<uint32_t>(),
+                                                        tape->offsets.as<uint32_t>(), K + 1, ctx->stream));
+        }
+        ++ctx->lib_calls;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags, tape->offsets.as<uint32_t>() + K, sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 1, dflags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        if (int rc = sync_and_check(ctx)) return rc;
+        std::memcpy(&pairs, ctx->h_flags, sizeof pairs);
+        tape->dropped_behind = ctx->h_flags[1];
+    } else {
+        tape->dropped_behind = 0;
+    }
+    tape->pairs = pairs;
+
+    if (pairs > 0) {
+        CUDA_TRY(ctx, tape->keys.ensure(sizeof(unsigned long long) * pairs));
+        CUDA_TRY(ctx, tape->keys_alt.ensure(sizeof(unsigned long long) * pairs));
+        CUDA_TRY(ctx, tape->vals.ensure(sizeof(int) * pairs));
+        CUDA_TRY(ctx, tape->vals_alt.ensure(sizeof(int) * pairs));
+        EmitParams ep;
+        ep.K = K;
+        ep.rec32 = tape->rec32.as<Rec32>();
+        ep.offsets = tape->offsets.as<uint32_t>();
+        ep.sel = sp;
+        ep.H = H;
+        ep.W = W;
+        ep.tile = tile;
+        ep.tiles_x = tiles_x;
+        ep.keys = tape->keys.as<unsigned long long>();
+        ep.vals = tape->vals.as<int>();
+        {
+            StageTimer st(ctx, ST_EMIT);
+            emit_pairs_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(ep);
+        }
+        LAUNCH_CHECK(ctx);
+
+        cub::DoubleBuffer<unsigned long long> dk(tape->keys.as<unsigned long long>(),
+                                                 tape->keys_alt.as<unsigned long long>());
+        cub::DoubleBuffer<int> dv(tape->vals.as<int>(), tape->vals_alt.as<int>());
+        const int end_bit = 32 + (sp.coarse ? ceil_log2((uint32_t)tiles) : 0);
+        size_t sort_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, dk, dv, (int)pairs, 0, end_bit, ctx->stream);
+        CUDA_TRY(ctx, tape->cub_tmp.ensure(sort_bytes));
+        {
+            StageTimer st(ctx, ST_SORT);
+            CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(tape->cub_tmp.p, sort_bytes, dk, dv, (int)pairs, 0,
+                                                          end_bit, ctx->stream));
+        }
+        ++ctx->lib_calls;
+        {
+            StageTimer st(ctx, ST_RANGES);
+            tile_ranges_kernel<<<blocks_for(pairs, 256), 256, 0, ctx->stream>>>(pairs, dk.Current(), ranges,
+                                                                               ranges + tiles);
+        }
+        LAUNCH_CHECK(ctx);
+        // keep the sorted ids where the forward reads them
+        if (dv.Current() != tape->vals.as<int>()) {
+            std::swap(tape->vals.p, tape->vals_alt.p);
+            std::swap(tape->vals.cap, tape->vals_alt.cap);
+        }
+        if (dk.Current() != tape->keys.as<unsigned long long>()) {
+            std::swap(tape->keys.p, tape->keys_alt.p);
+            std::swap(tape->keys.cap, tape->keys_alt.cap);
+        }
+    }
+
+    // K3 fused forward
+    FwdParams fp;
+    fp.cam = cp;
+    fp.sel = sp;
+    fp.D = D;
+    fp.Dc = Dc;
+    fp.tau = scene->tau;
+    fp.guard_abs = (float)ctx->guard;
+    fp.prefilter_c1 = ctx->guard > 1e3 ? 0.0f : 1.0f - 1e-4f;
+    fp.tiles_x = tiles_x;
+    fp.tile_start = ranges;
+    fp.tile_end = ranges + tiles;
+    fp.vals = tape->vals.as<int>();
+    fp.rec32 = tape->rec32.as<Rec32>();
+    fp.rec64 = tape->rec64.as<Rec64>();
+    fp.attr = scene->attr.as<double>();
+    fp.image = tape->image.as<double>();
+    fp.alpha = tape->alpha.as<double>();
+    fp.depth = tape->depth.as<double>();
+    fp.topk = tape->topk.as<int>();
+    fp.count = tape->count.as<int>();
+    fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
+    fp.nonfinite = dflags + 1;
+    int rc = GVR_OK;
+    if (tile == kFwdTileSmall) {
+        if (kp <= 8) rc = launch_forward<8, kFwdTileSmall>(ctx, fp, tiles);
+        else if (kp <= 16) rc = launch_forward<16, kFwdTileSmall>(ctx, fp, tiles);
+        else if (kp <= 20) rc = launch_forward<20, kFwdTileSmall>(ctx, fp, tiles);
+        else rc = launch_forward<24, kFwdTileSmall>(ctx, fp, tiles);
+    } else {
+        if (kp <= 32) rc = launch_forward<32, kFwdTileLarge>(ctx, fp, tiles);
+        else if (kp <= 48) rc = launch_forward<48, kFwdTileLarge>(ctx, fp, tiles);
+        else rc = launch_forward<64, kFwdTileLarge>(ctx, fp, tiles);
+    }
+    if (rc) return rc;
+    tape->valid = true;
+
+    if (out) {
+        bool host = false;
+        if ((rc = copy_out(ctx, out->image, tape->image.p, sizeof(double) * P * Dc, &host))) return rc;
+        if ((rc = copy_out(ctx, out->alpha, tape->alpha.p, sizeof(double) * P, &host))) return rc;
+        if ((rc = copy_out(ctx, out->depth, tape->depth.p, sizeof(double) * P, &host))) return rc;
+        if (out->topk_idx || out->topk_w) {
+            const bool dev_i = !out->topk_idx || is_device_ptr(out->topk_idx);
+            const bool dev_w = !out->topk_w || is_device_ptr(out->topk_w);
+            int* oi = out->topk_idx;
+            double* ow = out->topk_w;
+            if (!dev_i) {
+                CUDA_TRY(ctx, tape->stage_i.ensure(sizeof(int) * (size_t)P * kp));
+                oi = tape->stage_i.as<int>();
+            }
+            if (!dev_w) {
+                CUDA_TRY(ctx, tape->stage_w.ensure(sizeof(double) * (size_t)P * kp));
+                ow = tape->stage_w.as<double>();
+            }
+            expand_topk_kernel<<<blocks_for(P * kp, 256), 256, 0, ctx->stream>>>(
+                P, kp, tape->topk.as<int>(), tape->count.as<int>(), tape->topk_w.as<double>(), oi, ow);
+            LAUNCH_CHECK(ctx);
+            if (!dev_i) CUDA_TRY(ctx, cudaMemcpyAsync(out->topk_idx, oi, sizeof(int) * (size_t)P * kp,
+                                                      cudaMemcpyDeviceToHost, ctx->stream));
+            if (!dev_w) CUDA_TRY(ctx, cudaMemcpyAsync(out->topk_w, ow, sizeof(double) * (size_t)P * kp,
+                                                      cudaMemcpyDeviceToHost, ctx->stream));
+            host = host || !dev_i || !dev_w;
+        }
+        if (host) {
+            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 1, dflags + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            if ((rc = sync_and_check(ctx))) return rc;
+            if (ctx->h_flags[1]) {
+                tape->valid = false;
+                return set_err(ctx, GVR_ERR_VALIDATION, "image contains non-finite values");
+            }
+        }
+    }
+    return GVR_OK;
+}
+
+int gvr_tape_traced(gvr_context* ctx, const gvr_tape* t, int32_t* idx, double* l, double* q, double* sigma) {
+    if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    const long long P = (long long)t->H * t->W;
+    const int kp = t->cfg.k_prime;
+    const size_t n = (size_t)P * kp;
+    // stage everything on device, then copy out
+    Buf si, sl, sq, ss;
+    CUDA_TRY(ctx, si.ensure(sizeof(int) * n));
+    CUDA_TRY(ctx, sl.ensure(sizeof(double) * n));
+    CUDA_TRY(ctx, sq.ensure(sizeof(double) * n));
+    CUDA_TRY(ctx, ss.ensure(sizeof(double) * n));
+    traced_kernel<<<blocks_for((long long)n, 256), 256, 0, ctx->stream>>>(
+        t->camp, kp, t->topk.as<int>(), t->count.as<int>(), t->rec64.as<Rec64>(), si.as<int>(), sl.as<double>(),
+        sq.as<double>(), ss.as<double>());
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    int rc;
+    if ((rc = copy_out(ctx, idx, si.p, sizeof(int) * n, &host))) return rc;
+    if ((rc = copy_out(ctx, l, sl.p, sizeof(double) * n, &host))) return rc;
+    if ((rc = copy_out(ctx, q, sq.p, sizeof(double) * n, &host))) return rc;
+    if ((rc = copy_out(ctx, sigma, ss.p, sizeof(double) * n, &host))) return rc;
+    rc = sync_and_check(ctx);
+    si.release();
+    sl.release();
+    sq.release();
+    ss.release();
+    return rc;
+}
+
+// ---------------------------------------------------------------- loss / backward
+
+int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, const double* target_alpha,
+                    double w_image, double w_alpha, double* loss_out, double* d_image_out, double* d_alpha_out) {
+    if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (!target_image || !target_alpha) return set_err(ctx, GVR_ERR_RUNTIME, "targets must not be null");
+    const long long P = (long long)t->H * t->W;
+    const int Dc = t->D > 1 ? t->D : 1;
+    const long long n_img = P * Dc;
+    CUDA_TRY(ctx, t->d_image.ensure(sizeof(double) * (size_t)(n_img + P) * 2));
+    CUDA_TRY(ctx, t->d_alpha.ensure(sizeof(double) * (size_t)P));
+    double* timg = t->d_image.as<double>() + n_img;  // target staging after the gradient
+    double* talpha = timg + 0;                       // alpha target staged after the image target
+    const double* ti = target_image;
+    const double* ta = target_alpha;
+    if (!is_device_ptr(target_image)) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(timg, target_image, sizeof(double) * n_img, cudaMemcpyHostToDevice, ctx->stream));
+        ti = timg;
+    }
+    talpha = timg + n_img;
+    if (!is_device_ptr(target_alpha)) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(talpha, target_alpha, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+        ta = talpha;
+    }
+    double* dloss = reinterpret_cast<double*>(ctx->flags.as<int>() + 4);
+    CUDA_TRY(ctx, cudaMemsetAsync(dloss, 0, sizeof(double), ctx->stream));
+    const int threads = 256;
+    const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), 148 * 8);
+    {
+        StageTimer st(ctx, ST_LOSS);
+        scalar_loss_kernel<<<blocks, threads, 0, ctx->stream>>>(n_img, P, t->image.as<double>(), ti,
+                                                                t->alpha.as<double>(), ta, w_image, w_alpha,
+                                                                t->d_image.as<double>(), t->d_alpha.as<double>(),
+                                                                dloss);
+    }
+    LAUNCH_CHECK(ctx);
+    t->has_upstream = true;
+    bool host = false;
+    int rc;
+    if ((rc = copy_out(ctx, d_image_out, t->d_image.p, sizeof(double) * n_img, &host))) return rc;
+    if ((rc = copy_out(ctx, d_alpha_out, t->d_alpha.p, sizeof(double) * P, &host))) return rc;
+    if ((rc = copy_out(ctx, loss_out, dloss, sizeof(double), &host))) return rc;
+    if (host) return sync_and_check(ctx);
+    return GVR_OK;
+}
+
+int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
+                 const gvr_grad_flags* flags, const gvr_gradients* out) {
+    if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
+        return set_err(ctx, GVR_ERR_RUNTIME, "the scene changed after the forward render");
+    const gvr_scene* scene = t->scene;
+    const int K = t->K, D = t->D;
+    const long long P = (long long)t->H * t->W;
+    const double* di;
+    const double* da;
+    if (!d_image && !d_alpha) {
+        if (!t->has_upstream) return set_err(ctx, GVR_ERR_RUNTIME, "no upstream gradient stored in the tape");
+        // gvr_scalar_loss stores H*W*max(D,1); backward reads H*W*D (identical layout when D >= 1)
+        di = t->d_image.as<double>();
+        da = t->d_alpha.as<double>();
+    } else {
+        if (!d_alpha || (D > 0 && !d_image))
+            return set_err(ctx, GVR_ERR_VALIDATION, "backward: d_image shape does not match the forward render");
+        CUDA_TRY(ctx, t->d_image.ensure(sizeof(double) * (size_t)(P * (D > 0 ? D : 1) + P) * 2));
+        CUDA_TRY(ctx, t->d_alpha.ensure(sizeof(double) * (size_t)P));
+        di = d_image;
+        da = d_alpha;
+        int rc;
+        if (D > 0 && !is_device_ptr(d_image)) {
+            if ((rc = copy_in(ctx, t->d_image.p, d_image, sizeof(double) * P * D))) return rc;
+            di = t->d_image.as<double>();
+        }
+        if (!is_device_ptr(d_alpha)) {
+            if ((rc = copy_in(ctx, t->d_alpha.p, d_alpha, sizeof(double) * P))) return rc;
+            da = t->d_alpha.as<double>();
+        }
+    }
+    const int through_t = flags ? flags->through_transmittance : 1;
+    const int through_rho = flags ? flags->through_density : 1;
+
+    CUDA_TRY(ctx, t->acc.ensure(sizeof(double) * 9 * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, t->d_attr.ensure(sizeof(double) * (size_t)(D > 0 ? D : 1) * (K > 0 ? K : 1)));
+    CUDA_TRY(ctx, t->d_center.ensure(sizeof(double) * 3 * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, t->d_inv_cov.ensure(sizeof(double) * 9 * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, t->d_rt.ensure(sizeof(double) * 12));
+    CUDA_TRY(ctx, cudaMemsetAsync(t->acc.p, 0, sizeof(double) * 9 * (size_t)K, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(t->d_attr.p, 0, sizeof(double) * (size_t)D * K, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(t->d_rt.p, 0, sizeof(double) * 12, ctx->stream));
+
+    if (K > 0) {
+        BwdParams bp;
+        bp.cam = t->camp;
+        bp.kp = t->cfg.k_prime;
+        bp.D = D;
+        bp.Dc = D > 1 ? D : 1;
+        bp.tau = scene->tau;
+        bp.through_t = through_t;
+        bp.through_rho = through_rho;
+        const int btx = (t->W + kBwdTile - 1) / kBwdTile, bty = (t->H + kBwdTile - 1) / kBwdTile;
+        bp.tiles_x = btx;
+        bp.topk = t->topk.as<int>();
+        bp.count = t->count.as<int>();
+        bp.rec64 = t->rec64.as<Rec64>();
+        bp.attr = scene->attr.as<double>();
+        bp.d_image = di;
+        bp.d_alpha = da;
+        bp.acc = t->acc.as<double>();
+        bp.d_attr = t->d_attr.as<double>();
+        const int kp = t->cfg.k_prime;
+        int rc;
+        if (kp <= 8) rc = launch_backward<8>(ctx, bp, btx * bty);
+        else if (kp <= 16) rc = launch_backward<16>(ctx, bp, btx * bty);
+        else if (kp <= 20) rc = launch_backward<20>(ctx, bp, btx * bty);
+        else if (kp <= 24) rc = launch_backward<24>(ctx, bp, btx * bty);
+        else if (kp <= 32) rc = launch_backward<32>(ctx, bp, btx * bty);
+        else if (kp <= 48) rc = launch_backward<48>(ctx, bp, btx * bty);
+        else rc = launch_backward<64>(ctx, bp, btx * bty);
+        if (rc) return rc;
+
+        ObjParams op;
+        op.K = K;
+        op.cam = t->camp;
+        op.acc = t->acc.as<double>();
+        op.centers = scene->centers.as<double>();
+        op.inv_cov = scene->inv_cov.as<double>();
+        op.d_center = t->d_center.as<double>();
+        op.d_inv_cov = t->d_inv_cov.as<double>();
+        op.d_rt = t->d_rt.as<double>();
+        {
+            StageTimer st(ctx, ST_OBJECT);
+            object_space_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(op);
+        }
+        LAUNCH_CHECK(ctx);
+    }
+    if (out) {
+        bool host = false;
+        int rc;
+        if ((rc = copy_out(ctx, out->d_center, t->d_center.p, sizeof(double) * 3 * (size_t)K, &host))) return rc;
+        if ((rc = copy_out(ctx, out->d_inv_cov, t->d_inv_cov.p, sizeof(double) * 9 * (size_t)K, &host))) return rc;
+        if ((rc = copy_out(ctx, out->d_attr, t->d_attr.p, sizeof(double) * (size_t)D * K, &host))) return rc;
+        if ((rc = copy_out(ctx, out->d_rotation, t->d_rt.p, sizeof(double) * 9, &host))) return rc;
+        if ((rc = copy_out(ctx, out->d_translation, t->d_rt.as<double>() + 9, sizeof(double) * 3, &host))) return rc;
+        if (host) return sync_and_check(ctx);
+    }
+    return GVR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+// K0 scene validation and K1 per-kernel projection / culling.
+#pragma once
+
+#include "gvr_common.cuh"
+
+#include <float.h>
+#include <limits.h>
+
+namespace gvrk {
+
+// Smallest eigenvalue of the symmetric matrix read from the lower triangle
+// (Eigen's SelfAdjointEigenSolver reads the lower triangle), cyclic Jacobi —
+// same iteration as the oracle so boundary decisions agree.
+__device__ inline double min_eigenvalue_lower(const double* m) {
+    double a[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) a[3 * i + j] = i >= j ? m[3 * i + j] : m[3 * j + i];
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        const double off = a[1] * a[1] + a[2] * a[2] + a[5] * a[5];
+        if (off <= DBL_MIN) break;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = p + 1; q < 3; ++q) {
+                const double apq = a[3 * p + q];
+                if (apq == 0.0) continue;
+                const double theta = (a[3 * q + q] - a[3 * p + p]) / (2 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
+                const double c = 1 / sqrt(t * t + 1), s = t * c;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double akp = a[3 * k + p], akq = a[3 * k + q];
+                    a[3 * k + p] = c * akp - s * akq;
+                    a[3 * k + q] = s * akp + c * akq;
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double apk = a[3 * p + k], aqk = a[3 * q + k];
+                    a[3 * p + k] = c * apk - s * aqk;
+                    a[3 * q + k] = s * apk + c * aqk;
+                }
+            }
+    }
+    return fmin(a[0], fmin(a[4], a[8]));
+}
+
+// K0: GaussianKernel::validate (types.cpp:17-29) for every kernel; the first
+// failing kernel (lowest index) wins, encoded as (k << 2) | code with
+// code 1 = non-finite, 2 = not symmetric, 3 = not positive-definite.
+__global__ void validate_scene_kernel(int K, int D, const double* __restrict__ centers,
+                                      const double* __restrict__ inv_cov, const double* __restrict__ attr,
+                                      unsigned long long* __restrict__ first_error) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double s[9];
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        s[i] = inv_cov[9ll * k + i];
+        finite &= isfinite(s[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) finite &= isfinite(centers[3ll * k + i]);
+    for (int c = 0; c < D; ++c) finite &= isfinite(attr[(long long)D * k + c]);
+    unsigned code = 0;
+    if (!finite) {
+        code = 1;
+    } else {
+        double scale = 0.0, asym = 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) scale = fmax(scale, fabs(s[i]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) asym = fmax(asym, fabs(s[3 * i + j] - s[3 * j + i]));
+        if (scale != 0.0 && !(asym <= 1e-6 * scale)) {
+            code = 2;
+        } else if (min_eigenvalue_lower(s) <= 0.0) {
+            code = 3;
+        }
+    }
+    if (code) atomicMin(first_error, ((unsigned long long)k << 2) | code);
+}
+
+// 3x3 inverse by cofactors, exact emulation of the oracle / Eigen-shim order.
+__device__ __forceinline__ void xinverse3(const double* m, double* inv) {
+#define M(i, j) m[3 * (i) + (j)]
+    const double c00 = xsub(xmul(M(1, 1), M(2, 2)), xmul(M(1, 2), M(2, 1)));
+    const double c10 = xsub(xmul(M(1, 2), M(2, 0)), xmul(M(1, 0), M(2, 2)));
+    const double c20 = xsub(xmul(M(1, 0), M(2, 1)), xmul(M(1, 1), M(2, 0)));
+    const double det = xadd(xadd(xmul(M(0, 0), c00), xmul(M(0, 1), c10)), xmul(M(0, 2), c20));
+    const double id = xdiv(1.0, det);
+    inv[0] = xmul(c00, id);
+    inv[3] = xmul(c10, id);
+    inv[6] = xmul(c20, id);
+    inv[1] = xmul(xsub(xmul(M(0, 2), M(2, 1)), xmul(M(0, 1), M(2, 2))), id);
+    inv[4] = xmul(xsub(xmul(M(0, 0), M(2, 2)), xmul(M(0, 2), M(2, 0))), id);
+    inv[7] = xmul(xsub(xmul(M(0, 1), M(2, 0)), xmul(M(0, 0), M(2, 1))), id);
+    inv[2] = xmul(xsub(xmul(M(0, 1), M(1, 2)), xmul(M(0, 2), M(1, 1))), id);
+    inv[5] = xmul(xsub(xmul(M(0, 2), M(1, 0)), xmul(M(0, 0), M(1, 2))), id);
+    inv[8] = xmul(xsub(xmul(M(0, 0), M(1, 1)), xmul(M(0, 1), M(1, 0))), id);
+#undef M
+}
+
+// static_cast<int>(double) as compiled for x86-64 (cvttsd2si): out-of-range and
+// NaN give INT_MIN; the reference's box clamps depend on it for extreme boxes.
+__device__ __forceinline__ int x86_int(double v) {
+    if (!(v > -2147483649.0 && v < 2147483648.0)) return INT_MIN;
+    return (int)v;
+}
+
+__device__ __forceinline__ uint32_t float_order_bits(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+struct ProjectParams {
+    int K;
+    const double* centers;  // object space [K*3]
+    const double* inv_cov;  // object space [K*9]
+    CameraP cam;
+    SelP sel;
+    int tile;           // pixels per tile edge
+    int tiles_x, tiles_y;
+    Rec32* rec32;
+    Rec64* rec64;
+    uint32_t* counts;  // [K + 1], pairs each kernel emits (counts[K] = 0)
+    int* dropped_behind;
+};
+
+// K1: view transform (scene.cpp:5-17), coarse screen box (tracer.cpp:37-113) in
+// exact FP64, the FP32 pre-filter record and the depth key for early exit.
+__global__ void project_kernel(ProjectParams p) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) p.counts[p.K] = 0;
+    if (k >= p.K) return;
+    const CameraP& c = p.cam;
+
+    double mo[3], so[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) mo[i] = p.centers[3ll * k + i];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) so[i] = p.inv_cov[9ll * k + i];
+
+    // M' = R M + T ; S' = (R S) R^T
+    Rec64 r;
+    xmatvec(c.R, mo, r.m);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.m[i] = xadd(r.m[i], c.T[i]);
+    double rt[9], rs[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) rt[3 * j + i] = c.R[3 * i + j];
+    xmatmul(c.R, so, rs);
+    xmatmul(rs, rt, r.s);
+    xmatvec(r.s, r.m, r.sm);
+    r.pad = 0.0;
+    p.rec64[k] = r;
+
+    const double f = c.focal;
+    const double z = r.m[2];
+    Rec32 q;
+    q.s00 = (float)r.s[0];
+    q.s01 = (float)r.s[1];
+    q.s02 = (float)r.s[2];
+    q.s11 = (float)r.s[4];
+    q.s12 = (float)r.s[5];
+    q.s22 = (float)r.s[8];
+    q.cr_lo = 1;
+    q.cr_hi = 0;  // empty box
+    q.cc_lo = 1;
+    q.cc_hi = 0;
+    q.zmin = -FLT_MAX;
+    uint32_t count = 0;
+
+    if (z <= kBehindCameraEps) {
+        // behind the camera: dropped (tracer.cpp:52-56, blender.cpp:86)
+        atomicAdd(p.dropped_behind, 1);
+        q.zf = -1.0f;
+        q.ci_int = q.cj_int = 0;
+        q.ci_frac = q.cj_frac = 0.0f;
+        p.rec32[k] = q;
+        p.counts[k] = 0;
+        return;
+    }
+
+    double cov[9];
+    xinverse3(r.s, cov);
+    const double chi = p.sel.chi;
+    const double ci = xadd(c.oy, xdiv(xmul(f, r.m[0]), z));
+    const double cj = xadd(c.ox, xdiv(xmul(f, r.m[1]), z));
+    const double ext[3] = {__dsqrt_rn(fmax(0.0, xmul(chi, cov[0]))), __dsqrt_rn(fmax(0.0, xmul(chi, cov[4]))),
+                           __dsqrt_rn(fmax(0.0, xmul(chi, cov[8])))};
+    const double zmin = xsub(z, ext[2]);
+    const bool straddles = zmin <= kBehindCameraEps;
+
+    // Depth key: every selected kernel has l >= z - ext_z (its peak lies inside
+    // the eta-ellipsoid, whose camera-space z-extent is +-ext_z); conservative
+    // rounding keeps the bound strict under FP64/FP32 rounding.
+    if (zmin > 0.0) q.zmin = __double2float_rd(zmin - 1e-12 * zmin);
+
+    // Centre-relative FP32 pre-filter data; unusual geometry (near-plane
+    // straddlers, far off-axis centres) bypasses the pre-filter (zf < 0).
+    q.zf = (float)(z / f);
+    if (straddles || fabs(ci) > 1e7 || fabs(cj) > 1e7) {
+        q.zf = -1.0f;
+        q.ci_int = q.cj_int = 0;
+        q.ci_frac = q.cj_frac = 0.0f;
+    } else {
+        const double fi = floor(ci), fj = floor(cj);
+        q.ci_int = (int)fi;
+        q.cj_int = (int)fj;
+        q.ci_frac = (float)(ci - fi);
+        q.cj_frac = (float)(cj - fj);
+    }
+
+    if (!p.sel.coarse) {
+        // no coarse stage: every front kernel is a candidate of every pixel (blender.cpp:84-88)
+        count = 1;
+    } else {
+        // jac = [[f/z, 0, -f x/z^2], [0, f/z, -f y/z^2]]; cov2 = jac cov jac^T (tracer.cpp:61-66)
+        const double zz = xmul(z, z);
+        const double jac[6] = {xdiv(f, z), 0.0, xdiv(xmul(-f, r.m[0]), zz), 0.0, xdiv(f, z), xdiv(xmul(-f, r.m[1]), zz)};
+        double jc[6];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                double acc = xadd(0.0, xmul(jac[3 * i], cov[j]));
+                acc = xadd(acc, xmul(jac[3 * i + 1], cov[3 + j]));
+                jc[3 * i + j] = xadd(acc, xmul(jac[3 * i + 2], cov[6 + j]));
+            }
+        double cov2[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                double acc = xadd(0.0, xmul(jc[3 * i], jac[3 * j]));
+                acc = xadd(acc, xmul(jc[3 * i + 1], jac[3 * j + 1]));
+                cov2[2 * i + j] = xadd(acc, xmul(jc[3 * i + 2], jac[3 * j + 2]));
+            }
+        const double rh = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[0])));
+        const double rw = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[3])));
+        double top = xsub(ci, rh), bottom = xadd(ci, rh), left = xsub(cj, rw), right = xadd(cj, rw);
+        if (straddles) {
+            top = 0;
+            bottom = c.H - 1;
+            left = 0;
+            right = c.W - 1;
+        } else {
+#pragma unroll
+            for (int corner = 0; corner < 8; ++corner) {
+                const double px = xadd(r.m[0], (corner & 1) ? ext[0] : -ext[0]);
+                const double py = xadd(r.m[1], (corner & 2) ? ext[1] : -ext[1]);
+                const double pz = xadd(r.m[2], (corner & 4) ? ext[2] : -ext[2]);
+                const double pi = xadd(c.oy, xdiv(xmul(f, px), pz));
+                const double pj = xadd(c.ox, xdiv(xmul(f, py), pz));
+                top = pi < top ? pi : top;
+                bottom = pi > bottom ? pi : bottom;
+                left = pj < left ? pj : left;
+                right = pj > right ? pj : right;
+            }
+        }
+        // (tracer.cpp:100-103), with the reference's static_cast<int> semantics
+        const int lo_r = max(0, x86_int(floor(xsub(top, 1.0))));
+        const int hi_r = min(c.H - 1, x86_int(ceil(xadd(bottom, 1.0))));
+        const int lo_c = max(0, x86_int(floor(xsub(left, 1.0))));
+        const int hi_c = min(c.W - 1, x86_int(ceil(xadd(right, 1.0))));
+        if (lo_r <= hi_r && lo_c <= hi_c) {
+            const int ds = p.sel.ds;
+            q.cr_lo = lo_r / ds;
+            q.cr_hi = hi_r / ds;
+            q.cc_lo = lo_c / ds;
+            q.cc_hi = hi_c / ds;
+            // pixel extent of the pushed cells -> tile rectangle
+            const int r0 = q.cr_lo * ds, r1 = min(c.H, (q.cr_hi + 1) * ds) - 1;
+            const int c0 = q.cc_lo * ds, c1 = min(c.W, (q.cc_hi + 1) * ds) - 1;
+            count = (uint32_t)((r1 / p.tile - r0 / p.tile + 1) * (c1 / p.tile - c0 / p.tile + 1));
+        }
+    }
+    p.rec32[k] = q;
+    p.counts[k] = count;
+}
+
+struct EmitParams {
+    int K;
+    const Rec32* rec32;
+    const uint32_t* offsets;  // exclusive scan of counts
+    SelP sel;
+    int H, W, tile, tiles_x;
+    unsigned long long* keys;  // (tile << 32) | order(zmin)
+    int* vals;
+};
+
+// K2a: one (tile, depth) key per (kernel, overlapped tile).
+__global__ void emit_pairs_kernel(EmitParams p) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.K) return;
+    const uint32_t off = p.offsets[k];
+    const uint32_t n = p.offsets[k + 1] - off;
+    if (n == 0) return;
+    const Rec32 q = p.rec32[k];
+    const unsigned long long zbits = float_order_bits(q.zmin);
+    if (!p.sel.coarse) {
+        p.keys[off] = zbits;
+        p.vals[off] = k;
+        return;
+    }
+    const int ds = p.sel.ds;
+    const int r0 = q.cr_lo * ds, r1 = min(p.H, (q.cr_hi + 1) * ds) - 1;
+    const int c0 = q.cc_lo * ds, c1 = min(p.W, (q.cc_hi + 1) * ds) - 1;
+    const int tr0 = r0 / p.tile, tr1 = r1 / p.tile, tc0 = c0 / p.tile, tc1 = c1 / p.tile;
+    uint32_t o = off;
+    for (int tr = tr0; tr <= tr1; ++tr)
+        for (int tc = tc0; tc <= tc1; ++tc) {
+            const unsigned long long tile = (unsigned long long)(tr * p.tiles_x + tc);
+            p.keys[o] = (tile << 32) | zbits;
+            p.vals[o] = k;
+            ++o;
+        }
+}
+
+// K2c: per-tile [start, end) ranges of the sorted pair list.
+__global__ void tile_ranges_kernel(uint32_t n, const unsigned long long* __restrict__ keys, int* __restrict__ start,
+                                   int* __restrict__ end) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int t = (int)(keys[i] >> 32);
+    if (i == 0 || (int)(keys[i - 1] >> 32) != t) start[t] = (int)i;
+    if (i + 1 == n || (int)(keys[i + 1] >> 32) != t) end[t] = (int)i + 1;
+}
+
+}  // namespace gvrk

@@ -1,0 +1,324 @@
+"""Host-side mirror of the reference render API over the C ABI.
+
+Reference entry points (namespace ``gvr``, /root/reference/proj):
+
+* ``render(scene, camera, cfg, threads)``            blender.hpp:40-41
+* ``render_with_tape(scene, camera, cfg, threads)``  grad.hpp:41-42
+* ``backward(tape, d_image, d_alpha, flags)``        grad.hpp:53-54
+* ``ScalarLoss::value(buf, d_image*, d_alpha*)``     grad.hpp:68, grad.cpp:201-216
+
+Same argument meaning and error behaviour: invalid inputs raise
+:class:`ValidationError` with the reference's message text. ``threads`` is
+accepted for signature parity and ignored (the GPU grid replaces
+``parallel_for_partitions``). Every call goes through ``libgvr_cuda.so``.
+
+Buffers may be numpy arrays (host; copied over PCIe inside the call) or CUDA
+tensors / any object exposing ``data_ptr()`` (device-resident; no copy).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .types import (
+    Camera,
+    GaussianScene,
+    GradFlags,
+    GradientBundle,
+    RenderBuffers,
+    ScalarLoss,
+    SelectionConfig,
+    ValidationError,
+)
+
+
+class GvrRuntimeError(RuntimeError):
+    """Runtime / CUDA failure inside libgvr_cuda.so (status 2)."""
+
+
+def _ptr(x) -> Optional[int]:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    raise TypeError(f"unsupported buffer type {type(x)!r}")
+
+
+class Context:
+    """One CUDA device + stream + scratch arenas (``gvr_context``)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = ctypes.c_void_p()
+        rc = self.lib.gvr_context_create(device, ctypes.byref(h))
+        if rc != _lib.GVR_OK:
+            raise GvrRuntimeError(f"gvr_context_create(device={device}) failed: no usable sm_100 CUDA device")
+        self.handle = h
+        self.device = device
+
+    def check(self, rc: int) -> None:
+        if rc == _lib.GVR_OK:
+            return
+        msg = self.lib.gvr_last_error(self.handle).decode()
+        if rc == _lib.GVR_ERR_VALIDATION:
+            raise ValidationError(msg)
+        raise GvrRuntimeError(msg)
+
+    def set_stream(self, stream_handle: Optional[int]) -> None:
+        self.check(self.lib.gvr_context_set_stream(self.handle, stream_handle))
+
+    def synchronize(self) -> None:
+        self.check(self.lib.gvr_context_synchronize(self.handle))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.gvr_context_launch_count(self.handle))
+
+    @property
+    def library_call_count(self) -> int:
+        return int(self.lib.gvr_context_library_call_count(self.handle))
+
+    STAGES = ("project", "scan", "emit", "sort", "ranges", "forward", "loss", "backward", "object_space")
+
+    def enable_timing(self, on: bool = True) -> None:
+        self.check(self.lib.gvr_context_enable_timing(self.handle, int(on)))
+
+    def stage_times(self) -> dict:
+        """{stage: (total_ms, launches)} accumulated since enable_timing()."""
+        n = len(self.STAGES)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        self.check(self.lib.gvr_context_stage_times(self.handle, ms.ctypes.data, cnt.ctypes.data, n))
+        return {s: (float(ms[i]), int(cnt[i])) for i, s in enumerate(self.STAGES)}
+
+    def pipe_peak(self, kind: str = "fp32") -> float:
+        """Measured FMA-chain FLOP/s of the FP32 or FP64 pipe."""
+        out = ctypes.c_double()
+        self.check(self.lib.gvr_measure_pipe_peak(self.handle, 0 if kind == "fp32" else 1, ctypes.byref(out)))
+        return out.value
+
+    def set_prefilter_guard(self, guard: float) -> None:
+        self.check(self.lib.gvr_context_set_prefilter_guard(self.handle, float(guard)))
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.gvr_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = getattr(_default, "ctx", None)
+    if ctx is None or ctx.device != device:
+        ctx = Context(device)
+        _default.ctx = ctx
+    return ctx
+
+
+class DeviceScene:
+    """A validated, device-resident scene (``gvr_scene``).
+
+    ``set`` uploads + validates once (GaussianScene::validate, types.cpp:31-42);
+    renders then reuse it without re-validation."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.gvr_scene_create(self.ctx.handle, ctypes.byref(h)))
+        self.handle = h
+        self.K = 0
+        self.D = 0
+        self.tau = 1.0
+
+    def set(self, scene: GaussianScene) -> "DeviceScene":
+        return self.set_raw(scene.size, scene.attr_dim(), scene.tau, scene.centers, scene.inv_cov, scene.attr)
+
+    def set_raw(self, K: int, D: int, tau: float, centers, inv_cov, attr) -> "DeviceScene":
+        self.ctx.check(
+            self.ctx.lib.gvr_scene_set(self.ctx.handle, self.handle, int(K), int(D), float(tau), _ptr(centers),
+                                       _ptr(inv_cov), _ptr(attr) if D > 0 else None)
+        )
+        self.K, self.D, self.tau = int(K), int(D), float(tau)
+        return self
+
+    def close(self) -> None:
+        if self.handle:
+            self.ctx.lib.gvr_scene_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Tape:
+    """``gvr::Tape`` (grad.hpp:26-33): the device record of a forward render."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.gvr_tape_create(self.ctx.handle, ctypes.byref(h)))
+        self.handle = h
+        self.scene: Optional[DeviceScene] = None
+        self.camera: Optional[Camera] = None
+        self.cfg: Optional[SelectionConfig] = None
+        self.host_scene: Optional[GaussianScene] = None
+
+    def shape(self):
+        h, w, kp, d = (ctypes.c_int32() for _ in range(4))
+        self.ctx.check(self.ctx.lib.gvr_tape_shape(self.handle, ctypes.byref(h), ctypes.byref(w), ctypes.byref(kp),
+                                                   ctypes.byref(d)))
+        return h.value, w.value, kp.value, d.value
+
+    def traced(self):
+        """Per-pixel selected kernels (Tape::traced): idx, l, q, sigma as [H, W, K'] arrays."""
+        h, w, kp, _ = self.shape()
+        idx = np.empty((h, w, kp), dtype=np.int32)
+        l, q, s = (np.empty((h, w, kp)) for _ in range(3))
+        self.ctx.check(self.ctx.lib.gvr_tape_traced(self.ctx.handle, self.handle, _ptr(idx), _ptr(l), _ptr(q),
+                                                    _ptr(s)))
+        return idx, l, q, s
+
+    def close(self) -> None:
+        if self.handle:
+            self.ctx.lib.gvr_tape_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ForwardResult:
+    """``gvr::ForwardResult`` (grad.hpp:35-38)."""
+
+    buffers: RenderBuffers
+    tape: Tape
+
+
+def _camera_c(camera: Camera) -> _lib.GvrCamera:
+    c = _lib.GvrCamera()
+    c.rotation[:] = [float(v) for v in np.asarray(camera.rotation, dtype=np.float64).reshape(9)]
+    c.translation[:] = [float(v) for v in np.asarray(camera.translation, dtype=np.float64).reshape(3)]
+    c.focal, c.ox, c.oy = float(camera.focal), float(camera.ox), float(camera.oy)
+    c.height, c.width = int(camera.height), int(camera.width)
+    return c
+
+
+def _selection_c(cfg: SelectionConfig) -> _lib.GvrSelection:
+    return _lib.GvrSelection(float(cfg.eta), int(cfg.k_prime), int(bool(cfg.coarse_enabled)),
+                             int(cfg.coarse_downsample))
+
+
+def _as_device_scene(scene, ctx: Context) -> DeviceScene:
+    if isinstance(scene, DeviceScene):
+        return scene
+    return DeviceScene(ctx).set(scene)
+
+
+def render_into(ctx: Context, dscene: DeviceScene, camera: Camera, cfg: SelectionConfig, tape: Tape,
+                image=None, alpha=None, depth=None, topk_idx=None, topk_w=None) -> None:
+    """Low-level forward: outputs written into caller buffers (host or device, any may be None)."""
+    out = _lib.GvrRenderOutputs(_ptr(image), _ptr(alpha), _ptr(depth), _ptr(topk_idx), _ptr(topk_w))
+    cam_c, sel_c = _camera_c(camera), _selection_c(cfg)
+    ctx.check(ctx.lib.gvr_render(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c), tape.handle,
+                                 ctypes.byref(out)))
+    tape.scene, tape.camera, tape.cfg = dscene, camera, cfg
+
+
+def render_with_tape(scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(), threads: int = 0, *,
+                     weights: bool = True, ctx: Optional[Context] = None) -> ForwardResult:
+    """``gvr::render_with_tape`` (grad.cpp:38-47): render and keep the tape for backward."""
+    del threads
+    ctx = ctx or default_context()
+    dscene = _as_device_scene(scene, ctx)
+    h, w = int(camera.height), int(camera.width)
+    dc = max(dscene.D, 1)
+    kp = int(cfg.k_prime)
+    image = np.empty((h, w, dc))
+    alpha = np.empty((h, w, 1))
+    depth = np.empty((h, w, 1))
+    tidx = np.empty((h, w, kp), dtype=np.int32) if weights else None
+    tw = np.empty((h, w, kp)) if weights else None
+    tape = Tape(ctx)
+    render_into(ctx, dscene, camera, cfg, tape, image, alpha, depth, tidx, tw)
+    tape.host_scene = scene if isinstance(scene, GaussianScene) else None
+    return ForwardResult(RenderBuffers(image, alpha, depth, tidx, tw), tape)
+
+
+def render(scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(), threads: int = 0, *,
+           weights: bool = True, ctx: Optional[Context] = None) -> RenderBuffers:
+    """``gvr::render`` (blender.cpp:141-144)."""
+    return render_with_tape(scene, camera, cfg, threads, weights=weights, ctx=ctx).buffers
+
+
+def scalar_loss(tape: Tape, loss: ScalarLoss, *, want_grads: bool = True):
+    """``ScalarLoss::value`` evaluated on the device against the taped render.
+
+    Returns ``(loss, d_image, d_alpha)`` (host arrays when ``want_grads``); the
+    upstream gradient also stays in the tape for ``backward(tape, None, None)``."""
+    ctx = tape.ctx
+    h, w, kp, d = tape.shape()
+    out = np.zeros(1)
+    di = np.empty((h, w, max(d, 1))) if want_grads else None
+    da = np.empty((h, w, 1)) if want_grads else None
+    ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(np.ascontiguousarray(loss.target_image)),
+                                      _ptr(np.ascontiguousarray(loss.target_alpha)), float(loss.w_image),
+                                      float(loss.w_alpha), _ptr(out), _ptr(di), _ptr(da)))
+    return float(out[0]), di, da
+
+
+def backward_into(tape: Tape, d_image, d_alpha, flags: GradFlags = GradFlags(), d_center=None, d_inv_cov=None,
+                  d_attr=None, d_rotation=None, d_translation=None) -> None:
+    """Low-level backward: gradients written into caller buffers (host or device, any may be None)."""
+    ctx = tape.ctx
+    f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
+    g = _lib.GvrGradients(_ptr(d_center), _ptr(d_inv_cov), _ptr(d_attr), _ptr(d_rotation), _ptr(d_translation))
+    ctx.check(ctx.lib.gvr_backward(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f),
+                                   ctypes.byref(g)))
+
+
+def backward(tape, d_image, d_alpha, flags: GradFlags = GradFlags()) -> GradientBundle:
+    """``gvr::backward`` (grad.cpp:49-199). ``tape`` may be a Tape or a ForwardResult.
+
+    ``d_image`` must be [H, W, D] and ``d_alpha`` [H, W, 1] (reference shape rule,
+    grad.cpp:58-63); pass both as None to use the upstream from :func:`scalar_loss`."""
+    if isinstance(tape, ForwardResult):
+        tape = tape.tape
+    h, w, kp, d = tape.shape()
+    if d_image is not None or d_alpha is not None:
+        d_image = np.ascontiguousarray(d_image, dtype=np.float64) if isinstance(d_image, np.ndarray) else d_image
+        d_alpha = np.ascontiguousarray(d_alpha, dtype=np.float64) if isinstance(d_alpha, np.ndarray) else d_alpha
+        if isinstance(d_image, np.ndarray) and (d_image.ndim != 3 or d_image.shape != (h, w, d)):
+            raise ValidationError("backward: d_image shape does not match the forward render")
+        if isinstance(d_alpha, np.ndarray) and d_alpha.reshape(-1).shape[0] != h * w or (
+            isinstance(d_alpha, np.ndarray) and d_alpha.ndim == 3 and d_alpha.shape[2] != 1
+        ):
+            raise ValidationError("backward: d_alpha shape does not match the forward render")
+    k = tape.scene.K
+    gb = GradientBundle(np.empty((k, 3)), np.empty((k, 3, 3)), np.empty((k, d)), np.empty((3, 3)), np.empty(3))
+    backward_into(tape, d_image, d_alpha, flags, gb.d_center, gb.d_inv_cov, gb.d_attr if d > 0 else None,
+                  gb.d_rotation, gb.d_translation)
+    return gb
