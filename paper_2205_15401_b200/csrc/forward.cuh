@@ -13,6 +13,7 @@ struct FwdParams {
     float guard_abs;     // FP32 pre-filter guard band on q (absolute)
     float prefilter_c1;  // 1 - relative slack
     int tiles_x;
+    int need_predicate;  // coarse cells not aligned to tiles: per-pixel exact cell test
     const int* tile_start;
     const int* tile_end;
     const int* vals;   // sorted kernel ids
@@ -51,57 +52,67 @@ __device__ __forceinline__ bool prefilter_pass(const Rec32& r, int i, int j, flo
     return fmaf(dsd * c1, A, -B * B) < c2 * A;
 }
 
-// Sorted (ascending (l, idx)) register list with KMAX slots holding K' <= KMAX
-// live entries: slots [0, KMAX-K') are dead (-inf, never displaced), the rest
-// start empty (+inf); the current K'-th nearest is always slot KMAX-1.
-template <int KMAX>
+// Sorted (ascending (l, idx)) list with KMAX slots holding K' <= KMAX live
+// entries: slots [0, KMAX-K') are dead (-inf, never displaced), the rest start
+// empty (+inf); the current K'-th nearest is always slot KMAX-1. The FP64 keys
+// live in registers (static indices), the kernel ids in shared memory
+// ([slot][thread], read only to break exact ties and written on shifts).
+template <int KMAX, int NT>
 struct TopK {
     double l[KMAX];
-    int idx[KMAX];
+    int* id;  // smem + tid, stride NT
 
-    __device__ __forceinline__ void init(int kp) {
+    __device__ __forceinline__ void init(int kp, int* base) {
+        id = base;
 #pragma unroll
-        for (int s = 0; s < KMAX; ++s) {
-            l[s] = (s < KMAX - kp) ? -INFINITY : INFINITY;
-            idx[s] = -1;
-        }
+        for (int s = 0; s < KMAX; ++s) l[s] = (s < KMAX - kp) ? -INFINITY : INFINITY;
     }
     __device__ __forceinline__ double worst() const { return l[KMAX - 1]; }
-    __device__ __forceinline__ bool accepts(double cl, int ci) const {
-        return traced_less(cl, ci, l[KMAX - 1], idx[KMAX - 1]);
+    __device__ __forceinline__ bool less_than_slot(double cl, int ci, int s) const {
+        return cl < l[s] || (cl == l[s] && ci < id[s * NT]);
     }
+    __device__ __forceinline__ bool accepts(double cl, int ci) const { return less_than_slot(cl, ci, KMAX - 1); }
+    // Precondition: accepts(cl, ci). Candidates arrive roughly in ascending l
+    // (lists are sorted by the depth bound), so insert from the back; the
+    // shifting stops at the first slot that stays put, usually after 1-2 steps.
     __device__ __forceinline__ void insert(double cl, int ci) {
+        bool placed = false;
 #pragma unroll
-        for (int s = 0; s < KMAX; ++s) {
-            const bool lt = traced_less(cl, ci, l[s], idx[s]);
-            const double tl = l[s];
-            const int ti = idx[s];
-            l[s] = lt ? cl : tl;
-            idx[s] = lt ? ci : ti;
-            cl = lt ? tl : cl;
-            ci = lt ? ti : ci;
+        for (int s = KMAX - 1; s > 0; --s) {
+            if (!placed) {
+                if (less_than_slot(cl, ci, s - 1)) {
+                    l[s] = l[s - 1];
+                    id[s * NT] = id[(s - 1) * NT];
+                } else {
+                    l[s] = cl;
+                    id[s * NT] = ci;
+                    placed = true;
+                }
+            }
+        }
+        if (!placed) {
+            l[0] = cl;
+            id[0] = ci;
         }
     }
-};
-
-template <int TILE>
-struct TileGeom {
-    static constexpr int NT = TILE * TILE;
 };
 
 template <int KMAX, int TILE>
-__global__ void __launch_bounds__(TILE* TILE) fine_forward_kernel(FwdParams p) {
+__global__ void __launch_bounds__(TILE* TILE, KMAX <= 24 ? 8 : (KMAX <= 32 ? 5 : 4)) fine_forward_kernel(FwdParams p) {
     constexpr int NT = TILE * TILE;
     extern __shared__ __align__(16) unsigned char smem[];
+    // region A: candidate chunk (selection) / blend staging (after selection)
     Rec32* s32 = reinterpret_cast<Rec32*>(smem);
     Rec64* s64 = reinterpret_cast<Rec64*>(s32 + NT);
     int* sidx = reinterpret_cast<int*>(s64 + NT);
-    // blend staging, aliases the chunk buffers once selection is over:
-    // l relative to the nearest entry in FP64 (z = dl / sigma needs it), the rest FP32
-    double* b_dl = reinterpret_cast<double*>(smem);
+    double* b_dl = reinterpret_cast<double*>(smem);  // l relative to the nearest entry (FP64)
     float* b_pk = reinterpret_cast<float*>(b_dl + KMAX * NT);
     float* b_is = b_pk + KMAX * NT;
-    int* b_id = reinterpret_cast<int*>(b_is + KMAX * NT);
+    // region H: kernel ids of the selection list, [slot][thread]
+    constexpr size_t kRegionA = (sizeof(Rec32) + sizeof(Rec64) + sizeof(int)) * NT > 16 * KMAX * NT
+                                    ? (sizeof(Rec32) + sizeof(Rec64) + sizeof(int)) * NT
+                                    : 16 * KMAX * NT;
+    int* h_id = reinterpret_cast<int*>(smem + kRegionA);
 
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
@@ -121,8 +132,8 @@ __global__ void __launch_bounds__(TILE* TILE) fine_forward_kernel(FwdParams p) {
     const float c2 = 2.0f * (p.guard_abs - (float)p.sel.log_eta);
     const double log_eta = p.sel.log_eta;
 
-    TopK<KMAX> top;
-    top.init(p.sel.kp);
+    TopK<KMAX, NT> top;
+    top.init(p.sel.kp, h_id + tid);
     bool done = !inside;
 
     for (int base = start; base < end; base += NT) {
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__(TILE* TILE) fine_forward_kernel(FwdParams p) {
                     done = true;
                     break;
                 }
-                if (p.sel.coarse && !(ci >= r.cr_lo && ci <= r.cr_hi && cj >= r.cc_lo && cj <= r.cc_hi)) continue;
+                if (p.need_predicate && !(ci >= r.cr_lo && ci <= r.cr_hi && cj >= r.cc_lo && cj <= r.cc_hi)) continue;
                 if (!prefilter_pass(r, i, j, u, v, c2, p.prefilter_c1)) continue;
                 const Traced64 t = trace_exact(d, s64[c]);
                 if (!(t.q > log_eta)) continue;  // fine_select threshold (tracer.cpp:117-118)
@@ -158,25 +169,24 @@ __global__ void __launch_bounds__(TILE* TILE) fine_forward_kernel(FwdParams p) {
 
     if (!inside) return;
 
-    // Stage the selected entries: FP64 re-trace for q and sigma, l relative to
-    // the nearest entry so the pairwise differences keep FP64 accuracy in FP32.
+    // The selection (ascending (l, idx)) occupies slots [KMAX-K', KMAX-K'+n).
     int n = 0;
-    double l0 = 0.0, total_peak = 0.0;
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-        if (isfinite(top.l[s])) {
-            const int k = top.idx[s];
-            const Traced64 t = trace_exact(d, p.rec64[k]);
-            if (n == 0) l0 = t.l;
-            const double pk = exp(t.q);
-            total_peak += pk;
-            b_dl[n * NT + tid] = t.l - l0;
-            b_pk[n * NT + tid] = (float)pk;
-            b_is[n * NT + tid] = (float)__dsqrt_rn(t.a);  // 1/sigma
-            b_id[n * NT + tid] = k;
-            p.topk[pix * p.sel.kp + n] = k;
-            ++n;
-        }
+    for (int s = 0; s < KMAX; ++s) n += isfinite(top.l[s]) ? 1 : 0;
+    const int* b_id = h_id + (KMAX - p.sel.kp) * NT;
+    // Stage the selected entries: FP64 re-trace for q and sigma, l relative to
+    // the nearest entry so the pairwise differences keep FP64 accuracy.
+    double l0 = 0.0, total_peak = 0.0;
+    for (int s = 0; s < n; ++s) {
+        const int k = b_id[s * NT + tid];
+        const Traced64 t = trace_exact(d, p.rec64[k]);
+        if (s == 0) l0 = t.l;
+        const double pk = exp(t.q);
+        total_peak += pk;
+        b_dl[s * NT + tid] = t.l - l0;
+        b_pk[s * NT + tid] = (float)pk;
+        b_is[s * NT + tid] = (float)__dsqrt_rn(t.a);  // 1/sigma
+        p.topk[pix * p.sel.kp + s] = k;
     }
     p.count[pix] = n;
 
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(TILE* TILE) fine_forward_kernel(FwdParams p) {
         float acc = 0.0f;
         for (int m = 0; m < n; ++m) {
             const float z = (float)((dlk - b_dl[m * NT + tid]) * (double)b_is[m * NT + tid]);
-            acc = fmaf(b_pk[m * NT + tid], normal_cdf_f(z), acc);
+            acc = fmaf(b_pk[m * NT + tid], fast_normal_cdf(z), acc);
         }
         const float w = expf(-tau * acc) * b_pk[k * NT + tid];
         const double wd = (double)w;

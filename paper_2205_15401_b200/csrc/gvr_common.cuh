@@ -129,6 +129,27 @@ __device__ __forceinline__ float normal_cdf_f(float x) { return 0.5f * erfcf(-x 
 // phi(x) = exp(-x^2/2) / sqrt(2 pi)  (grad.cpp:16)
 __device__ __forceinline__ float normal_pdf_f(float x) { return 0.398942280401432678f * expf(-0.5f * x * x); }
 
+// Branch-free Phi for the forward blend: erfc(x) = t exp(-x^2 + P(t)),
+// t = 1 / (1 + x/2) (Chebyshev-fitted erfc, fractional error < 1.2e-7 for all
+// x >= 0), so |Phi - Phi_exact| < 6e-8 absolute: one reciprocal, one exp2, 10 FMA.
+__device__ __forceinline__ float fast_normal_cdf(float z) {
+    const float x = fabsf(z) * 0.70710678118654752f;
+    const float t = __fdividef(1.0f, fmaf(0.5f, x, 1.0f));
+    float p = 0.17087277f;
+    p = fmaf(p, t, -0.82215223f);
+    p = fmaf(p, t, 1.48851587f);
+    p = fmaf(p, t, -1.13520398f);
+    p = fmaf(p, t, 0.27886807f);
+    p = fmaf(p, t, -0.18628806f);
+    p = fmaf(p, t, 0.09678418f);
+    p = fmaf(p, t, 0.37409196f);
+    p = fmaf(p, t, 1.00002368f);
+    p = fmaf(p, t, -1.26551223f);
+    const float e = exp2f(fmaf(-x, x, p) * 1.4426950408889634f);
+    const float half_erfc = 0.5f * t * e;
+    return z >= 0.0f ? 1.0f - half_erfc : half_erfc;
+}
+
 // (l, idx) lexicographic order of fine_select (tracer.cpp:119-122)
 __device__ __forceinline__ bool traced_less(double la, int ia, double lb, int ib) {
     return la < lb || (la == lb && ia < ib);

@@ -26,8 +26,9 @@ using namespace gvrk;
 
 namespace {
 
-constexpr int kFwdTileSmall = 16;  // forward tile edge for k_prime <= 24
-constexpr int kFwdTileLarge = 8;   // forward tile edge for 24 < k_prime <= 64
+// Forward tile = 8x8 pixels = one default coarse cell (64 threads, 2 warps):
+// small CTAs balance the very uneven per-tile work and keep 8 CTAs per SM.
+constexpr int kFwdTile = 8;
 constexpr int kBwdTile = 8;
 constexpr int kMaxKPrime = 64;
 
@@ -260,8 +261,8 @@ template <int KMAX, int TILE>
 int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
     constexpr int NT = TILE * TILE;
     const size_t chunk = (size_t)NT * (sizeof(Rec32) + sizeof(Rec64) + sizeof(int));
-    const size_t blend = (size_t)KMAX * NT * 20;
-    const size_t smem = chunk > blend ? chunk : blend;
+    const size_t blend = (size_t)KMAX * NT * 16;
+    const size_t smem = (chunk > blend ? chunk : blend) + (size_t)KMAX * NT * sizeof(int);
     auto kern = fine_forward_kernel<KMAX, TILE>;
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
@@ -535,7 +536,7 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     const int Dc = D > 1 ? D : 1;
     const int kp = cfg->k_prime;
     const long long P = (long long)H * W;
-    const int tile = kp <= 24 ? kFwdTileSmall : kFwdTileLarge;
+    const int tile = kFwdTile;
     const int tiles_x = (W + tile - 1) / tile, tiles_y = (H + tile - 1) / tile;
     const int tiles = tiles_x * tiles_y;
 
@@ -693,6 +694,7 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.guard_abs = (float)ctx->guard;
     fp.prefilter_c1 = ctx->guard > 1e3 ? 0.0f : 1.0f - 1e-4f;
     fp.tiles_x = tiles_x;
+    fp.need_predicate = (sp.coarse && sp.ds % tile != 0) ? 1 : 0;
     fp.tile_start = ranges;
     fp.tile_end = ranges + tiles;
     fp.vals = tape->vals.as<int>();
@@ -707,16 +709,13 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
     fp.nonfinite = dflags + 1;
     int rc = GVR_OK;
-    if (tile == kFwdTileSmall) {
-        if (kp <= 8) rc = launch_forward<8, kFwdTileSmall>(ctx, fp, tiles);
-        else if (kp <= 16) rc = launch_forward<16, kFwdTileSmall>(ctx, fp, tiles);
-        else if (kp <= 20) rc = launch_forward<20, kFwdTileSmall>(ctx, fp, tiles);
-        else rc = launch_forward<24, kFwdTileSmall>(ctx, fp, tiles);
-    } else {
-        if (kp <= 32) rc = launch_forward<32, kFwdTileLarge>(ctx, fp, tiles);
-        else if (kp <= 48) rc = launch_forward<48, kFwdTileLarge>(ctx, fp, tiles);
-        else rc = launch_forward<64, kFwdTileLarge>(ctx, fp, tiles);
-    }
+    if (kp <= 8) rc = launch_forward<8, kFwdTile>(ctx, fp, tiles);
+    else if (kp <= 16) rc = launch_forward<16, kFwdTile>(ctx, fp, tiles);
+    else if (kp <= 20) rc = launch_forward<20, kFwdTile>(ctx, fp, tiles);
+    else if (kp <= 24) rc = launch_forward<24, kFwdTile>(ctx, fp, tiles);
+    else if (kp <= 32) rc = launch_forward<32, kFwdTile>(ctx, fp, tiles);
+    else if (kp <= 48) rc = launch_forward<48, kFwdTile>(ctx, fp, tiles);
+    else rc = launch_forward<64, kFwdTile>(ctx, fp, tiles);
     if (rc) return rc;
     tape->valid = true;
 
