@@ -163,10 +163,12 @@ class ClockSampler:
 
 
 def algorithmic_flops(wc, D=3):
-    """SURVEY.md §8d per-unit counts x oracle work counters (per render)."""
-    fwd = 40 * wc["C"] + 6 * wc["N2"] + (8 + 2 * D) * wc["N1"] + 300 * wc["kernels"]
-    bwd = 20 * wc["N2"] + (100 + 4 * D) * wc["N1"] + 150 * wc["kernels"]
-    return fwd, bwd
+    """SURVEY.md §8d per-unit FLOP counts x the reference's work counters
+    (C = sum_p |candidates(p)|, N1 = sum_p n_p, N2 = sum_p n_p^2), per launch:
+    select = 40 per candidate trace; blend = 6 per pair + (8 + 2D) per entry;
+    backward = 20 per pair + (100 + 4D) per entry."""
+    return {"select": 40.0 * wc["C"], "blend": 6.0 * wc["N2"] + (8 + 2 * D) * wc["N1"],
+            "backward": 20.0 * wc["N2"] + (100 + 4 * D) * wc["N1"]}
 
 
 def run_reference(args):
@@ -283,29 +285,31 @@ def run_ours(args):
     ctx.enable_timing(False)
     wc_all = json.load(open(os.path.join(ROOT, "bench_workcounts.json")))
     wc = wc_all["C2"]
-    fwd_flop, bwd_flop = algorithmic_flops(wc)
+    flops = algorithmic_flops(wc)
     fp32_peak = ctx.pipe_peak("fp32")
     fp64_peak = ctx.pipe_peak("fp64")
-    fwd_ms = stages["forward"][0] / max(stages["forward"][1], 1)
-    bwd_ms = stages["backward"][0] / max(stages["backward"][1], 1)
-    dominant = "forward" if fwd_ms >= bwd_ms else "backward"
-    dom_ms = fwd_ms if dominant == "forward" else bwd_ms
-    dom_flop = fwd_flop if dominant == "forward" else bwd_flop
-    achieved = dom_flop / (dom_ms * 1e-3) / 1e12
+    kern_names = {"select": "select_kernel", "blend": "blend_kernel", "backward": "backward_pixels_kernel"}
+    per_launch_ms = {k: stages[k][0] / max(stages[k][1], 1) for k in kern_names}
+    dominant = max(per_launch_ms, key=per_launch_ms.get)
+    dom_ms = per_launch_ms[dominant]
+    achieved = flops[dominant] / (dom_ms * 1e-3) / 1e12
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_json):
         try:
-            traffic = json.load(open(prof_json)).get(dominant)
+            traffic = json.load(open(prof_json)).get(kern_names[dominant])
         except (OSError, ValueError):
             traffic = None
     roofline = {
-        "bound": "fp32", "kernel": "fine_forward_kernel" if dominant == "forward" else "backward_pixels_kernel",
+        "bound": "fp32", "kernel": kern_names[dominant],
         "achieved": achieved, "peak": fp32_peak / 1e12, "unit": "TFLOP/s", "frac": achieved * 1e12 / fp32_peak,
         "traffic": traffic,
-        "peak_source": "measured in-run: FP32 FMA-chain microbenchmark (gvr_measure_pipe_peak)",
+        "peak_source": "measured in-run: FP32 FMA-chain microbenchmark (gvr_measure_pipe_peak); no tensor-core or "
+                       "HBM bound applies (SURVEY.md §8d)",
         "fp64_peak_tflops": fp64_peak / 1e12,
-        "algorithmic_gflop_per_launch": dom_flop / 1e9,
+        "algorithmic_gflop_per_launch": flops[dominant] / 1e9,
+        "kernel_ms_per_launch": per_launch_ms,
+        "kernel_frac_of_fp32_peak": {k: flops[k] / (per_launch_ms[k] * 1e-3) / fp32_peak for k in kern_names},
         "work_counts": {k: wc[k] for k in ("C", "N1", "N2", "kernels")},
         "stage_ms_per_step": {k: v[0] / max(prof_steps, 1) for k, v in stages.items()},
     }

@@ -112,8 +112,9 @@ int gvr_context_synchronize(gvr_context* ctx);
 int64_t gvr_context_launch_count(const gvr_context* ctx);
 int64_t gvr_context_library_call_count(const gvr_context* ctx);
 /* Per-stage device time via CUDA events around each launch (off by default).
- * Stages: 0 project, 1 scan, 2 emit, 3 sort, 4 ranges, 5 forward, 6 loss,
- * 7 backward, 8 object-space. Enabling resets the accumulators. */
+ * Stages: 0 project, 1 scan, 2 emit, 3 sort, 4 ranges/tile ordering,
+ * 5 select, 6 blend, 7 loss, 8 backward, 9 object-space. Enabling resets the
+ * accumulators. */
 int gvr_context_enable_timing(gvr_context* ctx, int on);
 int gvr_context_stage_times(gvr_context* ctx, double* ms, int64_t* count, int n);
 /* Calibration for the roofline: FMA-chain peak of the FP32 (kind 0) or FP64

@@ -11,8 +11,11 @@ struct BwdParams {
     double tau;
     int through_t, through_rho;
     int tiles_x;
+    const int* tile_order;  // tiles by descending sum_p n_p^2 (LPT); first *n_order valid
+    const int* n_order;
     const int* topk;   // [P*kp]
     const int* count;  // [P]
+    const double* tape_t;  // [P*kp] T(l_k) from the forward
     const Rec64* rec64;
     const double* attr;     // [K*D]
     const double* d_image;  // [P*D]
@@ -21,121 +24,120 @@ struct BwdParams {
     double* d_attr;         // [K*D]
 };
 
-// Per pixel (grad.cpp:75-174), one thread per pixel, TILE x TILE pixels per CTA.
-// Pair terms are evaluated "entry-major": for entry e all contributions to
-// d_peak_e, d_l_e, d_sigma_e are gathered in FP64 registers (the reference
-// scatters them pair by pair; the sums are the same), so no per-entry
-// accumulator arrays. Arithmetic is FP64; only Phi / phi are evaluated in FP32
-// from an FP64-accurate argument (the gradient bar is 1e-4 of a class-scaled
-// floor, i.e. ~1e-7 of the largest gradient, which FP32 products would miss).
-template <int KMAX, int TILE>
-__global__ void __launch_bounds__(TILE* TILE) backward_pixels_kernel(BwdParams p) {
-    constexpr int NT = TILE * TILE;
+// Per pixel (grad.cpp:75-174). CTA = one 8x8 tile, 4 threads per pixel (256
+// threads): the pixel's entries are split 4 ways in every pass, which cuts the
+// per-pixel serial chain (the latency limit of this kernel) by 4x.
+// T(l_k) comes from the forward's tape, so only the pair terms are O(n^2).
+// They are evaluated "entry-major": for entry e every contribution to
+// d_peak_e, d_l_e and d_sigma_e is gathered in FP64 registers (the reference
+// scatters them pair by pair; the sums are the same), so there are no
+// per-entry accumulator arrays. Phi / phi are FP32 (~1e-7) from an
+// FP64-accurate argument; products and sums are FP64 (the gradient bar is
+// 1e-4 of a class-scaled floor, ~1e-7 of the largest gradient).
+template <int KMAX>
+__global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
+    constexpr int TILE = 8, NP = 64;
     extern __shared__ __align__(16) unsigned char smem[];
-    // per-entry staging, [slot][thread]: FP64 except the kernel id
+    // per-entry staging, [slot][pixel]
     double* b_dl = reinterpret_cast<double*>(smem);  // l_k - l_0
-    double* b_pk = b_dl + KMAX * NT;                 // e^{q_k}
-    double* b_is = b_pk + KMAX * NT;                 // 1 / sigma_k
-    double* b_da = b_is + KMAX * NT;                 // d_acc_k = -tau T_k d_w_k e^{q_k}
-    double* b_dn = b_da + KMAX * NT;                 // density term d_w_k T_k (or 0)
-    int* b_id = reinterpret_cast<int*>(b_dn + KMAX * NT);
+    double* b_da = b_dl + KMAX * NP;                 // d_acc_k = -tau T_k d_w_k e^{q_k}
+    float* b_pk = reinterpret_cast<float*>(b_da + KMAX * NP);  // e^{q_k}
+    float* b_is = b_pk + KMAX * NP;                  // 1 / sigma_k
+    int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
 
-    const int tid = threadIdx.x;
-    const int tile = blockIdx.x;
-    const int i = (tile / p.tiles_x) * TILE + tid / TILE;
-    const int j = (tile % p.tiles_x) * TILE + tid % TILE;
+    if ((int)blockIdx.x >= *p.n_order) return;
+    const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    const int tile = p.tile_order[blockIdx.x];
+    const int i = (tile / p.tiles_x) * TILE + g / TILE;
+    const int j = (tile % p.tiles_x) * TILE + g % TILE;
     if (i >= p.cam.H || j >= p.cam.W) return;
     const long long pix = (long long)i * p.cam.W + j;
     const int n = p.count[pix];
-    if (n == 0) return;
+    if (n == 0) return;  // the pixel's 4 threads leave together
+    const unsigned grp = 0xfu << (threadIdx.x & 28);
 
     double d[3];
     pixel_ray(p.cam, i, j, d);
-
-    // re-trace the taped selection in exact FP64 (bit-identical to the forward)
-    double l0 = 0.0, total_peak = 0.0;
-    for (int s = 0; s < n; ++s) {
-        const int k = p.topk[pix * p.kp + s];
-        const Traced64 t = trace_exact(d, p.rec64[k]);
-        if (s == 0) l0 = t.l;
-        const double pk = exp(t.q);
-        total_peak += pk;
-        b_dl[s * NT + tid] = t.l - l0;
-        b_pk[s * NT + tid] = pk;
-        b_is[s * NT + tid] = __dsqrt_rn(t.a);
-        b_id[s * NT + tid] = k;
-    }
-
     const double tau = p.tau;
-    const double galpha = p.d_alpha[pix];
-    const double d_total = (p.through_t && galpha != 0.0) ? galpha * tau * exp(-tau * total_peak) : 0.0;
     double dimg[4] = {0, 0, 0, 0};
     for (int c = 0; c < p.D && c < 4; ++c) dimg[c] = p.d_image[pix * p.D + c];
+    const double l0 = trace_exact(d, p.rec64[p.topk[pix * p.kp]]).l;
 
-    // transmittance, d_weight, attribute gradient, d_acc (grad.cpp:81-120)
-    for (int k = 0; k < n; ++k) {
-        const double dlk = b_dl[k * NT + tid];
-        double a = 0.0;
-        for (int m = 0; m < n; ++m) {
-            const float z = (float)((dlk - b_dl[m * NT + tid]) * b_is[m * NT + tid]);
-            a += b_pk[m * NT + tid] * (double)normal_cdf_f(z);
-        }
-        const double trans = exp(-tau * a);
-        const double pk = b_pk[k * NT + tid];
-        const int kid = b_id[k * NT + tid];
+    // re-trace the taped selection in exact FP64 (bit-identical to the forward),
+    // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
+    double peak_part = 0.0;
+    for (int s = sub; s < n; s += 4) {
+        const int k = p.topk[pix * p.kp + s];
+        const Traced64 t = trace_exact(d, p.rec64[k]);
+        const double pk64 = exp(t.q);
+        const float pkf = (float)pk64;
+        const double pk = (double)pkf;
+        peak_part += pk64;
+        const double trans = p.tape_t[pix * p.kp + s];
         double dw = 0.0;
         if (p.D <= 4) {
-            for (int c = 0; c < p.D; ++c) dw += dimg[c] * p.attr[(long long)p.D * kid + c];
+            for (int c = 0; c < p.D; ++c) dw += dimg[c] * p.attr[(long long)p.D * k + c];
         } else {
-            for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * kid + c];
+            for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * k + c];
         }
         const double w = trans * pk;
         if (w != 0.0 || dw != 0.0) {
             for (int c = 0; c < p.D; ++c)
-                atomicAdd(&p.d_attr[(long long)p.D * kid + c], w * (p.D <= 4 ? dimg[c] : p.d_image[pix * p.D + c]));
+                atomicAdd(&p.d_attr[(long long)p.D * k + c], w * (p.D <= 4 ? dimg[c] : p.d_image[pix * p.D + c]));
         }
-        double dacc = 0.0, dens = 0.0;
-        if (dw != 0.0) {
-            if (p.through_rho) dens = dw * trans;
-            if (p.through_t) dacc = -tau * trans * (dw * pk);
-        }
-        b_da[k * NT + tid] = dacc;
-        b_dn[k * NT + tid] = dens;
+        b_dl[s * NP + g] = t.l - l0;
+        b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
+        b_pk[s * NP + g] = pkf;
+        b_is[s * NP + g] = (float)__dsqrt_rn(t.a);
+        b_id[s * NP + g] = k;
     }
+    peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
+    peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
+    __syncwarp(grp);
+    const double galpha = p.d_alpha[pix];
+    const double d_total = (p.through_t && galpha != 0.0) ? galpha * tau * exp(-tau * peak_part) : 0.0;
 
     // entry-major pair terms + chain to camera space (grad.cpp:121-173)
-    for (int e = 0; e < n; ++e) {
-        const double dle = b_dl[e * NT + tid];
-        const double ise = b_is[e * NT + tid];
-        const double pke = b_pk[e * NT + tid];
-        const double dae = b_da[e * NT + tid];
-        double dpk = d_total + b_dn[e * NT + tid];
+    for (int e = sub; e < n; e += 4) {
+        const double dle = b_dl[e * NP + g];
+        const float ise = b_is[e * NP + g];
+        const double pke = (double)b_pk[e * NP + g];
+        const double dae = b_da[e * NP + g];
+        const int kid = b_id[e * NP + g];
+        double dpk = d_total;
+        if (p.through_rho) {
+            double dw = 0.0;
+            if (p.D <= 4) {
+                for (int c = 0; c < p.D; ++c) dw += dimg[c] * p.attr[(long long)p.D * kid + c];
+            } else {
+                for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * kid + c];
+            }
+            if (dw != 0.0) dpk += dw * p.tape_t[pix * p.kp + e];  // density path (grad.cpp:120)
+        }
         double dl = 0.0, dsg = 0.0;
         for (int k = 0; k < n; ++k) {
-            const double dak = b_da[k * NT + tid];
-            const double dlk = b_dl[k * NT + tid];
+            const double dak = b_da[k * NP + g];
+            const double dlk = b_dl[k * NP + g];
             if (dak != 0.0) {
                 // pair (k, m = e): z = (l_k - l_e) / sigma_e
-                const double z = (dlk - dle) * ise;
-                const float zf = (float)z;
-                dpk += dak * (double)normal_cdf_f(zf);
+                const float z = (float)((dlk - dle) * (double)ise);
+                dpk += dak * (double)fast_normal_cdf(z);
                 if (k != e) {
-                    const double g = dak * pke * (double)normal_pdf_f(zf) * ise;
-                    dl -= g;
-                    dsg -= g * z;
+                    const double gg = dak * (double)(normal_pdf_fast(z) * ise) * pke;
+                    dl -= gg;
+                    dsg -= gg * (double)z;
                 }
             }
             if (dae != 0.0 && k != e) {
                 // pair (k = e, m = k): z = (l_e - l_k) / sigma_k
-                const double isk = b_is[k * NT + tid];
-                const float zf = (float)((dle - dlk) * isk);
-                dl += dae * b_pk[k * NT + tid] * (double)normal_pdf_f(zf) * isk;
+                const float isk = b_is[k * NP + g];
+                const float z = (float)((dle - dlk) * (double)isk);
+                dl += dae * (double)(b_pk[k * NP + g] * normal_pdf_fast(z) * isk);
             }
         }
         const double dq = dpk * pke;
         if (dl == 0.0 && dq == 0.0 && dsg == 0.0) continue;
 
-        const int kid = b_id[e * NT + tid];
         const Rec64 r = p.rec64[kid];
         double sd[3], v[3], sv[3];
         xmatvec(r.s, d, sd);

@@ -32,13 +32,16 @@ struct SelP {
     int kp, coarse, ds;
 };
 
-// Per-kernel FP32 record for the pre-filter and the exact cell predicate (64 B).
+// Per-kernel FP32 record for the pre-filters (64 B).
 struct __align__(16) Rec32 {
     float s00, s01, s02, s11;
     float s12, s22, zf, zmin;  // zf = z / F; zmin = conservative lower bound of l
     float ci_frac, cj_frac;
     int ci_int, cj_int;        // screen centre (row, col) = int + frac
-    int cr_lo, cr_hi, cc_lo, cc_hi;  // coarse cells pushed (tracer.cpp:100-110)
+    // Screen box of the eta-level set (tracer.cpp:61-98, before the +-1 padding
+    // and cell rounding), rounded outward: contains every pixel centre whose ray
+    // meets the eta-ellipsoid, i.e. every pixel where q > ln(eta) is possible.
+    float top, bottom, left, right;
 };
 
 // Per-kernel FP64 camera-space record for the exact trace (128 B).
@@ -148,6 +151,11 @@ __device__ __forceinline__ float fast_normal_cdf(float z) {
     const float e = exp2f(fmaf(-x, x, p) * 1.4426950408889634f);
     const float half_erfc = 0.5f * t * e;
     return z >= 0.0f ? 1.0f - half_erfc : half_erfc;
+}
+
+// phi(z) with the hardware exp2 (relative error ~2^-22 + |z^2/2| 2^-24).
+__device__ __forceinline__ float normal_pdf_fast(float z) {
+    return 0.398942280401432678f * exp2f(-0.72134752044448170f * z * z);
 }
 
 // (l, idx) lexicographic order of fine_select (tracer.cpp:119-122)

@@ -29,7 +29,6 @@ namespace {
 // Forward tile = 8x8 pixels = one default coarse cell (64 threads, 2 warps):
 // small CTAs balance the very uneven per-tile work and keep 8 CTAs per SM.
 constexpr int kFwdTile = 8;
-constexpr int kBwdTile = 8;
 constexpr int kMaxKPrime = 64;
 
 struct Buf {
@@ -68,7 +67,9 @@ bool is_device_ptr(const void* ptr) {
 
 }  // namespace
 
-enum Stage { ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_FORWARD, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT };
+enum Stage {
+    ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
+};
 
 struct gvr_context {
     int device = 0;
@@ -114,8 +115,9 @@ struct gvr_tape {
     Buf rec32, rec64, counts, offsets;
     // pairs
     Buf keys, keys_alt, vals, vals_alt, cub_tmp, ranges;
+    Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
     // per pixel
-    Buf topk, count, image, alpha, depth, topk_w;
+    Buf topk, count, image, alpha, depth, topk_w, tape_t;
     Buf d_image, d_alpha;
     // gradients
     Buf acc, d_attr, d_center, d_inv_cov, d_rt;
@@ -257,17 +259,28 @@ int ceil_log2(uint32_t v) {
     return b;
 }
 
-template <int KMAX, int TILE>
-int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
-    constexpr int NT = TILE * TILE;
-    const size_t chunk = (size_t)NT * (sizeof(Rec32) + sizeof(Rec64) + sizeof(int));
-    const size_t blend = (size_t)KMAX * NT * 16;
-    const size_t smem = (chunk > blend ? chunk : blend) + (size_t)KMAX * NT * sizeof(int);
-    auto kern = fine_forward_kernel<KMAX, TILE>;
-    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int KMAX>
+int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
     {
-        StageTimer st(ctx, ST_FORWARD);
+        constexpr int NT = 64;
+        const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT;
+        auto kern = select_kernel<KMAX>;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        StageTimer st(ctx, ST_SELECT);
         kern<<<tiles, NT, smem, ctx->stream>>>(fp);
+    }
+    LAUNCH_CHECK(ctx);
+    {
+        StageTimer st(ctx, ST_RANGES);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, 0, nullptr, nullptr, cost, order_b, n_b);
+    }
+    LAUNCH_CHECK(ctx);
+    {
+        const size_t smem = 28ull * KMAX * 64;
+        auto kern = blend_kernel<KMAX>;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        StageTimer st(ctx, ST_BLEND);
+        kern<<<tiles, 256, smem, ctx->stream>>>(fp);
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
@@ -275,13 +288,12 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
 
 template <int KMAX>
 int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
-    constexpr int NT = kBwdTile * kBwdTile;
-    const size_t smem = (size_t)KMAX * NT * 44;
-    auto kern = backward_pixels_kernel<KMAX, kBwdTile>;
+    const size_t smem = 28ull * KMAX * 64;
+    auto kern = backward_pixels_kernel<KMAX>;
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
         StageTimer st(ctx, ST_BACKWARD);
-        kern<<<tiles, NT, smem, ctx->stream>>>(bp);
+        kern<<<tiles, 256, smem, ctx->stream>>>(bp);
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
@@ -506,8 +518,8 @@ void gvr_tape_destroy(gvr_tape* t) {
     if (!t) return;
     cudaStreamSynchronize(t->ctx->stream);
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->counts, &t->offsets, &t->keys, &t->keys_alt, &t->vals,
-                   &t->vals_alt, &t->cub_tmp, &t->ranges, &t->topk, &t->count, &t->image, &t->alpha,
-                   &t->depth, &t->topk_w, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
+                   &t->vals_alt, &t->cub_tmp, &t->ranges, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
+                   &t->depth, &t->topk_w, &t->tape_t, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w};
     for (Buf* b : bufs) b->release();
     delete t;
@@ -575,8 +587,10 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     CUDA_TRY(ctx, tape->counts.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
     CUDA_TRY(ctx, tape->offsets.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
     CUDA_TRY(ctx, tape->ranges.ensure(sizeof(int) * 2 * (size_t)tiles));
+    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (2 + 3 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
+    CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->image.ensure(sizeof(double) * (size_t)P * Dc));
     CUDA_TRY(ctx, tape->alpha.ensure(sizeof(double) * (size_t)P));
     CUDA_TRY(ctx, tape->depth.ensure(sizeof(double) * (size_t)P));
@@ -657,7 +671,7 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
         cub::DoubleBuffer<unsigned long long> dk(tape->keys.as<unsigned long long>(),
                                                  tape->keys_alt.as<unsigned long long>());
         cub::DoubleBuffer<int> dv(tape->vals.as<int>(), tape->vals_alt.as<int>());
-        const int end_bit = 32 + (sp.coarse ? ceil_log2((uint32_t)tiles) : 0);
+        const int end_bit = 32 + ceil_log2((uint32_t)tiles);
         size_t sort_bytes = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, dk, dv, (int)pairs, 0, end_bit, ctx->stream);
         CUDA_TRY(ctx, tape->cub_tmp.ensure(sort_bytes));
@@ -684,7 +698,16 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
         }
     }
 
-    // K3 fused forward
+    // K3 fused forward over the non-empty tiles, most expensive first
+    int* sched = tape->sched.as<int>();
+    int* order_f = sched + 2;
+    float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
+    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (size_t)tiles, ctx->stream));
+    {
+        StageTimer st(ctx, ST_RANGES);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, 1, ranges, ranges + tiles, nullptr, order_f, sched);
+    }
+    LAUNCH_CHECK(ctx);
     FwdParams fp;
     fp.cam = cp;
     fp.sel = sp;
@@ -694,7 +717,11 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.guard_abs = (float)ctx->guard;
     fp.prefilter_c1 = ctx->guard > 1e3 ? 0.0f : 1.0f - 1e-4f;
     fp.tiles_x = tiles_x;
-    fp.need_predicate = (sp.coarse && sp.ds % tile != 0) ? 1 : 0;
+    fp.tile_order = order_f;
+    fp.n_order = sched;
+    fp.tile_order_blend = sched + 2 + tiles;
+    fp.n_order_blend = sched + 1;
+    fp.bwd_cost = bwd_cost;
     fp.tile_start = ranges;
     fp.tile_end = ranges + tiles;
     fp.vals = tape->vals.as<int>();
@@ -707,16 +734,21 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.topk = tape->topk.as<int>();
     fp.count = tape->count.as<int>();
     fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
+    fp.tape_t = tape->tape_t.as<double>();
     fp.nonfinite = dflags + 1;
     int rc = GVR_OK;
-    if (kp <= 8) rc = launch_forward<8, kFwdTile>(ctx, fp, tiles);
-    else if (kp <= 16) rc = launch_forward<16, kFwdTile>(ctx, fp, tiles);
-    else if (kp <= 20) rc = launch_forward<20, kFwdTile>(ctx, fp, tiles);
-    else if (kp <= 24) rc = launch_forward<24, kFwdTile>(ctx, fp, tiles);
-    else if (kp <= 32) rc = launch_forward<32, kFwdTile>(ctx, fp, tiles);
-    else if (kp <= 48) rc = launch_forward<48, kFwdTile>(ctx, fp, tiles);
-    else rc = launch_forward<64, kFwdTile>(ctx, fp, tiles);
+    int* order_b = sched + 2 + tiles;
+    if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 16) rc = launch_forward<16>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 20) rc = launch_forward<20>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 24) rc = launch_forward<24>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 32) rc = launch_forward<32>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 48) rc = launch_forward<48>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else rc = launch_forward<64>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     if (rc) return rc;
+    clear_empty_tiles_kernel<<<tiles, 64, 0, ctx->stream>>>(cp, Dc, tiles_x, bwd_cost, fp.image, fp.alpha, fp.depth,
+                                                            fp.count);
+    LAUNCH_CHECK(ctx);
     tape->valid = true;
 
     if (out) {
@@ -886,10 +918,16 @@ int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const dou
         bp.tau = scene->tau;
         bp.through_t = through_t;
         bp.through_rho = through_rho;
-        const int btx = (t->W + kBwdTile - 1) / kBwdTile, bty = (t->H + kBwdTile - 1) / kBwdTile;
+        const int btx = t->tiles_x, bty = t->tiles_y;
+        const int tiles = btx * bty;
+        int* sched = t->sched.as<int>();
+        int* order_b = sched + 2 + tiles;  // tiles by sum_p n_p^2, from the forward
         bp.tiles_x = btx;
+        bp.tile_order = order_b;
+        bp.n_order = sched + 1;
         bp.topk = t->topk.as<int>();
         bp.count = t->count.as<int>();
+        bp.tape_t = t->tape_t.as<double>();
         bp.rec64 = t->rec64.as<Rec64>();
         bp.attr = scene->attr.as<double>();
         bp.d_image = di;

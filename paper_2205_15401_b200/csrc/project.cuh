@@ -116,6 +116,19 @@ __device__ __forceinline__ uint32_t float_order_bits(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Tile rectangle of the pixel centres inside a kernel's screen box.
+__device__ __forceinline__ bool box_tiles(const Rec32& q, int H, int W, int tile, int& tr0, int& tr1, int& tc0,
+                                          int& tc1) {
+    const float r0 = fmaxf(0.0f, ceilf(q.top)), r1 = fminf((float)(H - 1), floorf(q.bottom));
+    const float c0 = fmaxf(0.0f, ceilf(q.left)), c1 = fminf((float)(W - 1), floorf(q.right));
+    if (!(r0 <= r1 && c0 <= c1)) return false;
+    tr0 = (int)r0 / tile;
+    tr1 = (int)r1 / tile;
+    tc0 = (int)c0 / tile;
+    tc1 = (int)c1 / tile;
+    return true;
+}
+
 struct ProjectParams {
     int K;
     const double* centers;  // object space [K*3]
@@ -169,10 +182,8 @@ __global__ void project_kernel(ProjectParams p) {
     q.s11 = (float)r.s[4];
     q.s12 = (float)r.s[5];
     q.s22 = (float)r.s[8];
-    q.cr_lo = 1;
-    q.cr_hi = 0;  // empty box
-    q.cc_lo = 1;
-    q.cc_hi = 0;
+    q.top = q.left = 1.0f;
+    q.bottom = q.right = 0.0f;  // empty box
     q.zmin = -FLT_MAX;
     uint32_t count = 0;
 
@@ -217,69 +228,76 @@ __global__ void project_kernel(ProjectParams p) {
         q.cj_frac = (float)(cj - fj);
     }
 
-    if (!p.sel.coarse) {
-        // no coarse stage: every front kernel is a candidate of every pixel (blender.cpp:84-88)
-        count = 1;
-    } else {
-        // jac = [[f/z, 0, -f x/z^2], [0, f/z, -f y/z^2]]; cov2 = jac cov jac^T (tracer.cpp:61-66)
-        const double zz = xmul(z, z);
-        const double jac[6] = {xdiv(f, z), 0.0, xdiv(xmul(-f, r.m[0]), zz), 0.0, xdiv(f, z), xdiv(xmul(-f, r.m[1]), zz)};
-        double jc[6];
+    // Screen box of the eta-level set exactly as coarse_select computes it
+    // (tracer.cpp:61-98): the linearised ellipse box widened by the projected
+    // corners of the camera-space AABB, full screen when that AABB reaches the
+    // near plane. jac = [[f/z, 0, -f x/z^2], [0, f/z, -f y/z^2]], cov2 = jac cov jac^T.
+    const double zz = xmul(z, z);
+    const double jac[6] = {xdiv(f, z), 0.0, xdiv(xmul(-f, r.m[0]), zz), 0.0, xdiv(f, z), xdiv(xmul(-f, r.m[1]), zz)};
+    double jc[6];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                double acc = xadd(0.0, xmul(jac[3 * i], cov[j]));
-                acc = xadd(acc, xmul(jac[3 * i + 1], cov[3 + j]));
-                jc[3 * i + j] = xadd(acc, xmul(jac[3 * i + 2], cov[6 + j]));
-            }
-        double cov2[4];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                double acc = xadd(0.0, xmul(jc[3 * i], jac[3 * j]));
-                acc = xadd(acc, xmul(jc[3 * i + 1], jac[3 * j + 1]));
-                cov2[2 * i + j] = xadd(acc, xmul(jc[3 * i + 2], jac[3 * j + 2]));
-            }
-        const double rh = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[0])));
-        const double rw = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[3])));
-        double top = xsub(ci, rh), bottom = xadd(ci, rh), left = xsub(cj, rw), right = xadd(cj, rw);
-        if (straddles) {
-            top = 0;
-            bottom = c.H - 1;
-            left = 0;
-            right = c.W - 1;
-        } else {
-#pragma unroll
-            for (int corner = 0; corner < 8; ++corner) {
-                const double px = xadd(r.m[0], (corner & 1) ? ext[0] : -ext[0]);
-                const double py = xadd(r.m[1], (corner & 2) ? ext[1] : -ext[1]);
-                const double pz = xadd(r.m[2], (corner & 4) ? ext[2] : -ext[2]);
-                const double pi = xadd(c.oy, xdiv(xmul(f, px), pz));
-                const double pj = xadd(c.ox, xdiv(xmul(f, py), pz));
-                top = pi < top ? pi : top;
-                bottom = pi > bottom ? pi : bottom;
-                left = pj < left ? pj : left;
-                right = pj > right ? pj : right;
-            }
+        for (int j = 0; j < 3; ++j) {
+            double acc = xadd(0.0, xmul(jac[3 * i], cov[j]));
+            acc = xadd(acc, xmul(jac[3 * i + 1], cov[3 + j]));
+            jc[3 * i + j] = xadd(acc, xmul(jac[3 * i + 2], cov[6 + j]));
         }
-        // (tracer.cpp:100-103), with the reference's static_cast<int> semantics
+    double cov2[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            double acc = xadd(0.0, xmul(jc[3 * i], jac[3 * j]));
+            acc = xadd(acc, xmul(jc[3 * i + 1], jac[3 * j + 1]));
+            cov2[2 * i + j] = xadd(acc, xmul(jc[3 * i + 2], jac[3 * j + 2]));
+        }
+    const double rh = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[0])));
+    const double rw = __dsqrt_rn(fmax(0.0, xmul(chi, cov2[3])));
+    double top = xsub(ci, rh), bottom = xadd(ci, rh), left = xsub(cj, rw), right = xadd(cj, rw);
+    if (straddles) {
+        top = 0;
+        bottom = c.H - 1;
+        left = 0;
+        right = c.W - 1;
+    } else {
+#pragma unroll
+        for (int corner = 0; corner < 8; ++corner) {
+            const double px = xadd(r.m[0], (corner & 1) ? ext[0] : -ext[0]);
+            const double py = xadd(r.m[1], (corner & 2) ? ext[1] : -ext[1]);
+            const double pz = xadd(r.m[2], (corner & 4) ? ext[2] : -ext[2]);
+            const double pi = xadd(c.oy, xdiv(xmul(f, px), pz));
+            const double pj = xadd(c.ox, xdiv(xmul(f, py), pz));
+            top = pi < top ? pi : top;
+            bottom = pi > bottom ? pi : bottom;
+            left = pj < left ? pj : left;
+            right = pj > right ? pj : right;
+        }
+    }
+    bool candidate = true;
+    if (p.sel.coarse) {
+        // pushed into the coarse map at all? (tracer.cpp:100-104, reference int semantics)
         const int lo_r = max(0, x86_int(floor(xsub(top, 1.0))));
         const int hi_r = min(c.H - 1, x86_int(ceil(xadd(bottom, 1.0))));
         const int lo_c = max(0, x86_int(floor(xsub(left, 1.0))));
         const int hi_c = min(c.W - 1, x86_int(ceil(xadd(right, 1.0))));
-        if (lo_r <= hi_r && lo_c <= hi_c) {
-            const int ds = p.sel.ds;
-            q.cr_lo = lo_r / ds;
-            q.cr_hi = hi_r / ds;
-            q.cc_lo = lo_c / ds;
-            q.cc_hi = hi_c / ds;
-            // pixel extent of the pushed cells -> tile rectangle
-            const int r0 = q.cr_lo * ds, r1 = min(c.H, (q.cr_hi + 1) * ds) - 1;
-            const int c0 = q.cc_lo * ds, c1 = min(c.W, (q.cc_hi + 1) * ds) - 1;
-            count = (uint32_t)((r1 / p.tile - r0 / p.tile + 1) * (c1 / p.tile - c0 / p.tile + 1));
-        }
+        candidate = lo_r <= hi_r && lo_c <= hi_c;
+    }
+    // Every pushed kernel is in the candidate list of every pixel of its padded
+    // box; among those it can only pass the eta test where the pixel centre lies
+    // in the unpadded box (the ray must cross the eta-ellipsoid, whose
+    // projection the box contains). So binning and testing by the unpadded box
+    // reproduces the reference's selection exactly, with far fewer traces.
+    if (candidate) {
+        const double mt = 1e-6 * (1.0 + fabs(top)), mb = 1e-6 * (1.0 + fabs(bottom));
+        const double ml = 1e-6 * (1.0 + fabs(left)), mr = 1e-6 * (1.0 + fabs(right));
+        q.top = __double2float_rd(fmax(top - mt, -1.0e30));
+        q.bottom = __double2float_ru(fmin(bottom + mb, 1.0e30));
+        q.left = __double2float_rd(fmax(left - ml, -1.0e30));
+        q.right = __double2float_ru(fmin(right + mr, 1.0e30));
+        int tr0, tr1, tc0, tc1;
+        if (box_tiles(q, c.H, c.W, p.tile, tr0, tr1, tc0, tc1))
+            count = (uint32_t)((tr1 - tr0 + 1) * (tc1 - tc0 + 1));
     }
     p.rec32[k] = q;
     p.counts[k] = count;
@@ -304,15 +322,8 @@ __global__ void emit_pairs_kernel(EmitParams p) {
     if (n == 0) return;
     const Rec32 q = p.rec32[k];
     const unsigned long long zbits = float_order_bits(q.zmin);
-    if (!p.sel.coarse) {
-        p.keys[off] = zbits;
-        p.vals[off] = k;
-        return;
-    }
-    const int ds = p.sel.ds;
-    const int r0 = q.cr_lo * ds, r1 = min(p.H, (q.cr_hi + 1) * ds) - 1;
-    const int c0 = q.cc_lo * ds, c1 = min(p.W, (q.cc_hi + 1) * ds) - 1;
-    const int tr0 = r0 / p.tile, tr1 = r1 / p.tile, tc0 = c0 / p.tile, tc1 = c1 / p.tile;
+    int tr0, tr1, tc0, tc1;
+    box_tiles(q, p.H, p.W, p.tile, tr0, tr1, tc0, tc1);
     uint32_t o = off;
     for (int tr = tr0; tr <= tr1; ++tr)
         for (int tc = tc0; tc <= tc1; ++tc) {

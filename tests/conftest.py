@@ -11,6 +11,20 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# (check, max err/tol) of every tolerance check; printed at session end so a
+# GPU run shows how much margin each parity class has.
+MARGINS = []
+
+
+def pytest_terminal_summary(terminalreporter):
+    if not MARGINS:
+        return
+    worst = {}
+    for what, m in MARGINS:
+        worst[what] = max(worst.get(what, 0.0), m)
+    terminalreporter.write_line("parity margins (max err / tolerance, < 1 passes): " +
+                                ", ".join(f"{k} {v:.3g}" for k, v in sorted(worst.items())))
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built libgvr_cuda.so")
@@ -78,6 +92,7 @@ def assert_close_rel(actual, ref, rel=1e-4, abs_floor=1e-7, what=""):
     ref = np.asarray(ref)
     err = np.abs(actual - ref)
     bad = err > rel * np.abs(ref) + abs_floor
+    MARGINS.append((what, float((err / (rel * np.abs(ref) + abs_floor)).max()) if err.size else 0.0))
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} entries out of tolerance; worst |err| "
                            f"{err.max():.3e} at ref {ref.reshape(-1)[np.argmax(err)]:.6e}")
 
@@ -92,5 +107,6 @@ def assert_grad_close(actual, ref, rel=1e-4, floor=1e-3, what=""):
     bad = err > tol
     if scale == 0.0:
         bad = err > 0.0
+    MARGINS.append((what, float((err / np.maximum(tol, 1e-300)).max()) if err.size else 0.0))
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} out of tolerance; worst rel to scale "
                            f"{(err / max(scale, 1e-300)).max():.3e} (class scale {scale:.3e})")

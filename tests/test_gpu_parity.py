@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import paper_2205_15401_b200 as gvr
-from conftest import assert_close_rel, assert_grad_close
+from conftest import assert_close_rel, assert_grad_close  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
