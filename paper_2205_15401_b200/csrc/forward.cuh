@@ -10,8 +10,9 @@ struct FwdParams {
     SelP sel;
     int D, Dc;
     double tau;
-    float guard_abs;     // FP32 pre-filter guard band on q (absolute)
-    float prefilter_c1;  // 1 - relative slack
+    float guard_abs;     // FP32 guard band on q (absolute)
+    float prefilter_c1;  // 1 - relative slack on delta.S.delta
+    int exact_only;      // test hook: every candidate through the exact FP64 trace
     int tiles_x;
     const int* tile_order;  // tiles by list length, longest first (LPT); first *n_order valid
     const int* n_order;
@@ -35,16 +36,23 @@ struct FwdParams {
     int* nonfinite; // flag
 };
 
-// FP32 centre-relative pre-filter (conservative): true unless q is certainly
-// <= ln(eta). With dt = ((i-Oy)/F, (j-Ox)/F, 1), delta = m - z dt =
-// (z/F)(c_i - i, c_j - j, 0) is formed without cancellation from the integer
-// and fractional parts of the projected centre, and
-//   q = -(delta.S.delta - (dt.S.delta)^2 / dt.S.dt) / 2
-// (the line minimum is parametrisation independent). Division-free test:
-//   dSd*A - B^2 < 2 (g - ln eta) A  (+ relative slack), A = dt.S.dt > 0.
-__device__ __forceinline__ bool prefilter_pass(const Rec32& r, int i, int j, float u, float v, float c2,
-                                               float c1) {
-    if (r.zf < 0.0f) return true;  // unusual geometry: exact path only
+// FP32 centre-relative classification of q against ln(eta).
+// With dt = ((i-Oy)/F, (j-Ox)/F, 1), delta = m - z dt = (z/F)(c_i - i, c_j - j, 0)
+// is formed without cancellation from the integer and fractional parts of the
+// projected centre, and (the line minimum is parametrisation independent)
+//   q = -T / (2A),  T = delta.S.delta * A - (dt.S.delta)^2 >= 0,  A = dt.S.dt > 0.
+// Division-free, with a guard band g on q and a relative slack on the
+// delta.S.delta * A term (FP32 cancellation):
+//   returns 0: q <= ln(eta) for certain      (reject)
+//           2: q >  ln(eta) for certain      (eligible)
+//           1: inside the band               (decide with the exact FP64 trace)
+struct QClass {
+    float c_rej, c_acc;   // 2(-ln eta + g), 2(-ln eta - g)
+    float slack_lo, slack_hi;  // 1 -/+ relative slack
+};
+
+__device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u, float v, const QClass& qc) {
+    if (r.zf < 0.0f) return 1;  // unusual geometry: exact path only
     const float di = (float)(r.ci_int - i) + r.ci_frac;
     const float dj = (float)(r.cj_int - j) + r.cj_frac;
     const float dx = r.zf * di, dy = r.zf * dj;
@@ -54,7 +62,10 @@ __device__ __forceinline__ bool prefilter_pass(const Rec32& r, int i, int j, flo
     const float A = fmaf(u, sd0, fmaf(v, sd1, sd2));
     const float B = fmaf(dx, sd0, dy * sd1);
     const float dsd = fmaf(dx, fmaf(r.s00, dx, 2.0f * r.s01 * dy), r.s11 * dy * dy);
-    return fmaf(dsd * c1, A, -B * B) < c2 * A;
+    const float bb = B * B;
+    if (fmaf(dsd * qc.slack_lo, A, -bb) > qc.c_rej * A) return 0;
+    if (fmaf(dsd * qc.slack_hi, A, -bb) < qc.c_acc * A) return 2;
+    return 1;
 }
 
 // Per-warp candidate chunk entry.
@@ -64,16 +75,60 @@ struct __align__(16) Cand {
     int pad[3];
 };
 
-// Worst (largest (l, idx)) of the n kept entries of this thread.
-__device__ __forceinline__ void find_worst(const double* s_l, const int* s_id, int n, int tid, double& wl, int& wid,
-                                           int& wslot) {
+// Fast FP64 peak distance l = d.(S m) / d.S.d (the reference's b/a with S
+// symmetric), contracted FMAs: within a few ulps (~1e-15 relative) of the
+// reference-order l of trace_exact. dd = (d0^2, d1^2, d2^2, 2 d0 d1, 2 d0 d2, 2 d1 d2).
+__device__ __forceinline__ double fast_l(const Rec64& r, const double* d, const double* dd) {
+    const double a = fma(r.s[0], dd[0], fma(r.s[4], dd[1], fma(r.s[8], dd[2],
+                         fma(r.s[1], dd[3], fma(r.s[2], dd[4], r.s[5] * dd[5])))));
+    const double b = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2]));
+    return b / a;
+}
+
+// Selection keys: (l, id) where l is either the fast l (error < 1e-11 |l|, a
+// 10^4 safety factor over the few-ulp actual error) or the exact reference l
+// (id carries kExact). Two keys closer than the error bound are upgraded to
+// exact before comparing, so every decision equals the reference's (l, idx) order.
+constexpr int kExact = 0x40000000;
+
+__device__ __forceinline__ bool keys_close(double a, double b) { return fabs(a - b) <= 1e-11 * fabs(a) + 1e-300; }
+
+__device__ __forceinline__ void make_exact(double& l, int& id, const double* d, const Rec64* rec64) {
+    if (!(id & kExact)) {
+        l = trace_exact(d, rec64[id]).l;
+        id |= kExact;
+    }
+}
+
+// (la, ia) < (lb, ib) in the reference order; may upgrade either key to exact.
+__device__ __forceinline__ bool key_less(double& la, int& ia, double& lb, int& ib, const double* d,
+                                         const Rec64* rec64) {
+    if (!keys_close(la, lb)) return la < lb;
+    make_exact(la, ia, d, rec64);
+    make_exact(lb, ib, d, rec64);
+    return la < lb || (la == lb && (ia & ~kExact) < (ib & ~kExact));
+}
+
+// Worst (largest key) of the n kept entries of this thread; upgrades near ties in place.
+__device__ __forceinline__ void find_worst(double* s_l, int* s_id, int n, int tid, const double* d,
+                                           const Rec64* rec64, double& wl, int& wid, int& wslot) {
     wl = s_l[tid];
     wid = s_id[tid];
     wslot = 0;
     for (int s = 1; s < n; ++s) {
-        const double ls = s_l[s * 64 + tid];
-        const int is = s_id[s * 64 + tid];
-        if (traced_less(wl, wid, ls, is)) {
+        double ls = s_l[s * 64 + tid];
+        int is = s_id[s * 64 + tid];
+        const int was_w = wid, was_s = is;
+        const bool less = key_less(wl, wid, ls, is, d, rec64);
+        if (wid != was_w) {  // upgraded: write back
+            s_l[wslot * 64 + tid] = wl;
+            s_id[wslot * 64 + tid] = wid;
+        }
+        if (is != was_s) {
+            s_l[s * 64 + tid] = ls;
+            s_id[s * 64 + tid] = is;
+        }
+        if (less) {
             wl = ls;
             wid = is;
             wslot = s;
@@ -83,13 +138,11 @@ __device__ __forceinline__ void find_worst(const double* s_l, const int* s_id, i
 
 // K3a selection. CTA = one 8x8 pixel tile = 2 warps that stream the tile's
 // list independently (no CTA barriers; a warp stops as soon as its 32 pixels
-// are done). Per pixel, the K' nearest (l, idx) are kept UNSORTED in shared
-// memory with the current worst tracked in registers; candidates arrive roughly
-// in ascending l (lists are sorted by the depth bound), so replacements after
-// the list fills are rare. The FP32 pre-filter of 4 consecutive candidates is
-// evaluated together (independent work: instruction-level parallelism for the
-// latency-bound pixels that scan whole lists). Output: the selection sorted by
-// (l, idx) into the tape, and the tile's backward/blend cost sum n_p^2.
+// are done). Per candidate: exact box test (pixel centre inside the eta box),
+// FP32 classification of q (exact FP64 trace only inside the guard band), then
+// the K' nearest by key (fast l, exact on near ties) are kept UNSORTED in shared
+// memory with the current worst tracked in registers. The blend kernel sorts
+// the set by exact (l, idx).
 template <int KMAX>
 __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     constexpr int TILE = 8, NT = 64;
@@ -111,14 +164,22 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
 
     double d[3];
     pixel_ray(p.cam, inside ? i : 0, inside ? j : 0, d);
+    const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
+                          2.0 * d[1] * d[2]};
     const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
     const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
     const float fi = (float)i, fj = (float)j;
-    const float c2 = 2.0f * (p.guard_abs - (float)p.sel.log_eta);
-    const float c1 = p.prefilter_c1;
+    const float neg_log_eta = -(float)p.sel.log_eta;
+    QClass qc;
+    qc.c_rej = 2.0f * (neg_log_eta + p.guard_abs);
+    qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
+    qc.slack_lo = p.prefilter_c1;
+    qc.slack_hi = 2.0f - p.prefilter_c1;
+    const bool exact_only = p.exact_only != 0;
     const double log_eta = p.sel.log_eta;
+    const Rec64* rec64 = p.rec64;
 
-    // selection state: n kept; once full, the worst kept (l, idx) and its slot
+    // selection state: n kept; once full, the worst kept key and its slot
     int n = 0, wslot = 0, wid = 0x7fffffff;
     double wl = INFINITY;
     bool done = !inside;
@@ -134,32 +195,46 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         __syncwarp();
         const int cnt = min(32, end - base);
         for (int c0 = 0; c0 < cnt && !done; c0 += 4) {
-            // early exit: every later candidate has l >= zmin > worst kept
-            if ((double)chunk[c0].r.zmin > wl) {
+            // early exit: every later candidate has l >= zmin > worst kept (+ key error)
+            if ((double)chunk[c0].r.zmin > wl + 1e-11 * fabs(wl)) {
                 done = true;
                 break;
             }
-            bool pass[4];
+            int cls[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const Rec32& r = chunk[min(c0 + q, cnt - 1)].r;
-                pass[q] = c0 + q < cnt && fi >= r.top && fi <= r.bottom && fj >= r.left && fj <= r.right &&
-                          prefilter_pass(r, i, j, u, v, c2, c1);
+                const bool in_box = c0 + q < cnt && fi >= r.top && fi <= r.bottom && fj >= r.left && fj <= r.right;
+                cls[q] = in_box ? classify_q(r, i, j, u, v, qc) : 0;
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (!pass[q]) continue;
-                const int k = chunk[c0 + q].k;
-                const Traced64 t = trace_exact(d, p.rec64[k]);
-                if (!(t.q > log_eta)) continue;  // fine_select threshold (tracer.cpp:117-118)
+                if (cls[q] == 0) continue;
+                int k = chunk[c0 + q].k;
+                double lk;
+                if (exact_only || cls[q] == 1) {
+                    const Traced64 t = trace_exact(d, rec64[k]);
+                    if (!(t.q > log_eta)) continue;  // fine_select threshold (tracer.cpp:117-118)
+                    lk = t.l;
+                    k |= kExact;
+                } else {
+                    lk = fast_l(rec64[k], d, dd);
+                }
                 if (n < kp) {
-                    s_l[n * NT + tid] = t.l;
+                    s_l[n * NT + tid] = lk;
                     s_id[n * NT + tid] = k;
-                    if (++n == kp) find_worst(s_l, s_id, n, tid, wl, wid, wslot);
-                } else if (traced_less(t.l, k, wl, wid)) {
-                    s_l[wslot * NT + tid] = t.l;
-                    s_id[wslot * NT + tid] = k;
-                    find_worst(s_l, s_id, n, tid, wl, wid, wslot);
+                    if (++n == kp) find_worst(s_l, s_id, n, tid, d, rec64, wl, wid, wslot);
+                } else {
+                    const int was_w = wid;
+                    const bool better = key_less(lk, k, wl, wid, d, rec64);
+                    if (better) {
+                        s_l[wslot * NT + tid] = lk;
+                        s_id[wslot * NT + tid] = k;
+                        find_worst(s_l, s_id, n, tid, d, rec64, wl, wid, wslot);
+                    } else if (wid != was_w) {  // the worst was upgraded to exact
+                        s_l[wslot * NT + tid] = wl;
+                        s_id[wslot * NT + tid] = wid;
+                    }
                 }
             }
         }
@@ -173,22 +248,123 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
     if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
     if (!inside) return;
-
-    // sort the selection ascending by (l, idx): insertion sort of nearly sorted input
-    for (int s = 1; s < n; ++s) {
-        const double ls = s_l[s * NT + tid];
-        const int is = s_id[s * NT + tid];
-        int t = s - 1;
-        while (t >= 0 && traced_less(ls, is, s_l[t * NT + tid], s_id[t * NT + tid])) {
-            s_l[(t + 1) * NT + tid] = s_l[t * NT + tid];
-            s_id[(t + 1) * NT + tid] = s_id[t * NT + tid];
-            --t;
-        }
-        s_l[(t + 1) * NT + tid] = ls;
-        s_id[(t + 1) * NT + tid] = is;
-    }
-    for (int s = 0; s < n; ++s) p.topk[pix * kp + s] = s_id[s * NT + tid];
+    for (int s = 0; s < n; ++s) p.topk[pix * kp + s] = s_id[s * NT + tid] & ~kExact;  // unsorted; the blend sorts
     p.count[pix] = n;
+}
+
+// K3a selection, warp-per-pixel form (K' <= 32). CTA = one 8x8 tile, 8 warps;
+// warp w handles pixels w, w+8, ... of the tile. Lanes stride the tile's list
+// 32 candidates at a time (box test + FP32 q classification fully
+// lane-parallel, fast l for the eligible lanes), and the K' nearest keys live
+// warp-distributed and sorted: lane s holds the s-th nearest. Eligible
+// candidates are inserted by ballot (position) + shuffle (shift). Near ties are
+// resolved with exact keys exactly as in the thread-per-pixel kernel.
+template <int KMAX>
+__global__ void __launch_bounds__(256) select_warp_kernel(FwdParams p) {
+    constexpr int TILE = 8;
+    if ((int)blockIdx.x >= *p.n_order) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = p.tile_order[blockIdx.x];
+    const int start = p.tile_start[tile];
+    const int end = p.tile_end[tile];
+    const int kp = p.sel.kp;
+    const Rec64* rec64 = p.rec64;
+    const double log_eta = p.sel.log_eta;
+    const float neg_log_eta = -(float)p.sel.log_eta;
+    QClass qc;
+    qc.c_rej = 2.0f * (neg_log_eta + p.guard_abs);
+    qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
+    qc.slack_lo = p.prefilter_c1;
+    qc.slack_hi = 2.0f - p.prefilter_c1;
+    const bool exact_only = p.exact_only != 0;
+    float cost = 0.0f;
+
+    for (int px = warp; px < TILE * TILE; px += 8) {
+        const int i = (tile / p.tiles_x) * TILE + px / TILE;
+        const int j = (tile % p.tiles_x) * TILE + px % TILE;
+        if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
+        const long long pix = (long long)i * p.cam.W + j;
+        double d[3];
+        pixel_ray(p.cam, i, j, d);
+        const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
+                              2.0 * d[1] * d[2]};
+        const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
+        const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
+        const float fi = (float)i, fj = (float)j;
+
+        // warp-distributed sorted list: lane s < n holds the s-th nearest key
+        double L = INFINITY;
+        int I = 0x3fffffff;
+        int n = 0;
+        double worst = INFINITY;  // key of lane kp-1 once full (uniform)
+
+        for (int base = start; base < end; base += 32) {
+            const int e = base + lane;
+            const bool valid = e < end;
+            int k = valid ? p.vals[e] : 0;
+            const Rec32 r = p.rec32[k];
+            // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
+            const float zmin0 = __shfl_sync(0xffffffffu, r.zmin, 0);
+            if ((double)zmin0 > worst + 1e-11 * fabs(worst)) break;
+            const bool in_box = valid && fi >= r.top && fi <= r.bottom && fj >= r.left && fj <= r.right;
+            int cls = 0;
+            if (in_box) cls = classify_q(r, i, j, u, v, qc);
+            double lk = INFINITY;
+            if (cls != 0) {
+                if (exact_only || cls == 1) {
+                    const Traced64 t = trace_exact(d, rec64[k]);
+                    if (t.q > log_eta) {  // fine_select threshold (tracer.cpp:117-118)
+                        lk = t.l;
+                        k |= kExact;
+                    } else {
+                        cls = 0;
+                    }
+                } else {
+                    lk = fast_l(rec64[k], d, dd);
+                }
+                // cannot enter a full list
+                if (cls != 0 && lk > worst + 1e-11 * fabs(worst)) cls = 0;
+            }
+            unsigned pend = __ballot_sync(0xffffffffu, cls != 0);
+            while (pend) {
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1;
+                double cl = __shfl_sync(0xffffffffu, lk, src);
+                int ci = __shfl_sync(0xffffffffu, k, src);
+                // position = number of kept keys smaller than the candidate
+                bool close = lane < n && keys_close(L, cl);
+                if (__any_sync(0xffffffffu, close)) {
+                    if (!(ci & kExact)) {  // warp-uniform exact key of the candidate
+                        cl = trace_exact(d, rec64[ci]).l;
+                        ci |= kExact;
+                    }
+                    if (close) make_exact(L, I, d, rec64);
+                }
+                const bool lt = lane < n && (L < cl || (L == cl && (I & ~kExact) < (ci & ~kExact)));
+                const int pos = __popc(__ballot_sync(0xffffffffu, lt));
+                if (pos >= kp) continue;  // not among the K' nearest
+                const double up_l = __shfl_up_sync(0xffffffffu, L, 1);
+                const int up_i = __shfl_up_sync(0xffffffffu, I, 1);
+                if (lane == pos) {
+                    L = cl;
+                    I = ci;
+                } else if (lane > pos) {
+                    L = up_l;
+                    I = up_i;
+                }
+                if (lane >= kp) {
+                    L = INFINITY;
+                    I = 0x3fffffff;
+                }
+                n = min(n + 1, kp);
+                if (n == kp) worst = __shfl_sync(0xffffffffu, L, kp - 1);
+            }
+        }
+        if (lane < n) p.topk[pix * kp + lane] = I & ~kExact;  // sorted by key; the blend sorts exactly
+        if (lane == 0) p.count[pix] = n;
+        cost += (float)(n * n);
+    }
+    if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
 }
 
 // K3b closed-form blend (blender.cpp:27-53, 98-128). CTA = one 8x8 tile with
@@ -229,20 +405,47 @@ __global__ void __launch_bounds__(256) blend_kernel(FwdParams p) {
 
     double d[3];
     pixel_ray(p.cam, i, j, d);
-    const double l0 = trace_exact(d, p.rec64[p.topk[pix * kp]]).l;
     double peak_part = 0.0;
     for (int s = sub; s < n; s += 4) {
         const int k = p.topk[pix * kp + s];
         const Traced64 t = trace_exact(d, p.rec64[k]);
         const double pk = exp(t.q);
         peak_part += pk;
-        b_dl[s * NP + g] = t.l - l0;
+        b_dl[s * NP + g] = t.l;  // exact l for now; relative to the nearest after the sort
         b_pk[s * NP + g] = (float)pk;
         b_is[s * NP + g] = (float)__dsqrt_rn(t.a);  // 1/sigma
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
     peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
+    __syncwarp(grp);
+    if (sub == 0) {
+        // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort
+        for (int s = 1; s < n; ++s) {
+            const double ls = b_dl[s * NP + g];
+            const int is = b_id[s * NP + g];
+            const float ps = b_pk[s * NP + g], ss = b_is[s * NP + g];
+            int t = s - 1;
+            while (t >= 0 && traced_less(ls, is, b_dl[t * NP + g], b_id[t * NP + g])) {
+                b_dl[(t + 1) * NP + g] = b_dl[t * NP + g];
+                b_id[(t + 1) * NP + g] = b_id[t * NP + g];
+                b_pk[(t + 1) * NP + g] = b_pk[t * NP + g];
+                b_is[(t + 1) * NP + g] = b_is[t * NP + g];
+                --t;
+            }
+            b_dl[(t + 1) * NP + g] = ls;
+            b_id[(t + 1) * NP + g] = is;
+            b_pk[(t + 1) * NP + g] = ps;
+            b_is[(t + 1) * NP + g] = ss;
+        }
+    }
+    __syncwarp(grp);
+    const double l0 = b_dl[g];
+    __syncwarp(grp);
+    for (int s = sub; s < n; s += 4) {
+        b_dl[s * NP + g] -= l0;
+        p.topk[pix * kp + s] = b_id[s * NP + g];
+    }
     __syncwarp(grp);
 
     for (int k = sub; k < n; k += 4) {

@@ -261,7 +261,10 @@ int ceil_log2(uint32_t v) {
 
 template <int KMAX>
 int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
-    {
+    if (KMAX <= 32) {
+        StageTimer st(ctx, ST_SELECT);
+        select_warp_kernel<KMAX><<<tiles, 256, 0, ctx->stream>>>(fp);
+    } else {
         constexpr int NT = 64;
         const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT;
         auto kern = select_kernel<KMAX>;
@@ -715,7 +718,8 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.Dc = Dc;
     fp.tau = scene->tau;
     fp.guard_abs = (float)ctx->guard;
-    fp.prefilter_c1 = ctx->guard > 1e3 ? 0.0f : 1.0f - 1e-4f;
+    fp.prefilter_c1 = 1.0f - 1e-4f;
+    fp.exact_only = ctx->guard > 1e3 ? 1 : 0;
     fp.tiles_x = tiles_x;
     fp.tile_order = order_f;
     fp.n_order = sched;
