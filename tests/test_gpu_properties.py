@@ -1,0 +1,433 @@
+"""GPU: the reference's hot-path property tests, re-run through the CUDA path.
+
+Ports of /root/reference/proj/tests/test_{tracer,blender,grad,scene}.cpp (each
+test cites the case it follows), plus full-size (C2 / C3-view) parity against
+the C oracle port, which is bit-identical to the reference build.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2205_15401_b200 as gvr
+from conftest import assert_close_rel, assert_grad_close
+from paper_2205_15401_b200.types import Camera, GaussianScene, GradFlags, SelectionConfig, ValidationError
+
+pytestmark = pytest.mark.gpu
+
+
+def default_camera(size=32, focal=16.0):
+    """oracle::default_camera (tests/oracles.hpp:153-161)."""
+    return Camera(np.eye(3), np.zeros(3), focal, (size - 1) / 2.0, (size - 1) / 2.0, size, size)
+
+
+def random_scene(seed, count, attr_dim=3, lo=2.0, hi=30.0, tau=1.0):
+    """Analogue of oracle::random_scene (tests/oracles.hpp:137-151)."""
+    rng = np.random.default_rng(seed)
+    c = np.stack([rng.uniform(-1, 1, count), rng.uniform(-1, 1, count), rng.uniform(3, 6, count)], 1)
+    inv = []
+    for _ in range(count):
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        m = q @ np.diag(rng.uniform(lo, hi, 3)) @ q.T
+        inv.append(0.5 * (m + m.T))
+    return GaussianScene(c, np.array(inv), rng.uniform(0, 1, (count, attr_dim)), tau)
+
+
+def so3_exp(w):
+    w = np.asarray(w, dtype=np.float64)
+    th = np.linalg.norm(w)
+    k = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
+    if th < 1e-12:
+        return np.eye(3) + k + 0.5 * k @ k
+    return np.eye(3) + np.sin(th) / th * k + (1 - np.cos(th)) / th**2 * k @ k
+
+
+def one_kernel(center, sigma, attr=(0.0, 0.0, 0.0)):
+    return GaussianScene(np.array([center], dtype=np.float64), (np.eye(3) / sigma**2)[None], np.array([attr]), 1.0)
+
+
+# ----------------------------------------------------------------- tracer (test_tracer.cpp)
+
+def test_kernel_on_axis_peaks_at_its_depth(ctx):
+    """test_tracer.cpp:24-31: l = 5, q = 0, sigma = s for a kernel on the ray."""
+    s = 0.7
+    fr = gvr.render_with_tape(one_kernel((0, 0, 5), s), Camera(np.eye(3), np.zeros(3), 10.0, 0, 0, 1, 1), ctx=ctx)
+    idx, l, q, sg = fr.tape.traced()
+    assert idx[0, 0, 0] == 0
+    assert l[0, 0, 0] == pytest.approx(5.0, rel=1e-12)
+    assert q[0, 0, 0] == pytest.approx(0.0, abs=1e-12)
+    assert sg[0, 0, 0] == pytest.approx(s, rel=1e-12)
+
+
+def test_perpendicular_offset_only_lowers_the_peak(ctx):
+    """test_tracer.cpp:33-41: q = -v^2 / (2 s^2)."""
+    s, v = 0.5, 0.8
+    fr = gvr.render_with_tape(one_kernel((v, 0, 5), s), Camera(np.eye(3), np.zeros(3), 10.0, 0, 0, 1, 1),
+                              SelectionConfig(eta=1e-3), ctx=ctx)
+    _, l, q, sg = fr.tape.traced()
+    assert l[0, 0, 0] == pytest.approx(5.0, rel=1e-12)
+    assert q[0, 0, 0] == pytest.approx(-v * v / (2 * s * s), rel=1e-12)
+
+
+def test_depth_ties_broken_by_kernel_index(ctx):
+    """test_tracer.cpp:153-160: k_prime = 1 keeps the lower index on an exact tie."""
+    scene = GaussianScene(np.array([[0, 0, 5.0], [0, 0, 5.0]]), np.stack([np.eye(3) * 4] * 2), np.eye(2, 3), 1.0)
+    b = gvr.render(scene, Camera(np.eye(3), np.zeros(3), 10.0, 0, 0, 1, 1), SelectionConfig(k_prime=1), ctx=ctx)
+    assert b.topk_idx[0, 0, 0] == 0
+
+
+def test_coarse_selection_equals_exhaustive(ctx):
+    """test_tracer.cpp:203-250 (coarse never misses an above-eta kernel): the culled
+    and exhaustive selections are identical, not merely within 1e-2."""
+    scene = random_scene(46, 500, 3, 8.0, 120.0)
+    cam = default_camera(64, 48.0)
+    a = gvr.render(scene, cam, SelectionConfig(), ctx=ctx)
+    b = gvr.render(scene, cam, SelectionConfig(coarse_enabled=False), ctx=ctx)
+    assert np.array_equal(a.topk_idx, b.topk_idx)
+    assert np.array_equal(a.image, b.image)
+
+
+def test_behind_camera_kernels_are_dropped(ctx):
+    """test_tracer.cpp:189-201."""
+    scene = GaussianScene(np.array([[0, 0, -3.0], [0, 0, 5.0]]), np.stack([np.eye(3) * 25] * 2),
+                          np.ones((2, 3)), 1.0)
+    b = gvr.render(scene, default_camera(), ctx=ctx)
+    assert set(np.unique(b.topk_idx)) <= {-1, 1}
+
+
+# ----------------------------------------------------------------- blender (test_blender.cpp)
+
+def test_single_on_axis_kernel_weight(ctx):
+    """test_blender.cpp:52-58: W = e^{-1/2}, alpha = 1 - e^{-1} (full-strength kernel)."""
+    fr = gvr.render_with_tape(one_kernel((0, 0, 5), 0.05, (1, 1, 1)), Camera(np.eye(3), np.zeros(3), 10.0, 0, 0, 1, 1),
+                              ctx=ctx)
+    assert fr.buffers.topk_w[0, 0, 0] == pytest.approx(np.exp(-0.5), rel=1e-6)
+    assert fr.buffers.alpha[0, 0, 0] == pytest.approx(1 - np.exp(-1.0), rel=1e-12)
+
+
+def test_empty_scene_renders_zeros(ctx):
+    """test_blender.cpp:213-219."""
+    scene = GaussianScene(np.zeros((0, 3)), np.zeros((0, 3, 3)), np.zeros((0, 3)), 1.0)
+    b = gvr.render(scene, default_camera(), ctx=ctx)
+    assert not b.image.any() and not b.alpha.any() and not b.depth.any()
+    assert (b.topk_idx == -1).all()
+
+
+def test_centered_kernel_radially_symmetric(ctx):
+    """test_blender.cpp:221-245."""
+    scene = GaussianScene(np.array([[0, 0, 4.0]]), (np.eye(3) / 0.09)[None], np.array([[1.0, 0, 0]]), 1.0)
+    b = gvr.render(scene, default_camera(33, 40.0), ctx=ctx)
+    img = b.image[..., 0]
+    for jj in range(16, 24):
+        assert img[16, jj] > img[16, jj + 1]
+    for off in range(1, 9):
+        assert img[16, 16 + off] == pytest.approx(img[16, 16 - off], rel=1e-9)
+        assert img[16 + off, 16] == pytest.approx(img[16, 16 + off], rel=1e-9)
+    assert not b.image[..., 1:].any()
+
+
+def test_image_is_weight_store_blend_exactly(ctx):
+    """test_blender.cpp:247-261: image == sum_k W_k attr_k, bit for bit."""
+    scene = random_scene(55, 20)
+    b = gvr.render(scene, default_camera(), ctx=ctx)
+    h, w, kp = b.topk_idx.shape
+    for i in range(h):
+        for j in range(w):
+            acc = np.zeros(3)
+            for s in range(kp):
+                k = b.topk_idx[i, j, s]
+                if k < 0:
+                    break
+                acc = acc + b.topk_w[i, j, s] * scene.attr[k]
+            assert np.array_equal(b.image[i, j], acc)
+
+
+def test_attribute_blending_is_linear(ctx):
+    """test_blender.cpp:263-282."""
+    c1 = random_scene(56, 8)
+    rng = np.random.default_rng(560)
+    c2 = c1.copy()
+    c2.attr = rng.uniform(0, 1, c1.attr.shape)
+    mix = c1.copy()
+    mix.attr = 0.3 * c1.attr + 1.7 * c2.attr
+    cam = default_camera()
+    r1, r2, rm = (gvr.render(s, cam, ctx=ctx).image for s in (c1, c2, mix))
+    np.testing.assert_allclose(rm, 0.3 * r1 + 1.7 * r2, rtol=0, atol=1e-9)
+
+
+def test_occluders_only_reduce_weight(ctx):
+    """test_blender.cpp:188-202 (a front kernel never raises a rear kernel's weight)."""
+    cam = Camera(np.eye(3), np.zeros(3), 10.0, 0, 0, 1, 1)
+    rear = one_kernel((0, 0, 6), 0.3, (1, 0, 0))
+    alone = gvr.render(rear, cam, ctx=ctx).topk_w[0, 0, 0]
+    both = GaussianScene(np.array([[0, 0, 6.0], [0, 0, 4.0]]), np.stack([np.eye(3) / 0.09, np.eye(3) / 0.25]),
+                         np.eye(2, 3), 1.0)
+    b = gvr.render(both, cam, ctx=ctx)
+    w_rear = b.topk_w[0, 0, list(b.topk_idx[0, 0]).index(0)]
+    assert w_rear < alone
+
+
+# ----------------------------------------------------------------- grad (test_grad.cpp)
+
+def _loss_upstream(rng, fr):
+    ti = rng.uniform(0, 1, fr.buffers.image.shape)
+    ta = rng.uniform(0, 1, fr.buffers.alpha.shape)
+    return fr.buffers.image - ti, fr.buffers.alpha - ta
+
+
+def test_zero_upstream_gives_zero_bundle(ctx):
+    """test_grad.cpp:24-39."""
+    scene = random_scene(61, 4)
+    cam = default_camera()
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    g = gvr.backward(fr, np.zeros((32, 32, 3)), np.zeros((32, 32, 1)))
+    for a in (g.d_center, g.d_inv_cov, g.d_attr, g.d_rotation, g.d_translation):
+        assert not a.any()
+
+
+def test_backward_rejects_mismatched_shapes(ctx):
+    """test_grad.cpp:41-49: ValidationError with the reference message."""
+    fr = gvr.render_with_tape(random_scene(62, 2), default_camera(), ctx=ctx)
+    with pytest.raises(ValidationError, match="d_image shape does not match"):
+        gvr.backward(fr, np.zeros((33, 32, 3)), np.zeros((32, 32, 1)))
+
+
+def test_attribute_gradient_identity(ctx):
+    """test_grad.cpp:133-156: d_attr = sum_p W_p d_image_p."""
+    scene = random_scene(66, 6)
+    cam = default_camera()
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    di, _ = _loss_upstream(np.random.default_rng(0), fr)
+    g = gvr.backward(fr, di, np.zeros((32, 32, 1)))
+    want = np.zeros_like(scene.attr)
+    b = fr.buffers
+    for i in range(32):
+        for j in range(32):
+            for s in range(b.topk_idx.shape[2]):
+                k = b.topk_idx[i, j, s]
+                if k < 0:
+                    break
+                want[k] += b.topk_w[i, j, s] * di[i, j]
+    np.testing.assert_allclose(g.d_attr, want, rtol=1e-12, atol=1e-13)
+
+
+def test_blocking_both_paths(ctx):
+    """test_grad.cpp:158-181: geometry gradients vanish, attributes do not."""
+    scene = random_scene(67, 4)
+    fr = gvr.render_with_tape(scene, default_camera(), ctx=ctx)
+    di, da = _loss_upstream(np.random.default_rng(1), fr)
+    both = gvr.backward(fr, di, da, GradFlags(False, False))
+    full = gvr.backward(fr, di, da)
+    assert not both.d_center.any() and not both.d_inv_cov.any()
+    assert not both.d_rotation.any() and not both.d_translation.any()
+    np.testing.assert_allclose(both.d_attr, full.d_attr, rtol=1e-13, atol=1e-15)
+    assert np.abs(both.d_attr).sum() > 0
+
+
+def test_blocking_transmittance_cuts_occluder_gradient(ctx):
+    """test_grad.cpp:183-214."""
+    scene = GaussianScene(np.array([[0, 0, 3.0], [0, 0, 5.0]]), np.stack([np.eye(3) / 0.04] * 2),
+                          np.array([[1.0, 0.0], [0.0, 1.0]]), 1.0)
+    cam = default_camera(15, 16.0)
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    di = np.zeros((15, 15, 2))
+    di[..., 1] = 1.0
+    da = np.zeros((15, 15, 1))
+    full = gvr.backward(fr, di, da)
+    assert np.linalg.norm(full.d_center[0]) > 1e-9
+    blocked = gvr.backward(fr, di, da, GradFlags(through_transmittance=False))
+    assert not blocked.d_center[0].any()
+    assert np.linalg.norm(blocked.d_center[1]) > 1e-9
+
+
+def test_hand_derived_two_kernel_formula(ctx):
+    """test_grad.cpp:216-277: density path blocked, dL/dl by hand, 1e-9 in the reference
+    (here 1e-6: the closed-form pair terms use FP32 Phi/phi)."""
+    from math import erfc, exp, pi, sqrt
+
+    tau = 1.0
+    scene = GaussianScene(np.array([[0, 0, 3.0], [0, 0, 3.6]]), np.stack([np.eye(3) / 0.25] * 2),
+                          np.array([[1.0], [0.5]]), tau)
+    cam = Camera(np.eye(3), np.zeros(3), 10.0, 0.0, 0.0, 1, 1)
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    _, l, q, sg = fr.tape.traced()
+    l1, l2, q1, q2, s1, s2 = l[0, 0, 0], l[0, 0, 1], q[0, 0, 0], q[0, 0, 1], sg[0, 0, 0], sg[0, 0, 1]
+    g = gvr.backward(fr, np.ones((1, 1, 1)), np.zeros((1, 1, 1)), GradFlags(through_density=False))
+
+    def cdf(x):
+        return 0.5 * erfc(-x / sqrt(2))
+
+    def pdf(x, s):
+        return 1 / sqrt(2 * pi) / s * exp(-0.5 * x * x / (s * s))
+
+    g1, g2 = exp(q1), exp(q2)
+    w1 = exp(-tau * (g1 * cdf(0) + g2 * cdf((l1 - l2) / s2))) * g1
+    w2 = exp(-tau * (g1 * cdf((l2 - l1) / s1) + g2 * cdf(0))) * g2
+    dl1 = 1.0 * (-tau * w1 * g2 * pdf(l1 - l2, s2)) + 0.5 * (-tau * w2 * (-g1 * pdf(l2 - l1, s1)))
+    dl2 = 1.0 * (-tau * w1 * (-g2 * pdf(l1 - l2, s2))) + 0.5 * (-tau * w2 * g1 * pdf(l2 - l1, s1))
+    assert g.d_center[0, 2] == pytest.approx(dl1, rel=1e-6)
+    assert g.d_center[1, 2] == pytest.approx(dl2, rel=1e-6)
+
+
+def test_inv_cov_gradients_exactly_symmetric(ctx):
+    """test_grad.cpp:298-311."""
+    scene = random_scene(69, 5)
+    cam = default_camera()
+    cam.rotation = so3_exp([0.1, -0.2, 0.05])
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    di, da = _loss_upstream(np.random.default_rng(2), fr)
+    g = gvr.backward(fr, di, da)
+    assert np.array_equal(g.d_inv_cov, np.transpose(g.d_inv_cov, (0, 2, 1)))
+
+
+def test_gradcheck_central_differences(ctx):
+    """test_grad.cpp:95-110 (gradcheck < 1e-3 on random 5-kernel scenes with a
+    rotated camera), with the GPU forward as the function being differentiated."""
+    rng = np.random.default_rng(64)
+    for trial in range(3):
+        scene = random_scene(640 + trial, 5, 3, 2.0, 20.0)
+        cam = Camera(so3_exp([0.05, -0.1, 0.03]), np.array([0.02, 0.01, 0.1]), 12.0, 11.5, 11.5, 24, 24)
+        ti = rng.uniform(0, 1, (24, 24, 3))
+        ta = rng.uniform(0, 1, (24, 24, 1))
+
+        def loss(s):
+            b = gvr.render_with_tape(s, cam, ctx=ctx)
+            return 0.5 * ((b.buffers.image - ti) ** 2).sum() + 0.5 * ((b.buffers.alpha - ta) ** 2).sum(), b
+
+        base, fr = loss(scene)
+        g = gvr.backward(fr, fr.buffers.image - ti, fr.buffers.alpha - ta)
+        worst, checked = 0.0, 0
+        for k in range(scene.size):
+            for dim in range(3):
+                h = 1e-4 * max(1.0, abs(scene.centers[k, dim]))
+                sp, sm = scene.copy(), scene.copy()
+                sp.centers[k, dim] += h
+                sm.centers[k, dim] -= h
+                (lp, bp), (lm, bm) = loss(sp), loss(sm)
+                if not (np.array_equal(bp.buffers.topk_idx, fr.buffers.topk_idx) and
+                        np.array_equal(bm.buffers.topk_idx, fr.buffers.topk_idx)):
+                    continue  # selection changed within +-h (grad.cpp:285-289)
+                num = (lp - lm) / (2 * h)
+                ana = g.d_center[k, dim]
+                if abs(ana) < 1e-7 and abs(num) < 1e-7:
+                    continue
+                worst = max(worst, abs(ana - num) / max(abs(ana) + abs(num), 1e-6))
+                checked += 1
+        assert checked > 0
+        assert worst < 1e-3
+
+
+# ----------------------------------------------------------------- scene (test_scene.cpp)
+
+def test_render_equivariance(ctx):
+    """test_scene.cpp:132-154: render(S, cam) == render(view_transform(S, cam), I) (< 1e-6)."""
+    cfg = SelectionConfig(coarse_enabled=False)
+    for trial in range(5):
+        scene = random_scene(23 + trial, 6)
+        cam = default_camera()
+        cam.rotation = so3_exp(np.array([0.1, -0.2, 0.3]) * (trial + 1) * 0.2)
+        cam.translation = np.array([0.05, -0.02, 0.4])
+        staged = scene.copy()
+        staged.centers = scene.centers @ cam.rotation.T + cam.translation
+        staged.inv_cov = np.einsum("ij,kjl,ml->kim", cam.rotation, scene.inv_cov, cam.rotation)
+        ident = default_camera()
+        a = gvr.render(scene, cam, cfg, ctx=ctx).image
+        b = gvr.render(staged, ident, cfg, ctx=ctx).image
+        assert np.abs(a - b).max() < 1e-6
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda s: s.inv_cov.__setitem__((0, 0, 1), 0.5), "inv_cov is not symmetric (kernel 0)"),
+    (lambda s: s.inv_cov.__setitem__((0, 2, 2), -1.0), "inv_cov is not positive-definite (kernel 0)"),
+    (lambda s: s.centers.__setitem__((0, 0), np.inf), "kernel has non-finite values (kernel 0)"),
+    (lambda s: setattr(s, "tau", -0.5), "tau must be finite and >= 0"),
+])
+def test_scene_validation_messages(ctx, mutate, msg):
+    """test_scene.cpp:156-183 + the reference's exact messages (types.cpp:17-42)."""
+    scene = GaussianScene(np.array([[0, 0, 4.0]]), np.eye(3)[None], np.zeros((1, 3)), 1.0)
+    mutate(scene)
+    with pytest.raises(ValidationError) as e:
+        gvr.render(scene, default_camera(), ctx=ctx)
+    assert str(e.value) == msg
+
+
+def test_camera_and_config_validation_messages(ctx):
+    scene = random_scene(1, 1)
+    cam = default_camera()
+    cam.rotation = np.diag([2.0, 1.0, 1.0])
+    with pytest.raises(ValidationError, match="camera rotation is not orthonormal"):
+        gvr.render(scene, cam, ctx=ctx)
+    with pytest.raises(ValidationError, match="camera focal length must be > 0"):
+        gvr.render(scene, Camera(np.eye(3), np.zeros(3), 0.0, 0, 0, 4, 4), ctx=ctx)
+    with pytest.raises(ValidationError, match="selection eta must be in"):
+        gvr.render(scene, default_camera(), SelectionConfig(eta=1.0), ctx=ctx)
+    with pytest.raises(ValidationError, match="selection k_prime must be >= 1"):
+        gvr.render(scene, default_camera(), SelectionConfig(k_prime=0), ctx=ctx)
+
+
+def test_degenerate_image_sizes(ctx):
+    """1x1, 1x2 and non-multiple-of-8 sizes (test_grad.cpp:233, test_blender.cpp:306, 15^2, 17^2, 21^2, 33^2)."""
+    scene = random_scene(5, 30)
+    for h, w in [(1, 1), (1, 2), (15, 15), (17, 17), (21, 21), (33, 33), (9, 70)]:
+        cam = Camera(np.eye(3), np.zeros(3), 0.8 * max(h, w), (w - 1) / 2, (h - 1) / 2, h, w)
+        a = gvr.render(scene, cam, ctx=ctx)
+        o = oracle.port_render(scene, cam, SelectionConfig(), threads=4)
+        assert np.array_equal(a.topk_idx, o["topk_idx"])
+        assert_close_rel(a.image, o["image"], what=f"image {h}x{w}")
+
+
+def test_attribute_dims_zero_to_five(ctx):
+    """D in {0, 1, 2, 3, 5}: D = 0 renders one zero channel (blender.cpp:91)."""
+    base = random_scene(9, 40)
+    cam = default_camera(24, 20.0)
+    for d in (0, 1, 2, 3, 5):
+        scene = GaussianScene(base.centers, base.inv_cov, np.random.default_rng(d).uniform(0, 1, (40, d)), 1.0)
+        a = gvr.render(scene, cam, ctx=ctx)
+        o = oracle.port_render(scene, cam, SelectionConfig(), threads=4)
+        assert a.image.shape == o["image"].shape
+        assert np.array_equal(a.topk_idx, o["topk_idx"])
+        assert_close_rel(a.image, o["image"], what=f"image D={d}")
+        if d > 0:
+            fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+            rng = np.random.default_rng(10 + d)
+            di, da = rng.uniform(-1, 1, (24, 24, d)), rng.uniform(-1, 1, (24, 24, 1))
+            g = gvr.backward(fr, di, da)
+            go = oracle.port_backward(scene, cam, SelectionConfig(), di, da, threads=4)
+            assert_grad_close(g.d_attr, go["d_attr"], what=f"d_attr D={d}")
+            assert_grad_close(g.d_center, go["d_center"], what=f"d_center D={d}")
+
+
+def test_tau_extremes(ctx):
+    """tau from 0 to 50 (tests/data/texture_scene.json, test_sampler.cpp:216)."""
+    base = random_scene(12, 60)
+    cam = default_camera(32, 24.0)
+    for tau in (0.0, 0.91, 50.0):
+        scene = GaussianScene(base.centers, base.inv_cov, base.attr, tau)
+        a = gvr.render(scene, cam, ctx=ctx)
+        o = oracle.port_render(scene, cam, SelectionConfig(), threads=4)
+        assert np.array_equal(a.topk_idx, o["topk_idx"])
+        assert_close_rel(a.image, o["image"], what=f"image tau={tau}")
+        assert_close_rel(a.alpha, o["alpha"], what=f"alpha tau={tau}")
+
+
+# ----------------------------------------------------------------- full-size parity vs the oracle
+
+@pytest.mark.parametrize("view", ["c2", "orbit"])
+def test_full_size_parity_against_oracle(ctx, view):
+    """C2 (512^2, 101,402 kernels) and one C3 orbit view: bit-exact selection and
+    tolerance parity of every output and gradient against the C oracle."""
+    scene = gvr.make_bench_scene(100000)
+    cam = gvr.make_bench_camera(512) if view == "c2" else gvr.make_orbit_camera(
+        2 * np.pi * 5 / 64, 0.3, 4.0, (0, 0, 4), 512, 512, 1.6 * 512)
+    cfg = SelectionConfig()
+    fr = gvr.render_with_tape(scene, cam, cfg, ctx=ctx)
+    o = oracle.port_render(scene, cam, cfg, threads=0)
+    assert np.array_equal(fr.buffers.topk_idx, o["topk_idx"])
+    for key in ("image", "alpha", "depth", "topk_w"):
+        assert_close_rel(getattr(fr.buffers, key), o[key], what=f"{view} {key}")
+    rng = np.random.default_rng(3)
+    di = fr.buffers.image - rng.uniform(0, 1, fr.buffers.image.shape)
+    da = fr.buffers.alpha - rng.uniform(0, 1, fr.buffers.alpha.shape)
+    g = gvr.backward(fr, di, da)
+    go = oracle.port_backward(scene, cam, cfg, di, da, threads=0)
+    for key in ("d_center", "d_inv_cov", "d_attr", "d_rotation", "d_translation"):
+        assert_grad_close(getattr(g, key), go[key], what=f"{view} {key}")
