@@ -1,0 +1,366 @@
+// gvr/gvr.hpp — C++ drop-in for the reference render API (namespace gvr) on top
+// of the C ABI in gvr_cuda.h. Header-only; link against libgvr_cuda.so.
+//
+// Mirrors /root/reference/proj/include/gvr/{types,tracer,blender,grad}.hpp:
+//   GaussianKernel / GaussianScene / Camera / Image / ValidationError   types.hpp:19-93
+//   SelectionConfig / TracedKernel                                      tracer.hpp:11-25
+//   RenderBuffers (weight_store) / render                               blender.hpp:18-41
+//   Tape / ForwardResult / GradFlags / GradientBundle / ScalarLoss /
+//   render_with_tape / backward                                         grad.hpp:13-70
+// Same field names, argument meaning and error behaviour (ValidationError with
+// the reference's message text). `threads` is accepted and ignored.
+//
+// Linear-algebra types: the reference uses Eigen (Vector3d / Matrix3d /
+// VectorXd). Define GVR_WITH_EIGEN (and put Eigen on the include path) to get
+// exactly those types; otherwise small value types with the same accessors
+// (x(), y(), z(), operator()(r, c), operator[], size()) are used.
+#pragma once
+
+#include "../gvr_cuda.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <initializer_list>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#ifdef GVR_WITH_EIGEN
+#include <Eigen/Dense>
+#endif
+
+namespace gvr {
+
+#ifdef GVR_WITH_EIGEN
+using Vec3 = Eigen::Vector3d;
+using Mat3 = Eigen::Matrix3d;
+using VecX = Eigen::VectorXd;
+#else
+struct Vec3 {
+    double v[3] = {0.0, 0.0, 0.0};
+    Vec3() = default;
+    Vec3(double x, double y, double z) : v{x, y, z} {}
+    static Vec3 Zero() { return Vec3(); }
+    static Vec3 UnitZ() { return Vec3(0, 0, 1); }
+    double& operator[](int i) { return v[i]; }
+    double operator[](int i) const { return v[i]; }
+    double& operator()(int i) { return v[i]; }
+    double operator()(int i) const { return v[i]; }
+    double x() const { return v[0]; }
+    double y() const { return v[1]; }
+    double z() const { return v[2]; }
+    int size() const { return 3; }
+};
+struct Mat3 {
+    double m[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // row-major
+    static Mat3 Identity() { return Mat3(); }
+    static Mat3 Zero() {
+        Mat3 z;
+        std::memset(z.m, 0, sizeof z.m);
+        return z;
+    }
+    double& operator()(int r, int c) { return m[3 * r + c]; }
+    double operator()(int r, int c) const { return m[3 * r + c]; }
+};
+struct VecX {
+    std::vector<double> v;
+    VecX() = default;
+    explicit VecX(int n) : v(static_cast<size_t>(n), 0.0) {}
+    VecX(std::initializer_list<double> l) : v(l) {}
+    static VecX Zero(int n) { return VecX(n); }
+    double& operator[](int i) { return v[static_cast<size_t>(i)]; }
+    double operator[](int i) const { return v[static_cast<size_t>(i)]; }
+    double& operator()(int i) { return v[static_cast<size_t>(i)]; }
+    double operator()(int i) const { return v[static_cast<size_t>(i)]; }
+    int size() const { return static_cast<int>(v.size()); }
+};
+#endif
+
+// types.hpp:19-22
+class ValidationError : public std::runtime_error {
+public:
+    explicit ValidationError(const std::string& msg) : std::runtime_error(msg) {}
+};
+
+// types.hpp:26-33
+struct GaussianKernel {
+    Vec3 center = Vec3::Zero();
+    Mat3 inv_cov = Mat3::Identity();
+    VecX attr;
+};
+
+// types.hpp:35-42
+struct GaussianScene {
+    std::vector<GaussianKernel> kernels;
+    double tau = 1.0;
+    int attr_dim() const { return kernels.empty() ? 0 : static_cast<int>(kernels.front().attr.size()); }
+    int size() const { return static_cast<int>(kernels.size()); }
+};
+
+// types.hpp:46-56
+struct Camera {
+    Mat3 rotation = Mat3::Identity();
+    Vec3 translation = Vec3::Zero();
+    double focal = 1.0;
+    double ox = 0.0;
+    double oy = 0.0;
+    int height = 1;
+    int width = 1;
+};
+
+enum class ChannelSemantics : std::uint8_t { Color, Alpha, Normal, Feature };
+
+// types.hpp:71-93
+struct Image {
+    int height = 0;
+    int width = 0;
+    int channels = 0;
+    ChannelSemantics semantics = ChannelSemantics::Color;
+    std::vector<double> data;
+
+    Image() = default;
+    Image(int h, int w, int c, ChannelSemantics sem = ChannelSemantics::Color)
+        : height(h), width(w), channels(c), semantics(sem), data(static_cast<size_t>(h) * w * c, 0.0) {}
+    double& at(int r, int c, int ch) { return data[(static_cast<size_t>(r) * width + c) * channels + ch]; }
+    double at(int r, int c, int ch) const { return data[(static_cast<size_t>(r) * width + c) * channels + ch]; }
+    size_t pixel_count() const { return static_cast<size_t>(height) * width; }
+};
+
+// tracer.hpp:11-25
+struct TracedKernel {
+    int kernel_index = 0;
+    double l = 0.0;
+    double q = 0.0;
+    double sigma = 1.0;
+};
+
+struct SelectionConfig {
+    double eta = 0.01;
+    int k_prime = 20;
+    bool coarse_enabled = true;
+    int coarse_downsample = 8;
+};
+
+// blender.hpp:18-25
+struct RenderBuffers {
+    Image image;
+    Image alpha;
+    Image depth;
+    std::vector<std::vector<std::pair<int, double>>> weight_store;
+};
+
+// grad.hpp:13-22
+struct GradientBundle {
+    std::vector<Vec3> d_center;
+    std::vector<Mat3> d_inv_cov;
+    std::vector<VecX> d_attr;
+    Mat3 d_rotation = Mat3::Zero();
+    Vec3 d_translation = Vec3::Zero();
+};
+
+// grad.hpp:46-49
+struct GradFlags {
+    bool through_transmittance = true;
+    bool through_density = true;
+};
+
+namespace detail {
+
+// One device context per host thread (the reference's API is free functions).
+struct Ctx {
+    gvr_context* ctx = nullptr;
+    Ctx() {
+        int dev = 0;
+        if (const char* e = std::getenv("GVR_DEVICE")) dev = std::atoi(e);
+        if (gvr_context_create(dev, &ctx) != GVR_OK) throw std::runtime_error("gvr: no usable sm_100 CUDA device");
+    }
+    ~Ctx() { gvr_context_destroy(ctx); }
+};
+
+inline gvr_context* context() {
+    thread_local Ctx c;
+    return c.ctx;
+}
+
+inline void check(int rc) {
+    if (rc == GVR_OK) return;
+    const std::string msg = gvr_last_error(context());
+    if (rc == GVR_ERR_VALIDATION) throw ValidationError(msg);
+    throw std::runtime_error(msg);
+}
+
+struct SceneHandle {
+    gvr_scene* s = nullptr;
+    SceneHandle() { check(gvr_scene_create(context(), &s)); }
+    ~SceneHandle() { gvr_scene_destroy(s); }
+};
+
+struct TapeHandle {
+    gvr_tape* t = nullptr;
+    TapeHandle() { check(gvr_tape_create(context(), &t)); }
+    ~TapeHandle() { gvr_tape_destroy(t); }
+};
+
+// GaussianScene (AoS) -> flat FP64 arrays -> gvr_scene_set (validates once).
+inline std::shared_ptr<SceneHandle> upload(const GaussianScene& scene) {
+    const int k = scene.size(), d = scene.attr_dim();
+    if (scene.tau < 0.0 || !std::isfinite(scene.tau)) throw ValidationError("tau must be finite and >= 0");
+    std::vector<double> c(3 * static_cast<size_t>(k)), s(9 * static_cast<size_t>(k)), a(static_cast<size_t>(d) * k);
+    for (int i = 0; i < k; ++i) {
+        const auto& g = scene.kernels[i];
+        if (g.attr.size() != d)
+            throw ValidationError("attribute dimension is not uniform (kernel " + std::to_string(i) + ")");
+        for (int t = 0; t < 3; ++t) c[3 * i + t] = g.center[t];
+        for (int r = 0; r < 3; ++r)
+            for (int t = 0; t < 3; ++t) s[9 * i + 3 * r + t] = g.inv_cov(r, t);
+        for (int t = 0; t < d; ++t) a[static_cast<size_t>(d) * i + t] = g.attr[t];
+    }
+    auto h = std::make_shared<SceneHandle>();
+    check(gvr_scene_set(context(), h->s, k, d, scene.tau, c.data(), s.data(), a.data()));
+    return h;
+}
+
+inline gvr_camera to_c(const Camera& cam) {
+    gvr_camera c;
+    for (int r = 0; r < 3; ++r)
+        for (int t = 0; t < 3; ++t) c.rotation[3 * r + t] = cam.rotation(r, t);
+    for (int t = 0; t < 3; ++t) c.translation[t] = cam.translation[t];
+    c.focal = cam.focal;
+    c.ox = cam.ox;
+    c.oy = cam.oy;
+    c.height = cam.height;
+    c.width = cam.width;
+    return c;
+}
+
+inline gvr_selection to_c(const SelectionConfig& s) {
+    return gvr_selection{s.eta, s.k_prime, s.coarse_enabled ? 1 : 0, s.coarse_downsample};
+}
+
+}  // namespace detail
+
+// grad.hpp:26-33. The device record of the forward; `traced` (Tape::traced) is
+// materialised on first use, `cam_scene` is not kept (it lives on the device).
+struct Tape {
+    GaussianScene scene;
+    Camera camera;
+    SelectionConfig cfg;
+    int threads = 0;
+    std::shared_ptr<detail::SceneHandle> device_scene;
+    std::shared_ptr<detail::TapeHandle> device_tape;
+
+    std::vector<std::vector<TracedKernel>> traced() const {
+        const size_t p = static_cast<size_t>(camera.height) * camera.width, kp = cfg.k_prime;
+        std::vector<int32_t> idx(p * kp);
+        std::vector<double> l(p * kp), q(p * kp), s(p * kp);
+        detail::check(gvr_tape_traced(detail::context(), device_tape->t, idx.data(), l.data(), q.data(), s.data()));
+        std::vector<std::vector<TracedKernel>> out(p);
+        for (size_t i = 0; i < p; ++i)
+            for (size_t k = 0; k < kp && idx[i * kp + k] >= 0; ++k)
+                out[i].push_back({idx[i * kp + k], l[i * kp + k], q[i * kp + k], s[i * kp + k]});
+        return out;
+    }
+};
+
+// grad.hpp:35-38
+struct ForwardResult {
+    RenderBuffers buffers;
+    Tape tape;
+};
+
+// grad.hpp:41-42 / grad.cpp:38-47
+inline ForwardResult render_with_tape(const GaussianScene& scene, const Camera& camera, const SelectionConfig& cfg,
+                                      int threads = 0) {
+    ForwardResult fr;
+    fr.tape.scene = scene;
+    fr.tape.camera = camera;
+    fr.tape.cfg = cfg;
+    fr.tape.threads = threads;
+    fr.tape.device_scene = detail::upload(scene);
+    fr.tape.device_tape = std::make_shared<detail::TapeHandle>();
+    const int h = camera.height, w = camera.width, dc = std::max(scene.attr_dim(), 1);
+    const size_t p = static_cast<size_t>(std::max(h, 0)) * std::max(w, 0), kp = std::max(cfg.k_prime, 0);
+    RenderBuffers& b = fr.buffers;
+    b.image = Image(h, w, dc, ChannelSemantics::Color);
+    b.alpha = Image(h, w, 1, ChannelSemantics::Alpha);
+    b.depth = Image(h, w, 1, ChannelSemantics::Feature);
+    std::vector<int32_t> idx(p * kp);
+    std::vector<double> wts(p * kp);
+    const gvr_camera cc = detail::to_c(camera);
+    const gvr_selection sc = detail::to_c(cfg);
+    const gvr_render_outputs out{b.image.data.data(), b.alpha.data.data(), b.depth.data.data(), idx.data(),
+                                 wts.data()};
+    detail::check(gvr_render(detail::context(), fr.tape.device_scene->s, &cc, &sc, fr.tape.device_tape->t, &out));
+    b.weight_store.assign(p, {});
+    for (size_t i = 0; i < p; ++i)
+        for (size_t k = 0; k < kp && idx[i * kp + k] >= 0; ++k) b.weight_store[i].emplace_back(idx[i * kp + k], wts[i * kp + k]);
+    return fr;
+}
+
+// blender.hpp:40-41
+inline RenderBuffers render(const GaussianScene& scene, const Camera& camera, const SelectionConfig& cfg,
+                            int threads = 0) {
+    return render_with_tape(scene, camera, cfg, threads).buffers;
+}
+
+// grad.hpp:53-54 / grad.cpp:49-199
+inline GradientBundle backward(const Tape& tape, const Image& d_image, const Image& d_alpha,
+                               const GradFlags& flags = {}) {
+    const int h = tape.camera.height, w = tape.camera.width, dim = tape.scene.attr_dim(), k = tape.scene.size();
+    if (d_image.height != h || d_image.width != w || d_image.channels != dim)
+        throw ValidationError("backward: d_image shape does not match the forward render");
+    if (d_alpha.height != h || d_alpha.width != w || d_alpha.channels != 1)
+        throw ValidationError("backward: d_alpha shape does not match the forward render");
+    std::vector<double> dc(3 * static_cast<size_t>(k)), ds(9 * static_cast<size_t>(k)),
+        da(static_cast<size_t>(dim) * k), dr(9), dt(3);
+    const gvr_grad_flags f{flags.through_transmittance ? 1 : 0, flags.through_density ? 1 : 0};
+    const gvr_gradients out{dc.data(), ds.data(), dim > 0 ? da.data() : nullptr, dr.data(), dt.data()};
+    detail::check(gvr_backward(detail::context(), tape.device_tape->t, dim > 0 ? d_image.data.data() : nullptr,
+                               d_alpha.data.data(), &f, &out));
+    GradientBundle g;
+    g.d_center.resize(k);
+    g.d_inv_cov.resize(k);
+    g.d_attr.assign(k, VecX::Zero(dim));
+    for (int i = 0; i < k; ++i) {
+        g.d_center[i] = Vec3(dc[3 * i], dc[3 * i + 1], dc[3 * i + 2]);
+        for (int r = 0; r < 3; ++r)
+            for (int t = 0; t < 3; ++t) g.d_inv_cov[i](r, t) = ds[9 * i + 3 * r + t];
+        for (int t = 0; t < dim; ++t) g.d_attr[i][t] = da[static_cast<size_t>(dim) * i + t];
+    }
+    for (int r = 0; r < 3; ++r)
+        for (int t = 0; t < 3; ++t) g.d_rotation(r, t) = dr[3 * r + t];
+    g.d_translation = Vec3(dt[0], dt[1], dt[2]);
+    return g;
+}
+
+// grad.hpp:62-70 / grad.cpp:201-216 (the reference's host-side loss functional).
+struct ScalarLoss {
+    Image target_image;
+    Image target_alpha;
+    double w_image = 1.0;
+    double w_alpha = 1.0;
+
+    double value(const RenderBuffers& buf, Image* d_image, Image* d_alpha) const {
+        double loss = 0.0;
+        if (d_image) *d_image = Image(buf.image.height, buf.image.width, buf.image.channels);
+        if (d_alpha) *d_alpha = Image(buf.alpha.height, buf.alpha.width, 1, ChannelSemantics::Alpha);
+        for (size_t i = 0; i < buf.image.data.size(); ++i) {
+            const double diff = buf.image.data[i] - target_image.data[i];
+            loss += 0.5 * w_image * diff * diff;
+            if (d_image) d_image->data[i] = w_image * diff;
+        }
+        for (size_t i = 0; i < buf.alpha.data.size(); ++i) {
+            const double diff = buf.alpha.data[i] - target_alpha.data[i];
+            loss += 0.5 * w_alpha * diff * diff;
+            if (d_alpha) d_alpha->data[i] = w_alpha * diff;
+        }
+        return loss;
+    }
+};
+
+}  // namespace gvr
