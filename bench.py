@@ -288,7 +288,7 @@ def run_ours(args):
     flops = algorithmic_flops(wc)
     fp32_peak = ctx.pipe_peak("fp32")
     fp64_peak = ctx.pipe_peak("fp64")
-    kern_names = {"select": "select_kernel", "blend": "blend_kernel", "backward": "backward_pixels_kernel"}
+    kern_names = {"select": "select_warp_kernel", "blend": "blend_kernel", "backward": "backward_pixels_kernel"}
     per_launch_ms = {k: stages[k][0] / max(stages[k][1], 1) for k in kern_names}
     dominant = max(per_launch_ms, key=per_launch_ms.get)
     dom_ms = per_launch_ms[dominant]

@@ -61,14 +61,14 @@ __global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
     const double tau = p.tau;
     double dimg[4] = {0, 0, 0, 0};
     for (int c = 0; c < p.D && c < 4; ++c) dimg[c] = p.d_image[pix * p.D + c];
-    const double l0 = trace_exact(d, p.rec64[p.topk[pix * p.kp]]).l;
+    const double l0 = trace_fast(d, p.rec64[p.topk[pix * p.kp]]).l;
 
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
     // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
     double peak_part = 0.0;
     for (int s = sub; s < n; s += 4) {
         const int k = p.topk[pix * p.kp + s];
-        const Traced64 t = trace_exact(d, p.rec64[k]);
+        const Traced64 t = trace_fast(d, p.rec64[k]);
         const double pk64 = exp(t.q);
         const float pkf = (float)pk64;
         const double pk = (double)pkf;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
         b_dl[s * NP + g] = t.l - l0;
         b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
         b_pk[s * NP + g] = pkf;
-        b_is[s * NP + g] = (float)__dsqrt_rn(t.a);
+        b_is[s * NP + g] = (float)sqrt(t.a);
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
@@ -118,21 +118,24 @@ __global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
         for (int k = 0; k < n; ++k) {
             const double dak = b_da[k * NP + g];
             const double dlk = b_dl[k * NP + g];
+            const float isk = b_is[k * NP + g];
+            // pair (k, m = e): z1 = (l_k - l_e) / sigma_e ; pair (k = e, m = k): z2 = (l_e - l_k) / sigma_k
+            const float dlf = (float)(dlk - dle);
+            const float z1 = dlf * ise;
+            float phi1 = 0.0f;
             if (dak != 0.0) {
-                // pair (k, m = e): z = (l_k - l_e) / sigma_e
-                const float z = (float)((dlk - dle) * (double)ise);
-                dpk += dak * (double)fast_normal_cdf(z);
+                dpk += dak * (double)fast_normal_cdf(z1);
                 if (k != e) {
-                    const double gg = dak * (double)(normal_pdf_fast(z) * ise) * pke;
+                    phi1 = normal_pdf_fast(z1);
+                    const double gg = dak * (double)(phi1 * ise) * pke;
                     dl -= gg;
-                    dsg -= gg * (double)z;
+                    dsg -= gg * (double)z1;
                 }
             }
             if (dae != 0.0 && k != e) {
-                // pair (k = e, m = k): z = (l_e - l_k) / sigma_k
-                const float isk = b_is[k * NP + g];
-                const float z = (float)((dle - dlk) * (double)isk);
-                dl += dae * (double)(b_pk[k * NP + g] * normal_pdf_fast(z) * isk);
+                // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
+                const float phi2 = (isk == ise && dak != 0.0) ? phi1 : normal_pdf_fast(-dlf * isk);
+                dl += dae * (double)(b_pk[k * NP + g] * phi2 * isk);
             }
         }
         const double dq = dpk * pke;
@@ -140,12 +143,17 @@ __global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
 
         const Rec64 r = p.rec64[kid];
         double sd[3], v[3], sv[3];
-        xmatvec(r.s, d, sd);
-        const double a = xdot(d, sd);
-        const double l = xdiv(xmul(0.5, xadd(xdot(r.m, sd), xdot(d, r.sm))), a);
+        const double s00 = r.s[0], s01 = r.s[1], s02 = r.s[2], s11 = r.s[4], s12 = r.s[5], s22 = r.s[8];
+        sd[0] = fma(s00, d[0], fma(s01, d[1], s02 * d[2]));
+        sd[1] = fma(s01, d[0], fma(s11, d[1], s12 * d[2]));
+        sd[2] = fma(s02, d[0], fma(s12, d[1], s22 * d[2]));
+        const double a = fma(d[0], sd[0], fma(d[1], sd[1], d[2] * sd[2]));
+        const double l = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2])) / a;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) v[t] = r.m[t] - l * d[t];
-        xmatvec(r.s, v, sv);
+        for (int t = 0; t < 3; ++t) v[t] = fma(-l, d[t], r.m[t]);
+        sv[0] = fma(s00, v[0], fma(s01, v[1], s02 * v[2]));
+        sv[1] = fma(s01, v[0], fma(s11, v[1], s12 * v[2]));
+        sv[2] = fma(s02, v[0], fma(s12, v[1], s22 * v[2]));
         const double scale = dl / a;
         const double sigma = 1.0 / sqrt(a);
         const double d_a = -0.5 * sigma * sigma * sigma * dsg;

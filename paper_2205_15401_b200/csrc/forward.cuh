@@ -82,7 +82,11 @@ __device__ __forceinline__ double fast_l(const Rec64& r, const double* d, const 
     const double a = fma(r.s[0], dd[0], fma(r.s[4], dd[1], fma(r.s[8], dd[2],
                          fma(r.s[1], dd[3], fma(r.s[2], dd[4], r.s[5] * dd[5])))));
     const double b = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2]));
-    return b / a;
+    double rc;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(a));
+    rc = rc * fma(-a, rc, 2.0);  // Newton: ~2^-40
+    rc = rc * fma(-a, rc, 2.0);  // ~1 ulp
+    return b * rc;
 }
 
 // Selection keys: (l, id) where l is either the fast l (error < 1e-11 |l|, a
@@ -252,18 +256,36 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     p.count[pix] = n;
 }
 
+// Exact order of two selection candidates (kernel ids a, b; l on the exact trace).
+__device__ __forceinline__ bool exact_less(int a, int b, const double* d, const Rec64* rec64) {
+    const double la = trace_exact(d, rec64[a]).l, lb = trace_exact(d, rec64[b]).l;
+    return la < lb || (la == lb && a < b);
+}
+
+// FP32 rank keys: lf = (float)fast l. |lf - l_exact| <= 2^-24 |l| + 1e-11 |l|, so two
+// keys farther apart than kKeyClose |l| order like the exact keys; closer ones
+// are compared on the exact trace.
+constexpr float kKeyClose = 4.0e-7f;
+
+__device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - b) <= kKeyClose * fabsf(b); }
+
 // K3a selection, warp-per-pixel form (K' <= 32). CTA = one 8x8 tile, 8 warps;
 // warp w handles pixels w, w+8, ... of the tile. Lanes stride the tile's list
-// 32 candidates at a time (box test + FP32 q classification fully
-// lane-parallel, fast l for the eligible lanes), and the K' nearest keys live
-// warp-distributed and sorted: lane s holds the s-th nearest. Eligible
-// candidates are inserted by ballot (position) + shuffle (shift). Near ties are
-// resolved with exact keys exactly as in the thread-per-pixel kernel.
+// 32 candidates at a time: box test (one 16-byte load), FP32 q classification
+// and fast l for the eligible lanes, all lane-parallel. The K' nearest live
+// warp-distributed and sorted (lane s holds the s-th nearest) as FP32 rank keys
+// + kernel ids; a batch's eligible candidates are merged in one step: ranks
+// from ballots, then one scatter through a per-warp shared-memory buffer. Any
+// comparison between keys within the FP32 bound is decided on the exact trace,
+// so the kept set is exactly the reference's.
 template <int KMAX>
-__global__ void __launch_bounds__(256) select_warp_kernel(FwdParams p) {
+__global__ void __launch_bounds__(256, 3) select_warp_kernel(FwdParams p) {
     constexpr int TILE = 8;
+    __shared__ float sh_l[8][64];
+    __shared__ int sh_i[8][64];
     if ((int)blockIdx.x >= *p.n_order) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned FULL = 0xffffffffu;
     const int tile = p.tile_order[blockIdx.x];
     const int start = p.tile_start[tile];
     const int end = p.tile_end[tile];
@@ -292,75 +314,98 @@ __global__ void __launch_bounds__(256) select_warp_kernel(FwdParams p) {
         const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
         const float fi = (float)i, fj = (float)j;
 
-        // warp-distributed sorted list: lane s < n holds the s-th nearest key
-        double L = INFINITY;
-        int I = 0x3fffffff;
+        float L = INFINITY;  // lane s < n: rank key of the s-th nearest
+        int I = 0x7fffffff;
         int n = 0;
-        double worst = INFINITY;  // key of lane kp-1 once full (uniform)
+        float worst = INFINITY;  // key of lane kp-1 once full (warp-uniform)
 
         for (int base = start; base < end; base += 32) {
             const int e = base + lane;
             const bool valid = e < end;
-            int k = valid ? p.vals[e] : 0;
-            const Rec32 r = p.rec32[k];
+            const int k = valid ? p.vals[e] : p.vals[start];
+            const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
+            const float4 box = __ldg(rp);        // top, bottom, left, right
+            const float4 zrec = __ldg(rp + 1);   // zmin, zf, ci_frac, cj_frac
             // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
-            const float zmin0 = __shfl_sync(0xffffffffu, r.zmin, 0);
-            if ((double)zmin0 > worst + 1e-11 * fabs(worst)) break;
-            const bool in_box = valid && fi >= r.top && fi <= r.bottom && fj >= r.left && fj <= r.right;
+            const float zmin0 = __shfl_sync(FULL, zrec.x, 0);
+            if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
+            const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w;
             int cls = 0;
-            if (in_box) cls = classify_q(r, i, j, u, v, qc);
-            double lk = INFINITY;
+            if (in_box) {
+                Rec32 r;
+                r.zmin = zrec.x;
+                r.zf = zrec.y;
+                r.ci_frac = zrec.z;
+                r.cj_frac = zrec.w;
+                const float4 c2 = __ldg(rp + 2), c3 = __ldg(rp + 3);
+                r.ci_int = __float_as_int(c2.x);
+                r.cj_int = __float_as_int(c2.y);
+                r.s00 = c2.z;
+                r.s01 = c2.w;
+                r.s02 = c3.x;
+                r.s11 = c3.y;
+                r.s12 = c3.z;
+                r.s22 = c3.w;
+                cls = classify_q(r, i, j, u, v, qc);
+            }
+            float lk = INFINITY;
             if (cls != 0) {
                 if (exact_only || cls == 1) {
                     const Traced64 t = trace_exact(d, rec64[k]);
                     if (t.q > log_eta) {  // fine_select threshold (tracer.cpp:117-118)
-                        lk = t.l;
-                        k |= kExact;
+                        lk = (float)t.l;
                     } else {
                         cls = 0;
                     }
                 } else {
-                    lk = fast_l(rec64[k], d, dd);
+                    lk = (float)fast_l(rec64[k], d, dd);
                 }
                 // cannot enter a full list
-                if (cls != 0 && lk > worst + 1e-11 * fabs(worst)) cls = 0;
+                if (cls != 0 && lk > worst + 2.0f * kKeyClose * fabsf(worst)) cls = 0;
             }
-            unsigned pend = __ballot_sync(0xffffffffu, cls != 0);
+            const unsigned elig = __ballot_sync(FULL, cls != 0);
+            if (elig == 0) continue;
+            const bool me = (elig >> lane) & 1u;
+            // ranks: for each eligible candidate (broadcast), the kept keys and the
+            // other candidates smaller than it; kept entries count the candidates
+            // that precede them.
+            int shift = 0, mypos = 0;
+            unsigned pend = elig;
             while (pend) {
                 const int src = __ffs(pend) - 1;
                 pend &= pend - 1;
-                double cl = __shfl_sync(0xffffffffu, lk, src);
-                int ci = __shfl_sync(0xffffffffu, k, src);
-                // position = number of kept keys smaller than the candidate
-                bool close = lane < n && keys_close(L, cl);
-                if (__any_sync(0xffffffffu, close)) {
-                    if (!(ci & kExact)) {  // warp-uniform exact key of the candidate
-                        cl = trace_exact(d, rec64[ci]).l;
-                        ci |= kExact;
-                    }
-                    if (close) make_exact(L, I, d, rec64);
+                const float bl = __shfl_sync(FULL, lk, src);
+                const int bi = __shfl_sync(FULL, k, src);
+                const bool in_ex = lane < n, in_c = me && lane != src;
+                bool ex_lt = in_ex && L < bl;
+                bool c_lt = in_c && lk < bl;
+                const bool ex_close = in_ex && keyf_close(L, bl);
+                const bool c_close = in_c && keyf_close(lk, bl);
+                if (__any_sync(FULL, ex_close || c_close)) {  // rare: decide on the exact trace
+                    if (ex_close) ex_lt = exact_less(I, bi, d, rec64);
+                    if (c_close) c_lt = exact_less(k, bi, d, rec64);
                 }
-                const bool lt = lane < n && (L < cl || (L == cl && (I & ~kExact) < (ci & ~kExact)));
-                const int pos = __popc(__ballot_sync(0xffffffffu, lt));
-                if (pos >= kp) continue;  // not among the K' nearest
-                const double up_l = __shfl_up_sync(0xffffffffu, L, 1);
-                const int up_i = __shfl_up_sync(0xffffffffu, I, 1);
-                if (lane == pos) {
-                    L = cl;
-                    I = ci;
-                } else if (lane > pos) {
-                    L = up_l;
-                    I = up_i;
-                }
-                if (lane >= kp) {
-                    L = INFINITY;
-                    I = 0x3fffffff;
-                }
-                n = min(n + 1, kp);
-                if (n == kp) worst = __shfl_sync(0xffffffffu, L, kp - 1);
+                const int pos = __popc(__ballot_sync(FULL, ex_lt)) + __popc(__ballot_sync(FULL, c_lt));
+                if (lane == src) mypos = pos;
+                if (in_ex && !ex_lt) ++shift;
             }
+            // scatter into the merged order, keep the first kp
+            if (lane < n && lane + shift < kp) {
+                sh_l[warp][lane + shift] = L;
+                sh_i[warp][lane + shift] = I;
+            }
+            if (me && mypos < kp) {
+                sh_l[warp][mypos] = lk;
+                sh_i[warp][mypos] = k;
+            }
+            __syncwarp();
+            n = min(n + __popc(elig), kp);
+            L = lane < n ? sh_l[warp][lane] : INFINITY;
+            I = lane < n ? sh_i[warp][lane] : 0x7fffffff;
+            __syncwarp();
+            if (n == kp) worst = __shfl_sync(FULL, L, kp - 1);
         }
-        if (lane < n) p.topk[pix * kp + lane] = I & ~kExact;  // sorted by key; the blend sorts exactly
+        if (lane < n) p.topk[pix * kp + lane] = I;  // exact order; the blend re-derives it
         if (lane == 0) p.count[pix] = n;
         cost += (float)(n * n);
     }
@@ -408,27 +453,34 @@ __global__ void __launch_bounds__(256) blend_kernel(FwdParams p) {
     double peak_part = 0.0;
     for (int s = sub; s < n; s += 4) {
         const int k = p.topk[pix * kp + s];
-        const Traced64 t = trace_exact(d, p.rec64[k]);
+        const Traced64 t = trace_fast(d, p.rec64[k]);
         const double pk = exp(t.q);
         peak_part += pk;
-        b_dl[s * NP + g] = t.l;  // exact l for now; relative to the nearest after the sort
+        b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
         b_pk[s * NP + g] = (float)pk;
-        b_is[s * NP + g] = (float)__dsqrt_rn(t.a);  // 1/sigma
+        b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
     peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
     __syncwarp(grp);
     if (sub == 0) {
-        // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort
+        // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort;
+        // keys closer than the fast-trace error are compared on exact l
         for (int s = 1; s < n; ++s) {
-            const double ls = b_dl[s * NP + g];
-            const int is = b_id[s * NP + g];
+            double ls = b_dl[s * NP + g];
+            int is = b_id[s * NP + g];
             const float ps = b_pk[s * NP + g], ss = b_is[s * NP + g];
             int t = s - 1;
-            while (t >= 0 && traced_less(ls, is, b_dl[t * NP + g], b_id[t * NP + g])) {
-                b_dl[(t + 1) * NP + g] = b_dl[t * NP + g];
-                b_id[(t + 1) * NP + g] = b_id[t * NP + g];
+            while (t >= 0) {
+                double lt = b_dl[t * NP + g];
+                int it = b_id[t * NP + g];
+                const bool less = key_less(ls, is, lt, it, d, p.rec64);
+                b_dl[t * NP + g] = lt;  // possibly upgraded to exact
+                b_id[t * NP + g] = it;
+                if (!less) break;
+                b_dl[(t + 1) * NP + g] = lt;
+                b_id[(t + 1) * NP + g] = it;
                 b_pk[(t + 1) * NP + g] = b_pk[t * NP + g];
                 b_is[(t + 1) * NP + g] = b_is[t * NP + g];
                 --t;
@@ -444,6 +496,7 @@ __global__ void __launch_bounds__(256) blend_kernel(FwdParams p) {
     __syncwarp(grp);
     for (int s = sub; s < n; s += 4) {
         b_dl[s * NP + g] -= l0;
+        b_id[s * NP + g] &= ~kExact;
         p.topk[pix * kp + s] = b_id[s * NP + g];
     }
     __syncwarp(grp);
@@ -452,7 +505,7 @@ __global__ void __launch_bounds__(256) blend_kernel(FwdParams p) {
         const double dlk = b_dl[k * NP + g];
         double acc = 0.0;
         for (int m = 0; m < n; ++m) {
-            const float z = (float)((dlk - b_dl[m * NP + g]) * (double)b_is[m * NP + g]);
+            const float z = (float)(dlk - b_dl[m * NP + g]) * b_is[m * NP + g];
             acc = fma((double)b_pk[m * NP + g], (double)fast_normal_cdf(z), acc);
         }
         const double trans = exp(-p.tau * acc);
