@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = (
     "gvr_context_stage_times",
     "gvr_measure_pipe_peak",
     "gvr_context_set_prefilter_guard",
+    "gvr_context_set_tile_capacity",
     "gvr_scene_create",
     "gvr_scene_destroy",
     "gvr_scene_set",
@@ -116,6 +117,7 @@ def load() -> ctypes.CDLL:
         "gvr_context_stage_times": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
         "gvr_measure_pipe_peak": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(dp)]),
         "gvr_context_set_prefilter_guard": (ctypes.c_int, [vp, dp]),
+        "gvr_context_set_tile_capacity": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_scene_create": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
         "gvr_scene_destroy": (None, [vp]),
         "gvr_scene_set": (ctypes.c_int, [vp, vp, i32, i32, dp, vp, vp, vp]),

@@ -16,11 +16,12 @@ struct FwdParams {
     int tiles_x;
     const int* tile_order;  // tiles by list length, longest first (LPT); first *n_order valid
     const int* n_order;
+    const int* tile_count;                 // [tiles] list lengths (may exceed cap)
+    const unsigned long long* tile_lists;  // [tiles * cap] (order(zmin) << 32 | id), unsorted
+    int cap;
+    int K;
     const int* tile_order_blend;  // tiles by sum_p n_p^2 (from the selection); first *n_order_blend valid
     const int* n_order_blend;
-    const int* tile_start;
-    const int* tile_end;
-    const int* vals;   // sorted kernel ids
     const Rec32* rec32;
     const Rec64* rec64;
     const double* attr;  // [K*D] object attributes (FP64)
@@ -66,6 +67,35 @@ __device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u,
     if (fmaf(dsd * qc.slack_lo, A, -bb) > qc.c_rej * A) return 0;
     if (fmaf(dsd * qc.slack_hi, A, -bb) < qc.c_acc * A) return 2;
     return 1;
+}
+
+// Loads a tile's candidate list into shared memory sorted ascending by
+// (depth bound zmin, id): CTA-wide bitonic sort (the lists are short: the
+// exact screen-box binning keeps C2 tiles at a few hundred entries). Returns
+// the list length, or -1 when the tile overflowed its capacity (the caller
+// then streams every kernel, unsorted, with the same exact tests).
+__device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys) {
+    const int count = p.tile_count[tile];
+    if (count > p.cap) return -1;
+    int pw = 1;
+    while (pw < count) pw <<= 1;
+    const unsigned long long* src = p.tile_lists + (size_t)tile * p.cap;
+    for (int e = threadIdx.x; e < pw; e += blockDim.x) keys[e] = e < count ? src[e] : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= pw; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int idx = threadIdx.x; idx < (pw >> 1); idx += blockDim.x) {
+                const int a = 2 * stride * (idx / stride) + (idx % stride), b = a + stride;
+                const unsigned long long ka = keys[a], kb = keys[b];
+                if ((ka > kb) == ((a & size) == 0)) {
+                    keys[a] = kb;
+                    keys[b] = ka;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    return count;
 }
 
 // Per-warp candidate chunk entry.
@@ -154,6 +184,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     Cand* chunk = reinterpret_cast<Cand*>(smem) + (threadIdx.x & ~31);
     double* s_l = reinterpret_cast<double*>(smem + sizeof(Cand) * NT);
     int* s_id = reinterpret_cast<int*>(s_l + KMAX * NT);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(s_id + KMAX * NT);
 
     if ((int)blockIdx.x >= *p.n_order) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -161,8 +192,10 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     const int i = (tile / p.tiles_x) * TILE + tid / TILE;
     const int j = (tile % p.tiles_x) * TILE + tid % TILE;
     const bool inside = i < p.cam.H && j < p.cam.W;
-    const int start = p.tile_start[tile];
-    const int end = p.tile_end[tile];
+    const int listed = load_sorted_list(p, tile, keys);
+    const bool overflow = listed < 0;  // stream every kernel, unsorted
+    const int start = 0;
+    const int end = overflow ? p.K : listed;
     const long long pix = (long long)i * p.cam.W + j;
     const int kp = p.sel.kp;
 
@@ -192,7 +225,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         if (__all_sync(0xffffffffu, done)) break;
         const int e = base + lane;
         if (e < end) {
-            const int k = p.vals[e];
+            const int k = overflow ? e : (int)(keys[e] & 0xffffffffu);
             chunk[lane].r = p.rec32[k];
             chunk[lane].k = k;
         }
@@ -200,7 +233,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         const int cnt = min(32, end - base);
         for (int c0 = 0; c0 < cnt && !done; c0 += 4) {
             // early exit: every later candidate has l >= zmin > worst kept (+ key error)
-            if ((double)chunk[c0].r.zmin > wl + 1e-11 * fabs(wl)) {
+            if (!overflow && (double)chunk[c0].r.zmin > wl + 1e-11 * fabs(wl)) {
                 done = true;
                 break;
             }
@@ -283,12 +316,16 @@ __global__ void __launch_bounds__(256, 3) select_warp_kernel(FwdParams p) {
     constexpr int TILE = 8;
     __shared__ float sh_l[8][64];
     __shared__ int sh_i[8][64];
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
     if ((int)blockIdx.x >= *p.n_order) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned FULL = 0xffffffffu;
     const int tile = p.tile_order[blockIdx.x];
-    const int start = p.tile_start[tile];
-    const int end = p.tile_end[tile];
+    const int listed = load_sorted_list(p, tile, keys);
+    const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
+    const int start = 0;
+    const int end = overflow ? p.K : listed;
     const int kp = p.sel.kp;
     const Rec64* rec64 = p.rec64;
     const double log_eta = p.sel.log_eta;
@@ -322,13 +359,15 @@ __global__ void __launch_bounds__(256, 3) select_warp_kernel(FwdParams p) {
         for (int base = start; base < end; base += 32) {
             const int e = base + lane;
             const bool valid = e < end;
-            const int k = valid ? p.vals[e] : p.vals[start];
+            const int k = overflow ? (valid ? e : 0) : (int)(keys[valid ? e : 0] & 0xffffffffu);
+            // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
+            if (!overflow) {
+                const float zmin0 = float_from_order_bits((uint32_t)(keys[base] >> 32));
+                if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
+            }
             const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
             const float4 box = __ldg(rp);        // top, bottom, left, right
             const float4 zrec = __ldg(rp + 1);   // zmin, zf, ci_frac, cj_frac
-            // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
-            const float zmin0 = __shfl_sync(FULL, zrec.x, 0);
-            if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
             const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w;
             int cls = 0;
             if (in_box) {
@@ -563,22 +602,16 @@ __global__ void clear_empty_tiles_kernel(CameraP cam, int Dc, int tiles_x, const
 
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
 // log-spaced cost buckets, descending). Zero-cost tiles are dropped and
-// *n_out receives the number kept. Cost = list length (fcost == null) or fcost[t].
-__global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, int coarse, const int* __restrict__ start,
-                                                           const int* __restrict__ end, const float* __restrict__ fcost,
-                                                           int* __restrict__ order, int* __restrict__ n_out) {
+// *n_out receives the number kept. Cost = icost[t] (list length) or fcost[t].
+__global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
+                                                           const float* __restrict__ fcost, int* __restrict__ order,
+                                                           int* __restrict__ n_out) {
     __shared__ int hist[256];
     __shared__ int offs[256];
     for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     auto bucket_of = [&](int t) -> int {
-        float c;
-        if (fcost) {
-            c = fcost[t];
-        } else {
-            const int l = coarse ? t : 0;
-            c = (float)(end[l] - start[l]);
-        }
+        const float c = fcost ? fcost[t] : (float)icost[t];
         if (!(c > 0.0f)) return -1;
         const int b = (int)(__log2f(c + 1.0f) * 8.0f);
         return 255 - min(b, 255);  // descending cost
@@ -588,13 +621,26 @@ __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, int coarse
         if (b >= 0) atomicAdd(&hist[b], 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int b = 0; b < 256; ++b) {
-            offs[b] = run;
-            run += hist[b];
+    if (threadIdx.x < 32) {  // warp scan over the 256 buckets
+        int vals[8], run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            vals[q] = hist[threadIdx.x * 8 + q];
+            run += vals[q];
         }
-        *n_out = run;
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (threadIdx.x >= o) incl += y;
+        }
+        int base = incl - run;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            offs[threadIdx.x * 8 + q] = base;
+            base += vals[q];
+        }
+        if (threadIdx.x == 31) *n_out = incl;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < tiles; t += blockDim.x) {

@@ -179,6 +179,15 @@ __device__ __forceinline__ float normal_pdf_fast(float z) {
     return 0.398942280401432678f * exp2f(-0.72134752044448170f * z * z);
 }
 
+// Order-preserving float <-> uint32 map (sort keys of the depth bound).
+__device__ __forceinline__ uint32_t float_order_bits(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_bits(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
 // (l, idx) lexicographic order of fine_select (tracer.cpp:119-122)
 __device__ __forceinline__ bool traced_less(double la, int ia, double lb, int ib) {
     return la < lb || (la == lb && ia < ib);

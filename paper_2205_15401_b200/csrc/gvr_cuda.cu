@@ -2,16 +2,15 @@
 // launch sequence (include/gvr_cuda.h documents the contract).
 //
 //   gvr_scene_set : H2D (or D2D) FP64 upload + K0 validate  [1 sync: error code]
-//   gvr_render    : K1 project -> scan -> [1 sync: pair count] -> K2a emit ->
-//                   radix sort (tile|depth) -> K2c ranges -> K3 fused forward
+//   gvr_render    : K1 project + bin (per-tile lists, atomics) -> tile order ->
+//                   K3a select (per-tile smem sort) -> order -> K3b blend;
+//                   fully asynchronous (no host synchronisation)
 //   gvr_scalar_loss, gvr_backward : K4 per-pixel backward -> K5 object space
 #include "../../include/gvr_cuda.h"
 #include "backward.cuh"
 #include "forward.cuh"
 #include "project.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -85,6 +84,7 @@ struct gvr_context {
     int64_t launches = 0;   // kernels of this library
     int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
     double guard = 0.02;
+    int tile_cap = 4096;  // per-tile candidate-list capacity
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
 };
@@ -109,12 +109,12 @@ struct gvr_tape {
     CameraP camp{};
     SelP selp{};
     int K = 0, D = 0, H = 0, W = 0, tile = 16, tiles_x = 0, tiles_y = 0;
-    uint32_t pairs = 0;
     int dropped_behind = 0;
     // per kernel
-    Buf rec32, rec64, counts, offsets;
-    // pairs
-    Buf keys, keys_alt, vals, vals_alt, cub_tmp, ranges;
+    Buf rec32, rec64;
+    // per-tile candidate lists
+    Buf tile_count, tile_lists;
+    int cap = 0;
     Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
     // per pixel
     Buf topk, count, image, alpha, depth, topk_w, tape_t;
@@ -261,12 +261,15 @@ int ceil_log2(uint32_t v) {
 
 template <int KMAX>
 int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
+    const size_t list_smem = sizeof(unsigned long long) * (size_t)fp.cap;
     if (KMAX <= 32) {
+        auto kern = select_warp_kernel<KMAX>;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem));
         StageTimer st(ctx, ST_SELECT);
-        select_warp_kernel<KMAX><<<tiles, 256, 0, ctx->stream>>>(fp);
+        kern<<<tiles, 256, list_smem, ctx->stream>>>(fp);
     } else {
         constexpr int NT = 64;
-        const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT;
+        const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT + list_smem;
         auto kern = select_kernel<KMAX>;
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_SELECT);
@@ -275,7 +278,7 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     LAUNCH_CHECK(ctx);
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, 0, nullptr, nullptr, cost, order_b, n_b);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b);
     }
     LAUNCH_CHECK(ctx);
     {
@@ -436,6 +439,12 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
     return GVR_OK;
 }
 
+int gvr_context_set_tile_capacity(gvr_context* ctx, int cap) {
+    if (!ctx || cap < 1 || cap > (1 << 20)) return GVR_ERR_RUNTIME;
+    ctx->tile_cap = cap;
+    return GVR_OK;
+}
+
 int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard) {
     if (!ctx || !(guard >= 0.0)) return GVR_ERR_RUNTIME;
     ctx->guard = guard;
@@ -520,8 +529,7 @@ int gvr_tape_create(gvr_context* ctx, gvr_tape** out) {
 void gvr_tape_destroy(gvr_tape* t) {
     if (!t) return;
     cudaStreamSynchronize(t->ctx->stream);
-    Buf* bufs[] = {&t->rec32, &t->rec64, &t->counts, &t->offsets, &t->keys, &t->keys_alt, &t->vals,
-                   &t->vals_alt, &t->cub_tmp, &t->ranges, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
+    Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_lists, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w};
     for (Buf* b : bufs) b->release();
@@ -587,9 +595,11 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
 
     CUDA_TRY(ctx, tape->rec32.ensure(sizeof(Rec32) * (size_t)(K > 0 ? K : 1)));
     CUDA_TRY(ctx, tape->rec64.ensure(sizeof(Rec64) * (size_t)(K > 0 ? K : 1)));
-    CUDA_TRY(ctx, tape->counts.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
-    CUDA_TRY(ctx, tape->offsets.ensure(sizeof(uint32_t) * ((size_t)K + 1)));
-    CUDA_TRY(ctx, tape->ranges.ensure(sizeof(int) * 2 * (size_t)tiles));
+    // Per-tile candidate-list capacity: lists beyond it are streamed (every
+    // kernel, exact tests, no early exit) instead of failing.
+    tape->cap = ctx->tile_cap;
+    CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * (size_t)tiles));
+    CUDA_TRY(ctx, tape->tile_lists.ensure(sizeof(unsigned long long) * (size_t)tiles * tape->cap));
     CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (2 + 3 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
@@ -601,13 +611,16 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     if (want_w) CUDA_TRY(ctx, tape->topk_w.ensure(sizeof(double) * (size_t)P * kp));
 
     int* dflags = ctx->flags.as<int>();
+    int* tile_count = tape->tile_count.as<int>();
+    int* sched = tape->sched.as<int>();
+    int* order_f = sched + 2;
+    float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
     CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 2 * sizeof(int), ctx->stream));
-    int* ranges = tape->ranges.as<int>();
-    CUDA_TRY(ctx, cudaMemsetAsync(ranges, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * (size_t)tiles, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (size_t)tiles, ctx->stream));
 
-    uint32_t pairs = 0;
     if (K > 0) {
-        // K1 projection + culling
+        // K1 projection + culling + binning into per-tile lists
         ProjectParams pp;
         pp.K = K;
         pp.centers = scene->centers.as<double>();
@@ -619,96 +632,21 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
         pp.tiles_y = tiles_y;
         pp.rec32 = tape->rec32.as<Rec32>();
         pp.rec64 = tape->rec64.as<Rec64>();
-        pp.counts = tape->counts.as<uint32_t>();
+        pp.tile_count = tile_count;
+        pp.tile_lists = tape->tile_lists.as<unsigned long long>();
+        pp.cap = tape->cap;
         pp.dropped_behind = dflags;
         {
             StageTimer st(ctx, ST_PROJECT);
             project_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(pp);
         }
         LAUNCH_CHECK(ctx);
-
-        // exclusive scan of per-kernel pair counts (counts[K] = 0 -> offsets[K] = total)
-        size_t scan_bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tape->counts.as<uint32_t>(), tape->offsets.as<uint32_t>(),
-                                      K + 1, ctx->stream);
-        CUDA_TRY(ctx, tape->cub_tmp.ensure(scan_bytes));
-        {
-            StageTimer st(ctx, ST_SCAN);
-            CUDA_TRY(ctx, cub::DeviceScan::ExclusiveSum(tape->cub_tmp.p, scan_bytes, tape->counts.as<uint32_t>(),
-                                                        tape->offsets.as<uint32_t>(), K + 1, ctx->stream));
-        }
-        ++ctx->lib_calls;
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags, tape->offsets.as<uint32_t>() + K, sizeof(uint32_t),
-                                      cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 1, dflags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        if (int rc = sync_and_check(ctx)) return rc;
-        std::memcpy(&pairs, ctx->h_flags, sizeof pairs);
-        tape->dropped_behind = ctx->h_flags[1];
-    } else {
-        tape->dropped_behind = 0;
-    }
-    tape->pairs = pairs;
-
-    if (pairs > 0) {
-        CUDA_TRY(ctx, tape->keys.ensure(sizeof(unsigned long long) * pairs));
-        CUDA_TRY(ctx, tape->keys_alt.ensure(sizeof(unsigned long long) * pairs));
-        CUDA_TRY(ctx, tape->vals.ensure(sizeof(int) * pairs));
-        CUDA_TRY(ctx, tape->vals_alt.ensure(sizeof(int) * pairs));
-        EmitParams ep;
-        ep.K = K;
-        ep.rec32 = tape->rec32.as<Rec32>();
-        ep.offsets = tape->offsets.as<uint32_t>();
-        ep.sel = sp;
-        ep.H = H;
-        ep.W = W;
-        ep.tile = tile;
-        ep.tiles_x = tiles_x;
-        ep.keys = tape->keys.as<unsigned long long>();
-        ep.vals = tape->vals.as<int>();
-        {
-            StageTimer st(ctx, ST_EMIT);
-            emit_pairs_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(ep);
-        }
-        LAUNCH_CHECK(ctx);
-
-        cub::DoubleBuffer<unsigned long long> dk(tape->keys.as<unsigned long long>(),
-                                                 tape->keys_alt.as<unsigned long long>());
-        cub::DoubleBuffer<int> dv(tape->vals.as<int>(), tape->vals_alt.as<int>());
-        const int end_bit = 32 + ceil_log2((uint32_t)tiles);
-        size_t sort_bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, dk, dv, (int)pairs, 0, end_bit, ctx->stream);
-        CUDA_TRY(ctx, tape->cub_tmp.ensure(sort_bytes));
-        {
-            StageTimer st(ctx, ST_SORT);
-            CUDA_TRY(ctx, cub::DeviceRadixSort::SortPairs(tape->cub_tmp.p, sort_bytes, dk, dv, (int)pairs, 0,
-                                                          end_bit, ctx->stream));
-        }
-        ++ctx->lib_calls;
-        {
-            StageTimer st(ctx, ST_RANGES);
-            tile_ranges_kernel<<<blocks_for(pairs, 256), 256, 0, ctx->stream>>>(pairs, dk.Current(), ranges,
-                                                                               ranges + tiles);
-        }
-        LAUNCH_CHECK(ctx);
-        // keep the sorted ids where the forward reads them
-        if (dv.Current() != tape->vals.as<int>()) {
-            std::swap(tape->vals.p, tape->vals_alt.p);
-            std::swap(tape->vals.cap, tape->vals_alt.cap);
-        }
-        if (dk.Current() != tape->keys.as<unsigned long long>()) {
-            std::swap(tape->keys.p, tape->keys_alt.p);
-            std::swap(tape->keys.cap, tape->keys_alt.cap);
-        }
     }
 
-    // K3 fused forward over the non-empty tiles, most expensive first
-    int* sched = tape->sched.as<int>();
-    int* order_f = sched + 2;
-    float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
-    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (size_t)tiles, ctx->stream));
+    // K3 over the non-empty tiles, longest list first
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, 1, ranges, ranges + tiles, nullptr, order_f, sched);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched);
     }
     LAUNCH_CHECK(ctx);
     FwdParams fp;
@@ -726,9 +664,10 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     fp.tile_order_blend = sched + 2 + tiles;
     fp.n_order_blend = sched + 1;
     fp.bwd_cost = bwd_cost;
-    fp.tile_start = ranges;
-    fp.tile_end = ranges + tiles;
-    fp.vals = tape->vals.as<int>();
+    fp.tile_count = tile_count;
+    fp.tile_lists = tape->tile_lists.as<unsigned long long>();
+    fp.cap = tape->cap;
+    fp.K = K;
     fp.rec32 = tape->rec32.as<Rec32>();
     fp.rec64 = tape->rec64.as<Rec64>();
     fp.attr = scene->attr.as<double>();

@@ -111,10 +111,6 @@ __device__ __forceinline__ int x86_int(double v) {
     return (int)v;
 }
 
-__device__ __forceinline__ uint32_t float_order_bits(float f) {
-    const uint32_t u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 // Tile rectangle of the pixel centres inside a kernel's screen box.
 __device__ __forceinline__ bool box_tiles(const Rec32& q, int H, int W, int tile, int& tr0, int& tr1, int& tc0,
@@ -139,7 +135,9 @@ struct ProjectParams {
     int tiles_x, tiles_y;
     Rec32* rec32;
     Rec64* rec64;
-    uint32_t* counts;  // [K + 1], pairs each kernel emits (counts[K] = 0)
+    int* tile_count;                 // [tiles] list lengths (zeroed before the launch)
+    unsigned long long* tile_lists;  // [tiles * cap] (order(zmin) << 32 | id), unsorted
+    int cap;                         // per-tile list capacity
     int* dropped_behind;
 };
 
@@ -147,7 +145,6 @@ struct ProjectParams {
 // exact FP64, the FP32 pre-filter record and the depth key for early exit.
 __global__ void project_kernel(ProjectParams p) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k == 0) p.counts[p.K] = 0;
     if (k >= p.K) return;
     const CameraP& c = p.cam;
 
@@ -185,7 +182,6 @@ __global__ void project_kernel(ProjectParams p) {
     q.top = q.left = 1.0f;
     q.bottom = q.right = 0.0f;  // empty box
     q.zmin = -FLT_MAX;
-    uint32_t count = 0;
 
     if (z <= kBehindCameraEps) {
         // behind the camera: dropped (tracer.cpp:52-56, blender.cpp:86)
@@ -194,7 +190,6 @@ __global__ void project_kernel(ProjectParams p) {
         q.ci_int = q.cj_int = 0;
         q.ci_frac = q.cj_frac = 0.0f;
         p.rec32[k] = q;
-        p.counts[k] = 0;
         return;
     }
 
@@ -296,52 +291,19 @@ __global__ void project_kernel(ProjectParams p) {
         q.left = __double2float_rd(fmax(left - ml, -1.0e30));
         q.right = __double2float_ru(fmin(right + mr, 1.0e30));
         int tr0, tr1, tc0, tc1;
-        if (box_tiles(q, c.H, c.W, p.tile, tr0, tr1, tc0, tc1))
-            count = (uint32_t)((tr1 - tr0 + 1) * (tc1 - tc0 + 1));
+        if (box_tiles(q, c.H, c.W, p.tile, tr0, tr1, tc0, tc1)) {
+            // bin: append (depth key, id) to every overlapped tile's list
+            const unsigned long long key = ((unsigned long long)float_order_bits(q.zmin) << 32) | (unsigned)k;
+            for (int tr = tr0; tr <= tr1; ++tr)
+                for (int tc = tc0; tc <= tc1; ++tc) {
+                    const int t = tr * p.tiles_x + tc;
+                    const int pos = atomicAdd(p.tile_count + t, 1);
+                    if (pos < p.cap) p.tile_lists[(size_t)t * p.cap + pos] = key;
+                }
+        }
     }
     p.rec32[k] = q;
-    p.counts[k] = count;
 }
 
-struct EmitParams {
-    int K;
-    const Rec32* rec32;
-    const uint32_t* offsets;  // exclusive scan of counts
-    SelP sel;
-    int H, W, tile, tiles_x;
-    unsigned long long* keys;  // (tile << 32) | order(zmin)
-    int* vals;
-};
-
-// K2a: one (tile, depth) key per (kernel, overlapped tile).
-__global__ void emit_pairs_kernel(EmitParams p) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= p.K) return;
-    const uint32_t off = p.offsets[k];
-    const uint32_t n = p.offsets[k + 1] - off;
-    if (n == 0) return;
-    const Rec32 q = p.rec32[k];
-    const unsigned long long zbits = float_order_bits(q.zmin);
-    int tr0, tr1, tc0, tc1;
-    box_tiles(q, p.H, p.W, p.tile, tr0, tr1, tc0, tc1);
-    uint32_t o = off;
-    for (int tr = tr0; tr <= tr1; ++tr)
-        for (int tc = tc0; tc <= tc1; ++tc) {
-            const unsigned long long tile = (unsigned long long)(tr * p.tiles_x + tc);
-            p.keys[o] = (tile << 32) | zbits;
-            p.vals[o] = k;
-            ++o;
-        }
-}
-
-// K2c: per-tile [start, end) ranges of the sorted pair list.
-__global__ void tile_ranges_kernel(uint32_t n, const unsigned long long* __restrict__ keys, int* __restrict__ start,
-                                   int* __restrict__ end) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int t = (int)(keys[i] >> 32);
-    if (i == 0 || (int)(keys[i - 1] >> 32) != t) start[t] = (int)i;
-    if (i + 1 == n || (int)(keys[i + 1] >> 32) != t) end[t] = (int)i + 1;
-}
 
 }  // namespace gvrk

@@ -106,6 +106,10 @@ class Context:
         self.check(self.lib.gvr_measure_pipe_peak(self.handle, 0 if kind == "fp32" else 1, ctypes.byref(out)))
         return out.value
 
+    def set_tile_capacity(self, cap: int) -> None:
+        """Test hook: per-tile candidate-list capacity (overflowing tiles stream every kernel)."""
+        self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
+
     def set_prefilter_guard(self, guard: float) -> None:
         self.check(self.lib.gvr_context_set_prefilter_guard(self.handle, float(guard)))
 

@@ -71,3 +71,16 @@ def test_forward_deterministic(ctx):
     b = gvr.render(g.scene, g.camera, g.cfg, ctx=ctx)
     for k in ("image", "alpha", "depth", "topk_idx", "topk_w"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_tile_list_overflow_path(golden, ctx):
+    """Tiles whose candidate list exceeds the capacity stream every kernel with
+    the same exact tests: outputs are bit-identical."""
+    a = gvr.render(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+    ctx.set_tile_capacity(8)
+    try:
+        b = gvr.render(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+    finally:
+        ctx.set_tile_capacity(4096)
+    assert np.array_equal(a.topk_idx, b.topk_idx)
+    assert np.array_equal(a.image, b.image)
