@@ -58,6 +58,7 @@ extern "C" {
 typedef struct gvr_context gvr_context;
 typedef struct gvr_scene gvr_scene;
 typedef struct gvr_tape gvr_tape;
+typedef struct gvr_graph gvr_graph;
 
 /* gvr::Camera (types.hpp:46-56) */
 typedef struct {
@@ -127,6 +128,16 @@ int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard);
  * Tiles whose list overflows stream every kernel through the same exact tests
  * (slower, same results); a small value exercises that path in tests. */
 int gvr_context_set_tile_capacity(gvr_context* ctx, int cap);
+
+/* ---- CUDA graphs ----------------------------------------------------------
+ * Capture a sequence of calls on the context stream (e.g. gvr_render +
+ * gvr_scalar_loss + gvr_backward with DEVICE pointers, after one uncaptured
+ * call has sized every buffer) and replay it with one launch. Calls that need
+ * a host synchronisation (host outputs, scene upload) fail while capturing. */
+int gvr_graph_begin(gvr_context* ctx);
+int gvr_graph_end(gvr_context* ctx, gvr_graph** out);
+int gvr_graph_launch(gvr_context* ctx, gvr_graph* graph);
+void gvr_graph_destroy(gvr_graph* graph);
 
 /* ---- scene: device-resident, validated once per upload ------------------ */
 int gvr_scene_create(gvr_context* ctx, gvr_scene** out);

@@ -16,6 +16,7 @@ from .types import (  # noqa: F401
 from .render import (  # noqa: F401
     Context,
     DeviceScene,
+    Graph,
     ForwardResult,
     GvrRuntimeError,
     Tape,
@@ -26,6 +27,7 @@ from .render import (  # noqa: F401
     render_into,
     render_with_tape,
     scalar_loss,
+    scalar_loss_into,
 )
 from .synthetic import make_bench_camera, make_bench_scene, make_orbit_camera  # noqa: F401
 from .scene_io import load_camera_json, load_scene_json  # noqa: F401

@@ -30,6 +30,10 @@ EXPORTED_SYMBOLS = (
     "gvr_measure_pipe_peak",
     "gvr_context_set_prefilter_guard",
     "gvr_context_set_tile_capacity",
+    "gvr_graph_begin",
+    "gvr_graph_end",
+    "gvr_graph_launch",
+    "gvr_graph_destroy",
     "gvr_scene_create",
     "gvr_scene_destroy",
     "gvr_scene_set",
@@ -118,6 +122,10 @@ def load() -> ctypes.CDLL:
         "gvr_measure_pipe_peak": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(dp)]),
         "gvr_context_set_prefilter_guard": (ctypes.c_int, [vp, dp]),
         "gvr_context_set_tile_capacity": (ctypes.c_int, [vp, ctypes.c_int]),
+        "gvr_graph_begin": (ctypes.c_int, [vp]),
+        "gvr_graph_end": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+        "gvr_graph_launch": (ctypes.c_int, [vp, vp]),
+        "gvr_graph_destroy": (None, [vp]),
         "gvr_scene_create": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
         "gvr_scene_destroy": (None, [vp]),
         "gvr_scene_set": (ctypes.c_int, [vp, vp, i32, i32, dp, vp, vp, vp]),

@@ -85,8 +85,15 @@ struct gvr_context {
     int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
     double guard = 0.02;
     int tile_cap = 4096;  // per-tile candidate-list capacity
+    bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
+};
+
+struct gvr_graph {
+    gvr_context* ctx = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
 };
 
 struct gvr_scene {
@@ -223,7 +230,7 @@ struct StageTimer {
     int stage;
     cudaEvent_t a = nullptr, b = nullptr;
     StageTimer(gvr_context* c, int st) : ctx(c), stage(st) {
-        if (ctx->timing) {
+        if (ctx->timing && !ctx->capturing) {
             a = take_event(ctx);
             b = take_event(ctx);
             cudaEventRecord(a, ctx->stream);
@@ -306,6 +313,8 @@ int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
 }
 
 int sync_and_check(gvr_context* ctx) {
+    if (ctx->capturing)
+        return set_err(ctx, GVR_ERR_RUNTIME, "operation needs a host synchronisation; not allowed while capturing a graph");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     if (!ctx->ev_pending.empty()) harvest_timings(ctx);
     return GVR_OK;
@@ -437,6 +446,47 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
     CUDA_TRY(ctx, cudaGetLastError());
     *flops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3);
     return GVR_OK;
+}
+
+// ---------------------------------------------------------------- CUDA graphs
+
+int gvr_graph_begin(gvr_context* ctx) {
+    if (!ctx || ctx->capturing) return GVR_ERR_RUNTIME;
+    if (int rc = sync_and_check(ctx)) return rc;
+    CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->capturing = true;
+    return GVR_OK;
+}
+
+int gvr_graph_end(gvr_context* ctx, gvr_graph** out) {
+    if (!ctx || !ctx->capturing || !out) return GVR_ERR_RUNTIME;
+    ctx->capturing = false;
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(ctx, cudaStreamEndCapture(ctx->stream, &g));
+    auto* gr = new gvr_graph();
+    gr->ctx = ctx;
+    gr->graph = g;
+    cudaError_t e = cudaGraphInstantiate(&gr->exec, g, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        delete gr;
+        return set_err(ctx, GVR_ERR_RUNTIME, "graph instantiation failed: %s", cudaGetErrorString(e));
+    }
+    *out = gr;
+    return GVR_OK;
+}
+
+int gvr_graph_launch(gvr_context* ctx, gvr_graph* g) {
+    if (!ctx || !g || g->ctx != ctx) return GVR_ERR_RUNTIME;
+    CUDA_TRY(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+    return GVR_OK;
+}
+
+void gvr_graph_destroy(gvr_graph* g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
 }
 
 int gvr_context_set_tile_capacity(gvr_context* ctx, int cap) {

@@ -106,6 +106,9 @@ class Context:
         self.check(self.lib.gvr_measure_pipe_peak(self.handle, 0 if kind == "fp32" else 1, ctypes.byref(out)))
         return out.value
 
+    def capture(self) -> "Graph":
+        return Graph(self)
+
     def set_tile_capacity(self, cap: int) -> None:
         """Test hook: per-tile candidate-list capacity (overflowing tiles stream every kernel)."""
         self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
@@ -121,6 +124,42 @@ class Context:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class Graph:
+    """A captured sequence of device-resident calls (``gvr_graph``), replayed
+    with one launch. Usage::
+
+        with ctx.capture() as g:        # after one uncaptured warm-up call
+            render_into(...); scalar_loss_into(...); backward_into(...)
+        g.launch()
+    """
+
+    def __init__(self, ctx: "Context"):
+        self.ctx = ctx
+        self.handle = None
+
+    def __enter__(self):
+        self.ctx.check(self.ctx.lib.gvr_graph_begin(self.ctx.handle))
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        h = ctypes.c_void_p()
+        rc = self.ctx.lib.gvr_graph_end(self.ctx.handle, ctypes.byref(h))
+        if exc_type is None:
+            self.ctx.check(rc)
+            self.handle = h
+        return False
+
+    def launch(self) -> None:
+        self.ctx.check(self.ctx.lib.gvr_graph_launch(self.ctx.handle, self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.ctx.lib.gvr_graph_destroy(self.handle)
         except Exception:
             pass
 
@@ -276,6 +315,16 @@ def render(scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(), thre
            weights: bool = True, ctx: Optional[Context] = None) -> RenderBuffers:
     """``gvr::render`` (blender.cpp:141-144)."""
     return render_with_tape(scene, camera, cfg, threads, weights=weights, ctx=ctx).buffers
+
+
+def scalar_loss_into(tape: Tape, target_image, target_alpha, w_image: float = 1.0, w_alpha: float = 1.0,
+                     loss_out=None, d_image_out=None, d_alpha_out=None) -> None:
+    """Low-level ``gvr_scalar_loss``: targets / outputs host or device; the
+    upstream gradient is also kept in the tape for ``backward_into(tape, None, None)``."""
+    ctx = tape.ctx
+    ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(target_image), _ptr(target_alpha),
+                                      float(w_image), float(w_alpha), _ptr(loss_out), _ptr(d_image_out),
+                                      _ptr(d_alpha_out)))
 
 
 def scalar_loss(tape: Tape, loss: ScalarLoss, *, want_grads: bool = True):

@@ -84,3 +84,44 @@ def test_tile_list_overflow_path(golden, ctx):
         ctx.set_tile_capacity(4096)
     assert np.array_equal(a.topk_idx, b.topk_idx)
     assert np.array_equal(a.image, b.image)
+
+
+def test_graph_replay_matches_eager(ctx):
+    """A captured render -> loss -> backward graph replays to the eager results."""
+    import torch
+
+    from conftest import Golden
+
+    g = Golden("texture_scene")
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device=dev)
+    torch.cuda.set_stream(stream)
+    s = g.scene
+    ds = gvr.DeviceScene(ctx).set_raw(s.size, s.attr_dim(), s.tau, torch.from_numpy(s.centers).to(dev),
+                                      torch.from_numpy(s.inv_cov).to(dev), torch.from_numpy(s.attr).to(dev))
+    tape = gvr.Tape(ctx)
+    h, w = g.camera.height, g.camera.width
+    img = torch.empty((h, w, s.attr_dim()), dtype=torch.float64, device=dev)
+    ti = torch.rand((h, w, s.attr_dim()), dtype=torch.float64, device=dev)
+    ta = torch.rand((h, w, 1), dtype=torch.float64, device=dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    gc = torch.empty((s.size, 3), dtype=torch.float64, device=dev)
+
+    def step():
+        gvr.render_into(ctx, ds, g.camera, g.cfg, tape, img)
+        gvr.scalar_loss_into(tape, ti, ta, 1.0, 1.0, loss)
+        gvr.backward_into(tape, None, None, gvr.GradFlags(), gc)
+
+    step()
+    ctx.synchronize()
+    eager_img, eager_loss, eager_gc = img.clone(), loss.clone(), gc.clone()
+    with ctx.capture() as graph:
+        step()
+    img.zero_()
+    gc.zero_()
+    graph.launch()
+    ctx.synchronize()
+    assert torch.equal(img, eager_img)
+    assert torch.allclose(loss, eager_loss, rtol=1e-14, atol=0)
+    assert torch.allclose(gc, eager_gc, rtol=1e-12, atol=1e-15)
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
