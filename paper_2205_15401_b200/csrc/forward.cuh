@@ -85,7 +85,7 @@ __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, un
     for (int size = 2; size <= pw; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int idx = threadIdx.x; idx < (pw >> 1); idx += blockDim.x) {
-                const int a = 2 * stride * (idx / stride) + (idx % stride), b = a + stride;
+                const int a = ((idx & ~(stride - 1)) << 1) | (idx & (stride - 1)), b = a + stride;
                 const unsigned long long ka = keys[a], kb = keys[b];
                 if ((ka > kb) == ((a & size) == 0)) {
                     keys[a] = kb;
