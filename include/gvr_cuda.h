@@ -159,6 +159,15 @@ void gvr_tape_destroy(gvr_tape* tape);
 int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
                const gvr_selection* cfg, gvr_tape* tape, const gvr_render_outputs* out);
 
+/* Tile-sharded render (C4: one large view split across GPUs): only tiles with
+ * tile_index % nshards == shard are rendered; every other pixel gets the
+ * empty-render outputs (0) and count 0, so the union over shards equals the
+ * full render bit for bit, and gvr_backward on a shard tape yields that
+ * shard's partial gradients (sum them across ranks). gvr_render = shard 0 of 1. */
+int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
+                     const gvr_selection* cfg, gvr_tape* tape, const gvr_render_outputs* out,
+                     int32_t shard, int32_t nshards);
+
 /* Copy out the taped selection (Tape::traced, grad.hpp:32): per pixel the selected
  * kernels ascending by (l, idx) with their FP64 (l, q, sigma); -1 / 0 padded.
  * Any pointer may be NULL. */
@@ -181,6 +190,17 @@ int gvr_scalar_loss(gvr_context* ctx, gvr_tape* tape, const double* target_image
  * upstream stored by gvr_scalar_loss. flags NULL = both paths on. */
 int gvr_backward(gvr_context* ctx, gvr_tape* tape, const double* d_image, const double* d_alpha,
                  const gvr_grad_flags* flags, const gvr_gradients* out);
+
+/* As gvr_backward but ADDS the gradients into the (device) outputs: the
+ * per-view accumulation of the fitting loop (fit.cpp:128-156). */
+int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* tape, const double* d_image, const double* d_alpha,
+                            const gvr_grad_flags* flags, const gvr_gradients* out);
+
+/* ---- fitting helpers ------------------------------------------------------ */
+/* AdamState::update (fit.cpp:20-42) on device arrays of n parameters; `step`
+ * is the 1-based step count used for the bias corrections. */
+int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
+                  int64_t step, double lr, double beta1, double beta2, double eps);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ from .render import (  # noqa: F401
     ForwardResult,
     GvrRuntimeError,
     Tape,
+    adam_step,
     backward,
     backward_into,
     default_context,

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgvr_cuda.so")
+LIB_PATH = os.environ.get("GVR_LIB_PATH") or os.path.join(HERE, "libgvr_cuda.so")  # override: A/B builds
 
 GVR_OK = 0
 GVR_ERR_VALIDATION = 1
@@ -42,10 +42,13 @@ EXPORTED_SYMBOLS = (
     "gvr_tape_create",
     "gvr_tape_destroy",
     "gvr_render",
+    "gvr_render_shard",
     "gvr_tape_traced",
     "gvr_tape_shape",
     "gvr_scalar_loss",
     "gvr_backward",
+    "gvr_backward_accumulate",
+    "gvr_adam_step",
 )
 
 
@@ -140,6 +143,11 @@ def load() -> ctypes.CDLL:
                                           ctypes.POINTER(i32)]),
         "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),
         "gvr_backward": (ctypes.c_int, [vp, vp, vp, vp, ctypes.POINTER(GvrGradFlags), ctypes.POINTER(GvrGradients)]),
+        "gvr_backward_accumulate": (ctypes.c_int, [vp, vp, vp, vp, ctypes.POINTER(GvrGradFlags),
+                                                   ctypes.POINTER(GvrGradients)]),
+        "gvr_render_shard": (ctypes.c_int, [vp, vp, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection), vp,
+                                            ctypes.POINTER(GvrRenderOutputs), i32, i32]),
+        "gvr_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

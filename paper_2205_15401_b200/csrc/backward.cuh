@@ -282,6 +282,26 @@ __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const dou
     }
 }
 
+// dst += src (gradient accumulation across views, fit.cpp:153).
+__global__ void axpy_kernel(long long n, const double* __restrict__ src, double* __restrict__ dst) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
+// AdamState::update (fit.cpp:20-42), bias corrections from the host in FP64.
+__global__ void adam_kernel(long long n, double* __restrict__ params, const double* __restrict__ grads,
+                            double* __restrict__ m, double* __restrict__ v, double lr, double beta1, double beta2,
+                            double eps, double bc1, double bc2) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double g = grads[i];
+    const double mi = beta1 * m[i] + (1.0 - beta1) * g;
+    const double vi = beta2 * v[i] + (1.0 - beta2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    params[i] -= lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+}
+
 // weight_store / traced copy-out: expand the compact per-pixel lists to K'-padded arrays.
 __global__ void expand_topk_kernel(long long P, int kp, const int* __restrict__ topk, const int* __restrict__ count,
                                    const double* __restrict__ topk_w, int* __restrict__ out_idx,

@@ -601,16 +601,18 @@ __global__ void clear_empty_tiles_kernel(CameraP cam, int Dc, int tiles_x, const
 }
 
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
-// log-spaced cost buckets, descending). Zero-cost tiles are dropped and
-// *n_out receives the number kept. Cost = icost[t] (list length) or fcost[t].
+// log-spaced cost buckets, descending). Zero-cost tiles and tiles of other
+// shards (t % nshards != shard) are dropped; *n_out receives the number kept.
+// Cost = icost[t] (list length) or fcost[t].
 __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
                                                            const float* __restrict__ fcost, int* __restrict__ order,
-                                                           int* __restrict__ n_out) {
+                                                           int* __restrict__ n_out, int shard, int nshards) {
     __shared__ int hist[256];
     __shared__ int offs[256];
     for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     auto bucket_of = [&](int t) -> int {
+        if (t % nshards != shard) return -1;  // tile owned by another rank (C4 tile sharding)
         const float c = fcost ? fcost[t] : (float)icost[t];
         if (!(c > 0.0f)) return -1;
         const int b = (int)(__log2f(c + 1.0f) * 8.0f);

@@ -285,7 +285,7 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     LAUNCH_CHECK(ctx);
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b, 0, 1);
     }
     LAUNCH_CHECK(ctx);
     {
@@ -337,6 +337,9 @@ __global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
 }
 
 }  // namespace
+
+static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
+                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate);
 
 extern "C" {
 
@@ -445,6 +448,21 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
     cudaFree(out);
     CUDA_TRY(ctx, cudaGetLastError());
     *flops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3);
+    return GVR_OK;
+}
+
+// ---------------------------------------------------------------- ADAM (fit.cpp:20-42)
+
+int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
+                  int64_t step, double lr, double beta1, double beta2, double eps) {
+    if (!ctx || step < 1 || n < 0) return GVR_ERR_RUNTIME;
+    if (n == 0) return GVR_OK;
+    if (!is_device_ptr(params) || !is_device_ptr(grads) || !is_device_ptr(m) || !is_device_ptr(v))
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step needs device pointers");
+    const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
+    const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
+    adam_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, params, grads, m, v, lr, beta1, beta2, eps, bc1, bc2);
+    LAUNCH_CHECK(ctx);
     return GVR_OK;
 }
 
@@ -597,7 +615,14 @@ int gvr_tape_shape(const gvr_tape* t, int32_t* h, int32_t* w, int32_t* kp, int32
 
 int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera, const gvr_selection* cfg,
                gvr_tape* tape, const gvr_render_outputs* out) {
+    return gvr_render_shard(ctx, scene, camera, cfg, tape, out, 0, 1);
+}
+
+int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera, const gvr_selection* cfg,
+                     gvr_tape* tape, const gvr_render_outputs* out, int32_t shard, int32_t nshards) {
     if (!ctx || !scene || !tape) return GVR_ERR_RUNTIME;
+    if (nshards < 1 || shard < 0 || shard >= nshards)
+        return set_err(ctx, GVR_ERR_RUNTIME, "bad tile shard %d of %d", shard, nshards);
     if (tape->ctx != ctx || scene->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!scene->valid) return set_err(ctx, GVR_ERR_VALIDATION, "scene has not been validated");
     if (int rc = validate_camera(ctx, camera)) return rc;
@@ -696,7 +721,7 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     // K3 over the non-empty tiles, longest list first
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards);
     }
     LAUNCH_CHECK(ctx);
     FwdParams fp;
@@ -860,6 +885,18 @@ int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, c
 
 int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
                  const gvr_grad_flags* flags, const gvr_gradients* out) {
+    return backward_impl(ctx, t, d_image, d_alpha, flags, out, false);
+}
+
+int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
+                            const gvr_grad_flags* flags, const gvr_gradients* out) {
+    return backward_impl(ctx, t, d_image, d_alpha, flags, out, true);
+}
+
+}  // extern "C"
+
+static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
+                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate) {
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
     if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
         return set_err(ctx, GVR_ERR_RUNTIME, "the scene changed after the forward render");
@@ -953,6 +990,20 @@ int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const dou
         }
         LAUNCH_CHECK(ctx);
     }
+    if (out && accumulate) {
+        const double* srcs[5] = {t->d_center.as<double>(), t->d_inv_cov.as<double>(), t->d_attr.as<double>(),
+                                 t->d_rt.as<double>(), t->d_rt.as<double>() + 9};
+        double* dsts[5] = {out->d_center, out->d_inv_cov, out->d_attr, out->d_rotation, out->d_translation};
+        const long long ns[5] = {3ll * K, 9ll * K, (long long)D * K, 9, 3};
+        for (int b = 0; b < 5; ++b) {
+            if (!dsts[b] || ns[b] == 0) continue;
+            if (!is_device_ptr(dsts[b]))
+                return set_err(ctx, GVR_ERR_RUNTIME, "gvr_backward_accumulate needs device output pointers");
+            axpy_kernel<<<blocks_for(ns[b], 256), 256, 0, ctx->stream>>>(ns[b], srcs[b], dsts[b]);
+            LAUNCH_CHECK(ctx);
+        }
+        return GVR_OK;
+    }
     if (out) {
         bool host = false;
         int rc;
@@ -965,5 +1016,7 @@ int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const dou
     }
     return GVR_OK;
 }
+
+extern "C" {
 
 }  // extern "C"

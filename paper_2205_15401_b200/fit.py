@@ -1,0 +1,137 @@
+"""Device fitting loop.
+
+Mirrors ``gvr::loss_and_grad`` + ``AdamState::update`` of ``fit_shape``
+(/root/reference/proj/src/fit.cpp:117-158, :20-42, :176-265) with everything on
+the GPU and the views sharded across ranks:
+
+  per iteration, on each rank, for each of its views v:
+      render_with_tape(scene, camera_v)                      (gvr_render)
+      loss_v = rgb |img - t|^2 / #img + sil |alpha - t_a|^2 / #alpha, scaled 1/#views
+      d_image = 2 rgb (img - t) / (#img #views), d_alpha likewise    (gvr_scalar_loss)
+      gradients += backward(tape, d_image, d_alpha)         (gvr_backward_accumulate)
+  all-reduce(sum) of [d_center | d_attr | loss] across ranks (NCCL over NVLink;
+  the only collective of the render path)
+  ADAM on [centers | attrs] (gvr_adam_step), identical on every rank.
+
+Differences from fit_shape: every view is used every iteration (the C5 config:
+32 views, no random batch sampling) and the edge / Laplacian regularisers are
+not applied (rgb + silhouette terms only).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .distributed import allreduce_gradients, shard_views
+from .render import Context, DeviceScene, Tape, adam_step, backward_into, render_into, scalar_loss_into
+from .types import Camera, GaussianScene, GradFlags, SelectionConfig
+
+
+@dataclass
+class AdamConfig:
+    """``gvr::AdamConfig`` (fit.hpp:18-23)."""
+
+    lr: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+class Fitter:
+    """Shape/texture fitting of centers and attributes against target views."""
+
+    def __init__(self, ctx: Context, scene: GaussianScene, views: Sequence[Tuple[Camera, np.ndarray, np.ndarray]],
+                 cfg: SelectionConfig = SelectionConfig(), rgb_weight: float = 1.0, silhouette_weight: float = 1.0,
+                 adam: AdamConfig = AdamConfig(), rank: int = 0, world: int = 1, device=None):
+        import torch
+
+        self.torch = torch
+        self.ctx = ctx
+        self.cfg = cfg
+        self.adam = adam
+        self.rank, self.world = rank, world
+        self.dev = device if device is not None else torch.device(f"cuda:{ctx.device}")
+        self.K, self.D = scene.size, scene.attr_dim()
+        self.tau = scene.tau
+        k3 = 3 * self.K
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.params = torch.cat([torch.from_numpy(scene.centers.reshape(-1)), torch.from_numpy(scene.attr.reshape(-1))]).to(**f64)
+        self.centers = self.params[:k3].view(self.K, 3)
+        self.attr = self.params[k3:].view(self.K, self.D)
+        self.inv_cov = torch.from_numpy(scene.inv_cov).to(**f64).contiguous()
+        self.grads = torch.zeros_like(self.params)
+        self.g_center = self.grads[:k3]
+        self.g_attr = self.grads[k3:]
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step_count = 0
+        self.n_views = len(views)
+        self.mine = shard_views(self.n_views, rank, world)
+        self.views: List[Tuple[Camera, object, object, float, float]] = []
+        for idx in self.mine:
+            cam, ti, ta = views[idx]
+            n_img = float(np.asarray(ti).size)
+            n_alpha = float(np.asarray(ta).size)
+            w_img = 2.0 * rgb_weight / (n_img * self.n_views)
+            w_alpha = 2.0 * silhouette_weight / (n_alpha * self.n_views)
+            self.views.append((cam, torch.as_tensor(np.ascontiguousarray(ti)).to(**f64),
+                               torch.as_tensor(np.ascontiguousarray(ta)).to(**f64), w_img, w_alpha))
+        self.loss_acc = torch.zeros(1, **f64)
+        self.loss_tmp = torch.zeros(1, **f64)
+        self.dscene = DeviceScene(ctx)
+        self.tape = Tape(ctx)
+        # torch work (accumulations, NCCL) on the context's stream, ordered with our kernels
+        self.stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device=self.dev)
+
+    def loss_and_grad(self) -> None:
+        """Accumulate this rank's loss and gradients (device, asynchronous)."""
+        with self.torch.cuda.stream(self.stream):
+            self._loss_and_grad()
+
+    def _loss_and_grad(self) -> None:
+        self.dscene.set_raw(self.K, self.D, self.tau, self.centers, self.inv_cov, self.attr)
+        self.grads.zero_()
+        self.loss_acc.zero_()
+        for cam, ti, ta, w_img, w_alpha in self.views:
+            render_into(self.ctx, self.dscene, cam, self.cfg, self.tape)
+            scalar_loss_into(self.tape, ti, ta, w_img, w_alpha, self.loss_tmp)
+            self.loss_acc += self.loss_tmp
+            backward_into(self.tape, None, None, GradFlags(), d_center=self.g_center, d_attr=self.g_attr,
+                          accumulate=True)
+
+    def step(self, group=None) -> None:
+        """One fit_shape iteration: loss_and_grad, NCCL all-reduce, ADAM."""
+        with self.torch.cuda.stream(self.stream):
+            self._loss_and_grad()
+            allreduce_gradients([self.grads, self.loss_acc], group)
+            self.step_count += 1
+            adam_step(self.ctx, self.params, self.grads, self.m, self.v, self.step_count, self.adam.lr,
+                      self.adam.beta1, self.adam.beta2, self.adam.eps)
+
+    def loss(self) -> float:
+        self.stream.synchronize()
+        return float(self.loss_acc.item())
+
+    def scene(self) -> GaussianScene:
+        return GaussianScene(self.centers.cpu().numpy().copy(), self.inv_cov.cpu().numpy().copy(),
+                             self.attr.cpu().numpy().copy(), self.tau)
+
+
+def make_fit_views(target: GaussianScene, n_views: int, size: int, cfg: SelectionConfig = SelectionConfig(),
+                   ctx: Optional[Context] = None):
+    """Target images of `target` from n orbit cameras (shapes.cpp:118-141),
+    rendered with this library (the reference renders its targets the same way,
+    tools/gvr_main.cpp:92-109)."""
+    from .render import default_context, render
+    from .synthetic import make_orbit_camera
+
+    ctx = ctx or default_context()
+    center = target.centers.mean(axis=0)
+    views = []
+    for v in range(n_views):
+        cam = make_orbit_camera(2 * np.pi * v / n_views, 0.3, 4.0, center, size, size, 1.6 * size)
+        buf = render(target, cam, cfg, weights=False, ctx=ctx)
+        views.append((cam, buf.image, buf.alpha))
+    return views

@@ -282,12 +282,13 @@ def _as_device_scene(scene, ctx: Context) -> DeviceScene:
 
 
 def render_into(ctx: Context, dscene: DeviceScene, camera: Camera, cfg: SelectionConfig, tape: Tape,
-                image=None, alpha=None, depth=None, topk_idx=None, topk_w=None) -> None:
-    """Low-level forward: outputs written into caller buffers (host or device, any may be None)."""
+                image=None, alpha=None, depth=None, topk_idx=None, topk_w=None, shard=(0, 1)) -> None:
+    """Low-level forward: outputs written into caller buffers (host or device, any may be None).
+    ``shard=(r, n)`` renders only tiles with index % n == r (C4 tile sharding)."""
     out = _lib.GvrRenderOutputs(_ptr(image), _ptr(alpha), _ptr(depth), _ptr(topk_idx), _ptr(topk_w))
     cam_c, sel_c = _camera_c(camera), _selection_c(cfg)
-    ctx.check(ctx.lib.gvr_render(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c), tape.handle,
-                                 ctypes.byref(out)))
+    ctx.check(ctx.lib.gvr_render_shard(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c),
+                                       tape.handle, ctypes.byref(out), int(shard[0]), int(shard[1])))
     tape.scene, tape.camera, tape.cfg = dscene, camera, cfg
 
 
@@ -344,13 +345,21 @@ def scalar_loss(tape: Tape, loss: ScalarLoss, *, want_grads: bool = True):
 
 
 def backward_into(tape: Tape, d_image, d_alpha, flags: GradFlags = GradFlags(), d_center=None, d_inv_cov=None,
-                  d_attr=None, d_rotation=None, d_translation=None) -> None:
-    """Low-level backward: gradients written into caller buffers (host or device, any may be None)."""
+                  d_attr=None, d_rotation=None, d_translation=None, accumulate: bool = False) -> None:
+    """Low-level backward: gradients written into caller buffers (host or device, any may
+    be None); ``accumulate=True`` adds into device buffers (per-view sums of a fit)."""
     ctx = tape.ctx
     f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
     g = _lib.GvrGradients(_ptr(d_center), _ptr(d_inv_cov), _ptr(d_attr), _ptr(d_rotation), _ptr(d_translation))
-    ctx.check(ctx.lib.gvr_backward(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f),
-                                   ctypes.byref(g)))
+    fn = ctx.lib.gvr_backward_accumulate if accumulate else ctx.lib.gvr_backward
+    ctx.check(fn(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f), ctypes.byref(g)))
+
+
+def adam_step(ctx: Context, params, grads, m, v, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
+              eps: float = 1e-8) -> None:
+    """``AdamState::update`` (fit.cpp:20-42) on device tensors (FP64, same length)."""
+    ctx.check(ctx.lib.gvr_adam_step(ctx.handle, _ptr(params), _ptr(grads), _ptr(m), _ptr(v), int(params.numel()),
+                                    int(step), float(lr), float(beta1), float(beta2), float(eps)))
 
 
 def backward(tape, d_image, d_alpha, flags: GradFlags = GradFlags()) -> GradientBundle:

@@ -1,0 +1,116 @@
+"""GPU: the fitting loop (C5) and tile sharding (C4) against the oracle.
+
+* one Fitter iteration's loss and summed per-view gradients == the oracle's
+  loss_and_grad semantics (fit.cpp:117-158) on the same inputs;
+* gvr_adam_step == AdamState::update (fit.cpp:20-42);
+* fitting reduces the loss (test_fit.cpp spirit);
+* the union of tile-sharded renders equals the full render bit for bit and the
+  shard gradients sum to the full gradient (C4 invariants).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2205_15401_b200 as gvr
+from conftest import assert_grad_close
+from paper_2205_15401_b200.fit import AdamConfig, Fitter
+from paper_2205_15401_b200.types import GaussianScene, SelectionConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def _views(target, n, size):
+    views = []
+    for v in range(n):
+        cam = gvr.make_orbit_camera(2 * np.pi * v / n, 0.3, 4.0, (0, 0, 4), size, size, 1.6 * size)
+        o = oracle.port_render(target, cam, SelectionConfig(), threads=4)
+        views.append((cam, o["image"], o["alpha"]))
+    return views
+
+
+def test_fitter_loss_and_grad_matches_oracle(ctx):
+    scene = gvr.make_bench_scene(1000)
+    target = scene.copy()
+    target.attr = target.attr[:, ::-1].copy()  # recoloured target
+    target.centers = target.centers * 1.02
+    views = _views(target, 4, 48)
+    fitter = Fitter(ctx, scene, views, rgb_weight=1.0, silhouette_weight=0.5)
+    fitter.loss_and_grad()
+    loss = fitter.loss()
+    g_center = fitter.g_center.cpu().numpy().reshape(-1, 3)
+    g_attr = fitter.g_attr.cpu().numpy().reshape(-1, 3)
+    want_loss, want_c, want_a = 0.0, np.zeros_like(g_center), np.zeros_like(g_attr)
+    for cam, ti, ta in views:
+        o = oracle.port_render(scene, cam, SelectionConfig(), threads=4)
+        di = 2.0 * (o["image"] - ti) / (ti.size * len(views))
+        da = 2.0 * 0.5 * (o["alpha"] - ta) / (ta.size * len(views))
+        want_loss += (((o["image"] - ti) ** 2).sum() / ti.size + 0.5 * ((o["alpha"] - ta) ** 2).sum() / ta.size) / len(views)
+        g = oracle.port_backward(scene, cam, SelectionConfig(), di, da, threads=4)
+        want_c += g["d_center"]
+        want_a += g["d_attr"]
+    assert loss == pytest.approx(want_loss, rel=1e-6)
+    assert_grad_close(g_center, want_c, what="fit d_center")
+    assert_grad_close(g_attr, want_a, what="fit d_attr")
+
+
+def test_adam_step_matches_reference_formula(ctx):
+    rng = np.random.default_rng(0)
+    p = rng.normal(size=1000)
+    g = rng.normal(size=1000)
+    m = rng.normal(size=1000) * 0.1
+    v = np.abs(rng.normal(size=1000)) * 0.1
+    dev = torch.device("cuda:0")
+    tp, tg, tm, tv = (torch.tensor(a, device=dev) for a in (p, g, m, v))
+    gvr.adam_step(ctx, tp, tg, tm, tv, 3, 0.01)
+    ctx.synchronize()
+    b1, b2, lr, eps = 0.9, 0.999, 0.01, 1e-8
+    m2 = b1 * m + (1 - b1) * g
+    v2 = b2 * v + (1 - b2) * g * g
+    p2 = p - lr * (m2 / (1 - b1**3)) / (np.sqrt(v2 / (1 - b2**3)) + eps)
+    np.testing.assert_allclose(tp.cpu().numpy(), p2, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(tm.cpu().numpy(), m2, rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(tv.cpu().numpy(), v2, rtol=1e-13, atol=1e-16)
+
+
+def test_fitting_reduces_loss(ctx):
+    scene = gvr.make_bench_scene(1000)
+    target = scene.copy()
+    target.attr = np.tile([0.2, 0.6, 0.9], (scene.size, 1))
+    views = _views(target, 4, 48)
+    fitter = Fitter(ctx, scene, views, adam=AdamConfig(lr=0.02))
+    fitter.loss_and_grad()
+    first = fitter.loss()
+    for _ in range(15):
+        fitter.step()
+    fitter.loss_and_grad()
+    assert fitter.loss() < 0.5 * first
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 8])
+def test_tile_shards_union_equals_full_render(ctx, nshards):
+    scene = gvr.make_bench_scene(20000)
+    cam = gvr.make_orbit_camera(0.4, 0.3, 4.0, (0, 0, 4), 200, 232, 320.0)
+    cfg = SelectionConfig()
+    ds = gvr.DeviceScene(ctx).set(scene)
+    full_tape = gvr.Tape(ctx)
+    h, w = cam.height, cam.width
+    img, alpha = np.empty((h, w, 3)), np.empty((h, w, 1))
+    gvr.render_into(ctx, ds, cam, cfg, full_tape, img, alpha)
+    rng = np.random.default_rng(1)
+    di, da = rng.uniform(-1, 1, (h, w, 3)), rng.uniform(-1, 1, (h, w, 1))
+    gfull = np.empty((scene.size, 3))
+    gvr.backward_into(full_tape, di, da, gvr.GradFlags(), d_center=gfull)
+    u_img, u_alpha, g_sum = np.zeros_like(img), np.zeros_like(alpha), np.zeros_like(gfull)
+    for r in range(nshards):
+        tape = gvr.Tape(ctx)
+        si, sa = np.empty_like(img), np.empty_like(alpha)
+        gvr.render_into(ctx, ds, cam, cfg, tape, si, sa, shard=(r, nshards))
+        u_img += si
+        u_alpha += sa
+        gs = np.empty_like(gfull)
+        gvr.backward_into(tape, di, da, gvr.GradFlags(), d_center=gs)
+        g_sum += gs
+    assert np.array_equal(u_img, img)
+    assert np.array_equal(u_alpha, alpha)
+    np.testing.assert_allclose(g_sum, gfull, rtol=1e-9, atol=1e-12 * np.abs(gfull).max())
