@@ -200,6 +200,59 @@ def port_coarse_boxes(scene, cam, cfg):
     return box, dropped.value
 
 
+def _u8p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte))
+
+
+def port_sample_attributes(scene, cam, cfg, observed, normalized=False, threads: int = 0):
+    """C-port ``sample_attributes`` (sampler.cpp:11-51): (attrs [K,C], support [K], masked [K] bool)."""
+    lib = port_lib()
+    c, s, a = _scene_arrays(scene)
+    obs = np.ascontiguousarray(observed, dtype=np.float64)
+    ch = obs.shape[2] if obs.ndim == 3 else 1
+    k = scene.size
+    attrs, support, masked = np.zeros((k, ch)), np.zeros(k), np.zeros(k, dtype=np.uint8)
+    camc, selc = _cam_c(cam), _sel_c(cfg)
+    rc = lib.gvro_sample_attributes(k, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s), _ptr(a),
+                                    ctypes.byref(camc), ctypes.byref(selc), threads, _ptr(obs), int(obs.shape[0]),
+                                    int(obs.shape[1]), ch, int(bool(normalized)), _ptr(attrs), _ptr(support),
+                                    _u8p(masked))
+    if rc:
+        raise OracleError(rc, lib.gvro_last_error().decode())
+    return attrs, support, masked.astype(bool)
+
+
+def port_pixel_helpers(scene, cam, cfg, t, eps=1e-8, threads: int = 0):
+    """C-port per-pixel ``transmittance_at`` at depth t[p] and ``normalized_weights`` (blender.cpp:19-25, 55-62)."""
+    lib = port_lib()
+    c, s, a = _scene_arrays(scene)
+    h, w, kp = int(cam.height), int(cam.width), int(cfg.k_prime)
+    tt = np.ascontiguousarray(t, dtype=np.float64).reshape(h, w)
+    trans, nw = np.zeros((h, w)), np.zeros((h, w, kp))
+    camc, selc = _cam_c(cam), _sel_c(cfg)
+    rc = lib.gvro_pixel_helpers(scene.size, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s), _ptr(a),
+                                ctypes.byref(camc), ctypes.byref(selc), threads, _ptr(tt), _ptr(trans),
+                                ctypes.c_double(eps), _ptr(nw))
+    if rc:
+        raise OracleError(rc, lib.gvro_last_error().decode())
+    return trans, nw
+
+
+def port_shade_lambert(cam, normals, alpha, depth, light_pos, light_color):
+    """C-port ``shade_lambert`` (blender.cpp:146-172)."""
+    lib = port_lib()
+    h, w = int(cam.height), int(cam.width)
+    n = np.ascontiguousarray(normals, dtype=np.float64)
+    al = np.ascontiguousarray(alpha, dtype=np.float64)
+    de = np.ascontiguousarray(depth, dtype=np.float64)
+    lp = np.ascontiguousarray(light_pos, dtype=np.float64)
+    lc = np.ascontiguousarray(light_color, dtype=np.float64)
+    out = np.zeros((h, w, 3))
+    camc = _cam_c(cam)
+    lib.gvro_shade_lambert(ctypes.byref(camc), _ptr(n), _ptr(al), _ptr(de), _ptr(lp), _ptr(lc), _ptr(out))
+    return out
+
+
 # ---------------------------------------------------------------- the reference build
 
 
@@ -307,3 +360,59 @@ def ref_make_orbit_camera(azimuth, elevation, distance, target, height, width, f
     _ref_call("gvr_ref_make_orbit_camera", ctypes.c_double(azimuth), ctypes.c_double(elevation),
               ctypes.c_double(distance), _ptr(t), int(height), int(width), ctypes.c_double(focal), _ptr(c17))
     return c17
+
+
+def ref_sample_attributes(scene, cam, cfg, observed, normalized=False, threads: int = 0):
+    """Reference ``gvr::sample_attributes`` (sampler.cpp:11-51)."""
+    c, s, a = _scene_arrays(scene)
+    obs = np.ascontiguousarray(observed, dtype=np.float64)
+    ch = obs.shape[2] if obs.ndim == 3 else 1
+    k = scene.size
+    attrs, support, masked = np.zeros((k, ch)), np.zeros(k), np.zeros(k, dtype=np.uint8)
+    c17 = _cam17(cam)
+    _ref_call("gvr_ref_sample_attributes", k, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s), _ptr(a),
+              _ptr(c17), ctypes.c_double(cfg.eta), int(cfg.k_prime), int(bool(cfg.coarse_enabled)),
+              int(cfg.coarse_downsample), threads, _ptr(obs), int(obs.shape[0]), int(obs.shape[1]), ch,
+              int(bool(normalized)), _ptr(attrs), _ptr(support), _u8p(masked))
+    return attrs, support, masked.astype(bool)
+
+
+def ref_resynthesize(scene, cam, cfg, attrs, masked, threads: int = 0) -> dict:
+    """Reference ``gvr::resynthesize`` (sampler.cpp:53-66): image, alpha, depth."""
+    c, s, a = _scene_arrays(scene)
+    at = np.ascontiguousarray(attrs, dtype=np.float64)
+    mk = np.ascontiguousarray(masked, dtype=np.uint8)
+    h, w = int(cam.height), int(cam.width)
+    out = dict(image=np.zeros((h, w, max(at.shape[1], 1))), alpha=np.zeros((h, w, 1)), depth=np.zeros((h, w, 1)))
+    c17 = _cam17(cam)
+    _ref_call("gvr_ref_resynthesize", scene.size, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s),
+              _ptr(a), _ptr(c17), ctypes.c_double(cfg.eta), int(cfg.k_prime), int(bool(cfg.coarse_enabled)),
+              int(cfg.coarse_downsample), threads, int(at.shape[0]), int(at.shape[1]), _ptr(at), _u8p(mk),
+              _ptr(out["image"]), _ptr(out["alpha"]), _ptr(out["depth"]))
+    return out
+
+
+def ref_pixel_helpers(scene, cam, cfg, t, eps=1e-8, threads: int = 0):
+    """Reference per-pixel ``transmittance_at`` / ``normalized_weights`` (blender.cpp:19-25, 55-62)."""
+    c, s, a = _scene_arrays(scene)
+    h, w, kp = int(cam.height), int(cam.width), int(cfg.k_prime)
+    tt = np.ascontiguousarray(t, dtype=np.float64).reshape(h, w)
+    trans, nw = np.zeros((h, w)), np.zeros((h, w, kp))
+    c17 = _cam17(cam)
+    _ref_call("gvr_ref_pixel_helpers", scene.size, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s),
+              _ptr(a), _ptr(c17), ctypes.c_double(cfg.eta), int(cfg.k_prime), int(bool(cfg.coarse_enabled)),
+              int(cfg.coarse_downsample), threads, _ptr(tt), _ptr(trans), ctypes.c_double(eps), _ptr(nw))
+    return trans, nw
+
+
+def ref_shade_lambert(cam, normals, alpha, depth, light_pos, light_color):
+    """Reference ``gvr::shade_lambert`` (blender.cpp:146-172)."""
+    h, w = int(cam.height), int(cam.width)
+    n = np.ascontiguousarray(normals, dtype=np.float64)
+    al = np.ascontiguousarray(alpha, dtype=np.float64)
+    de = np.ascontiguousarray(depth, dtype=np.float64)
+    lp = np.ascontiguousarray(light_pos, dtype=np.float64)
+    lc = np.ascontiguousarray(light_color, dtype=np.float64)
+    out = np.zeros((h, w, 3))
+    _ref_call("gvr_ref_shade_lambert", _ptr(_cam17(cam)), _ptr(n), _ptr(al), _ptr(de), _ptr(lp), _ptr(lc), _ptr(out))
+    return out

@@ -866,3 +866,122 @@ int gvro_coarse_boxes(int K, int D, double tau, const double* centers, const dou
     free(cs);
     return 0;
 }
+
+/* ------------------------------------------------------------------ sampler + helpers */
+
+/* sample_attributes (src/sampler.cpp:11-51): render, then per pixel in row-major
+ * order scatter W (or W / max(sum W, kSupportEps) when normalized) into the
+ * support and the weighted attribute sums; kernels with support < 1e-8
+ * (include/gvr/sampler.hpp:18) are zeroed and masked. */
+int gvro_sample_attributes(int K, int D, double tau, const double* centers, const double* inv_cov,
+                           const double* attr, const gvro_camera* cam, const gvro_selection* cfg, int threads,
+                           const double* observed, int obs_h, int obs_w, int channels, int normalized,
+                           double* attrs, double* support, unsigned char* masked) {
+    if (obs_h != cam->height || obs_w != cam->width) return fail("observed image size does not match the camera");
+    const int Dc = D > 1 ? D : 1;
+    const size_t P = (size_t)cam->height * cam->width;
+    double* image = malloc(sizeof(double) * P * Dc);
+    double* alpha = malloc(sizeof(double) * P);
+    double* depth = malloc(sizeof(double) * P);
+    forward_state_t st;
+    const int rc = render_core(K, D, tau, centers, inv_cov, attr, cam, cfg, threads, image, alpha, depth, &st);
+    free(image);
+    free(alpha);
+    free(depth);
+    if (rc) return rc;
+    memset(attrs, 0, sizeof(double) * (size_t)K * channels);
+    memset(support, 0, sizeof(double) * (size_t)K);
+    for (size_t p = 0; p < P; ++p) {
+        const int n = st.count[p];
+        double denom = 0.0;
+        if (normalized) {
+            for (int s = 0; s < n; ++s) denom += st.weights[p * st.kp + s];
+            denom = denom > 1e-8 ? denom : 1e-8;
+        }
+        for (int s = 0; s < n; ++s) {
+            const int k = st.tape[p * st.kp + s].idx;
+            const double w = st.weights[p * st.kp + s];
+            const double ww = normalized ? w / denom : w;
+            support[k] += ww;
+            for (int c = 0; c < channels; ++c) attrs[(size_t)channels * k + c] += ww * observed[p * channels + c];
+        }
+    }
+    for (int k = 0; k < K; ++k) {
+        if (support[k] < 1e-8) {
+            for (int c = 0; c < channels; ++c) attrs[(size_t)channels * k + c] = 0.0;
+            masked[k] = 1;
+        } else {
+            for (int c = 0; c < channels; ++c) attrs[(size_t)channels * k + c] /= support[k];
+            masked[k] = 0;
+        }
+    }
+    free_state(&st);
+    return 0;
+}
+
+/* Per pixel: transmittance_at (src/blender.cpp:19-25) over the pixel's selected
+ * traced kernels at depth t[p], and normalized_weights (src/blender.cpp:55-62)
+ * of its weights (K'-padded with 0). Outputs nullable. */
+int gvro_pixel_helpers(int K, int D, double tau, const double* centers, const double* inv_cov,
+                       const double* attr, const gvro_camera* cam, const gvro_selection* cfg, int threads,
+                       const double* t, double* trans_out, double eps, double* norm_w) {
+    const int Dc = D > 1 ? D : 1;
+    const size_t P = (size_t)cam->height * cam->width;
+    double* image = malloc(sizeof(double) * P * Dc);
+    double* alpha = malloc(sizeof(double) * P);
+    double* depth = malloc(sizeof(double) * P);
+    forward_state_t st;
+    const int rc = render_core(K, D, tau, centers, inv_cov, attr, cam, cfg, threads, image, alpha, depth, &st);
+    free(image);
+    free(alpha);
+    free(depth);
+    if (rc) return rc;
+    for (size_t p = 0; p < P; ++p) {
+        const int n = st.count[p];
+        if (trans_out) {
+            double acc = 0.0;
+            for (int s = 0; s < n; ++s) {
+                const traced_t* k = &st.tape[p * st.kp + s];
+                acc += exp(k->q) * normal_cdf((t[p] - k->l) / k->sigma);
+            }
+            trans_out[p] = exp(-tau * acc);
+        }
+        if (norm_w) {
+            double total = 0.0;
+            for (int s = 0; s < n; ++s) total += st.weights[p * st.kp + s];
+            const double denom = total > eps ? total : eps;
+            for (int s = 0; s < st.kp; ++s) norm_w[p * st.kp + s] = s < n ? st.weights[p * st.kp + s] / denom : 0.0;
+        }
+    }
+    free_state(&st);
+    return 0;
+}
+
+/* shade_lambert (src/blender.cpp:146-172); normals[H*W*3], alpha/depth[H*W], out[H*W*3]. */
+int gvro_shade_lambert(const gvro_camera* cam, const double* normals, const double* alpha, const double* depth,
+                       const double* light_pos, const double* light_color, double* out) {
+    const int H = cam->height, W = cam->width;
+    double rt[9];
+    transpose3(cam->rotation, rt);
+    memset(out, 0, sizeof(double) * (size_t)H * W * 3);
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) {
+            const size_t p = (size_t)i * W + j;
+            if (alpha[p] <= 0.0) continue;
+            double n[3] = {normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]};
+            const double len = sqrt(dot3(n, n));
+            if (len < 1e-12) continue;
+            for (int c = 0; c < 3; ++c) n[c] /= len;
+            double d[3], pc[3], po[3], tl[3];
+            pixel_ray(cam, i, j, d);
+            for (int c = 0; c < 3; ++c) pc[c] = depth[p] * d[c] - cam->translation[c];
+            mat_vec(rt, pc, po);
+            for (int c = 0; c < 3; ++c) tl[c] = light_pos[c] - po[c];
+            const double tn = sqrt(dot3(tl, tl));
+            for (int c = 0; c < 3; ++c) tl[c] /= tn;
+            double intensity = dot3(n, tl);
+            if (intensity < 0.0) intensity = 0.0;
+            for (int c = 0; c < 3; ++c) out[3 * p + c] = intensity * light_color[c];
+        }
+    return 0;
+}

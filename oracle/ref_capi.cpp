@@ -9,12 +9,16 @@
 //   gvr::coarse_select               (proj/src/tracer.cpp:37)
 //   gvr::make_bench_scene / camera   (proj/src/bench.cpp:9-24)
 //   gvr::make_orbit_camera           (proj/src/shapes.cpp:118)
+//   gvr::sample_attributes / resynthesize (proj/src/sampler.cpp:11-66)
+//   gvr::transmittance_at / normalized_weights / shade_lambert
+//                                    (proj/src/blender.cpp:19-25, 55-62, 146-172)
 // Per-pixel variable-length lists come back padded to k_prime (index -1).
 // Errors: return 1 for gvr::ValidationError, 2 for anything else; the message
 // is available from gvr_ref_last_error().
 #include "gvr/bench.hpp"
 #include "gvr/blender.hpp"
 #include "gvr/grad.hpp"
+#include "gvr/sampler.hpp"
 #include "gvr/scene.hpp"
 #include "gvr/shapes.hpp"
 #include "gvr/tracer.hpp"
@@ -293,6 +297,96 @@ int gvr_ref_make_orbit_camera(double azimuth, double elevation, double distance,
                                              gvr::Vec3(target[0], target[1], target[2]), height,
                                              width, focal),
                       cam);
+    });
+}
+
+// gvr::sample_attributes (proj/src/sampler.cpp:11-51). observed[H*W*C] with the
+// camera's H, W. Outputs: attrs[K*C], support[K], masked[K] (0/1).
+int gvr_ref_sample_attributes(int k, int d, double tau, const double* centers, const double* inv_cov,
+                              const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                              int ds, int threads, const double* observed, int obs_h, int obs_w,
+                              int channels, int normalized, double* attrs, double* support,
+                              unsigned char* masked) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        gvr::Image obs(obs_h, obs_w, channels);
+        std::memcpy(obs.data.data(), observed, obs.data.size() * sizeof(double));
+        const gvr::SampledAttributes sa =
+            gvr::sample_attributes(obs, scene, camera, cfg, normalized != 0, threads);
+        for (int i = 0; i < k; ++i) {
+            for (int c = 0; c < channels; ++c) attrs[static_cast<size_t>(channels) * i + c] = sa.attrs[i][c];
+            support[i] = sa.support[i];
+            masked[i] = sa.masked[i] ? 1 : 0;
+        }
+    });
+}
+
+// gvr::resynthesize (proj/src/sampler.cpp:53-66): render with attributes
+// replaced (masked -> zero). n_attrs = number of sampled rows (checked).
+int gvr_ref_resynthesize(int k, int d, double tau, const double* centers, const double* inv_cov,
+                         const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                         int ds, int threads, int n_attrs, int channels, const double* attrs,
+                         const unsigned char* masked, double* image, double* alpha, double* depth) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        gvr::SampledAttributes sa;
+        for (int i = 0; i < n_attrs; ++i) {
+            gvr::VecX a(channels);
+            for (int c = 0; c < channels; ++c) a[c] = attrs[static_cast<size_t>(channels) * i + c];
+            sa.attrs.push_back(a);
+            sa.support.push_back(1.0);
+            sa.masked.push_back(masked[i] != 0);
+        }
+        export_buffers(gvr::resynthesize(sa, scene, camera, cfg, threads), image, alpha, depth);
+    });
+}
+
+// Per-pixel gvr::transmittance_at over the pixel's selected traced kernels
+// (Tape::traced of render_with_tape) at depth t[p], and gvr::normalized_weights
+// of the pixel's RayBlend (weight_store + alpha). Outputs nullable.
+int gvr_ref_pixel_helpers(int k, int d, double tau, const double* centers, const double* inv_cov,
+                          const double* attr, const double* cam, double eta, int k_prime, int coarse,
+                          int ds, int threads, const double* t, double* trans_out, double eps,
+                          double* norm_w) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto camera = make_camera(cam);
+        const auto cfg = make_cfg(eta, k_prime, coarse, ds);
+        const gvr::ForwardResult fr = gvr::render_with_tape(scene, camera, cfg, threads);
+        const size_t p_count = static_cast<size_t>(camera.height) * camera.width;
+        for (size_t p = 0; p < p_count; ++p) {
+            if (trans_out) trans_out[p] = gvr::transmittance_at(fr.tape.traced[p], tau, t[p]);
+            if (norm_w) {
+                gvr::RayBlend rb;
+                rb.weights = fr.buffers.weight_store[p];
+                rb.alpha = fr.buffers.alpha.data[p];
+                const auto nw = gvr::normalized_weights(rb, eps);
+                for (int s = 0; s < k_prime; ++s)
+                    norm_w[p * k_prime + s] = s < static_cast<int>(nw.size()) ? nw[s].second : 0.0;
+            }
+        }
+    });
+}
+
+// gvr::shade_lambert (proj/src/blender.cpp:146-172); normals[H*W*3], alpha/depth[H*W].
+int gvr_ref_shade_lambert(const double* cam, const double* normals, const double* alpha,
+                          const double* depth, const double* light_pos, const double* light_color,
+                          double* out) {
+    return guarded([&] {
+        const auto camera = make_camera(cam);
+        const int h = camera.height, w = camera.width;
+        gvr::Image n(h, w, 3), a(h, w, 1, gvr::ChannelSemantics::Alpha), z(h, w, 1);
+        std::memcpy(n.data.data(), normals, n.data.size() * sizeof(double));
+        std::memcpy(a.data.data(), alpha, a.data.size() * sizeof(double));
+        std::memcpy(z.data.data(), depth, z.data.size() * sizeof(double));
+        const gvr::Image o = gvr::shade_lambert(
+            n, a, z, camera, gvr::Vec3(light_pos[0], light_pos[1], light_pos[2]),
+            gvr::Vec3(light_color[0], light_color[1], light_color[2]));
+        std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
     });
 }
 

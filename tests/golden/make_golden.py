@@ -52,7 +52,7 @@ def default_camera(size: int, focal: float) -> Camera:
 
 
 def save(name: str, scene: GaussianScene, cam: Camera, cfg: SelectionConfig, seed: int, traced: bool = True,
-         flags=(True, True)) -> None:
+         flags=(True, True), extra=None) -> None:
     out = oracle.ref_render(scene, cam, cfg, threads=8)
     rng = np.random.default_rng(seed)
     h, w, d = cam.height, cam.width, scene.attr_dim()
@@ -69,10 +69,32 @@ def save(name: str, scene: GaussianScene, cam: Camera, cfg: SelectionConfig, see
     )
     if traced:
         rec.update(topk_l=out["topk_l"], topk_q=out["topk_q"], topk_sigma=out["topk_sigma"])
+    if extra is not None:
+        rec.update(extra(scene, cam, cfg, out, rng))
     path = os.path.join(HERE, name + ".npz")
     np.savez_compressed(path, **rec)
     n = (out["topk_idx"] >= 0).sum()
     print(f"{name}: K={scene.size} {h}x{w} selected entries={n} -> {os.path.getsize(path) / 1e3:.0f} kB")
+
+
+def sampler_extra(scene, cam, cfg, out, rng) -> dict:
+    """Reference outputs of the render-path helpers on the same inputs:
+    sample_attributes (raw + normalized) of a noisy observation of the render,
+    resynthesize with those attributes, per-pixel transmittance_at and
+    normalized_weights, and shade_lambert of the rendered image as normals
+    (proj/src/sampler.cpp:11-66, proj/src/blender.cpp:19-25, 55-62, 146-172)."""
+    h, w = cam.height, cam.width
+    observed = out["image"] + rng.uniform(-0.05, 0.05, out["image"].shape)
+    sa, ss, sm = oracle.ref_sample_attributes(scene, cam, cfg, observed, False, threads=8)
+    na, ns, nm = oracle.ref_sample_attributes(scene, cam, cfg, observed, True, threads=8)
+    rs = oracle.ref_resynthesize(scene, cam, cfg, sa, sm, threads=8)
+    t = out["depth"][..., 0] + rng.uniform(-0.3, 0.3, (h, w))
+    trans, nw = oracle.ref_pixel_helpers(scene, cam, cfg, t, 1e-8, threads=8)
+    light_pos, light_color = np.array([1.5, -1.0, 12.0]), np.array([1.0, 0.5, 0.25])
+    shade = oracle.ref_shade_lambert(cam, out["image"], out["alpha"], out["depth"], light_pos, light_color)
+    return dict(observed=observed, s_attrs=sa, s_support=ss, s_masked=sm, n_attrs=na, n_support=ns, n_masked=nm,
+                resynth_image=rs["image"], resynth_alpha=rs["alpha"], t_query=t, trans_at=trans, norm_w=nw,
+                light_pos=light_pos, light_color=light_color, shade=shade)
 
 
 def main() -> None:
@@ -100,6 +122,10 @@ def main() -> None:
     save("orbit_rect", synthetic.make_bench_scene(2000), rot, cfg, 10)
     save("blocked_t", rs, default_camera(64, 48.0), cfg, 11, flags=(False, True))
     save("blocked_rho", rs, default_camera(64, 48.0), cfg, 12, flags=(True, False))
+    # sampler + helpers (sampler.cpp, blender.cpp helpers); a far kernel stays unobserved (masked)
+    hs = random_frustum_scene(13, 200, 3, 8.0, 120.0)
+    hs.centers[-1] = (0.0, 0.0, 300.0)
+    save("sampler_random", hs, default_camera(48, 40.0), SelectionConfig(k_prime=12), 13, extra=sampler_extra)
 
 
 if __name__ == "__main__":

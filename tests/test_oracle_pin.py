@@ -18,7 +18,7 @@ from conftest import Golden, golden_names
 from paper_2205_15401_b200.types import Camera, GaussianScene, SelectionConfig
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-REF_TESTS = ["test_scene", "test_tracer", "test_blender", "test_grad", "test_convert"]
+REF_TESTS = ["test_scene", "test_tracer", "test_blender", "test_grad", "test_convert", "test_sampler"]
 
 
 @pytest.mark.parametrize("suite", REF_TESTS)
@@ -125,3 +125,44 @@ def test_validation_messages_match_reference():
             oracle.ref_render(scene, c, cfg, threads=1)
         assert str(ea.value) == str(eb.value)
         assert ea.value.code == eb.value.code == 1
+
+
+def test_port_sampler_and_helpers_bit_identical_to_golden():
+    """sample_attributes / resynthesize inputs, transmittance_at, normalized_weights,
+    shade_lambert (sampler.cpp:11-66, blender.cpp:19-25, 55-62, 146-172)."""
+    g = Golden("sampler_random")
+    for norm, pre in ((False, "s_"), (True, "n_")):
+        a, s, m = oracle.port_sample_attributes(g.scene, g.camera, g.cfg, g["observed"], norm, threads=8)
+        assert np.array_equal(a, g[pre + "attrs"])
+        assert np.array_equal(s, g[pre + "support"])
+        assert np.array_equal(m, g[pre + "masked"])
+    trans, nw = oracle.port_pixel_helpers(g.scene, g.camera, g.cfg, g["t_query"], 1e-8, threads=8)
+    assert np.array_equal(trans, g["trans_at"])
+    assert np.array_equal(nw, g["norm_w"])
+    sh = oracle.port_shade_lambert(g.camera, g["image"], g["alpha"], g["depth"], g["light_pos"], g["light_color"])
+    assert np.array_equal(sh, g["shade"])
+    assert g["s_masked"][-1] and not g["s_masked"].all()
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference build not present")
+def test_port_sampler_equals_reference_random():
+    scene = _random_scene(21, k=80)
+    cam = Camera(np.eye(3), np.zeros(3), 30.0, 15.5, 13.0, 32, 28)
+    cfg = SelectionConfig(k_prime=7, coarse_downsample=4)
+    rng = np.random.default_rng(5)
+    obs = rng.uniform(0, 1, (32, 28, 2))
+    for norm in (False, True):
+        a = oracle.port_sample_attributes(scene, cam, cfg, obs, norm, threads=3)
+        b = oracle.ref_sample_attributes(scene, cam, cfg, obs, norm, threads=3)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    with pytest.raises(oracle.OracleError) as ea:
+        oracle.port_sample_attributes(scene, cam, cfg, obs[:16], False)
+    with pytest.raises(oracle.OracleError) as eb:
+        oracle.ref_sample_attributes(scene, cam, cfg, obs[:16], False)
+    assert str(ea.value) == str(eb.value) == "observed image size does not match the camera"
+    n = rng.normal(size=(32, 28, 3))
+    al = rng.uniform(-0.2, 1, (32, 28, 1))
+    de = rng.uniform(2, 6, (32, 28, 1))
+    assert np.array_equal(oracle.port_shade_lambert(cam, n, al, de, [1.0, 2.0, -3.0], [0.9, 0.5, 0.1]),
+                          oracle.ref_shade_lambert(cam, n, al, de, [1.0, 2.0, -3.0], [0.9, 0.5, 0.1]))
