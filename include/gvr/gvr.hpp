@@ -363,4 +363,101 @@ struct ScalarLoss {
     }
 };
 
+// ---------------------------------------------------------------- sampler (sampler.hpp)
+
+// sampler.hpp:8-15
+struct SampledAttributes {
+    std::vector<VecX> attrs;      // K x D
+    std::vector<double> support;  // sum of observed weights per kernel
+    std::vector<bool> masked;     // true where support fell below the threshold
+    int masked_count() const {
+        int n = 0;
+        for (bool m : masked) n += m ? 1 : 0;
+        return n;
+    }
+};
+
+inline constexpr double kSupportEps = 1e-8;  // sampler.hpp:18
+
+// sampler.hpp:23-25 / sampler.cpp:11-51 (gvr_sample_attributes: render + device scatter).
+inline SampledAttributes sample_attributes(const Image& observed, const GaussianScene& scene, const Camera& camera,
+                                           const SelectionConfig& cfg, bool normalized = false, int threads = 0) {
+    (void)threads;
+    if (observed.height != camera.height || observed.width != camera.width)
+        throw ValidationError("observed image size does not match the camera");
+    const auto dscene = detail::upload(scene);
+    const int k = scene.size(), dim = observed.channels;
+    std::vector<double> a(static_cast<size_t>(k) * dim), sp(k);
+    std::vector<uint8_t> m(k);
+    const gvr_camera cc = detail::to_c(camera);
+    const gvr_selection sc = detail::to_c(cfg);
+    detail::check(gvr_sample_attributes(detail::context(), dscene->s, &cc, &sc, observed.data.data(), observed.height,
+                                        observed.width, dim, normalized ? 1 : 0, a.data(), sp.data(), m.data()));
+    SampledAttributes out;
+    out.attrs.assign(k, VecX::Zero(dim));
+    out.support = sp;
+    out.masked.assign(k, false);
+    for (int i = 0; i < k; ++i) {
+        for (int c = 0; c < dim; ++c) out.attrs[i][c] = a[static_cast<size_t>(dim) * i + c];
+        out.masked[i] = m[i] != 0;
+    }
+    return out;
+}
+
+// sampler.hpp:29-30 / sampler.cpp:53-66 (gvr_scene_resynthesize + gvr_render).
+inline RenderBuffers resynthesize(const SampledAttributes& attrs, const GaussianScene& scene, const Camera& camera,
+                                  const SelectionConfig& cfg, int threads = 0) {
+    if (attrs.attrs.size() != static_cast<size_t>(scene.size()))
+        throw ValidationError("sampled attribute count does not match the scene");
+    GaussianScene recolored = scene;
+    for (int k = 0; k < scene.size(); ++k)
+        recolored.kernels[k].attr = attrs.masked[k] ? VecX::Zero(attrs.attrs[k].size()) : attrs.attrs[k];
+    return render(recolored, camera, cfg, threads);
+}
+
+// ---------------------------------------------------------------- helpers (blender.hpp)
+
+// transmittance_at (blender.hpp:29) for every pixel of a taped render: T(t(i,j))
+// over that pixel's selected kernels (the reference's per-ray span form, batched).
+inline Image transmittance_at(const Tape& tape, const Image& t) {
+    if (t.height != tape.camera.height || t.width != tape.camera.width || t.channels != 1)
+        throw ValidationError("transmittance_at: depth image shape does not match the forward render");
+    Image out(t.height, t.width, 1, ChannelSemantics::Feature);
+    detail::check(gvr_tape_transmittance(detail::context(), tape.device_tape->t, t.data.data(), out.data.data()));
+    return out;
+}
+
+// normalized_weights (blender.hpp:36) of every pixel's weight_store, same layout.
+inline std::vector<std::vector<std::pair<int, double>>> normalized_weights(const ForwardResult& fr,
+                                                                           double eps = 1e-8) {
+    const size_t p = fr.buffers.weight_store.size(), kp = static_cast<size_t>(fr.tape.cfg.k_prime);
+    std::vector<double> nw(p * kp);
+    detail::check(gvr_tape_normalized_weights(detail::context(), fr.tape.device_tape->t, eps, nw.data()));
+    std::vector<std::vector<std::pair<int, double>>> out(p);
+    for (size_t i = 0; i < p; ++i)
+        for (size_t k = 0; k < fr.buffers.weight_store[i].size(); ++k)
+            out[i].emplace_back(fr.buffers.weight_store[i][k].first, nw[i * kp + k]);
+    return out;
+}
+
+// blender.hpp:46-47 / blender.cpp:146-172 (gvr_shade_lambert).
+inline Image shade_lambert(const Image& normals, const Image& alpha, const Image& depth, const Camera& camera,
+                           const Vec3& light_pos, const Vec3& light_color) {
+    if (normals.channels != 3) throw ValidationError("shade_lambert expects a 3-channel normal image");
+    if (normals.height != alpha.height || normals.width != alpha.width || normals.height != depth.height ||
+        normals.width != depth.width)
+        throw ValidationError("shade_lambert: buffer sizes do not match");
+    Image out(normals.height, normals.width, 3, ChannelSemantics::Color);
+    Camera cam = camera;
+    cam.height = normals.height;
+    cam.width = normals.width;
+    const gvr_camera cc = detail::to_c(cam);
+    const double lp[3] = {light_pos[0], light_pos[1], light_pos[2]};
+    const double lc[3] = {light_color[0], light_color[1], light_color[2]};
+    if (out.pixel_count() == 0) return out;
+    detail::check(gvr_shade_lambert(detail::context(), &cc, normals.data.data(), alpha.data.data(), depth.data.data(),
+                                    lp, lc, out.data.data()));
+    return out;
+}
+
 }  // namespace gvr

@@ -21,6 +21,15 @@
  *                                      grad.hpp:53-54               gvr_backward
  *   double ScalarLoss::value(buf, d_image*, d_alpha*)
  *                                      grad.hpp:68, grad.cpp:201    gvr_scalar_loss
+ *   SampledAttributes sample_attributes(observed, scene, camera, cfg, normalized, threads)
+ *                                      sampler.hpp:23-25            gvr_sample_attributes
+ *   RenderBuffers resynthesize(attrs, scene, camera, cfg, threads)
+ *                                      sampler.hpp:29-30            gvr_scene_resynthesize + gvr_render
+ *   double transmittance_at(traced, tau, t)
+ *                                      blender.hpp:29               gvr_tape_transmittance (per pixel)
+ *   normalized_weights(RayBlend, eps)  blender.hpp:36               gvr_tape_normalized_weights
+ *   Image shade_lambert(normals, alpha, depth, camera, light_pos, light_color)
+ *                                      blender.hpp:46-47            gvr_shade_lambert
  *   ValidationError (std::runtime_error)
  *                                      types.hpp:19-22              return GVR_ERR_VALIDATION +
  *                                                                   gvr_last_error() (same text)
@@ -201,6 +210,37 @@ int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* tape, const double* d_im
  * is the 1-based step count used for the bias corrections. */
 int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
                   int64_t step, double lr, double beta1, double beta2, double eps);
+
+/* ---- sampler and render-path helpers -------------------------------------- */
+/* gvr::sample_attributes (sampler.hpp:23-25, sampler.cpp:11-51): render (as
+ * gvr_render), then per kernel alpha_k = sum_p W_pk obs_p / sum_p W_pk using the
+ * rendering weights (normalized != 0: W / max(sum_p W, 1e-8) per pixel);
+ * kernels with support < 1e-8 get zero attributes and masked = 1.
+ * observed: obs_height*obs_width*channels; must match the camera size
+ * (GVR_ERR_VALIDATION "observed image size does not match the camera").
+ * Outputs attrs[K*channels], support[K], masked[K] (host or device, nullable). */
+int gvr_sample_attributes(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
+                          const gvr_selection* cfg, const double* observed, int32_t obs_height, int32_t obs_width,
+                          int32_t channels, int32_t normalized, double* attrs, double* support, uint8_t* masked);
+/* The same on an existing taped render (the weights of gvr_render on that tape). */
+int gvr_tape_sample_attributes(gvr_context* ctx, const gvr_tape* tape, const double* observed, int32_t channels,
+                               int32_t normalized, double* attrs, double* support, uint8_t* masked);
+/* gvr::resynthesize (sampler.cpp:53-66), scene part: dst = src with attributes
+ * replaced by attrs[n_attrs*channels] (masked[k] != 0 -> zero; masked nullable),
+ * validated like a render would. n_attrs != K -> GVR_ERR_VALIDATION
+ * "sampled attribute count does not match the scene". Render dst to finish. */
+int gvr_scene_resynthesize(gvr_context* ctx, gvr_scene* dst, const gvr_scene* src, int32_t n_attrs, int32_t channels,
+                           const double* attrs, const uint8_t* masked);
+/* gvr::transmittance_at (blender.hpp:29, blender.cpp:19-25) for every pixel of a
+ * taped render: T(t[p]) over the pixel's selected kernels; t, out: H*W. */
+int gvr_tape_transmittance(gvr_context* ctx, const gvr_tape* tape, const double* t, double* out);
+/* gvr::normalized_weights (blender.hpp:36, blender.cpp:55-62) for every pixel:
+ * out[H*W*k_prime] = W_k / max(sum W, eps), ascending (l, idx), 0 padded. */
+int gvr_tape_normalized_weights(gvr_context* ctx, const gvr_tape* tape, double eps, double* out);
+/* gvr::shade_lambert (blender.hpp:46-47, blender.cpp:146-172): normals H*W*3,
+ * alpha/depth H*W (camera size), light_pos/light_color host double[3], out H*W*3. */
+int gvr_shade_lambert(gvr_context* ctx, const gvr_camera* camera, const double* normals, const double* alpha,
+                      const double* depth, const double* light_pos, const double* light_color, double* out);
 
 #ifdef __cplusplus
 }

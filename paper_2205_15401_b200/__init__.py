@@ -9,6 +9,7 @@ from .types import (  # noqa: F401
     GradFlags,
     GradientBundle,
     RenderBuffers,
+    SampledAttributes,
     ScalarLoss,
     SelectionConfig,
     ValidationError,
@@ -27,8 +28,14 @@ from .render import (  # noqa: F401
     render,
     render_into,
     render_with_tape,
+    resynthesize,
+    resynthesize_scene,
+    sample_attributes,
     scalar_loss,
     scalar_loss_into,
+    shade_lambert,
+    normalized_weights,
+    transmittance_at,
 )
 from .synthetic import make_bench_camera, make_bench_scene, make_orbit_camera  # noqa: F401
 from .scene_io import load_camera_json, load_scene_json  # noqa: F401

@@ -49,6 +49,12 @@ EXPORTED_SYMBOLS = (
     "gvr_backward",
     "gvr_backward_accumulate",
     "gvr_adam_step",
+    "gvr_sample_attributes",
+    "gvr_tape_sample_attributes",
+    "gvr_scene_resynthesize",
+    "gvr_tape_transmittance",
+    "gvr_tape_normalized_weights",
+    "gvr_shade_lambert",
 )
 
 
@@ -148,6 +154,13 @@ def load() -> ctypes.CDLL:
         "gvr_render_shard": (ctypes.c_int, [vp, vp, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection), vp,
                                             ctypes.POINTER(GvrRenderOutputs), i32, i32]),
         "gvr_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]),
+        "gvr_sample_attributes": (ctypes.c_int, [vp, vp, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection), vp,
+                                                 i32, i32, i32, i32, vp, vp, vp]),
+        "gvr_tape_sample_attributes": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, vp]),
+        "gvr_scene_resynthesize": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp]),
+        "gvr_tape_transmittance": (ctypes.c_int, [vp, vp, vp, vp]),
+        "gvr_tape_normalized_weights": (ctypes.c_int, [vp, vp, dp, vp]),
+        "gvr_shade_lambert": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -10,6 +10,7 @@
 #include "backward.cuh"
 #include "forward.cuh"
 #include "project.cuh"
+#include "sampler.cuh"
 
 #include <cuda_runtime.h>
 
@@ -88,6 +89,8 @@ struct gvr_context {
     bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
+    Buf scratch[4];           // staging of host inputs / outputs of the helper entry points
+    gvr_tape* aux_tape = nullptr;  // render behind gvr_sample_attributes
 };
 
 struct gvr_graph {
@@ -260,12 +263,6 @@ void harvest_timings(gvr_context* ctx) {
 
 unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
-int ceil_log2(uint32_t v) {
-    int b = 0;
-    while ((1ull << b) < v) ++b;
-    return b;
-}
-
 template <int KMAX>
 int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
     const size_t list_smem = sizeof(unsigned long long) * (size_t)fp.cap;
@@ -317,6 +314,32 @@ int sync_and_check(gvr_context* ctx) {
         return set_err(ctx, GVR_ERR_RUNTIME, "operation needs a host synchronisation; not allowed while capturing a graph");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     if (!ctx->ev_pending.empty()) harvest_timings(ctx);
+    return GVR_OK;
+}
+
+// K0 on an uploaded scene (GaussianKernel::validate, types.cpp:17-29); one sync.
+int validate_uploaded(gvr_context* ctx, gvr_scene* s) {
+    const int K = s->K, D = s->D;
+    if (K > 0) {
+        unsigned long long* first = reinterpret_cast<unsigned long long*>(ctx->flags.as<int>() + 2);
+        CUDA_TRY(ctx, cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
+        validate_scene_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(K, D, s->centers.as<double>(),
+                                                                           s->inv_cov.as<double>(),
+                                                                           s->attr.as<double>(), first);
+        LAUNCH_CHECK(ctx);
+        unsigned long long h = 0;
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, first, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        if (int rc = sync_and_check(ctx)) return rc;
+        std::memcpy(&h, ctx->h_flags + 2, sizeof h);
+        if (h != ~0ull) {
+            const long long k = (long long)(h >> 2);
+            switch ((int)(h & 3)) {
+                case 1: return set_err(ctx, GVR_ERR_VALIDATION, "kernel has non-finite values (kernel %lld)", k);
+                case 2: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not symmetric (kernel %lld)", k);
+                default: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not positive-definite (kernel %lld)", k);
+            }
+        }
+    }
     return GVR_OK;
 }
 
@@ -375,6 +398,8 @@ void gvr_context_destroy(gvr_context* ctx) {
     harvest_timings(ctx);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     ctx->flags.release();
+    for (Buf& b : ctx->scratch) b.release();
+    if (ctx->aux_tape) gvr_tape_destroy(ctx->aux_tape);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -560,26 +585,7 @@ int gvr_scene_set(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double t
     s->K = K;
     s->D = D;
     s->tau = tau;
-    if (K > 0) {
-        unsigned long long* first = reinterpret_cast<unsigned long long*>(ctx->flags.as<int>() + 2);
-        CUDA_TRY(ctx, cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
-        validate_scene_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(K, D, s->centers.as<double>(),
-                                                                           s->inv_cov.as<double>(),
-                                                                           s->attr.as<double>(), first);
-        LAUNCH_CHECK(ctx);
-        unsigned long long h = 0;
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, first, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-        if (int rc = sync_and_check(ctx)) return rc;
-        std::memcpy(&h, ctx->h_flags + 2, sizeof h);
-        if (h != ~0ull) {
-            const long long k = (long long)(h >> 2);
-            switch ((int)(h & 3)) {
-                case 1: return set_err(ctx, GVR_ERR_VALIDATION, "kernel has non-finite values (kernel %lld)", k);
-                case 2: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not symmetric (kernel %lld)", k);
-                default: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not positive-definite (kernel %lld)", k);
-            }
-        }
-    }
+    if (int rc = validate_uploaded(ctx, s)) return rc;
     s->valid = true;
     return GVR_OK;
 }
@@ -1017,6 +1023,235 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     return GVR_OK;
 }
 
+namespace {
+
+TapeView tape_view(const gvr_tape* t) {
+    TapeView v;
+    v.cam = t->camp;
+    v.kp = t->cfg.k_prime;
+    v.topk = t->topk.as<int>();
+    v.count = t->count.as<int>();
+    v.tape_t = t->tape_t.as<double>();
+    v.rec64 = t->rec64.as<Rec64>();
+    return v;
+}
+
+// Device view of an input that may live in host memory (staged through `buf`).
+int stage_in(gvr_context* ctx, Buf& buf, const void* src, size_t bytes, const void** dev) {
+    if (!src || is_device_ptr(src) || bytes == 0) {
+        *dev = src;
+        return GVR_OK;
+    }
+    CUDA_TRY(ctx, buf.ensure(bytes));
+    CUDA_TRY(ctx, cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *dev = buf.p;
+    return GVR_OK;
+}
+
+// Device target for an output that may live in host memory; *host set when a
+// copy back (copy_out of `buf`) is needed.
+int stage_out(gvr_context* ctx, Buf& buf, void* dst, size_t bytes, void** dev, bool* host) {
+    *host = dst && !is_device_ptr(dst);
+    if (!*host) {
+        *dev = dst;
+        return GVR_OK;
+    }
+    CUDA_TRY(ctx, buf.ensure(bytes));
+    *dev = buf.p;
+    return GVR_OK;
+}
+
+int tape_ready(gvr_context* ctx, const gvr_tape* t) {
+    if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
+    if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
+        return set_err(ctx, GVR_ERR_RUNTIME, "the scene changed after the forward render");
+    return GVR_OK;
+}
+
+}  // namespace
+
 extern "C" {
+
+int gvr_tape_sample_attributes(gvr_context* ctx, const gvr_tape* t, const double* observed, int32_t channels,
+                               int32_t normalized, double* attrs, double* support, uint8_t* masked) {
+    if (int rc = tape_ready(ctx, t)) return rc;
+    if (channels < 0) return set_err(ctx, GVR_ERR_VALIDATION, "channels must be >= 0");
+    const long long P = (long long)t->H * t->W;
+    const int K = t->K, C = channels;
+    if (P * C > 0 && !observed) return set_err(ctx, GVR_ERR_RUNTIME, "observed image must not be null");
+    const void* obs = nullptr;
+    if (int rc = stage_in(ctx, ctx->scratch[0], observed, sizeof(double) * P * C, &obs)) return rc;
+    void *da, *ds, *dm;
+    bool ha, hs, hm;
+    if (int rc = stage_out(ctx, ctx->scratch[1], attrs, sizeof(double) * (size_t)K * C + 8, &da, &ha)) return rc;
+    if (int rc = stage_out(ctx, ctx->scratch[2], support, sizeof(double) * (size_t)K + 8, &ds, &hs)) return rc;
+    if (int rc = stage_out(ctx, ctx->scratch[3], masked, (size_t)K + 8, &dm, &hm)) return rc;
+    // support is needed even when the caller does not want it
+    if (!ds) {
+        CUDA_TRY(ctx, ctx->scratch[2].ensure(sizeof(double) * (size_t)K + 8));
+        ds = ctx->scratch[2].p;
+    }
+    if (!da && C > 0) {
+        CUDA_TRY(ctx, ctx->scratch[1].ensure(sizeof(double) * (size_t)K * C + 8));
+        da = ctx->scratch[1].p;
+    }
+    if (!dm) {
+        CUDA_TRY(ctx, ctx->scratch[3].ensure((size_t)K + 8));
+        dm = ctx->scratch[3].p;
+    }
+    if (K > 0) {
+        CUDA_TRY(ctx, cudaMemsetAsync(ds, 0, sizeof(double) * (size_t)K, ctx->stream));
+        if (C > 0) CUDA_TRY(ctx, cudaMemsetAsync(da, 0, sizeof(double) * (size_t)K * C, ctx->stream));
+        if (P > 0) {
+            sample_scatter_kernel<<<blocks_for(P, 128), 128, 0, ctx->stream>>>(
+                tape_view(t), static_cast<const double*>(obs), C, normalized ? 1 : 0, static_cast<double*>(ds),
+                static_cast<double*>(da));
+            LAUNCH_CHECK(ctx);
+        }
+        sample_finalize_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(
+            K, C, static_cast<const double*>(ds), static_cast<double*>(da), static_cast<unsigned char*>(dm));
+        LAUNCH_CHECK(ctx);
+    }
+    bool host = false;
+    int rc;
+    if (ha && (rc = copy_out(ctx, attrs, da, sizeof(double) * (size_t)K * C, &host))) return rc;
+    if (hs && (rc = copy_out(ctx, support, ds, sizeof(double) * (size_t)K, &host))) return rc;
+    if (hm && (rc = copy_out(ctx, masked, dm, (size_t)K, &host))) return rc;
+    if (host) return sync_and_check(ctx);
+    return GVR_OK;
+}
+
+int gvr_sample_attributes(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
+                          const gvr_selection* cfg, const double* observed, int32_t obs_height, int32_t obs_width,
+                          int32_t channels, int32_t normalized, double* attrs, double* support, uint8_t* masked) {
+    if (!ctx || !scene || !camera) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (obs_height != camera->height || obs_width != camera->width)
+        return set_err(ctx, GVR_ERR_VALIDATION, "observed image size does not match the camera");
+    if (!ctx->aux_tape)
+        if (int rc = gvr_tape_create(ctx, &ctx->aux_tape)) return rc;
+    if (int rc = gvr_render(ctx, scene, camera, cfg, ctx->aux_tape, nullptr)) return rc;
+    return gvr_tape_sample_attributes(ctx, ctx->aux_tape, observed, channels, normalized, attrs, support, masked);
+}
+
+int gvr_scene_resynthesize(gvr_context* ctx, gvr_scene* dst, const gvr_scene* src, int32_t n_attrs, int32_t channels,
+                           const double* attrs, const uint8_t* masked) {
+    if (!ctx || !dst || !src) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (!src->valid) return set_err(ctx, GVR_ERR_VALIDATION, "scene has not been validated");
+    if (n_attrs != src->K) return set_err(ctx, GVR_ERR_VALIDATION, "sampled attribute count does not match the scene");
+    if (channels < 0) return set_err(ctx, GVR_ERR_VALIDATION, "channels must be >= 0");
+    const int K = src->K, C = channels;
+    if ((size_t)K * C > 0 && !attrs) return set_err(ctx, GVR_ERR_RUNTIME, "attrs must not be null");
+    const void* da = nullptr;
+    const void* dm = nullptr;
+    if (int rc = stage_in(ctx, ctx->scratch[0], attrs, sizeof(double) * (size_t)K * C, &da)) return rc;
+    if (int rc = stage_in(ctx, ctx->scratch[1], masked, (size_t)K, &dm)) return rc;
+    if (dst != src) {
+        dst->valid = false;
+        CUDA_TRY(ctx, dst->centers.ensure(sizeof(double) * 3 * (size_t)K));
+        CUDA_TRY(ctx, dst->inv_cov.ensure(sizeof(double) * 9 * (size_t)K));
+        if (K > 0) {
+            CUDA_TRY(ctx, cudaMemcpyAsync(dst->centers.p, src->centers.p, sizeof(double) * 3 * (size_t)K,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+            CUDA_TRY(ctx, cudaMemcpyAsync(dst->inv_cov.p, src->inv_cov.p, sizeof(double) * 9 * (size_t)K,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    }
+    dst->valid = false;
+    ++dst->version;
+    CUDA_TRY(ctx, dst->attr.ensure(sizeof(double) * (size_t)K * C));
+    const long long n = (long long)K * C;
+    if (n > 0) {
+        resynth_attr_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+            n, C, static_cast<const double*>(da), static_cast<const unsigned char*>(dm), dst->attr.as<double>());
+        LAUNCH_CHECK(ctx);
+    }
+    dst->K = K;
+    dst->D = C;
+    dst->tau = src->tau;
+    // render() re-validates the recolored scene (blender.cpp:70): same decisions
+    if (int rc = validate_uploaded(ctx, dst)) return rc;
+    dst->valid = true;
+    return GVR_OK;
+}
+
+int gvr_tape_transmittance(gvr_context* ctx, const gvr_tape* t, const double* depth_t, double* out) {
+    if (int rc = tape_ready(ctx, t)) return rc;
+    const long long P = (long long)t->H * t->W;
+    if (!depth_t || !out) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    const void* dt = nullptr;
+    void* dout = nullptr;
+    bool host = false;
+    if (int rc = stage_in(ctx, ctx->scratch[0], depth_t, sizeof(double) * P, &dt)) return rc;
+    if (int rc = stage_out(ctx, ctx->scratch[1], out, sizeof(double) * P, &dout, &host)) return rc;
+    transmittance_kernel<<<blocks_for(P, 128), 128, 0, ctx->stream>>>(tape_view(t), t->scene->tau,
+                                                                       static_cast<const double*>(dt),
+                                                                       static_cast<double*>(dout));
+    LAUNCH_CHECK(ctx);
+    if (host) {
+        bool h2 = false;
+        if (int rc = copy_out(ctx, out, dout, sizeof(double) * P, &h2)) return rc;
+        return sync_and_check(ctx);
+    }
+    return GVR_OK;
+}
+
+int gvr_tape_normalized_weights(gvr_context* ctx, const gvr_tape* t, double eps, double* out) {
+    if (int rc = tape_ready(ctx, t)) return rc;
+    if (!out) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    const long long P = (long long)t->H * t->W;
+    const size_t bytes = sizeof(double) * (size_t)P * t->cfg.k_prime;
+    void* dout = nullptr;
+    bool host = false;
+    if (int rc = stage_out(ctx, ctx->scratch[1], out, bytes, &dout, &host)) return rc;
+    normalized_weights_kernel<<<blocks_for(P, 128), 128, 0, ctx->stream>>>(tape_view(t), eps,
+                                                                            static_cast<double*>(dout));
+    LAUNCH_CHECK(ctx);
+    if (host) {
+        bool h2 = false;
+        if (int rc = copy_out(ctx, out, dout, bytes, &h2)) return rc;
+        return sync_and_check(ctx);
+    }
+    return GVR_OK;
+}
+
+int gvr_shade_lambert(gvr_context* ctx, const gvr_camera* camera, const double* normals, const double* alpha,
+                      const double* depth, const double* light_pos, const double* light_color, double* out) {
+    if (!ctx || !camera || !normals || !alpha || !depth || !light_pos || !light_color || !out)
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (camera->height < 0 || camera->width < 0) return set_err(ctx, GVR_ERR_VALIDATION, "bad image size");
+    const long long P = (long long)camera->height * camera->width;
+    if (P == 0) return GVR_OK;
+    CameraP cp;
+    std::memcpy(cp.R, camera->rotation, sizeof cp.R);
+    std::memcpy(cp.T, camera->translation, sizeof cp.T);
+    cp.focal = camera->focal;
+    cp.ox = camera->ox;
+    cp.oy = camera->oy;
+    cp.H = camera->height;
+    cp.W = camera->width;
+    const void *dn, *da, *dd;
+    void* dout;
+    bool host = false;
+    if (int rc = stage_in(ctx, ctx->scratch[0], normals, sizeof(double) * 3 * P, &dn)) return rc;
+    if (int rc = stage_in(ctx, ctx->scratch[1], alpha, sizeof(double) * P, &da)) return rc;
+    if (int rc = stage_in(ctx, ctx->scratch[2], depth, sizeof(double) * P, &dd)) return rc;
+    if (int rc = stage_out(ctx, ctx->scratch[3], out, sizeof(double) * 3 * P, &dout, &host)) return rc;
+    double lp[3], lc[3];
+    if (is_device_ptr(light_pos) || is_device_ptr(light_color))
+        return set_err(ctx, GVR_ERR_RUNTIME, "light_pos / light_color must be host arrays");
+    std::memcpy(lp, light_pos, sizeof lp);
+    std::memcpy(lc, light_color, sizeof lc);
+    shade_lambert_kernel<<<blocks_for(P, 128), 128, 0, ctx->stream>>>(
+        cp, static_cast<const double*>(dn), static_cast<const double*>(da), static_cast<const double*>(dd), lp[0],
+        lp[1], lp[2], lc[0], lc[1], lc[2], static_cast<double*>(dout));
+    LAUNCH_CHECK(ctx);
+    if (host) {
+        bool h2 = false;
+        if (int rc = copy_out(ctx, out, dout, sizeof(double) * 3 * P, &h2)) return rc;
+        return sync_and_check(ctx);
+    }
+    return GVR_OK;
+}
 
 }  // extern "C"

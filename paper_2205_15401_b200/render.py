@@ -6,6 +6,9 @@ Reference entry points (namespace ``gvr``, /root/reference/proj):
 * ``render_with_tape(scene, camera, cfg, threads)``  grad.hpp:41-42
 * ``backward(tape, d_image, d_alpha, flags)``        grad.hpp:53-54
 * ``ScalarLoss::value(buf, d_image*, d_alpha*)``     grad.hpp:68, grad.cpp:201-216
+* ``sample_attributes`` / ``resynthesize``           sampler.hpp:23-30, sampler.cpp:11-66
+* ``transmittance_at`` / ``normalized_weights``      blender.hpp:29-36 (per pixel of a tape)
+* ``shade_lambert``                                  blender.hpp:46-47, blender.cpp:146-172
 
 Same argument meaning and error behaviour: invalid inputs raise
 :class:`ValidationError` with the reference's message text. ``threads`` is
@@ -31,6 +34,7 @@ from .types import (
     GradFlags,
     GradientBundle,
     RenderBuffers,
+    SampledAttributes,
     ScalarLoss,
     SelectionConfig,
     ValidationError,
@@ -338,8 +342,9 @@ def scalar_loss(tape: Tape, loss: ScalarLoss, *, want_grads: bool = True):
     out = np.zeros(1)
     di = np.empty((h, w, max(d, 1))) if want_grads else None
     da = np.empty((h, w, 1)) if want_grads else None
-    ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(np.ascontiguousarray(loss.target_image)),
-                                      _ptr(np.ascontiguousarray(loss.target_alpha)), float(loss.w_image),
+    t_img = np.ascontiguousarray(loss.target_image, dtype=np.float64)  # kept alive across the call
+    t_alpha = np.ascontiguousarray(loss.target_alpha, dtype=np.float64)
+    ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(t_img), _ptr(t_alpha), float(loss.w_image),
                                       float(loss.w_alpha), _ptr(out), _ptr(di), _ptr(da)))
     return float(out[0]), di, da
 
@@ -384,3 +389,113 @@ def backward(tape, d_image, d_alpha, flags: GradFlags = GradFlags()) -> Gradient
     backward_into(tape, d_image, d_alpha, flags, gb.d_center, gb.d_inv_cov, gb.d_attr if d > 0 else None,
                   gb.d_rotation, gb.d_translation)
     return gb
+
+
+# ---------------------------------------------------------------- sampler + helpers
+
+
+def _image3(x, what: str) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.ndim == 2:
+        a = a[..., None]
+    if a.ndim != 3:
+        raise ValidationError(f"{what} must be an H x W x C image")
+    return a
+
+
+def sample_attributes(observed, scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(),
+                      normalized: bool = False, threads: int = 0, *, ctx: Optional[Context] = None,
+                      tape: Optional[Tape] = None) -> SampledAttributes:
+    """``gvr::sample_attributes`` (sampler.cpp:11-51): weighted-mean inverse
+    reconstruction alpha_k = sum_p W_pk phi_p / sum_p W_pk with the rendering
+    weights. Pass ``tape`` (a render of the same scene/camera/cfg) to reuse it."""
+    del threads
+    ctx = ctx or (tape.ctx if tape is not None else default_context())
+    obs = _image3(observed, "observed image")
+    h, w, ch = obs.shape
+    k = scene.K if isinstance(scene, DeviceScene) else scene.size
+    attrs, support, masked = np.empty((k, ch)), np.empty(k), np.empty(k, dtype=np.uint8)
+    if tape is not None:
+        th, tw, _, _ = tape.shape()
+        if (h, w) != (th, tw):
+            raise ValidationError("observed image size does not match the camera")
+        ctx.check(ctx.lib.gvr_tape_sample_attributes(ctx.handle, tape.handle, _ptr(obs), ch, int(bool(normalized)),
+                                                     _ptr(attrs), _ptr(support), _ptr(masked)))
+    else:
+        dscene = _as_device_scene(scene, ctx)
+        cam_c, sel_c = _camera_c(camera), _selection_c(cfg)
+        ctx.check(ctx.lib.gvr_sample_attributes(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c),
+                                                _ptr(obs), h, w, ch, int(bool(normalized)), _ptr(attrs),
+                                                _ptr(support), _ptr(masked)))
+    return SampledAttributes(attrs, support, masked.astype(bool))
+
+
+def resynthesize_scene(attrs: SampledAttributes, scene, ctx: Optional[Context] = None) -> DeviceScene:
+    """Device scene with the sampled attributes (masked -> 0), sampler.cpp:53-63."""
+    ctx = ctx or default_context()
+    src = _as_device_scene(scene, ctx)
+    a = np.ascontiguousarray(attrs.attrs, dtype=np.float64)
+    if a.ndim == 1:
+        a = a[:, None]
+    m = np.ascontiguousarray(attrs.masked, dtype=np.uint8)
+    n = a.shape[0]
+    if m.shape[0] != n:
+        raise ValidationError("sampled attribute count does not match the scene")
+    dst = DeviceScene(ctx)
+    ctx.check(ctx.lib.gvr_scene_resynthesize(ctx.handle, dst.handle, src.handle, n, a.shape[1], _ptr(a), _ptr(m)))
+    dst.K, dst.D, dst.tau = src.K, a.shape[1], src.tau
+    return dst
+
+
+def resynthesize(attrs: SampledAttributes, scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(),
+                 threads: int = 0, *, ctx: Optional[Context] = None) -> RenderBuffers:
+    """``gvr::resynthesize`` (sampler.cpp:53-66): render with the sampled attributes."""
+    ctx = ctx or default_context()
+    return render(resynthesize_scene(attrs, scene, ctx), camera, cfg, threads, ctx=ctx)
+
+
+def transmittance_at(tape, t) -> np.ndarray:
+    """``gvr::transmittance_at`` (blender.cpp:19-25) evaluated for every pixel of
+    a taped render over that pixel's selected kernels, at depth ``t[H, W]``."""
+    if isinstance(tape, ForwardResult):
+        tape = tape.tape
+    h, w, _, _ = tape.shape()
+    tt = np.ascontiguousarray(t, dtype=np.float64).reshape(h, w)
+    out = np.empty((h, w))
+    tape.ctx.check(tape.ctx.lib.gvr_tape_transmittance(tape.ctx.handle, tape.handle, _ptr(tt), _ptr(out)))
+    return out
+
+
+def normalized_weights(tape, eps: float = 1e-8) -> np.ndarray:
+    """``gvr::normalized_weights`` (blender.cpp:55-62) for every pixel: [H, W, K'],
+    ascending (l, idx) like ``topk_idx``, 0 padded."""
+    if isinstance(tape, ForwardResult):
+        tape = tape.tape
+    h, w, kp, _ = tape.shape()
+    out = np.empty((h, w, kp))
+    tape.ctx.check(tape.ctx.lib.gvr_tape_normalized_weights(tape.ctx.handle, tape.handle, float(eps), _ptr(out)))
+    return out
+
+
+def shade_lambert(normals, alpha, depth, camera: Camera, light_pos, light_color, *,
+                  ctx: Optional[Context] = None) -> np.ndarray:
+    """``gvr::shade_lambert`` (blender.cpp:146-172), same validation messages."""
+    ctx = ctx or default_context()
+    n = _image3(normals, "normals")
+    al = _image3(alpha, "alpha")
+    de = _image3(depth, "depth")
+    if n.shape[2] != 3:
+        raise ValidationError("shade_lambert expects a 3-channel normal image")
+    if n.shape[:2] != al.shape[:2] or n.shape[:2] != de.shape[:2]:
+        raise ValidationError("shade_lambert: buffer sizes do not match")
+    h, w = n.shape[:2]
+    cam = Camera(camera.rotation, camera.translation, camera.focal, camera.ox, camera.oy, h, w)
+    out = np.empty((h, w, 3))
+    lp = np.ascontiguousarray(light_pos, dtype=np.float64).reshape(3)
+    lc = np.ascontiguousarray(light_color, dtype=np.float64).reshape(3)
+    cam_c = _camera_c(cam)
+    al1 = np.ascontiguousarray(al[..., :1])  # kept alive across the call
+    de1 = np.ascontiguousarray(de[..., :1])
+    ctx.check(ctx.lib.gvr_shade_lambert(ctx.handle, ctypes.byref(cam_c), _ptr(n), _ptr(al1), _ptr(de1), _ptr(lp),
+                                        _ptr(lc), _ptr(out)))
+    return out

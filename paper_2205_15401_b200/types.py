@@ -161,3 +161,19 @@ class ScalarLoss:
     target_alpha: np.ndarray
     w_image: float = 1.0
     w_alpha: float = 1.0
+
+
+@dataclass
+class SampledAttributes:
+    """``gvr::SampledAttributes`` (sampler.hpp:8-15): per-kernel recovered
+    attributes [K, D], support (sum of observed weights) [K], masked [K] bool."""
+
+    attrs: np.ndarray
+    support: np.ndarray
+    masked: np.ndarray
+
+    def masked_count(self) -> int:
+        return int(np.count_nonzero(self.masked))
+
+
+K_SUPPORT_EPS = 1e-8  # gvr::kSupportEps (sampler.hpp:18)

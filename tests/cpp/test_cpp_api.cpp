@@ -184,3 +184,96 @@ TEST_CASE("selection config validation") {  // test_tracer.cpp:252-259
     cfg.k_prime = 0;
     CHECK_THROWS_AS(render(scene, default_camera(), cfg), ValidationError);
 }
+
+TEST_CASE("sampling a constant image recovers the constant") {  // test_sampler.cpp:71-82
+    std::mt19937_64 rng(5);
+    const GaussianScene scene = random_scene(rng, 150);
+    const Camera cam = default_camera(48, 48.0);
+    Image observed(48, 48, 3);
+    for (auto& v : observed.data) v = 0.7;
+    const SampledAttributes attrs = sample_attributes(observed, scene, cam, SelectionConfig{});
+    int tested = 0;
+    for (size_t k = 0; k < attrs.attrs.size(); ++k) {
+        if (attrs.masked[k]) continue;
+        ++tested;
+        for (int c = 0; c < 3; ++c) CHECK(attrs.attrs[k][c] == doctest::Approx(0.7).epsilon(1e-9));
+    }
+    CHECK(tested > 20);
+}
+
+TEST_CASE("sampling weights are exactly the rendering weights") {  // test_sampler.cpp:162-176
+    std::mt19937_64 rng(6);
+    const GaussianScene scene = random_scene(rng, 120);
+    const Camera cam = default_camera(40, 40.0);
+    const RenderBuffers buf = render(scene, cam, SelectionConfig{}, 1);
+    std::vector<double> support(scene.size(), 0.0);
+    for (const auto& ws : buf.weight_store)
+        for (const auto& [k, w] : ws) support[k] += w;
+    Image observed(cam.height, cam.width, 3);
+    const SampledAttributes attrs = sample_attributes(observed, scene, cam, SelectionConfig{});
+    for (int k = 0; k < scene.size(); ++k) CHECK(attrs.support[k] == doctest::Approx(support[k]).epsilon(1e-12));
+}
+
+TEST_CASE("zeroed attributes render black") {  // test_sampler.cpp:131-143
+    std::mt19937_64 rng(7);
+    const GaussianScene scene = random_scene(rng, 100);
+    SampledAttributes attrs;
+    attrs.attrs.assign(scene.size(), VecX::Zero(3));
+    attrs.support.assign(scene.size(), 1.0);
+    attrs.masked.assign(scene.size(), false);
+    const RenderBuffers buf = resynthesize(attrs, scene, default_camera(32, 32.0), SelectionConfig{}, 1);
+    for (double v : buf.image.data) CHECK(v == 0.0);
+}
+
+TEST_CASE("sampler size checks") {  // test_sampler.cpp:190-205
+    std::mt19937_64 rng(8);
+    const GaussianScene scene = random_scene(rng, 50);
+    const Camera cam = default_camera(32, 32.0);
+    Image observed(16, 16, 3);
+    CHECK_THROWS_AS(sample_attributes(observed, scene, cam, SelectionConfig{}), ValidationError);
+    SampledAttributes attrs;
+    attrs.attrs.assign(10, VecX::Zero(3));
+    attrs.support.assign(10, 1.0);
+    attrs.masked.assign(10, false);
+    CHECK_THROWS_AS(resynthesize(attrs, scene, cam, SelectionConfig{}), ValidationError);
+}
+
+TEST_CASE("normalized weights and transmittance of a taped render") {  // test_blender.cpp:11-21, 197-211
+    GaussianScene scene;
+    scene.kernels.push_back(isotropic(0, 0, 5, 0.8, VecX{1, 1, 1}));
+    Camera cam = default_camera(1, 10.0);
+    cam.ox = cam.oy = 0.0;
+    const ForwardResult fr = render_with_tape(scene, cam, SelectionConfig{}, 1);
+    Image t(1, 1, 1);
+    t.data[0] = -100.0;
+    CHECK(transmittance_at(fr.tape, t).data[0] == doctest::Approx(1.0));
+    t.data[0] = 5.0 + 60 * 0.8;
+    CHECK(transmittance_at(fr.tape, t).data[0] == doctest::Approx(std::exp(-1.0)));
+    const auto nw = normalized_weights(fr);
+    REQUIRE(nw[0].size() == 1);
+    CHECK(nw[0][0].second == doctest::Approx(1.0));
+}
+
+TEST_CASE("lambert shading basics") {  // test_blender.cpp:294-320
+    Image normals(1, 2, 3, ChannelSemantics::Normal);
+    Image alpha(1, 2, 1, ChannelSemantics::Alpha);
+    Image depth(1, 2, 1, ChannelSemantics::Feature);
+    normals.at(0, 0, 2) = -1.0;
+    normals.at(0, 1, 0) = 1.0;
+    alpha.at(0, 0, 0) = 1.0;
+    alpha.at(0, 1, 0) = 1.0;
+    depth.at(0, 0, 0) = 4.0;
+    depth.at(0, 1, 0) = 4.0;
+    Camera cam = default_camera(1, 8.0);
+    cam.width = 2;
+    cam.ox = 0.0;
+    cam.oy = 0.0;
+    const Image lit = shade_lambert(normals, alpha, depth, cam, Vec3(0, 0, -10), Vec3(1, 1, 1));
+    CHECK(lit.at(0, 0, 0) == doctest::Approx(1.0).epsilon(1e-3));
+    CHECK(lit.at(0, 1, 0) == doctest::Approx(0.0).epsilon(1e-2));
+    alpha.at(0, 0, 0) = 0.0;
+    const Image masked = shade_lambert(normals, alpha, depth, cam, Vec3(0, 0, -10), Vec3(1, 1, 1));
+    CHECK(masked.at(0, 0, 0) == 0.0);
+    Image bad(1, 2, 2);
+    CHECK_THROWS_AS(shade_lambert(bad, alpha, depth, cam, Vec3(0, 0, -10), Vec3(1, 1, 1)), ValidationError);
+}
