@@ -35,7 +35,7 @@ struct BwdParams {
 // FP64-accurate argument; products and sums are FP64 (the gradient bar is
 // 1e-4 of a class-scaled floor, ~1e-7 of the largest gradient).
 template <int KMAX>
-__global__ void __launch_bounds__(256) backward_pixels_kernel(BwdParams p) {
+__global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdParams p) {
     constexpr int TILE = 8, NP = 64;
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]

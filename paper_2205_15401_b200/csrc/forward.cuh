@@ -312,7 +312,7 @@ __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - 
 // comparison between keys within the FP32 bound is decided on the exact trace,
 // so the kept set is exactly the reference's.
 template <int KMAX>
-__global__ void __launch_bounds__(256, 3) select_warp_kernel(FwdParams p) {
+__global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParams p) {
     constexpr int TILE = 8;
     __shared__ float sh_l[8][64];
     __shared__ int sh_i[8][64];
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(256, 3) select_warp_kernel(FwdParams p) {
 //   W_k = exp(-tau sum_m e^{q_m} Phi((l_k - l_m)/sigma_m)) e^{q_k}
 // The sum is accumulated in FP64 and T(l_k) is taped for the backward.
 template <int KMAX>
-__global__ void __launch_bounds__(256) blend_kernel(FwdParams p) {
+__global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p) {
     constexpr int TILE = 8, NP = 64;
     extern __shared__ __align__(16) unsigned char smem[];
     double* b_dl = reinterpret_cast<double*>(smem);  // [slot][pixel] l - l0

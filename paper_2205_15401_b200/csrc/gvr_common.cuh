@@ -16,6 +16,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Minimum resident CTAs per SM of the per-tile kernels (register budget).
+#ifndef GVR_SEL_MINB
+#define GVR_SEL_MINB 3
+#endif
+#ifndef GVR_BLEND_MINB
+#define GVR_BLEND_MINB 1
+#endif
+#ifndef GVR_BWD_MINB
+#define GVR_BWD_MINB 4
+#endif
+
 namespace gvrk {
 
 constexpr double kBehindCameraEps = 1e-4;  // include/gvr/tracer.hpp:28
