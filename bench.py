@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured graph")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 multi-view batch measurement")
+    ap.add_argument("--c3-views", type=int, default=64, help="C3 batch size (views over all ranks)")
     return ap.parse_args()
 
 
@@ -195,6 +197,81 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def measure_c3(args, ctx, stream, dev, scene, cfg, rank, world):
+    """C3 (BASELINE.json configs[2]): a batch of 64 orbit views of the C2 scene at
+    512x512 (make_orbit_camera(2 pi v / 64, 0.3, 4, (0,0,4), 512, 512, 1.6*512),
+    shapes.cpp:118-141), fwd + ScalarLoss + bwd per view, sharded by view over the
+    ranks (64/N views each; strong scaling, no data-path collective). All of a
+    rank's views run concurrently (gvr_render_views / _loss_views / _backward_views
+    on worker streams), captured as one CUDA graph; per-view gradient bundles are
+    written to device buffers."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_15401_b200 as gvr
+    from paper_2205_15401_b200 import synthetic
+
+    V_all = args.c3_views
+    mine = [v for v in range(V_all) if v % world == rank]
+    cams = [synthetic.make_orbit_camera(2 * np.pi * v / V_all, 0.3, 4.0, (0, 0, 4), IMAGE, IMAGE, 1.6 * IMAGE)
+            for v in mine]
+    K = scene.size
+    dscene = gvr.DeviceScene(ctx)
+    dscene.set_raw(K, 3, scene.tau, torch.from_numpy(scene.centers).to(dev), torch.from_numpy(scene.inv_cov).to(dev),
+                   torch.from_numpy(scene.attr).to(dev))
+    tapes = [gvr.Tape(ctx) for _ in mine]
+    rng = np.random.default_rng(1000)
+    imgs = [torch.empty((IMAGE, IMAGE, 3), dtype=torch.float64, device=dev) for _ in mine]
+    alphas = [torch.empty((IMAGE, IMAGE, 1), dtype=torch.float64, device=dev) for _ in mine]
+    depths = [torch.empty((IMAGE, IMAGE, 1), dtype=torch.float64, device=dev) for _ in mine]
+    ti = [torch.tensor(rng.uniform(0, 1, (IMAGE, IMAGE, 3)), device=dev) for _ in mine]
+    ta = [torch.tensor(rng.uniform(0, 1, (IMAGE, IMAGE, 1)), device=dev) for _ in mine]
+    losses = torch.zeros(len(mine), dtype=torch.float64, device=dev)
+    outs = [dict(d_center=torch.empty((K, 3), dtype=torch.float64, device=dev),
+                 d_inv_cov=torch.empty((K, 3, 3), dtype=torch.float64, device=dev),
+                 d_attr=torch.empty((K, 3), dtype=torch.float64, device=dev),
+                 d_rotation=torch.empty((3, 3), dtype=torch.float64, device=dev),
+                 d_translation=torch.empty(3, dtype=torch.float64, device=dev)) for _ in mine]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        gvr.render_views_into(ctx, dscene, cams, cfg, tapes, images=imgs, alphas=alphas, depths=depths)
+        gvr.scalar_loss_views_into(ctx, tapes, ti, ta, 1.0, 1.0, losses)
+        gvr.backward_views_into(ctx, tapes, gvr.GradFlags(), outs)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    n0 = ctx.launch_count
+    step()
+    launches_per_step = ctx.launch_count - n0
+    with ctx.capture() as graph:
+        step()
+    for _ in range(3):
+        graph.launch()
+    torch.cuda.synchronize(dev)
+    steps = max(3, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record(stream)
+        graph.launch()
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    total = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    return {"workload": f"C3: {V_all} orbit views 512x512 of the C2 scene, fwd+bwd per view, sharded by view "
+                        f"({len(mine)} views on rank 0 of {world})",
+            "value": V_all / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "views_per_step": V_all,
+            "scaling": "strong", "steps": steps, "gpu_launches": launches_per_step * steps,
+            "mean_loss": float(losses.mean().item())}
 
 
 def run_ours(args):
@@ -371,6 +448,11 @@ def run_ours(args):
                "path": "gvr_scene_set(host) -> gvr_render(host image/alpha/depth) -> gvr_scalar_loss(host targets, "
                        "host loss) -> gvr_backward(host GradientBundle)"}
 
+    # ---------------- C3 multi-view batch (configs[2])
+    c3 = None
+    if not args.no_c3:
+        c3 = measure_c3(args, ctx, stream, dev, scene, cfg, rank, world)
+
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -391,7 +473,7 @@ def run_ours(args):
                        "views": "every rank renders the C2 view (weak scaling)",
                        "l2": "flushed (256 MB write) between timed steps, outside the timed window",
                        "step": "render_with_tape -> ScalarLoss (device) -> backward, inputs resident in HBM"},
-            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks, "c3": c3,
             "gpu_launches": launches, "graph": not args.no_graph,
             "loss": float(loss.item()),
         }

@@ -242,6 +242,22 @@ int gvr_tape_normalized_weights(gvr_context* ctx, const gvr_tape* tape, double e
 int gvr_shade_lambert(gvr_context* ctx, const gvr_camera* camera, const double* normals, const double* alpha,
                       const double* depth, const double* light_pos, const double* light_color, double* out);
 
+/* ---- multi-view batches (C3 view-sharded renders, C5 fitting) ------------- */
+/* n_views independent renders of one scene (SURVEY.md §8b "batched variants
+ * over V cameras"): view v uses cameras[v], tapes[v] (distinct tapes) and
+ * outs[v] (outs nullable). The views run concurrently on internal worker
+ * streams forked from and joined into the context stream (graph-capturable). */
+int gvr_render_views(gvr_context* ctx, const gvr_scene* scene, int32_t n_views, const gvr_camera* cameras,
+                     const gvr_selection* cfg, gvr_tape* const* tapes, const gvr_render_outputs* outs);
+/* ScalarLoss of every view against its own targets; losses[n_views] nullable. */
+int gvr_scalar_loss_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes, const double* const* target_images,
+                          const double* const* target_alphas, double w_image, double w_alpha, double* losses);
+/* Backward of every view from the upstream stored by gvr_scalar_loss_views.
+ * outs[n_views] (per-view bundles) and / or sum (+= the sum over views, views
+ * added in ascending order) — DEVICE pointers, either nullable. */
+int gvr_backward_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes, const gvr_grad_flags* flags,
+                       const gvr_gradients* outs, const gvr_gradients* sum);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,9 @@ from .render import (  # noqa: F401
     adam_step,
     backward,
     backward_into,
+    backward_views_into,
+    render_views_into,
+    scalar_loss_views_into,
     default_context,
     render,
     render_into,

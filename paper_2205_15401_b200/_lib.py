@@ -55,6 +55,9 @@ EXPORTED_SYMBOLS = (
     "gvr_tape_transmittance",
     "gvr_tape_normalized_weights",
     "gvr_shade_lambert",
+    "gvr_render_views",
+    "gvr_scalar_loss_views",
+    "gvr_backward_views",
 )
 
 
@@ -160,6 +163,12 @@ def load() -> ctypes.CDLL:
         "gvr_scene_resynthesize": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp]),
         "gvr_tape_transmittance": (ctypes.c_int, [vp, vp, vp, vp]),
         "gvr_tape_normalized_weights": (ctypes.c_int, [vp, vp, dp, vp]),
+        "gvr_render_views": (ctypes.c_int, [vp, vp, i32, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection),
+                                            ctypes.POINTER(vp), ctypes.POINTER(GvrRenderOutputs)]),
+        "gvr_scalar_loss_views": (ctypes.c_int, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                                 dp, dp, vp]),
+        "gvr_backward_views": (ctypes.c_int, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(GvrGradFlags),
+                                              ctypes.POINTER(GvrGradients), ctypes.POINTER(GvrGradients)]),
         "gvr_shade_lambert": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():

@@ -90,6 +90,11 @@ struct gvr_context {
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
     Buf scratch[4];           // staging of host inputs / outputs of the helper entry points
+    // multi-view calls: views run on worker streams forked from / joined into `stream`
+    std::vector<cudaStream_t> workers;
+    std::vector<cudaEvent_t> join_ev;
+    cudaEvent_t fork_ev = nullptr;
+    Buf ptr_table;
     gvr_tape* aux_tape = nullptr;  // render behind gvr_sample_attributes
 };
 
@@ -133,6 +138,9 @@ struct gvr_tape {
     Buf acc, d_attr, d_center, d_inv_cov, d_rt;
     // host copy-out staging
     Buf stage_i, stage_w;
+    // [0] dropped_behind (int), [1] nonfinite (int), [2..3] loss (double); pinned mirror
+    Buf flags;
+    int* h_flags = nullptr;
 };
 
 namespace {
@@ -399,6 +407,10 @@ void gvr_context_destroy(gvr_context* ctx) {
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     ctx->flags.release();
     for (Buf& b : ctx->scratch) b.release();
+    ctx->ptr_table.release();
+    for (cudaStream_t w : ctx->workers) cudaStreamDestroy(w);
+    for (cudaEvent_t e : ctx->join_ev) cudaEventDestroy(e);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     if (ctx->aux_tape) gvr_tape_destroy(ctx->aux_tape);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -596,6 +608,11 @@ int gvr_tape_create(gvr_context* ctx, gvr_tape** out) {
     if (!ctx || !out) return GVR_ERR_RUNTIME;
     auto* t = new gvr_tape();
     t->ctx = ctx;
+    if (t->flags.ensure(64) != cudaSuccess || cudaMallocHost(&t->h_flags, 64) != cudaSuccess) {
+        t->flags.release();
+        delete t;
+        return set_err(ctx, GVR_ERR_RUNTIME, "tape allocation failed");
+    }
     *out = t;
     return GVR_OK;
 }
@@ -605,8 +622,9 @@ void gvr_tape_destroy(gvr_tape* t) {
     cudaStreamSynchronize(t->ctx->stream);
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_lists, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
-                   &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w};
+                   &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags};
     for (Buf* b : bufs) b->release();
+    if (t->h_flags) cudaFreeHost(t->h_flags);
     delete t;
 }
 
@@ -624,8 +642,14 @@ int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camer
     return gvr_render_shard(ctx, scene, camera, cfg, tape, out, 0, 1);
 }
 
-int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera, const gvr_selection* cfg,
-                     gvr_tape* tape, const gvr_render_outputs* out, int32_t shard, int32_t nshards) {
+}  // extern "C"
+
+// Enqueues one render on ctx->stream. Host outputs are copied asynchronously;
+// *host_out is set when the caller must synchronise (then check the tape's
+// nonfinite flag, mirrored into tape->h_flags[1]).
+static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera, const gvr_selection* cfg,
+                       gvr_tape* tape, const gvr_render_outputs* out, int32_t shard, int32_t nshards, bool* host_out) {
+    *host_out = false;
     if (!ctx || !scene || !tape) return GVR_ERR_RUNTIME;
     if (nshards < 1 || shard < 0 || shard >= nshards)
         return set_err(ctx, GVR_ERR_RUNTIME, "bad tile shard %d of %d", shard, nshards);
@@ -691,7 +715,7 @@ int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera*
     const bool want_w = out && out->topk_w;
     if (want_w) CUDA_TRY(ctx, tape->topk_w.ensure(sizeof(double) * (size_t)P * kp));
 
-    int* dflags = ctx->flags.as<int>();
+    int* dflags = tape->flags.as<int>();
     int* tile_count = tape->tile_count.as<int>();
     int* sched = tape->sched.as<int>();
     int* order_f = sched + 2;
@@ -803,16 +827,33 @@ int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera*
             host = host || !dev_i || !dev_w;
         }
         if (host) {
-            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 1, dflags + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-            if ((rc = sync_and_check(ctx))) return rc;
-            if (ctx->h_flags[1]) {
-                tape->valid = false;
-                return set_err(ctx, GVR_ERR_VALIDATION, "image contains non-finite values");
-            }
+            CUDA_TRY(ctx, cudaMemcpyAsync(tape->h_flags + 1, dflags + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            *host_out = true;
         }
     }
     return GVR_OK;
 }
+
+// validate_finite (blender.cpp:132-134) after the host copy-out has completed.
+static int check_finite(gvr_context* ctx, gvr_tape* tape) {
+    if (tape->h_flags[1]) {
+        tape->valid = false;
+        return set_err(ctx, GVR_ERR_VALIDATION, "image contains non-finite values");
+    }
+    return GVR_OK;
+}
+
+extern "C" int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
+                                const gvr_selection* cfg, gvr_tape* tape, const gvr_render_outputs* out, int32_t shard,
+                                int32_t nshards) {
+    bool host = false;
+    if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
+    if (!host) return GVR_OK;
+    if (int rc = sync_and_check(ctx)) return rc;
+    return check_finite(ctx, tape);
+}
+
+extern "C" {
 
 int gvr_tape_traced(gvr_context* ctx, const gvr_tape* t, int32_t* idx, double* l, double* q, double* sigma) {
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
@@ -845,8 +886,15 @@ int gvr_tape_traced(gvr_context* ctx, const gvr_tape* t, int32_t* idx, double* l
 
 // ---------------------------------------------------------------- loss / backward
 
-int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, const double* target_alpha,
-                    double w_image, double w_alpha, double* loss_out, double* d_image_out, double* d_alpha_out) {
+}  // extern "C"
+
+// ScalarLoss on ctx->stream; the loss lands in the tape (flags + 8 B) and, when
+// loss_dev is given, is also added into *loss_dev (zeroed first). *host_out
+// set when host copies are pending (caller synchronises).
+static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_image, const double* target_alpha,
+                            double w_image, double w_alpha, double* loss_out, double* d_image_out, double* d_alpha_out,
+                            bool* host_out) {
+    *host_out = false;
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
     if (!target_image || !target_alpha) return set_err(ctx, GVR_ERR_RUNTIME, "targets must not be null");
     const long long P = (long long)t->H * t->W;
@@ -867,7 +915,7 @@ int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, c
         CUDA_TRY(ctx, cudaMemcpyAsync(talpha, target_alpha, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
         ta = talpha;
     }
-    double* dloss = reinterpret_cast<double*>(ctx->flags.as<int>() + 4);
+    double* dloss = reinterpret_cast<double*>(t->flags.as<int>() + 2);
     CUDA_TRY(ctx, cudaMemsetAsync(dloss, 0, sizeof(double), ctx->stream));
     const int threads = 256;
     const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), 148 * 8);
@@ -885,9 +933,21 @@ int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, c
     if ((rc = copy_out(ctx, d_image_out, t->d_image.p, sizeof(double) * n_img, &host))) return rc;
     if ((rc = copy_out(ctx, d_alpha_out, t->d_alpha.p, sizeof(double) * P, &host))) return rc;
     if ((rc = copy_out(ctx, loss_out, dloss, sizeof(double), &host))) return rc;
-    if (host) return sync_and_check(ctx);
+    *host_out = host;
     return GVR_OK;
 }
+
+extern "C" int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* target_image, const double* target_alpha,
+                               double w_image, double w_alpha, double* loss_out, double* d_image_out,
+                               double* d_alpha_out) {
+    bool host = false;
+    if (int rc = scalar_loss_impl(ctx, t, target_image, target_alpha, w_image, w_alpha, loss_out, d_image_out,
+                                  d_alpha_out, &host))
+        return rc;
+    return host ? sync_and_check(ctx) : GVR_OK;
+}
+
+extern "C" {
 
 int gvr_backward(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
                  const gvr_grad_flags* flags, const gvr_gradients* out) {
@@ -1250,6 +1310,195 @@ int gvr_shade_lambert(gvr_context* ctx, const gvr_camera* camera, const double* 
         bool h2 = false;
         if (int rc = copy_out(ctx, out, dout, sizeof(double) * 3 * P, &h2)) return rc;
         return sync_and_check(ctx);
+    }
+    return GVR_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- multi-view (C3 / C5 batches)
+//
+// The views of one call are independent renders of the same scene (SURVEY.md
+// §8b "batched variants over V cameras"). A single C2 view fills only part of
+// the B200 (its per-tile kernels are latency bound at ~1000 tiles), so the
+// views are spread round-robin over worker streams forked from the context
+// stream and joined back into it: kernels of different views overlap, and the
+// whole fork/join pattern is capturable in one CUDA graph.
+
+namespace {
+
+constexpr int kViewStreams = 8;
+constexpr int kSumViews = 64;  // views per gradient-sum launch (kernel parameter space)
+
+struct ViewSumParams {
+    int V;
+    long long n[5];
+    const double* src[kSumViews][5];
+    double* dst[5];
+};
+
+// sum[b][i] += sum_v src[v][b][i], views in ascending order (deterministic).
+__global__ void view_sum_kernel(ViewSumParams p) {
+    for (int b = 0; b < 5; ++b) {
+        if (!p.dst[b]) continue;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n[b];
+             i += (long long)gridDim.x * blockDim.x) {
+            double acc = p.dst[b][i];
+            for (int v = 0; v < p.V; ++v) acc += p.src[v][b][i];
+            p.dst[b][i] = acc;
+        }
+    }
+}
+
+int ensure_workers(gvr_context* ctx, int n) {
+    if (!ctx->fork_ev) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    while ((int)ctx->workers.size() < n) {
+        cudaStream_t s;
+        cudaEvent_t e;
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->workers.push_back(s);
+        ctx->join_ev.push_back(e);
+    }
+    return GVR_OK;
+}
+
+int fork_workers(gvr_context* ctx, int n) {
+    if (int rc = ensure_workers(ctx, n)) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, ctx->stream));
+    for (int w = 0; w < n; ++w) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->workers[w], ctx->fork_ev, 0));
+    return GVR_OK;
+}
+
+int join_workers(gvr_context* ctx, cudaStream_t home, int n) {
+    ctx->stream = home;
+    for (int w = 0; w < n; ++w) {
+        CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev[w], ctx->workers[w]));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(home, ctx->join_ev[w], 0));
+    }
+    return GVR_OK;
+}
+
+// Runs fn(v) for every view on worker stream v % n, then joins; the first
+// error is returned after the join (so a capture is never left forked).
+template <typename F>
+int for_views(gvr_context* ctx, int V, F&& fn) {
+    if (V <= 0) return GVR_OK;
+    const int n = V < kViewStreams ? V : kViewStreams;
+    cudaStream_t home = ctx->stream;
+    if (int rc = fork_workers(ctx, n)) return rc;
+    int first = GVR_OK;
+    std::string err;
+    for (int v = 0; v < V && first == GVR_OK; ++v) {
+        ctx->stream = ctx->workers[v % n];
+        const int rc = fn(v);
+        if (rc != GVR_OK) {
+            first = rc;
+            err = ctx->err;
+        }
+    }
+    const int jr = join_workers(ctx, home, n);
+    if (first != GVR_OK) {
+        ctx->err = err;
+        return first;
+    }
+    return jr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gvr_render_views(gvr_context* ctx, const gvr_scene* scene, int32_t n_views, const gvr_camera* cameras,
+                     const gvr_selection* cfg, gvr_tape* const* tapes, const gvr_render_outputs* outs) {
+    if (!ctx || !scene || !tapes || (n_views > 0 && !cameras)) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (n_views < 0) return set_err(ctx, GVR_ERR_RUNTIME, "n_views must be >= 0");
+    for (int v = 0; v < n_views; ++v) {  // host-side checks first: nothing is enqueued for an invalid batch
+        if (!tapes[v]) return set_err(ctx, GVR_ERR_RUNTIME, "tape %d is null", v);
+        for (int u = 0; u < v; ++u)
+            if (tapes[u] == tapes[v]) return set_err(ctx, GVR_ERR_RUNTIME, "views %d and %d share a tape", u, v);
+        if (int rc = validate_camera(ctx, cameras + v)) return rc;
+    }
+    if (int rc = validate_cfg(ctx, cfg)) return rc;
+    bool any_host = false;
+    const int rc = for_views(ctx, n_views, [&](int v) {
+        bool host = false;
+        const int r = render_impl(ctx, scene, cameras + v, cfg, tapes[v], outs ? outs + v : nullptr, 0, 1, &host);
+        any_host = any_host || host;
+        return r;
+    });
+    if (rc) return rc;
+    if (!any_host) return GVR_OK;
+    if (int r = sync_and_check(ctx)) return r;
+    for (int v = 0; v < n_views; ++v)
+        if (int r = check_finite(ctx, tapes[v])) return r;
+    return GVR_OK;
+}
+
+int gvr_scalar_loss_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes, const double* const* target_images,
+                          const double* const* target_alphas, double w_image, double w_alpha, double* losses) {
+    if (!ctx || !tapes || (n_views > 0 && (!target_images || !target_alphas)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    bool any_host = false;
+    const int rc = for_views(ctx, n_views, [&](int v) {
+        bool host = false;
+        const int r = scalar_loss_impl(ctx, tapes[v], target_images[v], target_alphas[v], w_image, w_alpha,
+                                       losses ? losses + v : nullptr, nullptr, nullptr, &host);
+        any_host = any_host || host;
+        return r;
+    });
+    if (rc) return rc;
+    return any_host ? sync_and_check(ctx) : GVR_OK;
+}
+
+int gvr_backward_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes, const gvr_grad_flags* flags,
+                       const gvr_gradients* outs, const gvr_gradients* sum) {
+    if (!ctx || !tapes) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    auto dev_ok = [](const gvr_gradients* g) {
+        const void* ps[5] = {g->d_center, g->d_inv_cov, g->d_attr, g->d_rotation, g->d_translation};
+        for (const void* q : ps)
+            if (q && !is_device_ptr(q)) return false;
+        return true;
+    };
+    for (int v = 0; v < n_views; ++v) {
+        if (!tapes[v] || !tapes[v]->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape %d is not valid", v);
+        if (!tapes[v]->has_upstream)
+            return set_err(ctx, GVR_ERR_RUNTIME, "tape %d has no upstream gradient (gvr_scalar_loss_views first)", v);
+        if (outs && !dev_ok(outs + v)) return set_err(ctx, GVR_ERR_RUNTIME, "gvr_backward_views needs device outputs");
+    }
+    if (sum && !dev_ok(sum)) return set_err(ctx, GVR_ERR_RUNTIME, "gvr_backward_views needs device outputs");
+    if (sum)
+        for (int v = 1; v < n_views; ++v)
+            if (tapes[v]->K != tapes[0]->K || tapes[v]->D != tapes[0]->D)
+                return set_err(ctx, GVR_ERR_RUNTIME, "summed views must share the scene size");
+    int rc = for_views(ctx, n_views, [&](int v) {
+        return backward_impl(ctx, tapes[v], nullptr, nullptr, flags, outs ? outs + v : nullptr, false);
+    });
+    if (rc || !sum || n_views == 0) return rc;
+    const int K = tapes[0]->K, D = tapes[0]->D;
+    for (int v0 = 0; v0 < n_views; v0 += kSumViews) {
+        ViewSumParams sp{};
+        sp.V = std::min(kSumViews, n_views - v0);
+        sp.n[0] = 3ll * K;
+        sp.n[1] = 9ll * K;
+        sp.n[2] = (long long)D * K;
+        sp.n[3] = 9;
+        sp.n[4] = 3;
+        sp.dst[0] = sum->d_center;
+        sp.dst[1] = sum->d_inv_cov;
+        sp.dst[2] = D > 0 ? sum->d_attr : nullptr;
+        sp.dst[3] = sum->d_rotation;
+        sp.dst[4] = sum->d_translation;
+        for (int v = 0; v < sp.V; ++v) {
+            const gvr_tape* t = tapes[v0 + v];
+            sp.src[v][0] = t->d_center.as<double>();
+            sp.src[v][1] = t->d_inv_cov.as<double>();
+            sp.src[v][2] = t->d_attr.as<double>();
+            sp.src[v][3] = t->d_rt.as<double>();
+            sp.src[v][4] = t->d_rt.as<double>() + 9;
+        }
+        view_sum_kernel<<<148 * 4, 256, 0, ctx->stream>>>(sp);
+        LAUNCH_CHECK(ctx);
     }
     return GVR_OK;
 }

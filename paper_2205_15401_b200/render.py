@@ -499,3 +499,60 @@ def shade_lambert(normals, alpha, depth, camera: Camera, light_pos, light_color,
     ctx.check(ctx.lib.gvr_shade_lambert(ctx.handle, ctypes.byref(cam_c), _ptr(n), _ptr(al1), _ptr(de1), _ptr(lp),
                                         _ptr(lc), _ptr(out)))
     return out
+
+
+# ---------------------------------------------------------------- multi-view batches (C3 / C5)
+
+
+def _ptr_array(objs):
+    arr = (ctypes.c_void_p * max(len(objs), 1))()
+    for i, o in enumerate(objs):
+        arr[i] = _ptr(o) if not isinstance(o, Tape) else o.handle.value
+    return arr
+
+
+def render_views_into(ctx: Context, dscene: DeviceScene, cameras, cfg: SelectionConfig, tapes, images=None,
+                      alphas=None, depths=None, topk_idx=None, topk_w=None) -> None:
+    """``gvr_render_views``: one render per camera, the views running concurrently
+    on the context's worker streams. Output lists (host or device buffers, any
+    may be None or contain None) are indexed like ``cameras``."""
+    n = len(cameras)
+    if len(tapes) != n:
+        raise ValueError("one tape per view")
+    cams = (_lib.GvrCamera * max(n, 1))(*[_camera_c(c) for c in cameras])
+    pick = lambda lst, v: None if lst is None else lst[v]  # noqa: E731
+    outs = (_lib.GvrRenderOutputs * max(n, 1))(*[
+        _lib.GvrRenderOutputs(_ptr(pick(images, v)), _ptr(pick(alphas, v)), _ptr(pick(depths, v)),
+                              _ptr(pick(topk_idx, v)), _ptr(pick(topk_w, v))) for v in range(n)])
+    th = _ptr_array(tapes)
+    sel_c = _selection_c(cfg)
+    ctx.check(ctx.lib.gvr_render_views(ctx.handle, dscene.handle, n, cams, ctypes.byref(sel_c), th, outs))
+    for v, t in enumerate(tapes):
+        t.scene, t.camera, t.cfg = dscene, cameras[v], cfg
+
+
+def scalar_loss_views_into(ctx: Context, tapes, target_images, target_alphas, w_image: float = 1.0,
+                           w_alpha: float = 1.0, losses=None) -> None:
+    """``gvr_scalar_loss_views``: per-view ScalarLoss; ``losses`` [V] host or device (nullable)."""
+    n = len(tapes)
+    ctx.check(ctx.lib.gvr_scalar_loss_views(ctx.handle, n, _ptr_array(tapes), _ptr_array(target_images),
+                                            _ptr_array(target_alphas), float(w_image), float(w_alpha),
+                                            _ptr(losses)))
+
+
+def backward_views_into(ctx: Context, tapes, flags: GradFlags = GradFlags(), outs=None, total=None) -> None:
+    """``gvr_backward_views``: per-view gradients into ``outs`` (list of dicts of device
+    tensors with keys d_center, d_inv_cov, d_attr, d_rotation, d_translation; entries
+    may be missing) and / or their sum added into ``total`` (same dict form)."""
+    n = len(tapes)
+
+    def bundle(g):
+        g = g or {}
+        return _lib.GvrGradients(*[_ptr(g.get(k)) for k in ("d_center", "d_inv_cov", "d_attr", "d_rotation",
+                                                               "d_translation")])
+
+    f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
+    o = (_lib.GvrGradients * max(n, 1))(*[bundle(outs[v]) for v in range(n)]) if outs is not None else None
+    t = bundle(total) if total is not None else None
+    ctx.check(ctx.lib.gvr_backward_views(ctx.handle, n, _ptr_array(tapes), ctypes.byref(f), o,
+                                         ctypes.byref(t) if t is not None else None))
