@@ -69,32 +69,79 @@ __device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u,
     return 1;
 }
 
-// Loads a tile's candidate list into shared memory sorted ascending by
-// (depth bound zmin, id): CTA-wide bitonic sort (the lists are short: the
-// exact screen-box binning keeps C2 tiles at a few hundred entries). Returns
-// the list length, or -1 when the tile overflowed its capacity (the caller
-// then streams every kernel, unsorted, with the same exact tests).
+// Loads a tile's candidate list into shared memory in ascending order of a
+// depth bound: a CTA counting sort over 256 buckets spanning the tile's own
+// zmin range (3 passes over the list, 4 barriers; entries inside a bucket stay
+// in arbitrary order). The high word of each key is replaced by its bucket's
+// lower bound, so keys[e] >> 32 is non-decreasing along the list and bounds the
+// zmin (hence the l) of every entry at or after e -- all the early exit needs.
+// The selection itself is exact and independent of the visiting order.
+// Returns the list length, or -1 when the tile overflowed its capacity (the
+// caller then streams every kernel, unsorted, with the same exact tests).
 __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys) {
+    constexpr int NB = 256;
+    __shared__ unsigned s_lo, s_hi;
+    __shared__ int s_hist[NB];
     const int count = p.tile_count[tile];
     if (count > p.cap) return -1;
-    int pw = 1;
-    while (pw < count) pw <<= 1;
     const unsigned long long* src = p.tile_lists + (size_t)tile * p.cap;
-    for (int e = threadIdx.x; e < pw; e += blockDim.x) keys[e] = e < count ? src[e] : ~0ull;
+    if (threadIdx.x == 0) {
+        s_lo = 0xffffffffu;
+        s_hi = 0u;
+    }
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) s_hist[b] = 0;
     __syncthreads();
-    for (int size = 2; size <= pw; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int idx = threadIdx.x; idx < (pw >> 1); idx += blockDim.x) {
-                const int a = ((idx & ~(stride - 1)) << 1) | (idx & (stride - 1)), b = a + stride;
-                const unsigned long long ka = keys[a], kb = keys[b];
-                if ((ka > kb) == ((a & size) == 0)) {
-                    keys[a] = kb;
-                    keys[b] = ka;
-                }
-            }
-            __syncthreads();
+    unsigned lo = 0xffffffffu, hi = 0u;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const unsigned z = (unsigned)(src[e] >> 32);
+        lo = min(lo, z);
+        hi = max(hi, z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && count > 0) {
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+    }
+    __syncthreads();
+    lo = s_lo;
+    const unsigned range = count > 0 ? s_hi - lo : 0u;
+    int shift = 0;
+    while ((range >> shift) >= (unsigned)NB) ++shift;
+    for (int e = threadIdx.x; e < count; e += blockDim.x)
+        atomicAdd(&s_hist[((unsigned)(src[e] >> 32) - lo) >> shift], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 buckets, 8 per lane
+        int vals[8], run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            vals[q] = s_hist[threadIdx.x * 8 + q];
+            run += vals[q];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (threadIdx.x >= o) incl += y;
+        }
+        int base = incl - run;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            s_hist[threadIdx.x * 8 + q] = base;
+            base += vals[q];
         }
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const unsigned long long k = src[e];
+        const unsigned b = ((unsigned)(k >> 32) - lo) >> shift;
+        const unsigned long long bound = (unsigned long long)(lo + (b << shift));
+        keys[atomicAdd(&s_hist[b], 1)] = (bound << 32) | (k & 0xffffffffull);
+    }
+    __syncthreads();
     return count;
 }
 
@@ -233,7 +280,8 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         const int cnt = min(32, end - base);
         for (int c0 = 0; c0 < cnt && !done; c0 += 4) {
             // early exit: every later candidate has l >= zmin > worst kept (+ key error)
-            if (!overflow && (double)chunk[c0].r.zmin > wl + 1e-11 * fabs(wl)) {
+            if (!overflow &&
+                (double)float_from_order_bits((uint32_t)(keys[base + c0] >> 32)) > wl + 1e-11 * fabs(wl)) {
                 done = true;
                 break;
             }
