@@ -36,12 +36,13 @@ struct BwdParams {
 // 1e-4 of a class-scaled floor, ~1e-7 of the largest gradient).
 template <int KMAX>
 __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdParams p) {
-    constexpr int TILE = 8, NP = 64;
+    constexpr int TILE = 8, NP = 64, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]
     double* b_dl = reinterpret_cast<double*>(smem);  // l_k - l_0
     double* b_da = b_dl + KMAX * NP;                 // d_acc_k = -tau T_k d_w_k e^{q_k}
-    float* b_pk = reinterpret_cast<float*>(b_da + KMAX * NP);  // e^{q_k}
+    double* b_dt = b_da + KMAX * NP;                 // density path d_w_k T_k (grad.cpp:120)
+    float* b_pk = reinterpret_cast<float*>(b_dt + KMAX * NP);  // e^{q_k}
     float* b_is = b_pk + KMAX * NP;                  // 1 / sigma_k
     int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
 
@@ -66,8 +67,17 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
     // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
     double peak_part = 0.0;
-    for (int s = sub; s < n; s += 4) {
-        const int k = p.topk[pix * p.kp + s];
+    int ids[PER];  // ids first: the id -> record load chains of the entries overlap
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        ids[q] = s < n ? p.topk[pix * p.kp + s] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        if (s >= n) continue;
+        const int k = ids[q];
         const Traced64 t = trace_fast(d, p.rec64[k]);
         const double pk64 = exp(t.q);
         const float pkf = (float)pk64;
@@ -87,6 +97,7 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
         }
         b_dl[s * NP + g] = t.l - l0;
         b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
+        b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
         b_pk[s * NP + g] = pkf;
         b_is[s * NP + g] = (float)sqrt(t.a);
         b_id[s * NP + g] = k;
@@ -104,16 +115,7 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
         const double pke = (double)b_pk[e * NP + g];
         const double dae = b_da[e * NP + g];
         const int kid = b_id[e * NP + g];
-        double dpk = d_total;
-        if (p.through_rho) {
-            double dw = 0.0;
-            if (p.D <= 4) {
-                for (int c = 0; c < p.D; ++c) dw += dimg[c] * p.attr[(long long)p.D * kid + c];
-            } else {
-                for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * kid + c];
-            }
-            if (dw != 0.0) dpk += dw * p.tape_t[pix * p.kp + e];  // density path (grad.cpp:120)
-        }
+        double dpk = d_total + b_dt[e * NP + g];  // density path (grad.cpp:120)
         double dl = 0.0, dsg = 0.0;
         for (int k = 0; k < n; ++k) {
             const double dak = b_da[k * NP + g];

@@ -34,6 +34,7 @@ struct FwdParams {
     double* topk_w; // [P*kp] or null
     double* tape_t; // [P*kp] T(l_k) of the selected entries (backward input)
     float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
+    int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
     int* nonfinite; // flag
 };
 
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
 // The sum is accumulated in FP64 and T(l_k) is taped for the backward.
 template <int KMAX>
 __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p) {
-    constexpr int TILE = 8, NP = 64;
+    constexpr int TILE = 8, NP = 64, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
     double* b_dl = reinterpret_cast<double*>(smem);  // [slot][pixel] l - l0
     double* b_w = b_dl + KMAX * NP;                  // W_k
@@ -538,20 +539,32 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     double d[3];
     pixel_ray(p.cam, i, j, d);
     double peak_part = 0.0;
-    for (int s = sub; s < n; s += 4) {
-        const int k = p.topk[pix * kp + s];
-        const Traced64 t = trace_fast(d, p.rec64[k]);
-        const double pk = exp(t.q);
-        peak_part += pk;
-        b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
-        b_pk[s * NP + g] = (float)pk;
-        b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
-        b_id[s * NP + g] = k;
+    // ids first (independent loads), then the traces: the id -> record load
+    // chains of a thread's entries overlap instead of running back to back
+    int ids[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        ids[q] = s < n ? p.topk[pix * kp + s] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        if (s < n) {
+            const int k = ids[q];
+            const Traced64 t = trace_fast(d, p.rec64[k]);
+            const double pk = exp(t.q);
+            peak_part += pk;
+            b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
+            b_pk[s * NP + g] = (float)pk;
+            b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
+            b_id[s * NP + g] = k;
+        }
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
     peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
     __syncwarp(grp);
-    if (sub == 0) {
+    if (sub == 0 && !p.presorted) {
         // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort;
         // keys closer than the fast-trace error are compared on exact l
         for (int s = 1; s < n; ++s) {
@@ -583,8 +596,10 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     __syncwarp(grp);
     for (int s = sub; s < n; s += 4) {
         b_dl[s * NP + g] -= l0;
-        b_id[s * NP + g] &= ~kExact;
-        p.topk[pix * kp + s] = b_id[s * NP + g];
+        if (!p.presorted) {
+            b_id[s * NP + g] &= ~kExact;
+            p.topk[pix * kp + s] = b_id[s * NP + g];
+        }
     }
     __syncwarp(grp);
 
@@ -602,29 +617,49 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
         if (p.topk_w) p.topk_w[pix * kp + k] = wd;
     }
     __syncwarp(grp);
+    const double alpha = 1.0 - exp(-p.tau * peak_part);
+    if (p.D <= 3) {
+        // ordered sums, one thread per output, products loaded 4 ahead:
+        // image[c] = sum_k W_k attr_k[c] exactly in ascending (l, idx) order
+        if (sub < p.D) {
+            double img = 0.0;
+            int k = 0;
+            for (; k + 4 <= n; k += 4) {
+                double a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = p.attr[(long long)p.D * b_id[(k + u) * NP + g] + sub];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) img = xadd(img, xmul(b_w[(k + u) * NP + g], a[u]));
+            }
+            for (; k < n; ++k) img = xadd(img, xmul(b_w[k * NP + g], p.attr[(long long)p.D * b_id[k * NP + g] + sub]));
+            p.image[pix * p.Dc + sub] = img;
+        } else if (sub == 3) {
+            if (p.D == 0) p.image[pix * p.Dc] = 0.0;
+            double wsum = 0.0, wld = 0.0;
+            for (int k = 0; k < n; ++k) {
+                const double wd = b_w[k * NP + g];
+                wsum += wd;
+                wld += wd * (l0 + b_dl[k * NP + g]);
+            }
+            const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
+            p.alpha[pix] = alpha;
+            p.depth[pix] = depth;
+            if (!isfinite(alpha) || !isfinite(depth) || !isfinite(wsum)) atomicExch(p.nonfinite, 1);
+        }
+        return;
+    }
     if (sub != 0) return;
-
-    double img[4] = {0.0, 0.0, 0.0, 0.0};
     double wsum = 0.0, wld = 0.0;
     for (int k = 0; k < n; ++k) {
         const double wd = b_w[k * NP + g];
         const int kid = b_id[k * NP + g];
-        if (p.D <= 4) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (c < p.D) img[c] = xadd(img[c], xmul(wd, p.attr[(long long)p.D * kid + c]));
-        } else {
-            for (int c = 0; c < p.D; ++c) {
-                const long long o = pix * p.Dc + c;
-                p.image[o] = xadd(k == 0 ? 0.0 : p.image[o], xmul(wd, p.attr[(long long)p.D * kid + c]));
-            }
+        for (int c = 0; c < p.D; ++c) {
+            const long long o = pix * p.Dc + c;
+            p.image[o] = xadd(k == 0 ? 0.0 : p.image[o], xmul(wd, p.attr[(long long)p.D * kid + c]));
         }
         wsum += wd;
         wld += wd * (l0 + b_dl[k * NP + g]);
     }
-    if (p.D <= 4)
-        for (int c = 0; c < p.Dc; ++c) p.image[pix * p.Dc + c] = img[c];
-    const double alpha = 1.0 - exp(-p.tau * peak_part);
     const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
     p.alpha[pix] = alpha;
     p.depth[pix] = depth;

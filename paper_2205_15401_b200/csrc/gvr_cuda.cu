@@ -306,7 +306,7 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
 
 template <int KMAX>
 int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
-    const size_t smem = 28ull * KMAX * 64;
+    const size_t smem = 36ull * KMAX * 64;
     auto kern = backward_pixels_kernel<KMAX>;
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
@@ -784,6 +784,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
     fp.tape_t = tape->tape_t.as<double>();
     fp.nonfinite = dflags + 1;
+    fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     int rc = GVR_OK;
     int* order_b = sched + 2 + tiles;
     if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
