@@ -229,25 +229,33 @@ __global__ void object_space_kernel(ObjParams p) {
 #pragma unroll
         for (int t = 0; t < 3; ++t) part[9 + t] = dm[t];
     }
-    // block reduction of the 12 camera-gradient components
-#pragma unroll
-    for (int t = 0; t < 12; ++t) {
-        double v = part[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        part[t] = v;
-    }
-    __shared__ double red[32][12];
+    // block reduction of the 12 camera-gradient components: a 16-value
+    // butterfly (each step halves the values a lane carries), then lane 2v
+    // holds the warp total of value v
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0)
+    double a[16];
 #pragma unroll
-        for (int t = 0; t < 12; ++t) red[warp][t] = part[t];
+    for (int t = 0; t < 16; ++t) a[t] = t < 12 ? part[t] : 0.0;
+#pragma unroll
+    for (int half = 8, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
+        const bool hi = lane & bit;
+#pragma unroll
+        for (int t = 0; t < half; ++t) {
+            const double send = hi ? a[t] : a[t + half];
+            const double keep = hi ? a[t + half] : a[t];
+            a[t] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+        }
+    }
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+    __shared__ double red[32][12];
+    const int v = lane >> 1;
+    if (!(lane & 1) && v < 12) red[warp][v] = a[0];
     __syncthreads();
     if (threadIdx.x < 12) {
-        double v = 0.0;
+        double acc = 0.0;
         const int nw = (blockDim.x + 31) / 32;
-        for (int w = 0; w < nw; ++w) v += red[w][threadIdx.x];
-        if (v != 0.0) atomicAdd(p.d_rt + threadIdx.x, v);
+        for (int w = 0; w < nw; ++w) acc += red[w][threadIdx.x];
+        if (acc != 0.0) atomicAdd(p.d_rt + threadIdx.x, acc);
     }
 }
 

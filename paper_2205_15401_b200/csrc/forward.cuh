@@ -594,8 +594,14 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     __syncwarp(grp);
     const double l0 = b_dl[g];
     __syncwarp(grp);
+    // l_k - l_0 as an unevaluated float pair hi + lo (replaces the double in place):
+    // hi_k - hi_m is exact whenever the pair's z is moderate (Sterbenz), so the
+    // argument z = (l_k - l_m) / sigma_m keeps ~1e-7 relative accuracy in FP32.
+    float2* b_hl = reinterpret_cast<float2*>(b_dl);
     for (int s = sub; s < n; s += 4) {
-        b_dl[s * NP + g] -= l0;
+        const double dl = b_dl[s * NP + g] - l0;
+        const float hi = (float)dl;
+        b_hl[s * NP + g] = make_float2(hi, (float)(dl - (double)hi));
         if (!p.presorted) {
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
@@ -604,12 +610,19 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     __syncwarp(grp);
 
     for (int k = sub; k < n; k += 4) {
-        const double dlk = b_dl[k * NP + g];
-        double acc = 0.0;
+        const float2 hk = b_hl[k * NP + g];
+        // sum_m e^{q_m} Phi(z_km): non-negative FP32 terms, Kahan-compensated
+        // (error ~2^-24 of the sum, below the 6e-8 of the Phi approximation)
+        float sum = 0.0f, comp = 0.0f;
         for (int m = 0; m < n; ++m) {
-            const float z = (float)(dlk - b_dl[m * NP + g]) * b_is[m * NP + g];
-            acc = fma((double)b_pk[m * NP + g], (double)fast_normal_cdf(z), acc);
+            const float2 hm = b_hl[m * NP + g];
+            const float z = ((hk.x - hm.x) + (hk.y - hm.y)) * b_is[m * NP + g];
+            const float y = fmaf(b_pk[m * NP + g], fast_normal_cdf(z), -comp);
+            const float t = sum + y;
+            comp = (t - sum) - y;
+            sum = t;
         }
+        const double acc = (double)sum - (double)comp;
         const double trans = exp(-p.tau * acc);
         const double wd = trans * (double)b_pk[k * NP + g];
         p.tape_t[pix * kp + k] = trans;
@@ -639,7 +652,8 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
             for (int k = 0; k < n; ++k) {
                 const double wd = b_w[k * NP + g];
                 wsum += wd;
-                wld += wd * (l0 + b_dl[k * NP + g]);
+                const float2 h = b_hl[k * NP + g];
+                wld += wd * (l0 + ((double)h.x + (double)h.y));
             }
             const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
             p.alpha[pix] = alpha;
@@ -658,7 +672,8 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
             p.image[o] = xadd(k == 0 ? 0.0 : p.image[o], xmul(wd, p.attr[(long long)p.D * kid + c]));
         }
         wsum += wd;
-        wld += wd * (l0 + b_dl[k * NP + g]);
+        const float2 h = b_hl[k * NP + g];
+        wld += wd * (l0 + ((double)h.x + (double)h.y));
     }
     const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
     p.alpha[pix] = alpha;
