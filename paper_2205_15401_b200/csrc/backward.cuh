@@ -116,30 +116,49 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
         const double dae = b_da[e * NP + g];
         const int kid = b_id[e * NP + g];
         double dpk = d_total + b_dt[e * NP + g];  // density path (grad.cpp:120)
-        double dl = 0.0, dsg = 0.0;
-        for (int k = 0; k < n; ++k) {
+        // branch-free pair terms, two independent accumulator sets (even / odd k)
+        // so that consecutive pairs overlap instead of serialising on one chain
+        double dpk2 = 0.0, dl = 0.0, dl2 = 0.0, dsg = 0.0, dsg2 = 0.0;
+        auto pair = [&](int k, double& a_pk, double& a_l, double& a_sg) {
             const double dak = b_da[k * NP + g];
             const double dlk = b_dl[k * NP + g];
             const float isk = b_is[k * NP + g];
             // pair (k, m = e): z1 = (l_k - l_e) / sigma_e ; pair (k = e, m = k): z2 = (l_e - l_k) / sigma_k
             const float dlf = (float)(dlk - dle);
             const float z1 = dlf * ise;
-            float phi1 = 0.0f;
-            if (dak != 0.0) {
-                dpk += dak * (double)fast_normal_cdf(z1);
-                if (k != e) {
-                    phi1 = normal_pdf_fast(z1);
-                    const double gg = dak * (double)(phi1 * ise) * pke;
-                    dl -= gg;
-                    dsg -= gg * (double)z1;
-                }
-            }
-            if (dae != 0.0 && k != e) {
-                // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
-                const float phi2 = (isk == ise && dak != 0.0) ? phi1 : normal_pdf_fast(-dlf * isk);
-                dl += dae * (double)(b_pk[k * NP + g] * phi2 * isk);
-            }
+            const float phi1 = normal_pdf_fast(z1);
+            // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
+            const float phi2 = isk == ise ? phi1 : normal_pdf_fast(-dlf * isk);
+            a_pk = fma(dak, (double)fast_normal_cdf(z1), a_pk);
+            const double gg = k != e ? dak * (double)(phi1 * ise) * pke : 0.0;
+            a_l -= gg;
+            a_sg -= gg * (double)z1;
+            if (k != e) a_l = fma(dae, (double)(b_pk[k * NP + g] * phi2 * isk), a_l);
+        };
+        int k = 0;
+#if GVR_BWD_WAYS == 4
+        double dpk3 = 0.0, dpk4 = 0.0, dl3 = 0.0, dl4 = 0.0, dsg3 = 0.0, dsg4 = 0.0;
+        for (; k + 4 <= n; k += 4) {
+            pair(k, dpk, dl, dsg);
+            pair(k + 1, dpk2, dl2, dsg2);
+            pair(k + 2, dpk3, dl3, dsg3);
+            pair(k + 3, dpk4, dl4, dsg4);
         }
+        dpk2 += dpk4;
+        dpk += dpk3;
+        dl += dl3;
+        dl2 += dl4;
+        dsg += dsg3;
+        dsg2 += dsg4;
+#endif
+        for (; k + 2 <= n; k += 2) {
+            pair(k, dpk, dl, dsg);
+            pair(k + 1, dpk2, dl2, dsg2);
+        }
+        if (k < n) pair(k, dpk, dl, dsg);
+        dpk += dpk2;
+        dl += dl2;
+        dsg += dsg2;
         const double dq = dpk * pke;
         if (dl == 0.0 && dq == 0.0 && dsg == 0.0) continue;
 

@@ -23,6 +23,9 @@
 #ifndef GVR_BLEND_MINB
 #define GVR_BLEND_MINB 1
 #endif
+#ifndef GVR_BWD_WAYS
+#define GVR_BWD_WAYS 2
+#endif
 #ifndef GVR_BWD_MINB
 #define GVR_BWD_MINB 4
 #endif
