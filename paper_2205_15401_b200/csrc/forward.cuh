@@ -338,6 +338,8 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     p.count[pix] = n;
 }
 
+constexpr int kWarpListCap = 512;  // per-warp compacted list capacity (entries)
+
 // Exact order of two selection candidates (kernel ids a, b; l on the exact trace).
 __device__ __forceinline__ bool exact_less(int a, int b, const double* d, const Rec64* rec64) {
     const double la = trace_exact(d, rec64[a]).l, lb = trace_exact(d, rec64[b]).l;
@@ -374,7 +376,38 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
     const int listed = load_sorted_list(p, tile, keys);
     const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
     const int start = 0;
-    const int end = overflow ? p.K : listed;
+    // Each warp owns a 2x4-pixel sub-block of the tile and first compacts the
+    // tile list to the entries whose screen box meets the sub-block (stable, so
+    // the depth order survives): its pixels then scan ~half the list. Lists
+    // longer than kWarpListCap stay on the tile list.
+    const int sr0 = (tile / p.tiles_x) * TILE + (warp >> 1) * 2;
+    const int sc0 = (tile % p.tiles_x) * TILE + (warp & 1) * 4;
+    unsigned long long* wlist = keys + p.cap + warp * kWarpListCap;
+    const unsigned long long* list = keys;
+    int end = overflow ? p.K : listed;
+    if (!overflow) {
+        const float fr0 = (float)sr0, fr1 = (float)(sr0 + 1), fc0 = (float)sc0, fc1 = (float)(sc0 + 3);
+        int cnt = 0;
+        for (int base = 0; base < listed && cnt <= kWarpListCap; base += 32) {
+            const int e = base + lane;
+            bool hit = false;
+            unsigned long long key = 0;
+            if (e < listed) {
+                key = keys[e];
+                const float4 box = __ldg(reinterpret_cast<const float4*>(p.rec32 + (int)(key & 0xffffffffu)));
+                hit = box.x <= fr1 && box.y >= fr0 && box.z <= fc1 && box.w >= fc0;
+            }
+            const unsigned b = __ballot_sync(FULL, hit);
+            const int off = cnt + __popc(b & ((1u << lane) - 1u));
+            if (hit && off < kWarpListCap) wlist[off] = key;
+            cnt += __popc(b);
+        }
+        __syncwarp();
+        if (cnt <= kWarpListCap) {
+            list = wlist;
+            end = cnt;
+        }
+    }
     const int kp = p.sel.kp;
     const Rec64* rec64 = p.rec64;
     const double log_eta = p.sel.log_eta;
@@ -387,9 +420,9 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
     const bool exact_only = p.exact_only != 0;
     float cost = 0.0f;
 
-    for (int px = warp; px < TILE * TILE; px += 8) {
-        const int i = (tile / p.tiles_x) * TILE + px / TILE;
-        const int j = (tile % p.tiles_x) * TILE + px % TILE;
+    for (int px = 0; px < 8; ++px) {
+        const int i = sr0 + (px >> 2);
+        const int j = sc0 + (px & 3);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
         const long long pix = (long long)i * p.cam.W + j;
         double d[3];
@@ -408,10 +441,10 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
         for (int base = start; base < end; base += 32) {
             const int e = base + lane;
             const bool valid = e < end;
-            const int k = overflow ? (valid ? e : 0) : (int)(keys[valid ? e : 0] & 0xffffffffu);
+            const int k = overflow ? (valid ? e : 0) : (int)(list[valid ? e : 0] & 0xffffffffu);
             // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
             if (!overflow) {
-                const float zmin0 = float_from_order_bits((uint32_t)(keys[base] >> 32));
+                const float zmin0 = float_from_order_bits((uint32_t)(list[base] >> 32));
                 if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
             }
             const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);

@@ -276,9 +276,10 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     const size_t list_smem = sizeof(unsigned long long) * (size_t)fp.cap;
     if (KMAX <= 32) {
         auto kern = select_warp_kernel<KMAX>;
-        CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem));
+        const size_t smem = list_smem + sizeof(unsigned long long) * 8 * kWarpListCap;  // + per-warp lists
+        CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_SELECT);
-        kern<<<tiles, 256, list_smem, ctx->stream>>>(fp);
+        kern<<<tiles, 256, smem, ctx->stream>>>(fp);
     } else {
         constexpr int NT = 64;
         const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT + list_smem;
