@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured graph")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 multi-view batch measurement")
     ap.add_argument("--c3-views", type=int, default=64, help="C3 batch size (views over all ranks)")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 1024^2 / 1M-kernel tile-sharded measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 fitting-loop measurement")
     return ap.parse_args()
 
 
@@ -274,6 +276,109 @@ def measure_c3(args, ctx, stream, dev, scene, cfg, rank, world):
             "mean_loss": float(losses.mean().item())}
 
 
+def _timed(fn, steps, stream, dev, world, flush=None):
+    """Max-over-ranks device time (ms) of `steps` calls of fn, CUDA events on `stream`."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        if flush is not None:
+            flush.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measure_c4(args, ctx, stream, dev, rank, world):
+    """C4 (BASELINE.json configs[3]): one 1024x1024 view of make_bench_scene(1e6)
+    (1,003,688 kernels), fwd + ScalarLoss + bwd, image tiles dealt round-robin to
+    the ranks (gvr_render_shard: tile % N == rank); the partial gradients of the
+    ranks are summed with one NCCL all-reduce. One step = one whole render."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_15401_b200 as gvr
+    from paper_2205_15401_b200 import synthetic
+
+    S = 1024
+    scene = synthetic.make_bench_scene(1_000_000)
+    cam = synthetic.make_bench_camera(S)
+    cfg = gvr.SelectionConfig()
+    K = scene.size
+    dscene = gvr.DeviceScene(ctx)
+    dscene.set_raw(K, 3, scene.tau, torch.from_numpy(scene.centers).to(dev), torch.from_numpy(scene.inv_cov).to(dev),
+                   torch.from_numpy(scene.attr).to(dev))
+    tape = gvr.Tape(ctx)
+    rng = np.random.default_rng(4)
+    ti = torch.tensor(rng.uniform(0, 1, (S, S, 3)), device=dev)
+    ta = torch.tensor(rng.uniform(0, 1, (S, S, 1)), device=dev)
+    img = torch.empty((S, S, 3), dtype=torch.float64, device=dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    grads = torch.zeros(K * 15 + 12, dtype=torch.float64, device=dev)
+    g_c, g_s, g_a = grads[:3 * K].view(K, 3), grads[3 * K:12 * K].view(K, 3, 3), grads[12 * K:15 * K].view(K, 3)
+    g_r, g_t = grads[15 * K:15 * K + 9].view(3, 3), grads[15 * K + 9:]
+
+    def step():
+        gvr.render_into(ctx, dscene, cam, cfg, tape, img, shard=(rank, world))
+        gvr.scalar_loss_into(tape, ti, ta, 1.0, 1.0, loss)
+        gvr.backward_into(tape, None, None, gvr.GradFlags(), g_c, g_s, g_a, g_r, g_t)
+        if world > 1:
+            dist.all_reduce(grads, op=dist.ReduceOp.SUM)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    steps = max(3, min(args.steps, 10))
+    n0 = ctx.launch_count
+    ms = _timed(step, steps, stream, dev, world) / steps
+    return {"workload": f"C4: 1024x1024 view of make_bench_scene(1e6) ({K} kernels), fwd+bwd, image tiles "
+                        f"round-robin over {world} rank(s), NCCL all-reduce of the partial gradients",
+            "value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "steps": steps,
+            "gpu_launches": ctx.launch_count - n0}
+
+
+def measure_c5(args, ctx, stream, dev, rank, world):
+    """C5 (BASELINE.json configs[4]): the shape/texture fitting loop on
+    make_bench_scene(5e4) (50,786 kernels), 32 orbit views at 256x256, per
+    iteration fwd + loss + bwd of every view (views sharded over the ranks),
+    one NCCL all-reduce(sum) of [d_center | d_attr | loss], ADAM on
+    [centers | attrs] (fit.cpp:117-158, 20-42). Targets: the scene with other
+    colours, rendered from the same cameras; the fit starts from jittered centres."""
+    import torch  # noqa: F401
+
+    from paper_2205_15401_b200 import synthetic
+    from paper_2205_15401_b200.fit import AdamConfig, Fitter, make_fit_views
+
+    target = synthetic.make_bench_scene(50_000)
+    target.attr[:] = (0.2, 0.5, 0.8)
+    views = make_fit_views(target, 32, 256, ctx=ctx)
+    start = target.copy()
+    start.attr[:] = (0.8, 0.3, 0.2)
+    start.centers = start.centers + np.random.default_rng(5).normal(0.0, 0.002, start.centers.shape)
+    fitter = Fitter(ctx, start, views, adam=AdamConfig(lr=0.002), rank=rank, world=world, device=dev)
+    fitter.loss_and_grad()
+    first = fitter.loss()
+    for _ in range(max(args.warmup, 3)):
+        fitter.step()
+    steps = max(3, min(args.steps, 10))
+    n0 = ctx.launch_count
+    ms = _timed(fitter.step, steps, stream, dev, world) / steps
+    last = fitter.loss()
+    return {"workload": f"C5: fitting loop, make_bench_scene(5e4) ({target.size} kernels), 32 orbit views 256x256 "
+                        f"sharded over {world} rank(s), fwd+loss+bwd per view, NCCL all-reduce, ADAM",
+            "value": 1e3 / ms, "unit": "iterations/s", "renders_per_s": 32e3 / ms, "ms_per_step": ms,
+            "scaling": "strong", "steps": steps, "gpu_launches": ctx.launch_count - n0,
+            "loss_first": first, "loss_last": last}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -453,6 +558,9 @@ def run_ours(args):
     if not args.no_c3:
         c3 = measure_c3(args, ctx, stream, dev, scene, cfg, rank, world)
 
+    c4 = None if args.no_c4 else measure_c4(args, ctx, stream, dev, rank, world)
+    c5 = None if args.no_c5 else measure_c5(args, ctx, stream, dev, rank, world)
+
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -473,7 +581,7 @@ def run_ours(args):
                        "views": "every rank renders the C2 view (weak scaling)",
                        "l2": "flushed (256 MB write) between timed steps, outside the timed window",
                        "step": "render_with_tape -> ScalarLoss (device) -> backward, inputs resident in HBM"},
-            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks, "c3": c3,
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks, "c3": c3, "c4": c4, "c5": c5,
             "gpu_launches": launches, "graph": not args.no_graph,
             "loss": float(loss.item()),
         }

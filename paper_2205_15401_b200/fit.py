@@ -4,11 +4,12 @@ Mirrors ``gvr::loss_and_grad`` + ``AdamState::update`` of ``fit_shape``
 (/root/reference/proj/src/fit.cpp:117-158, :20-42, :176-265) with everything on
 the GPU and the views sharded across ranks:
 
-  per iteration, on each rank, for each of its views v:
-      render_with_tape(scene, camera_v)                      (gvr_render)
+  per iteration, on each rank, for all of its views v at once (the views run
+  concurrently on the context's worker streams):
+      render_with_tape(scene, camera_v)                      (gvr_render_views)
       loss_v = rgb |img - t|^2 / #img + sil |alpha - t_a|^2 / #alpha, scaled 1/#views
-      d_image = 2 rgb (img - t) / (#img #views), d_alpha likewise    (gvr_scalar_loss)
-      gradients += backward(tape, d_image, d_alpha)         (gvr_backward_accumulate)
+      d_image = 2 rgb (img - t) / (#img #views), d_alpha likewise    (gvr_scalar_loss_views)
+      gradients = sum_v backward(tape_v, d_image_v, d_alpha_v)   (gvr_backward_views, view sum)
   all-reduce(sum) of [d_center | d_attr | loss] across ranks (NCCL over NVLink;
   the only collective of the render path)
   ADAM on [centers | attrs] (gvr_adam_step), identical on every rank.
@@ -25,7 +26,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from .distributed import allreduce_gradients, shard_views
-from .render import Context, DeviceScene, Tape, adam_step, backward_into, render_into, scalar_loss_into
+from .render import (Context, DeviceScene, Tape, adam_step, backward_views_into, render_views_into,
+                     scalar_loss_views_into)
 from .types import Camera, GaussianScene, GradFlags, SelectionConfig
 
 
@@ -69,19 +71,24 @@ class Fitter:
         self.step_count = 0
         self.n_views = len(views)
         self.mine = shard_views(self.n_views, rank, world)
-        self.views: List[Tuple[Camera, object, object, float, float]] = []
+        # views grouped by loss weights (2 rgb / (#img #views) etc.): one batched call per group
+        groups = {}
         for idx in self.mine:
             cam, ti, ta = views[idx]
             n_img = float(np.asarray(ti).size)
             n_alpha = float(np.asarray(ta).size)
-            w_img = 2.0 * rgb_weight / (n_img * self.n_views)
-            w_alpha = 2.0 * silhouette_weight / (n_alpha * self.n_views)
-            self.views.append((cam, torch.as_tensor(np.ascontiguousarray(ti)).to(**f64),
-                               torch.as_tensor(np.ascontiguousarray(ta)).to(**f64), w_img, w_alpha))
+            w = (2.0 * rgb_weight / (n_img * self.n_views), 2.0 * silhouette_weight / (n_alpha * self.n_views))
+            g = groups.setdefault(w, ([], [], [], []))
+            g[0].append(cam)
+            g[1].append(torch.as_tensor(np.ascontiguousarray(ti)).to(**f64))
+            g[2].append(torch.as_tensor(np.ascontiguousarray(ta)).to(**f64))
+            g[3].append(Tape(ctx))
+        self.groups: List[Tuple[Tuple[float, float], list, list, list, list, object]] = [
+            (w, cams, tis, tas, tapes, torch.zeros(len(cams), **f64)) for w, (cams, tis, tas, tapes) in groups.items()]
         self.loss_acc = torch.zeros(1, **f64)
-        self.loss_tmp = torch.zeros(1, **f64)
         self.dscene = DeviceScene(ctx)
-        self.tape = Tape(ctx)
+        self.total = dict(d_center=self.g_center.view(self.K, 3),
+                          d_attr=self.g_attr.view(self.K, self.D) if self.D > 0 else None)
         # torch work (accumulations, NCCL) on the context's stream, ordered with our kernels
         self.stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device=self.dev)
 
@@ -94,12 +101,11 @@ class Fitter:
         self.dscene.set_raw(self.K, self.D, self.tau, self.centers, self.inv_cov, self.attr)
         self.grads.zero_()
         self.loss_acc.zero_()
-        for cam, ti, ta, w_img, w_alpha in self.views:
-            render_into(self.ctx, self.dscene, cam, self.cfg, self.tape)
-            scalar_loss_into(self.tape, ti, ta, w_img, w_alpha, self.loss_tmp)
-            self.loss_acc += self.loss_tmp
-            backward_into(self.tape, None, None, GradFlags(), d_center=self.g_center, d_attr=self.g_attr,
-                          accumulate=True)
+        for (w_img, w_alpha), cams, tis, tas, tapes, losses in self.groups:
+            render_views_into(self.ctx, self.dscene, cams, self.cfg, tapes)
+            scalar_loss_views_into(self.ctx, tapes, tis, tas, w_img, w_alpha, losses)
+            backward_views_into(self.ctx, tapes, GradFlags(), None, self.total)
+            self.loss_acc += losses.sum()
 
     def step(self, group=None) -> None:
         """One fit_shape iteration: loss_and_grad, NCCL all-reduce, ADAM."""
