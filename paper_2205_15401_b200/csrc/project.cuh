@@ -143,9 +143,14 @@ struct ProjectParams {
 
 // K1: view transform (scene.cpp:5-17), coarse screen box (tracer.cpp:37-113) in
 // exact FP64, the FP32 pre-filter record and the depth key for early exit.
-__global__ void project_kernel(ProjectParams p) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= p.K) return;
+struct BinJob {
+    int nt = 0;  // tiles to append to (row-major rectangle from (tr0, tc0), ntc per row)
+    int tr0 = 0, tc0 = 0, ntc = 1;
+    unsigned long long key = 0;
+};
+
+__device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
+    BinJob job;
     const CameraP& c = p.cam;
 
     double mo[3], so[9];
@@ -190,7 +195,7 @@ __global__ void project_kernel(ProjectParams p) {
         q.ci_int = q.cj_int = 0;
         q.ci_frac = q.cj_frac = 0.0f;
         p.rec32[k] = q;
-        return;
+        return job;
     }
 
     double cov[9];
@@ -292,17 +297,50 @@ __global__ void project_kernel(ProjectParams p) {
         q.right = __double2float_ru(fmin(right + mr, 1.0e30));
         int tr0, tr1, tc0, tc1;
         if (box_tiles(q, c.H, c.W, p.tile, tr0, tr1, tc0, tc1)) {
-            // bin: append (depth key, id) to every overlapped tile's list
-            const unsigned long long key = ((unsigned long long)float_order_bits(q.zmin) << 32) | (unsigned)k;
-            for (int tr = tr0; tr <= tr1; ++tr)
-                for (int tc = tc0; tc <= tc1; ++tc) {
-                    const int t = tr * p.tiles_x + tc;
-                    const int pos = atomicAdd(p.tile_count + t, 1);
-                    if (pos < p.cap) p.tile_lists[(size_t)t * p.cap + pos] = key;
-                }
+            job.key = ((unsigned long long)float_order_bits(q.zmin) << 32) | (unsigned)k;
+            job.tr0 = tr0;
+            job.tc0 = tc0;
+            job.ntc = tc1 - tc0 + 1;
+            job.nt = (tr1 - tr0 + 1) * job.ntc;
         }
     }
     p.rec32[k] = q;
+    return job;
+}
+
+// K1. Binning: every kernel appends (depth key, id) to the list of every tile
+// its box overlaps. Appends are warp-aggregated: lanes that hit the same tile
+// in the same round (neighbouring kernels usually do) share one atomicAdd on
+// the tile's counter, and four rounds of returned atomics are kept in flight.
+__global__ void project_kernel(ProjectParams p) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    BinJob job;
+    if (k < p.K) job = project_one(p, k);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int it0 = 0; __any_sync(FULL, it0 < job.nt); it0 += 4) {
+        int t[4];
+        unsigned mk[4];
+        int base[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int it = it0 + u;
+            t[u] = it < job.nt ? (job.tr0 + it / job.ntc) * p.tiles_x + job.tc0 + it % job.ntc : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mk[u] = __match_any_sync(FULL, t[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            base[u] = 0;
+            if (t[u] >= 0 && (mk[u] & lt) == 0) base[u] = atomicAdd(p.tile_count + t[u], __popc(mk[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int pos = __shfl_sync(FULL, base[u], __ffs(mk[u]) - 1) + __popc(mk[u] & lt);
+            if (t[u] >= 0 && pos < p.cap) p.tile_lists[(size_t)t[u] * p.cap + pos] = job.key;
+        }
+    }
 }
 
 
