@@ -209,19 +209,58 @@ struct ObjParams {
 
 // K5: camera -> object space once per kernel (grad.cpp:184-197):
 // d_center = R^T dm, d_inv_cov = R^T dS R, d_T = sum dm, d_R = sum dm m^T + 2 dS R S.
-__global__ void object_space_kernel(ObjParams p) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    double part[12];
+constexpr int kObjThreads = 128;
+
+// Block-contiguous rows of `width` doubles staged through shared memory so the
+// global side is coalesced 16-byte traffic (rows are 24 / 72 bytes apart).
+__device__ __forceinline__ void stage_rows_in(double* dst, const double* __restrict__ src, int k0, int count,
+                                              int width) {
+    const long long n = (long long)count * width, off = (long long)k0 * width;
+    if (((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const double2* s2 = reinterpret_cast<const double2*>(src + off);
+        for (long long i = threadIdx.x; i < n / 2; i += blockDim.x) reinterpret_cast<double2*>(dst)[i] = __ldg(s2 + i);
+        if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[off + n - 1];
+    } else {
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[off + i];
+    }
+}
+
+__device__ __forceinline__ void stage_rows_out(double* __restrict__ dst, const double* src, int k0, int count,
+                                               int width) {
+    const long long n = (long long)count * width, off = (long long)k0 * width;
+    if (((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        double2* d2 = reinterpret_cast<double2*>(dst + off);
+        for (long long i = threadIdx.x; i < n / 2; i += blockDim.x) d2[i] = reinterpret_cast<const double2*>(src)[i];
+        if ((n & 1) && threadIdx.x == 0) dst[off + n - 1] = src[n - 1];
+    } else {
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[off + i] = src[i];
+    }
+}
+
+__global__ void __launch_bounds__(kObjThreads) object_space_kernel(ObjParams p) {
+    __shared__ __align__(16) double s_acc[kObjThreads * 9];
+    __shared__ __align__(16) double s_cov[kObjThreads * 9];
+    __shared__ __align__(16) double s_ctr[kObjThreads * 3];
+    const int k0 = blockIdx.x * kObjThreads;
+    const int count = min(kObjThreads, p.K - k0);
+    stage_rows_in(s_acc, p.acc, k0, count, 9);
+    stage_rows_in(s_cov, p.inv_cov, k0, count, 9);
+    stage_rows_in(s_ctr, p.centers, k0, count, 3);
+    __syncthreads();
+    const int t0 = threadIdx.x;
+    const int k = k0 + t0;
+    double part[12], dc[3] = {0.0, 0.0, 0.0}, dcov[9];
 #pragma unroll
     for (int t = 0; t < 12; ++t) part[t] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) dcov[t] = 0.0;
     if (k < p.K) {
-        const double* a = p.acc + 9ll * k;
+        const double* a = s_acc + 9 * t0;
         const double dm[3] = {a[0], a[1], a[2]};
         const double ds[9] = {a[3], a[4], a[5], a[4], a[6], a[7], a[5], a[7], a[8]};
         const double* R = p.cam.R;
-        // d_center = R^T dm
 #pragma unroll
-        for (int r = 0; r < 3; ++r) p.d_center[3ll * k + r] = R[r] * dm[0] + R[3 + r] * dm[1] + R[6 + r] * dm[2];
+        for (int r = 0; r < 3; ++r) dc[r] = R[r] * dm[0] + R[3 + r] * dm[1] + R[6 + r] * dm[2];
         // T1 = dS R; out = R^T T1 (symmetric: compute upper, mirror)
         double t1[9];
 #pragma unroll
@@ -233,12 +272,12 @@ __global__ void object_space_kernel(ObjParams p) {
 #pragma unroll
             for (int c = r; c < 3; ++c) {
                 const double val = R[r] * t1[c] + R[3 + r] * t1[3 + c] + R[6 + r] * t1[6 + c];
-                p.d_inv_cov[9ll * k + 3 * r + c] = val;
-                p.d_inv_cov[9ll * k + 3 * c + r] = val;
+                dcov[3 * r + c] = val;
+                dcov[3 * c + r] = val;
             }
         // d_R += dm m_obj^T + 2 (dS R) S_obj
-        const double* mo = p.centers + 3ll * k;
-        const double* so = p.inv_cov + 9ll * k;
+        const double* mo = s_ctr + 3 * t0;
+        const double* so = s_cov + 9 * t0;
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -248,6 +287,14 @@ __global__ void object_space_kernel(ObjParams p) {
 #pragma unroll
         for (int t = 0; t < 3; ++t) part[9 + t] = dm[t];
     }
+    __syncthreads();  // the staging rows are reused for the outputs
+#pragma unroll
+    for (int t = 0; t < 9; ++t) s_acc[9 * t0 + t] = dcov[t];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) s_ctr[3 * t0 + t] = dc[t];
+    __syncthreads();
+    stage_rows_out(p.d_inv_cov, s_acc, k0, count, 9);
+    stage_rows_out(p.d_center, s_ctr, k0, count, 3);
     // block reduction of the 12 camera-gradient components: a 16-value
     // butterfly (each step halves the values a lane carries), then lane 2v
     // holds the warp total of value v

@@ -1054,7 +1054,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         op.d_rt = t->d_rt.as<double>();
         {
             StageTimer st(ctx, ST_OBJECT);
-            object_space_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(op);
+            object_space_kernel<<<blocks_for(K, kObjThreads), kObjThreads, 0, ctx->stream>>>(op);
         }
         LAUNCH_CHECK(ctx);
     }
