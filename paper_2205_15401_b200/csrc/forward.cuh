@@ -450,7 +450,10 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
             const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
             const float4 box = __ldg(rp);        // top, bottom, left, right
             const float4 zrec = __ldg(rp + 1);   // zmin, zf, ci_frac, cj_frac
-            const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w;
+            // zmin <= l for any kernel that can pass eta: a candidate whose bound is
+            // past the worst kept key cannot enter the full list (skip the tests)
+            const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w &&
+                                !(zrec.x > worst + 2.0f * kKeyClose * fabsf(worst));
             int cls = 0;
             if (in_box) {
                 Rec32 r;
