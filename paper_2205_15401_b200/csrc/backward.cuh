@@ -16,6 +16,7 @@ struct BwdParams {
     const int* topk;   // [P*kp]
     const int* count;  // [P]
     const double* tape_t;  // [P*kp] T(l_k) from the forward
+    const EntryRec* ent;   // [P*kp] traced entries (l, e^q, 1/sigma) from the forward
     const Rec64* rec64;
     const double* attr;     // [K*D]
     const double* d_image;  // [P*D]
@@ -62,27 +63,17 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
     const double tau = p.tau;
     double dimg[4] = {0, 0, 0, 0};
     for (int c = 0; c < p.D && c < 4; ++c) dimg[c] = p.d_image[pix * p.D + c];
-    const double l0 = trace_fast(d, p.rec64[p.topk[pix * p.kp]]).l;
+    const double l0 = p.ent[pix * p.kp].l;
 
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
     // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
     double peak_part = 0.0;
-    int ids[PER];  // ids first: the id -> record load chains of the entries overlap
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int s = sub + 4 * q;
-        ids[q] = s < n ? p.topk[pix * p.kp + s] : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int s = sub + 4 * q;
-        if (s >= n) continue;
-        const int k = ids[q];
-        const Traced64 t = trace_fast(d, p.rec64[k]);
-        const double pk64 = exp(t.q);
-        const float pkf = (float)pk64;
+    for (int s = sub; s < n; s += 4) {
+        const int k = p.topk[pix * p.kp + s];
+        const EntryRec er = p.ent[pix * p.kp + s];  // traced by the forward
+        const float pkf = er.pk;
         const double pk = (double)pkf;
-        peak_part += pk64;
+        peak_part += pk;
         const double trans = p.tape_t[pix * p.kp + s];
         double dw = 0.0;
         if (p.D <= 4) {
@@ -95,11 +86,11 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
             for (int c = 0; c < p.D; ++c)
                 atomicAdd(&p.d_attr[(long long)p.D * k + c], w * (p.D <= 4 ? dimg[c] : p.d_image[pix * p.D + c]));
         }
-        b_dl[s * NP + g] = t.l - l0;
+        b_dl[s * NP + g] = er.l - l0;
         b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
         b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
         b_pk[s * NP + g] = pkf;
-        b_is[s * NP + g] = (float)sqrt(t.a);
+        b_is[s * NP + g] = er.is;
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);

@@ -33,6 +33,7 @@ struct FwdParams {
     int* count;     // [P]
     double* topk_w; // [P*kp] or null
     double* tape_t; // [P*kp] T(l_k) of the selected entries (backward input)
+    EntryRec* ent;  // [P*kp] traced selected entries (written by the blend)
     float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
     int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
     int* nonfinite; // flag
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
             __syncwarp();
             if (n == kp) worst = __shfl_sync(FULL, L, kp - 1);
         }
-        if (lane < n) p.topk[pix * kp + lane] = I;  // exact order; the blend re-derives it
+        if (lane < n) p.topk[pix * kp + lane] = I;  // exact (l, idx) order
         if (lane == 0) p.count[pix] = n;
         cost += (float)(n * n);
     }
@@ -577,24 +578,27 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     double peak_part = 0.0;
     // ids first (independent loads), then the traces: the id -> record load
     // chains of a thread's entries overlap instead of running back to back
-    int ids[PER];
+    {
+        int ids[PER];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int s = sub + 4 * q;
-        ids[q] = s < n ? p.topk[pix * kp + s] : 0;
-    }
+        for (int q = 0; q < PER; ++q) {
+            const int s = sub + 4 * q;
+            ids[q] = s < n ? p.topk[pix * kp + s] : 0;
+        }
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int s = sub + 4 * q;
-        if (s < n) {
-            const int k = ids[q];
-            const Traced64 t = trace_fast(d, p.rec64[k]);
-            const double pk = exp(t.q);
-            peak_part += pk;
-            b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
-            b_pk[s * NP + g] = (float)pk;
-            b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
-            b_id[s * NP + g] = k;
+        for (int q = 0; q < PER; ++q) {
+            const int s = sub + 4 * q;
+            if (s < n) {
+                const int k = ids[q];
+                const Traced64 t = trace_fast(d, p.rec64[k]);
+                const double pk = exp(t.q);
+                const float pkf = (float)pk;
+                peak_part += pk;
+                b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
+                b_pk[s * NP + g] = pkf;
+                b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
+                b_id[s * NP + g] = k;
+            }
         }
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
@@ -635,13 +639,20 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     // argument z = (l_k - l_m) / sigma_m keeps ~1e-7 relative accuracy in FP32.
     float2* b_hl = reinterpret_cast<float2*>(b_dl);
     for (int s = sub; s < n; s += 4) {
-        const double dl = b_dl[s * NP + g] - l0;
+        const double lval = b_dl[s * NP + g];
+        const double dl = lval - l0;
         const float hi = (float)dl;
         b_hl[s * NP + g] = make_float2(hi, (float)(dl - (double)hi));
         if (!p.presorted) {
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
         }
+        // tape the traced entry for the backward and the sampler
+        EntryRec er;
+        er.l = lval;
+        er.pk = b_pk[s * NP + g];
+        er.is = b_is[s * NP + g];
+        p.ent[pix * kp + s] = er;
     }
     __syncwarp(grp);
 

@@ -122,6 +122,13 @@ struct Traced64 {
     double l, q, a;
 };
 
+// Per selected entry, taped by the selection for the blend, the backward and
+// the sampler: l (FP64), e^q and 1/sigma (FP32, as blended). 16 bytes.
+struct __align__(16) EntryRec {
+    double l;
+    float pk, is;
+};
+
 // trace_kernel (tracer.cpp:20-35), bit-exact: a = d.Sd, b = (m.Sd + d.Sm)/2,
 // l = b/a, v = m - l d, q = min(0, -v.Sv/2), sigma = 1/sqrt(a).
 __device__ __forceinline__ Traced64 trace_exact(const double* d, const Rec64& r) {

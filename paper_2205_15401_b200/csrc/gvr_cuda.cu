@@ -132,7 +132,7 @@ struct gvr_tape {
     int cap = 0;
     Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
     // per pixel
-    Buf topk, count, image, alpha, depth, topk_w, tape_t;
+    Buf topk, count, image, alpha, depth, topk_w, tape_t, ent;
     Buf d_image, d_alpha;
     // gradients
     Buf acc, d_attr, d_center, d_inv_cov, d_rt;
@@ -622,7 +622,7 @@ void gvr_tape_destroy(gvr_tape* t) {
     if (!t) return;
     cudaStreamSynchronize(t->ctx->stream);
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_lists, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
-                   &t->depth, &t->topk_w, &t->tape_t, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
+                   &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags};
     for (Buf* b : bufs) b->release();
     if (t->h_flags) cudaFreeHost(t->h_flags);
@@ -710,6 +710,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
     CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
+    CUDA_TRY(ctx, tape->ent.ensure(sizeof(EntryRec) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->image.ensure(sizeof(double) * (size_t)P * Dc));
     CUDA_TRY(ctx, tape->alpha.ensure(sizeof(double) * (size_t)P));
     CUDA_TRY(ctx, tape->depth.ensure(sizeof(double) * (size_t)P));
@@ -784,6 +785,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.count = tape->count.as<int>();
     fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
     fp.tape_t = tape->tape_t.as<double>();
+    fp.ent = tape->ent.as<EntryRec>();
     fp.nonfinite = dflags + 1;
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     int rc = GVR_OK;
@@ -1026,6 +1028,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.topk = t->topk.as<int>();
         bp.count = t->count.as<int>();
         bp.tape_t = t->tape_t.as<double>();
+        bp.ent = t->ent.as<EntryRec>();
         bp.rec64 = t->rec64.as<Rec64>();
         bp.attr = scene->attr.as<double>();
         bp.d_image = di;
@@ -1094,6 +1097,7 @@ TapeView tape_view(const gvr_tape* t) {
     v.topk = t->topk.as<int>();
     v.count = t->count.as<int>();
     v.tape_t = t->tape_t.as<double>();
+    v.ent = t->ent.as<EntryRec>();
     v.rec64 = t->rec64.as<Rec64>();
     return v;
 }

@@ -24,13 +24,14 @@ struct TapeView {
     const int* topk;       // [P*kp] ascending (l, idx)
     const int* count;      // [P]
     const double* tape_t;  // [P*kp] T(l_k)
+    const EntryRec* ent;   // [P*kp] traced entries (e^q as blended)
     const Rec64* rec64;    // [K]
 };
 
 // W of the taped entry (pix, s); identical to blend_kernel's wd.
 __device__ __forceinline__ double taped_weight(const TapeView& v, const double* d, long long pix, int s) {
-    const Traced64 t = trace_fast(d, v.rec64[v.topk[pix * v.kp + s]]);
-    return v.tape_t[pix * v.kp + s] * (double)(float)exp(t.q);
+    (void)d;
+    return v.tape_t[pix * v.kp + s] * (double)v.ent[pix * v.kp + s].pk;
 }
 
 // One thread per pixel, row-major pixels; FP64 atomics into the per-kernel sums.
