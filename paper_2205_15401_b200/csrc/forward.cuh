@@ -20,8 +20,9 @@ struct FwdParams {
     const unsigned long long* tile_lists;  // [tiles * cap] (order(zmin) << 32 | id), unsorted
     int cap;
     int K;
-    const int* tile_order_blend;  // tiles by sum_p n_p^2 (from the selection); first *n_order_blend valid
-    const int* n_order_blend;
+    const int* tile_order_blend;  // tiles by sum_p n_p^2 (from the selection), then the tiles with no
+    const int* n_order_blend;     // selection (cleared by the blend); first *n_order_blend valid
+    int* n_order_blend_all;       // written by the ordering kernel
     const Rec32* rec32;
     const Rec64* rec64;
     const double* attr;  // [K*D] object attributes (FP64)
@@ -562,12 +563,15 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     const bool inside = i < p.cam.H && j < p.cam.W;
     const long long pix = (long long)i * p.cam.W + j;
     const int kp = p.sel.kp;
-    const int n = inside ? p.count[pix] : 0;
+    // tiles without any selection (or not visited: other shards, empty lists) are cleared
+    const bool visited = p.bwd_cost[tile] > 0.0f;
+    const int n = inside && visited ? p.count[pix] : 0;
     if (n == 0) {
         if (inside && sub == 0) {
             for (int c = 0; c < p.Dc; ++c) p.image[pix * p.Dc + c] = 0.0;
             p.alpha[pix] = 0.0;
             p.depth[pix] = 0.0;
+            if (!visited) p.count[pix] = 0;
         }
         return;  // the 4 threads of a pixel leave together
     }
@@ -751,9 +755,11 @@ __global__ void clear_empty_tiles_kernel(CameraP cam, int Dc, int tiles_x, const
 // Cost = icost[t] (list length) or fcost[t].
 __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
                                                            const float* __restrict__ fcost, int* __restrict__ order,
-                                                           int* __restrict__ n_out, int shard, int nshards) {
+                                                           int* __restrict__ n_out, int shard, int nshards,
+                                                           int* __restrict__ n_all_out) {
     __shared__ int hist[256];
     __shared__ int offs[256];
+    __shared__ int s_tail;
     for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     auto bucket_of = [&](int t) -> int {
@@ -787,12 +793,21 @@ __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int*
             offs[threadIdx.x * 8 + q] = base;
             base += vals[q];
         }
-        if (threadIdx.x == 31) *n_out = incl;
+        if (threadIdx.x == 31) {
+            *n_out = incl;
+            s_tail = incl;
+        }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
         const int b = bucket_of(t);
         if (b >= 0) order[atomicAdd(&offs[b], 1)] = t;
+    }
+    if (n_all_out) {  // then every other tile (the blend clears them): order holds all tiles
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+            if (bucket_of(t) < 0) order[atomicAdd(&s_tail, 1)] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) *n_all_out = s_tail;
     }
 }
 

@@ -291,7 +291,8 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     LAUNCH_CHECK(ctx);
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b, 0, 1);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b, 0, 1,
+                                                        fp.n_order_blend_all);
     }
     LAUNCH_CHECK(ctx);
     {
@@ -706,7 +707,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     tape->cap = ctx->tile_cap;
     CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * (size_t)tiles));
     CUDA_TRY(ctx, tape->tile_lists.ensure(sizeof(unsigned long long) * (size_t)tiles * tape->cap));
-    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (2 + 3 * (size_t)tiles)));
+    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 3 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
     CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
@@ -753,7 +754,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     // K3 over the non-empty tiles, longest list first
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards);
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
+                                                        nullptr);
     }
     LAUNCH_CHECK(ctx);
     FwdParams fp;
@@ -769,7 +771,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.tile_order = order_f;
     fp.n_order = sched;
     fp.tile_order_blend = sched + 2 + tiles;
-    fp.n_order_blend = sched + 1;
+    fp.n_order_blend = sched + 2 + 3 * (size_t)tiles;  // all tiles: selected first, then cleared ones
+    fp.n_order_blend_all = sched + 2 + 3 * (size_t)tiles;
     fp.bwd_cost = bwd_cost;
     fp.tile_count = tile_count;
     fp.tile_lists = tape->tile_lists.as<unsigned long long>();
@@ -798,9 +801,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     else if (kp <= 48) rc = launch_forward<48>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     else rc = launch_forward<64>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     if (rc) return rc;
-    clear_empty_tiles_kernel<<<tiles, 64, 0, ctx->stream>>>(cp, Dc, tiles_x, bwd_cost, fp.image, fp.alpha, fp.depth,
-                                                            fp.count);
-    LAUNCH_CHECK(ctx);
+
     tape->valid = true;
 
     if (out) {
