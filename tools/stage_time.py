@@ -1,5 +1,6 @@
 """Per-stage device times of the C2 fwd+bwd step for one or more library builds
 (A/B experiments): python tools/stage_time.py build_ab/a.so build_ab/b.so ...
+(GVR_NK / GVR_S select another bench scene size / image size, e.g. C4: 1000000 / 1024)
 Each build runs in a fresh subprocess (GVR_LIB_PATH); prints ms per stage and per step,
 plus a checksum of the outputs so that variants can be compared for equality."""
 import json
@@ -16,9 +17,10 @@ import paper_2205_15401_b200 as gvr
 ctx = gvr.Context(0)
 stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device="cuda:0")
 torch.cuda.set_stream(stream)
-scene = gvr.make_bench_scene(100000); cam = gvr.make_bench_camera(512); cfg = gvr.SelectionConfig()
+NK = int(os.environ.get("GVR_NK", "100000")); S = int(os.environ.get("GVR_S", "512"))
+scene = gvr.make_bench_scene(NK); cam = gvr.make_bench_camera(S); cfg = gvr.SelectionConfig()
 ds = gvr.DeviceScene(ctx).set(scene); tape = gvr.Tape(ctx)
-dev = torch.device("cuda:0"); H = W = 512
+dev = torch.device("cuda:0"); H = W = S
 img = torch.empty((H, W, 3), dtype=torch.float64, device=dev)
 al = torch.empty((H, W, 1), dtype=torch.float64, device=dev); dp = torch.empty((H, W, 1), dtype=torch.float64, device=dev)
 rng = np.random.default_rng(0)
