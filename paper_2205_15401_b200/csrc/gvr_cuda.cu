@@ -1334,7 +1334,10 @@ int gvr_shade_lambert(gvr_context* ctx, const gvr_camera* camera, const double* 
 
 namespace {
 
-constexpr int kViewStreams = 8;
+#ifndef GVR_VIEW_STREAMS
+#define GVR_VIEW_STREAMS 16
+#endif
+constexpr int kViewStreams = GVR_VIEW_STREAMS;
 constexpr int kSumViews = 64;  // views per gradient-sum launch (kernel parameter space)
 
 struct ViewSumParams {
