@@ -491,6 +491,13 @@ def run_ours(args):
             traffic = json.load(open(prof_json)).get(kern_names[dominant])
         except (OSError, ValueError):
             traffic = None
+    issue_active = None
+    issue_json = os.path.join(ROOT, "profiles", "ncu_issue.json")
+    if os.path.exists(issue_json):
+        try:
+            issue_active = json.load(open(issue_json))
+        except (OSError, ValueError):
+            issue_active = None
     roofline = {
         "bound": "fp32", "kernel": kern_names[dominant],
         "achieved": achieved, "peak": fp32_peak / 1e12, "unit": "TFLOP/s", "frac": achieved * 1e12 / fp32_peak,
@@ -503,6 +510,9 @@ def run_ours(args):
         "kernel_frac_of_fp32_peak": {k: flops[k] / (per_launch_ms[k] * 1e-3) / fp32_peak for k in kern_names},
         "work_counts": {k: wc[k] for k in ("C", "N1", "N2", "kernels")},
         "stage_ms_per_step": {k: v[0] / max(prof_steps, 1) for k, v in stages.items()},
+        "issue_active_pct": issue_active,
+        "note": "control-heavy per-pixel kernels: bounded by instruction issue and dependency latency at "
+                "24-32 resident warps/SM (ncu smsp__issue_active in issue_active_pct), not by a pipe",
     }
 
     # ---------------- end-to-end through the public API with host buffers

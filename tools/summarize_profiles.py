@@ -24,7 +24,7 @@ METRICS = [
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
     "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
-    "sm__maximum_warps_per_active_cycle_pct",
+    "sm__maximum_warps_per_active_cycle_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -77,6 +77,7 @@ def main():
             md.append(f"| `{k.split('(')[0][:70]}` | {v / 1e3:.1f} | {100 * v / total:.1f}% |")
         md.append("")
     traffic = {}
+    issue = {}
     for f in sorted(os.listdir(OUT)):
         if f.startswith("full_") and f.endswith(".ncu-rep"):
             m = ncu_metrics(os.path.join(OUT, f))
@@ -84,12 +85,17 @@ def main():
             rb = to_bytes(*m["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in m else 0.0
             wb = to_bytes(*m["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in m else 0.0
             traffic[name] = rb + wb
+            key = "smsp__issue_active.avg.pct_of_peak_sustained_active"
+            if key in m:
+                issue[name] = float(m[key][0].replace(",", ""))
             md += [f"## `{name}` (ncu --set full)", "", "| metric | value |", "|---|---|"]
             for k in METRICS:
                 if k in m:
                     md.append(f"| {k} | {m[k][0]} {m[k][1]} |")
             md.append("")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    if issue:
+        json.dump(issue, open(os.path.join(PROF, "ncu_issue.json"), "w"), indent=1)
     open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md))
 
