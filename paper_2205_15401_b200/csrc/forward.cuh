@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
                 const Traced64 t = trace_fast(d, p.rec64[k]);
                 const double pk = exp(t.q);
                 const float pkf = (float)pk;
-                peak_part += pk;
+                b_w[s * NP + g] = pk;    // FP64 peak until W overwrites it (alpha sum, after the sort)
                 b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
                 b_pk[s * NP + g] = pkf;
                 b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
@@ -605,8 +605,6 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
             }
         }
     }
-    peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
-    peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
     __syncwarp(grp);
     if (sub == 0 && !p.presorted) {
         // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort;
@@ -615,6 +613,7 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
             double ls = b_dl[s * NP + g];
             int is = b_id[s * NP + g];
             const float ps = b_pk[s * NP + g], ss = b_is[s * NP + g];
+            const double ws = b_w[s * NP + g];
             int t = s - 1;
             while (t >= 0) {
                 double lt = b_dl[t * NP + g];
@@ -627,15 +626,22 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
                 b_id[(t + 1) * NP + g] = it;
                 b_pk[(t + 1) * NP + g] = b_pk[t * NP + g];
                 b_is[(t + 1) * NP + g] = b_is[t * NP + g];
+                b_w[(t + 1) * NP + g] = b_w[t * NP + g];
                 --t;
             }
             b_dl[(t + 1) * NP + g] = ls;
             b_id[(t + 1) * NP + g] = is;
             b_pk[(t + 1) * NP + g] = ps;
             b_is[(t + 1) * NP + g] = ss;
+            b_w[(t + 1) * NP + g] = ws;
         }
     }
     __syncwarp(grp);
+    // sum of peaks in the (exact) entry order: deterministic whatever order the
+    // selection produced the set in
+    for (int s = sub; s < n; s += 4) peak_part += b_w[s * NP + g];
+    peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
+    peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
     const double l0 = b_dl[g];
     __syncwarp(grp);
     // l_k - l_0 as an unevaluated float pair hi + lo (replaces the double in place):

@@ -27,16 +27,18 @@ def _grad_bufs(k, d, dev):
     return {n: torch.zeros(s, dtype=torch.float64, device=dev) for n, s in shapes.items()}
 
 
-def test_views_equal_single_renders(ctx):
+@pytest.mark.parametrize("k_prime", [20, 40])
+def test_views_equal_single_renders(ctx, k_prime):
+    """K' = 20 (warp selection, presorted) and K' = 40 (CTA selection, blend sorts)."""
     scene = gvr.make_bench_scene(2000)
     cams = _views(11)
-    cfg = SelectionConfig()
+    cfg = SelectionConfig(k_prime=k_prime)
     dev = torch.device("cuda:0")
     ds = gvr.DeviceScene(ctx).set(scene)
     tapes = [gvr.Tape(ctx) for _ in cams]
     imgs = [torch.empty((48, 48, 3), dtype=torch.float64, device=dev) for _ in cams]
     alphas = [torch.empty((48, 48, 1), dtype=torch.float64, device=dev) for _ in cams]
-    tk = [np.empty((48, 48, 20), dtype=np.int32) for _ in cams]  # host outputs in a batch
+    tk = [np.empty((48, 48, k_prime), dtype=np.int32) for _ in cams]  # host outputs in a batch
     gvr.render_views_into(ctx, ds, cams, cfg, tapes, images=imgs, alphas=alphas, topk_idx=tk)
     rng = np.random.default_rng(0)
     ti = [torch.tensor(rng.uniform(0, 1, (48, 48, 3)), device=dev) for _ in cams]

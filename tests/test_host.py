@@ -111,3 +111,21 @@ def test_mixed_attribute_dims_rejected():
 
     with pytest.raises(ValidationError, match="attribute dimension is not uniform"):
         GaussianScene.from_kernels([((0, 0, 4), np.eye(3), [1, 2, 3]), ((0, 0, 5), np.eye(3), [1, 2])])
+
+
+def test_cpp_dropin_header_compiles_and_links():
+    """include/gvr/gvr.hpp + the ported reference cases compile and link against
+    libgvr_cuda.so on the CPU (they run in the GPU suite)."""
+    import shutil
+    import subprocess
+    import tempfile
+
+    if shutil.which("g++") is None or not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("g++ or the built library missing")
+    root = os.path.dirname(PKG)
+    with tempfile.TemporaryDirectory() as tmp:
+        exe = os.path.join(tmp, "t")
+        r = subprocess.run(["g++", "-std=c++17", "-O0", "-Wall", "-Werror", f"-I{root}/include", f"-I{root}/oracle/shim",
+                            os.path.join(root, "tests", "cpp", "test_cpp_api.cpp"), f"-L{PKG}", "-lgvr_cuda",
+                            f"-Wl,-rpath,{PKG}", "-o", exe], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
