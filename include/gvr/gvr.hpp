@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <initializer_list>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -458,6 +459,204 @@ inline Image shade_lambert(const Image& normals, const Image& alpha, const Image
     detail::check(gvr_shade_lambert(detail::context(), &cc, normals.data.data(), alpha.data.data(), depth.data.data(),
                                     lp, lc, out.data.data()));
     return out;
+}
+
+// ---------------------------------------------------------------- gradcheck (grad.hpp:67-88)
+
+// so3.cpp:7-65 on row-major double[9] (usable with either Vec3 / Mat3 flavour).
+namespace detail {
+inline void so3_exp_raw(const double w[3], double r[9]) {
+    const double th = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    const double k[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+    double kk[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) kk[3 * i + j] = k[3 * i] * k[j] + k[3 * i + 1] * k[3 + j] + k[3 * i + 2] * k[6 + j];
+    const double s = th < 1e-12 ? 1.0 : std::sin(th) / th;
+    const double c = th < 1e-12 ? 0.5 : (1.0 - std::cos(th)) / (th * th);
+    for (int i = 0; i < 9; ++i) r[i] = (i % 4 == 0 ? 1.0 : 0.0) + s * k[i] + c * kk[i];
+}
+inline void so3_log_raw(const double r[9], double w[3]) {
+    const double ct = std::clamp((r[0] + r[4] + r[8] - 1.0) * 0.5, -1.0, 1.0);
+    const double th = std::acos(ct);
+    if (th < 1e-9) {
+        w[0] = 0.5 * (r[7] - r[5]);
+        w[1] = 0.5 * (r[2] - r[6]);
+        w[2] = 0.5 * (r[3] - r[1]);
+        return;
+    }
+    if (th > M_PI - 1e-6) {
+        double a[9];
+        for (int i = 0; i < 9; ++i) a[i] = 0.5 * (r[i] + (i % 4 == 0 ? 1.0 : 0.0));
+        double ax[3] = {std::sqrt(std::max(0.0, a[0])), std::sqrt(std::max(0.0, a[4])), std::sqrt(std::max(0.0, a[8]))};
+        int major = 0;
+        for (int i = 1; i < 3; ++i)
+            if (a[4 * i] > a[4 * major]) major = i;
+        for (int i = 0; i < 3; ++i)
+            if (i != major && a[3 * major + i] < 0.0) ax[i] = -ax[i];
+        const double n = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+        for (int i = 0; i < 3; ++i) w[i] = n < 1e-12 ? 0.0 : th * ax[i] / n;
+        return;
+    }
+    const double f = th / (2.0 * std::sin(th));
+    w[0] = (r[7] - r[5]) * f;
+    w[1] = (r[2] - r[6]) * f;
+    w[2] = (r[3] - r[1]) * f;
+}
+inline void so3_exp_gradient_raw(const double w[3], const double dr[9], double g[3]) {
+    const double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    double r[9];
+    so3_exp_raw(w, r);
+    auto hat = [](const double v[3], double h[9]) {
+        const double t[9] = {0, -v[2], v[1], v[2], 0, -v[0], -v[1], v[0], 0};
+        std::memcpy(h, t, sizeof t);
+    };
+    for (int i = 0; i < 3; ++i) {
+        double e[3] = {0, 0, 0};
+        e[i] = 1.0;
+        double d[9];
+        if (th2 < 1e-16) {
+            hat(e, d);
+        } else {
+            double ire[3];  // (I - R) e
+            for (int a = 0; a < 3; ++a) ire[a] = e[a] - r[3 * a + i];
+            const double v[3] = {w[1] * ire[2] - w[2] * ire[1], w[2] * ire[0] - w[0] * ire[2], w[0] * ire[1] - w[1] * ire[0]};
+            double hw[9], hv[9], m[9];
+            hat(w, hw);
+            hat(v, hv);
+            for (int a = 0; a < 9; ++a) m[a] = (w[i] * hw[a] + hv[a]) / th2;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) d[3 * a + b] = m[3 * a] * r[b] + m[3 * a + 1] * r[3 + b] + m[3 * a + 2] * r[6 + b];
+        }
+        double acc = 0.0;
+        for (int a = 0; a < 9; ++a) acc += dr[a] * d[a];
+        g[i] = acc;
+    }
+}
+}  // namespace detail
+
+struct GradCheckEntry {
+    double max_rel_err = 0.0;
+    int checked = 0;
+    int skipped_boundary = 0;
+    double worst_analytic = 0.0;
+    double worst_numeric = 0.0;
+};
+
+struct GradCheckReport {
+    std::map<std::string, GradCheckEntry> per_class;
+    double max_rel_err = 0.0;
+    int total_checked = 0;
+    int total_skipped = 0;
+    bool passed(double tol) const { return max_rel_err < tol; }
+};
+
+// grad.cpp:242-350: central differences of the loss over center / inv_cov /
+// attr / pose against backward(); directions whose selection sets change
+// within +-h are skipped. Forward evaluations run in the library's
+// verification mode (exact FP64 pair terms, gvr_context_set_precise).
+inline GradCheckReport gradcheck(const GaussianScene& scene, const Camera& camera, const SelectionConfig& cfg,
+                                 const ScalarLoss& loss, double h = 1e-4, double tol = 1e-3, int threads = 0) {
+    (void)tol;
+    struct Precise {
+        Precise() { detail::check(gvr_context_set_precise(detail::context(), 1)); }
+        ~Precise() { gvr_context_set_precise(detail::context(), 0); }
+    } precise;
+    double rr[9], w0[3];
+    for (int i = 0; i < 9; ++i) rr[i] = camera.rotation(i / 3, i % 3);
+    detail::so3_log_raw(rr, w0);
+    Camera cam = camera;
+    detail::so3_exp_raw(w0, rr);
+    for (int i = 0; i < 9; ++i) cam.rotation(i / 3, i % 3) = rr[i];
+
+    ForwardResult base = render_with_tape(scene, cam, cfg, threads);
+    Image d_image, d_alpha;
+    loss.value(base.buffers, &d_image, &d_alpha);
+    const GradientBundle bundle = backward(base.tape, d_image, d_alpha);
+    auto sets_of = [](const RenderBuffers& b) {
+        std::vector<std::vector<int>> s(b.weight_store.size());
+        for (size_t p = 0; p < s.size(); ++p)
+            for (const auto& e : b.weight_store[p]) s[p].push_back(e.first);
+        return s;
+    };
+    const auto base_sets = sets_of(base.buffers);
+    struct Eval {
+        double loss = 0.0;
+        bool valid = false;
+        std::vector<std::vector<int>> sets;
+    };
+    auto evaluate = [&](const GaussianScene& s, const Camera& c) {
+        Eval e;
+        try {
+            const RenderBuffers b = render(s, c, cfg, threads);
+            e.loss = loss.value(b, nullptr, nullptr);
+            e.sets = sets_of(b);
+            e.valid = true;
+        } catch (const ValidationError&) {
+            e.valid = false;
+        }
+        return e;
+    };
+    GradCheckReport report;
+    auto rel_err = [](double a, double n) {
+        if (std::abs(a) < 1e-7 && std::abs(n) < 1e-7) return 0.0;
+        return std::abs(a - n) / std::max(std::abs(a) + std::abs(n), 1e-6);
+    };
+    auto check = [&](const std::string& cls, double analytic, auto apply, double step) {
+        auto& entry = report.per_class[cls];
+        GaussianScene sp = scene, sm = scene;
+        Camera cp = cam, cm = cam;
+        apply(sp, cp, step);
+        apply(sm, cm, -step);
+        const Eval plus = evaluate(sp, cp), minus = evaluate(sm, cm);
+        if (!plus.valid || !minus.valid || plus.sets != base_sets || minus.sets != base_sets) {
+            ++entry.skipped_boundary;
+            ++report.total_skipped;
+            return;
+        }
+        const double numeric = (plus.loss - minus.loss) / (2.0 * step);
+        const double rel = rel_err(analytic, numeric);
+        ++entry.checked;
+        ++report.total_checked;
+        if (rel > entry.max_rel_err) {
+            entry.max_rel_err = rel;
+            entry.worst_analytic = analytic;
+            entry.worst_numeric = numeric;
+        }
+        report.max_rel_err = std::max(report.max_rel_err, rel);
+    };
+    for (int k = 0; k < scene.size(); ++k) {
+        for (int d = 0; d < 3; ++d)
+            check("center", bundle.d_center[k][d],
+                  [k, d](GaussianScene& s, Camera&, double e) { s.kernels[k].center[d] += e; },
+                  h * std::max(1.0, std::abs(scene.kernels[k].center[d])));
+        for (int i = 0; i < 3; ++i)
+            for (int j = i; j < 3; ++j)
+                check("inv_cov", i == j ? bundle.d_inv_cov[k](i, i) : 2.0 * bundle.d_inv_cov[k](i, j),
+                      [k, i, j](GaussianScene& s, Camera&, double e) {
+                          s.kernels[k].inv_cov(i, j) += e;
+                          if (i != j) s.kernels[k].inv_cov(j, i) += e;
+                      },
+                      h * std::max(1.0, std::abs(scene.kernels[k].inv_cov(i, j))));
+        for (int d = 0; d < scene.attr_dim(); ++d)
+            check("attr", bundle.d_attr[k][d], [k, d](GaussianScene& s, Camera&, double e) { s.kernels[k].attr[d] += e; },
+                  h);
+    }
+    double dr[9], dw[3];
+    for (int i = 0; i < 9; ++i) dr[i] = bundle.d_rotation(i / 3, i % 3);
+    detail::so3_exp_gradient_raw(w0, dr, dw);
+    for (int d = 0; d < 3; ++d)
+        check("pose", dw[d],
+              [&w0, d](GaussianScene&, Camera& c, double e) {
+                  double w[3] = {w0[0], w0[1], w0[2]}, r[9];
+                  w[d] += e;
+                  detail::so3_exp_raw(w, r);
+                  for (int i = 0; i < 9; ++i) c.rotation(i / 3, i % 3) = r[i];
+              },
+              h);
+    for (int d = 0; d < 3; ++d)
+        check("pose", bundle.d_translation[d], [d](GaussianScene&, Camera& c, double e) { c.translation[d] += e; },
+              h * std::max(1.0, std::abs(cam.translation[d])));
+    return report;
 }
 
 }  // namespace gvr

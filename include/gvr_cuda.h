@@ -133,6 +133,10 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops);
 /* Test hook: FP32 pre-filter guard band on q (default 0.02); a huge value sends
  * every candidate through the exact FP64 trace. Results must not change. */
 int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard);
+/* Verification mode: the blend evaluates every pair term from the exact FP64
+ * trace and erfc (the reference's arithmetic, ~1e-15) instead of the FP32
+ * closed-form pipeline. Slow; used by gradcheck's finite differences. */
+int gvr_context_set_precise(gvr_context* ctx, int on);
 /* Per-tile candidate-list capacity (default 4096 entries of 8 B per 8x8 tile).
  * Tiles whose list overflows stream every kernel through the same exact tests
  * (slower, same results); a small value exercises that path in tests. */

@@ -41,4 +41,5 @@ from .render import (  # noqa: F401
     transmittance_at,
 )
 from .synthetic import make_bench_camera, make_bench_scene, make_orbit_camera  # noqa: F401
+from .gradcheck import GradCheckEntry, GradCheckReport, gradcheck, so3_exp, so3_exp_gradient, so3_log  # noqa: F401
 from .scene_io import load_camera_json, load_scene_json  # noqa: F401

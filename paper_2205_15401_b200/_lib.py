@@ -58,6 +58,7 @@ EXPORTED_SYMBOLS = (
     "gvr_render_views",
     "gvr_scalar_loss_views",
     "gvr_backward_views",
+    "gvr_context_set_precise",
 )
 
 
@@ -133,6 +134,7 @@ def load() -> ctypes.CDLL:
         "gvr_context_stage_times": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
         "gvr_measure_pipe_peak": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(dp)]),
         "gvr_context_set_prefilter_guard": (ctypes.c_int, [vp, dp]),
+        "gvr_context_set_precise": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_context_set_tile_capacity": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_graph_begin": (ctypes.c_int, [vp]),
         "gvr_graph_end": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),

@@ -37,6 +37,7 @@ struct FwdParams {
     EntryRec* ent;  // [P*kp] traced selected entries (written by the blend)
     float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
     int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
+    int precise;     // verification mode: FP64 exact traces and erfc in the blend sums (gradcheck)
     int* nonfinite; // flag
 };
 
@@ -666,7 +667,24 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     }
     __syncwarp(grp);
 
-    for (int k = sub; k < n; k += 4) {
+    if (p.precise) {
+        // verification mode (gvr_context_set_precise): every pair term from the
+        // exact FP64 trace and erfc, W in FP64 -- the reference's arithmetic
+        for (int k = sub; k < n; k += 4) {
+            const Traced64 tk = trace_exact(d, p.rec64[b_id[k * NP + g]]);
+            double acc = 0.0;
+            for (int m = 0; m < n; ++m) {
+                const Traced64 tm = trace_exact(d, p.rec64[b_id[m * NP + g]]);
+                acc += exp(tm.q) * (0.5 * erfc(-((tk.l - tm.l) / sigma_of(tm.a)) * 0.7071067811865476));
+            }
+            const double trans = exp(-p.tau * acc);
+            const double wd = trans * exp(tk.q);
+            p.tape_t[pix * kp + k] = trans;
+            b_w[k * NP + g] = wd;
+            if (p.topk_w) p.topk_w[pix * kp + k] = wd;
+        }
+    }
+    for (int k = sub; k < n && !p.precise; k += 4) {
         const float2 hk = b_hl[k * NP + g];
         // sum_m e^{q_m} Phi(z_km): non-negative FP32 terms, Kahan-compensated
         // (error ~2^-24 of the sum, below the 6e-8 of the Phi approximation)

@@ -85,6 +85,7 @@ struct gvr_context {
     int64_t launches = 0;   // kernels of this library
     int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
     double guard = 0.02;
+    bool precise = false;  // verification mode of the blend (gvr_context_set_precise)
     int tile_cap = 4096;  // per-tile candidate-list capacity
     bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
@@ -552,6 +553,12 @@ int gvr_context_set_tile_capacity(gvr_context* ctx, int cap) {
     return GVR_OK;
 }
 
+int gvr_context_set_precise(gvr_context* ctx, int on) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    ctx->precise = on != 0;
+    return GVR_OK;
+}
+
 int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard) {
     if (!ctx || !(guard >= 0.0)) return GVR_ERR_RUNTIME;
     ctx->guard = guard;
@@ -791,6 +798,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.ent = tape->ent.as<EntryRec>();
     fp.nonfinite = dflags + 1;
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
+    fp.precise = ctx->precise ? 1 : 0;
     int rc = GVR_OK;
     int* order_b = sched + 2 + tiles;
     if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);

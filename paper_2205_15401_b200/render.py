@@ -117,6 +117,10 @@ class Context:
         """Test hook: per-tile candidate-list capacity (overflowing tiles stream every kernel)."""
         self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
 
+    def set_precise(self, on: bool = True) -> None:
+        """Verification mode: FP64 exact traces and erfc in the blend (gradcheck)."""
+        self.check(self.lib.gvr_context_set_precise(self.handle, int(bool(on))))
+
     def set_prefilter_guard(self, guard: float) -> None:
         self.check(self.lib.gvr_context_set_prefilter_guard(self.handle, float(guard)))
 

@@ -277,3 +277,21 @@ TEST_CASE("lambert shading basics") {  // test_blender.cpp:294-320
     Image bad(1, 2, 2);
     CHECK_THROWS_AS(shade_lambert(bad, alpha, depth, cam, Vec3(0, 0, -10), Vec3(1, 1, 1)), ValidationError);
 }
+
+TEST_CASE("gradcheck passes on random five-kernel scenes") {  // test_grad.cpp:95-110
+    std::mt19937_64 rng(64);
+    std::uniform_real_distribution<double> u01(0.0, 1.0);
+    for (int trial = 0; trial < 2; ++trial) {
+        const GaussianScene scene = random_scene(rng, 5);
+        Camera cam = default_camera(24, 12.0);
+        cam.translation = Vec3(0.02, 0.01, 0.1);
+        ScalarLoss loss;
+        loss.target_image = Image(24, 24, 3);
+        loss.target_alpha = Image(24, 24, 1, ChannelSemantics::Alpha);
+        for (auto& v : loss.target_image.data) v = u01(rng);
+        for (auto& v : loss.target_alpha.data) v = u01(rng);
+        const GradCheckReport report = gradcheck(scene, cam, SelectionConfig{}, loss, 1e-4, 1e-3, 1);
+        CHECK(report.max_rel_err < 1e-3);
+        CHECK(report.total_checked > 0);
+    }
+}

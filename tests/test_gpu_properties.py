@@ -431,3 +431,44 @@ def test_full_size_parity_against_oracle(ctx, view):
     go = oracle.port_backward(scene, cam, cfg, di, da, threads=0)
     for key in ("d_center", "d_inv_cov", "d_attr", "d_rotation", "d_translation"):
         assert_grad_close(getattr(g, key), go[key], what=f"{view} {key}")
+
+
+# ----------------------------------------------------------------- gradcheck (grad.cpp:242-350)
+
+def _random_loss(rng, cam, d=3):
+    """tests/test_grad.cpp random_loss: uniform targets."""
+    return gvr.ScalarLoss(rng.uniform(0, 1, (cam.height, cam.width, d)), rng.uniform(0, 1, (cam.height, cam.width, 1)))
+
+
+def test_gradcheck_passes_on_random_five_kernel_scenes(ctx):
+    """test_grad.cpp:95-110: central differences of the device forward agree with
+    the device backward to < 1e-3 over center / inv_cov / attr / pose; skips rare."""
+    rng = np.random.default_rng(64)
+    for trial in range(3):
+        scene = random_scene(100 + trial, 5, 3, 2.0, 20.0)
+        cam = default_camera(24, 12.0)
+        cam = Camera(gvr.so3_exp([0.05, -0.1, 0.03]), np.array([0.02, 0.01, 0.1]), cam.focal, cam.ox, cam.oy, 24, 24)
+        report = gvr.gradcheck(scene, cam, SelectionConfig(), _random_loss(rng, cam), 1e-4, 1e-3, ctx=ctx)
+        assert report.max_rel_err < 1e-3, {k: (v.max_rel_err, v.worst_analytic, v.worst_numeric)
+                                           for k, v in report.per_class.items()}
+        assert report.total_checked > 0
+        assert report.total_skipped <= (report.total_checked + report.total_skipped) // 20
+
+
+def test_gradcheck_on_the_reference_fixture(ctx):
+    """tests/data/gradcheck_{scene,camera}.json (golden gradcheck_scene)."""
+    from conftest import Golden
+
+    g = Golden("gradcheck_scene")
+    loss = gvr.ScalarLoss(g["image"] - g["d_image"], g["alpha"] - g["d_alpha"])
+    report = gvr.gradcheck(g.scene, g.camera, g.cfg, loss, 1e-4, 1e-3, ctx=ctx)
+    assert report.passed(1e-3)
+    assert report.total_checked > 0
+
+
+def test_gradcheck_kernels_behind_the_camera(ctx):
+    """test_grad.cpp:112-131: zero gradients, nothing skipped, max_rel_err == 0."""
+    scene = GaussianScene(np.array([[0, 0, -5.0]]), np.eye(3)[None], np.ones((1, 3)), 1.0)
+    cam = default_camera()
+    report = gvr.gradcheck(scene, cam, SelectionConfig(), _random_loss(np.random.default_rng(65), cam), ctx=ctx)
+    assert report.max_rel_err == 0.0

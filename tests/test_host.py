@@ -129,3 +129,23 @@ def test_cpp_dropin_header_compiles_and_links():
                             os.path.join(root, "tests", "cpp", "test_cpp_api.cpp"), f"-L{PKG}", "-lgvr_cuda",
                             f"-Wl,-rpath,{PKG}", "-o", exe], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_so3_chart_round_trip():
+    import importlib
+
+    gvr_so3 = importlib.import_module("paper_2205_15401_b200.gradcheck")
+
+    """so3_log(so3_exp(w)) == w and so3_exp_gradient matches central differences."""
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        w = rng.normal(size=3) * 0.7
+        assert np.allclose(gvr_so3.so3_log(gvr_so3.so3_exp(w)), w, atol=1e-12)
+        dr = rng.normal(size=(3, 3))
+        g = gvr_so3.so3_exp_gradient(w, dr)
+        num = np.zeros(3)
+        for i in range(3):
+            e = np.zeros(3)
+            e[i] = 1e-6
+            num[i] = ((gvr_so3.so3_exp(w + e) - gvr_so3.so3_exp(w - e)) * dr).sum() / 2e-6
+        assert np.allclose(g, num, rtol=1e-6, atol=1e-8)
