@@ -30,6 +30,9 @@
  *   normalized_weights(RayBlend, eps)  blender.hpp:36               gvr_tape_normalized_weights
  *   Image shade_lambert(normals, alpha, depth, camera, light_pos, light_color)
  *                                      blender.hpp:46-47            gvr_shade_lambert
+ *   ShapeRegularizer::make / edge_reg / laplacian_reg
+ *                                      fit.hpp:50-67                gvr_regularizer_create / gvr_edge_reg /
+ *                                                                   gvr_laplacian_reg
  *   ValidationError (std::runtime_error)
  *                                      types.hpp:19-22              return GVR_ERR_VALIDATION +
  *                                                                   gvr_last_error() (same text)
@@ -68,6 +71,7 @@ typedef struct gvr_context gvr_context;
 typedef struct gvr_scene gvr_scene;
 typedef struct gvr_tape gvr_tape;
 typedef struct gvr_graph gvr_graph;
+typedef struct gvr_regularizer gvr_regularizer;
 
 /* gvr::Camera (types.hpp:46-56) */
 typedef struct {
@@ -261,6 +265,20 @@ int gvr_scalar_loss_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* ta
  * added in ascending order) — DEVICE pointers, either nullable. */
 int gvr_backward_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes, const gvr_grad_flags* flags,
                        const gvr_gradients* outs, const gvr_gradients* sum);
+
+/* ---- fitting regularizers (fit.hpp:50-67, fit.cpp:44-115) ----------------- */
+/* ShapeRegularizer::make: host edges[2*n_edges] (vertex pairs), rest_centers[3*n_vertices]
+ * (host or device). No edges -> GVR_ERR_VALIDATION "regularizer needs a non-empty neighbor graph". */
+int gvr_regularizer_create(gvr_context* ctx, int32_t n_vertices, int32_t n_edges, const int32_t* edges,
+                           const double* rest_centers, gvr_regularizer** out);
+void gvr_regularizer_destroy(gvr_regularizer* reg);
+/* edge_reg / laplacian_reg at centers[3N]: *value = the (unweighted) term;
+ * grad[3N] (nullable, host or device) receives weight * d(term)/d(centers),
+ * added when accumulate != 0 (the fit loop's gradient), else overwritten. */
+int gvr_edge_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* centers, double weight, double* value,
+                 double* grad, int32_t accumulate);
+int gvr_laplacian_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* centers, double weight,
+                      double* value, double* grad, int32_t accumulate);
 
 #ifdef __cplusplus
 }

@@ -416,3 +416,14 @@ def ref_shade_lambert(cam, normals, alpha, depth, light_pos, light_color):
     out = np.zeros((h, w, 3))
     _ref_call("gvr_ref_shade_lambert", _ptr(_cam17(cam)), _ptr(n), _ptr(al), _ptr(de), _ptr(lp), _ptr(lc), _ptr(out))
     return out
+
+
+def ref_shape_reg(edges, rest, centers):
+    """Reference ShapeRegularizer::make + edge_reg / laplacian_reg (fit.cpp:44-113):
+    (edge value, edge grad [N,3], laplacian value, laplacian grad [N,3])."""
+    e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+    r = np.ascontiguousarray(rest, dtype=np.float64).reshape(-1, 3)
+    c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+    vals, ge, gl = np.zeros(2), np.zeros_like(c), np.zeros_like(c)
+    _ref_call("gvr_ref_shape_reg", r.shape[0], e.shape[0], _ptr(e, _ip), _ptr(r), _ptr(c), _ptr(vals), _ptr(ge), _ptr(gl))
+    return vals[0], ge, vals[1], gl

@@ -10,6 +10,7 @@
 //   gvr::make_bench_scene / camera   (proj/src/bench.cpp:9-24)
 //   gvr::make_orbit_camera           (proj/src/shapes.cpp:118)
 //   gvr::sample_attributes / resynthesize (proj/src/sampler.cpp:11-66)
+//   gvr::ShapeRegularizer::make / edge_reg / laplacian_reg (proj/src/fit.cpp:44-113)
 //   gvr::transmittance_at / normalized_weights / shade_lambert
 //                                    (proj/src/blender.cpp:19-25, 55-62, 146-172)
 // Per-pixel variable-length lists come back padded to k_prime (index -1).
@@ -18,6 +19,7 @@
 #include "gvr/bench.hpp"
 #include "gvr/blender.hpp"
 #include "gvr/grad.hpp"
+#include "gvr/fit.hpp"
 #include "gvr/sampler.hpp"
 #include "gvr/scene.hpp"
 #include "gvr/shapes.hpp"
@@ -387,6 +389,32 @@ int gvr_ref_shade_lambert(const double* cam, const double* normals, const double
             n, a, z, camera, gvr::Vec3(light_pos[0], light_pos[1], light_pos[2]),
             gvr::Vec3(light_color[0], light_color[1], light_color[2]));
         std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+    });
+}
+
+// ShapeRegularizer::make(edges, rest) then edge_reg / laplacian_reg at centers
+// (proj/src/fit.cpp:44-113). Outputs: values[2] = (edge, laplacian), grads
+// [N*3] each (nullable).
+int gvr_ref_shape_reg(int n_vertices, int n_edges, const int* edges, const double* rest, const double* centers,
+                      double* values, double* edge_grad, double* lap_grad) {
+    return guarded([&] {
+        std::vector<std::pair<int, int>> e;
+        for (int i = 0; i < n_edges; ++i) e.emplace_back(edges[2 * i], edges[2 * i + 1]);
+        std::vector<gvr::Vec3> r(n_vertices), c(n_vertices);
+        for (int i = 0; i < n_vertices; ++i) {
+            r[i] = gvr::Vec3(rest[3 * i], rest[3 * i + 1], rest[3 * i + 2]);
+            c[i] = gvr::Vec3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+        }
+        const gvr::ShapeRegularizer reg = gvr::ShapeRegularizer::make(e, r);
+        std::vector<gvr::Vec3> g;
+        values[0] = gvr::edge_reg(c, reg, &g);
+        if (edge_grad)
+            for (int i = 0; i < n_vertices; ++i)
+                for (int d = 0; d < 3; ++d) edge_grad[3 * i + d] = g[i][d];
+        values[1] = gvr::laplacian_reg(c, reg, &g);
+        if (lap_grad)
+            for (int i = 0; i < n_vertices; ++i)
+                for (int d = 0; d < 3; ++d) lap_grad[3 * i + d] = g[i][d];
     });
 }
 

@@ -59,6 +59,10 @@ EXPORTED_SYMBOLS = (
     "gvr_scalar_loss_views",
     "gvr_backward_views",
     "gvr_context_set_precise",
+    "gvr_regularizer_create",
+    "gvr_regularizer_destroy",
+    "gvr_edge_reg",
+    "gvr_laplacian_reg",
 )
 
 
@@ -171,6 +175,10 @@ def load() -> ctypes.CDLL:
                                                  dp, dp, vp]),
         "gvr_backward_views": (ctypes.c_int, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(GvrGradFlags),
                                               ctypes.POINTER(GvrGradients), ctypes.POINTER(GvrGradients)]),
+        "gvr_regularizer_create": (ctypes.c_int, [vp, i32, i32, vp, vp, ctypes.POINTER(vp)]),
+        "gvr_regularizer_destroy": (None, [vp]),
+        "gvr_edge_reg": (ctypes.c_int, [vp, vp, vp, dp, vp, vp, i32]),
+        "gvr_laplacian_reg": (ctypes.c_int, [vp, vp, vp, dp, vp, vp, i32]),
         "gvr_shade_lambert": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():

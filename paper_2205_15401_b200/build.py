@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgvr_cuda.so")
 SOURCES = ["gvr_cuda.cu"]
-DEPS = ["gvr_cuda.cu", "gvr_common.cuh", "project.cuh", "forward.cuh", "backward.cuh", "sampler.cuh"]
+DEPS = ["gvr_cuda.cu", "gvr_common.cuh", "project.cuh", "forward.cuh", "backward.cuh", "sampler.cuh", "fit.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

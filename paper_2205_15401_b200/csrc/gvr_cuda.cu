@@ -8,6 +8,7 @@
 //   gvr_scalar_loss, gvr_backward : K4 per-pixel backward -> K5 object space
 #include "../../include/gvr_cuda.h"
 #include "backward.cuh"
+#include "fit.cuh"
 #include "forward.cuh"
 #include "project.cuh"
 #include "sampler.cuh"
@@ -1519,6 +1520,150 @@ int gvr_backward_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes
         LAUNCH_CHECK(ctx);
     }
     return GVR_OK;
+}
+
+}  // extern "C"
+
+
+// ---------------------------------------------------------------- fitting regularizers (fit.cpp:44-115)
+
+struct gvr_regularizer {
+    gvr_context* ctx = nullptr;
+    int N = 0, E = 0;
+    Buf edges, rest_len, adj_start, adj, rest_lap, value;
+};
+
+namespace {
+
+RegView reg_view(const gvr_regularizer* r) {
+    RegView v;
+    v.N = r->N;
+    v.E = r->E;
+    v.edges = r->edges.as<int>();
+    v.rest_len = r->rest_len.as<double>();
+    v.adj_start = r->adj_start.as<int>();
+    v.adj = r->adj.as<int>();
+    v.rest_lap = r->rest_lap.as<double>();
+    return v;
+}
+
+int reg_term(gvr_context* ctx, const gvr_regularizer* r, const double* centers, double weight, double* value,
+             double* grad, int32_t accumulate, bool laplacian) {
+    if (!ctx || !r || !centers) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (r->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
+    const void* dc = nullptr;
+    if (int rc = stage_in(ctx, ctx->scratch[0], centers, sizeof(double) * 3 * (size_t)r->N, &dc)) return rc;
+    void* dg = nullptr;
+    bool host_g = false;
+    if (grad) {
+        if (int rc = stage_out(ctx, ctx->scratch[1], grad, sizeof(double) * 3 * (size_t)r->N, &dg, &host_g)) return rc;
+        if (!accumulate || host_g) {
+            if (host_g && accumulate)
+                CUDA_TRY(ctx, cudaMemcpyAsync(dg, grad, sizeof(double) * 3 * (size_t)r->N, cudaMemcpyHostToDevice,
+                                              ctx->stream));
+            else
+                CUDA_TRY(ctx, cudaMemsetAsync(dg, 0, sizeof(double) * 3 * (size_t)r->N, ctx->stream));
+        }
+    }
+    double* dv = r->value.as<double>();
+    CUDA_TRY(ctx, cudaMemsetAsync(dv, 0, sizeof(double), ctx->stream));
+    const RegView v = reg_view(r);
+    if (laplacian)
+        laplacian_reg_kernel<<<blocks_for(r->N, 256), 256, 0, ctx->stream>>>(v, static_cast<const double*>(dc), weight,
+                                                                              dv, static_cast<double*>(dg));
+    else
+        edge_reg_kernel<<<blocks_for(r->E, 256), 256, 0, ctx->stream>>>(v, static_cast<const double*>(dc), weight, dv,
+                                                                         static_cast<double*>(dg));
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (value)
+        if (int rc = copy_out(ctx, value, dv, sizeof(double), &host)) return rc;
+    if (host_g)
+        if (int rc = copy_out(ctx, grad, dg, sizeof(double) * 3 * (size_t)r->N, &host)) return rc;
+    return host ? sync_and_check(ctx) : GVR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gvr_regularizer_create(gvr_context* ctx, int32_t n_vertices, int32_t n_edges, const int32_t* edges,
+                           const double* rest_centers, gvr_regularizer** out) {
+    if (!ctx || !out) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    *out = nullptr;
+    if (n_edges <= 0 || !edges) return set_err(ctx, GVR_ERR_VALIDATION, "regularizer needs a non-empty neighbor graph");
+    if (n_vertices < 0 || (n_vertices > 0 && !rest_centers)) return set_err(ctx, GVR_ERR_RUNTIME, "bad vertex array");
+    if (is_device_ptr(edges)) return set_err(ctx, GVR_ERR_RUNTIME, "edges must be a host array");
+    // CSR adjacency, each vertex's neighbours in the order the edges list them
+    // (adjacency[a].push_back(b); adjacency[b].push_back(a), fit.cpp:53-55)
+    std::vector<int> start(n_vertices + 1, 0), fill, adj(2 * (size_t)n_edges);
+    for (int e = 0; e < n_edges; ++e) {
+        const int a = edges[2 * e], b = edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= n_vertices || b >= n_vertices)
+            return set_err(ctx, GVR_ERR_VALIDATION, "regularizer edge index out of range");
+        ++start[a + 1];
+        ++start[b + 1];
+    }
+    for (int i = 0; i < n_vertices; ++i) start[i + 1] += start[i];
+    fill.assign(start.begin(), start.end() - 1);
+    for (int e = 0; e < n_edges; ++e) {
+        const int a = edges[2 * e], b = edges[2 * e + 1];
+        adj[fill[a]++] = b;
+        adj[fill[b]++] = a;
+    }
+    auto* r = new gvr_regularizer();
+    r->ctx = ctx;
+    r->N = n_vertices;
+    r->E = n_edges;
+    auto fail = [&](int rc) {
+        delete r;
+        return rc;
+    };
+    const size_t vb = sizeof(double) * 3 * (size_t)std::max(n_vertices, 1);
+    if (r->edges.ensure(sizeof(int) * 2 * (size_t)n_edges) != cudaSuccess ||
+        r->rest_len.ensure(sizeof(double) * (size_t)n_edges) != cudaSuccess ||
+        r->adj_start.ensure(sizeof(int) * (size_t)(n_vertices + 1)) != cudaSuccess ||
+        r->adj.ensure(sizeof(int) * adj.size()) != cudaSuccess || r->rest_lap.ensure(vb) != cudaSuccess ||
+        r->value.ensure(sizeof(double)) != cudaSuccess)
+        return fail(set_err(ctx, GVR_ERR_RUNTIME, "regularizer allocation failed"));
+    cudaError_t e1 = cudaMemcpyAsync(r->edges.p, edges, sizeof(int) * 2 * (size_t)n_edges, cudaMemcpyHostToDevice,
+                                     ctx->stream);
+    cudaError_t e2 = cudaMemcpyAsync(r->adj_start.p, start.data(), sizeof(int) * start.size(), cudaMemcpyHostToDevice,
+                                     ctx->stream);
+    cudaError_t e3 = cudaMemcpyAsync(r->adj.p, adj.data(), sizeof(int) * adj.size(), cudaMemcpyHostToDevice, ctx->stream);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+        return fail(set_err(ctx, GVR_ERR_RUNTIME, "regularizer upload failed"));
+    const void* dc = nullptr;
+    if (int rc = stage_in(ctx, ctx->scratch[0], rest_centers, sizeof(double) * 3 * (size_t)n_vertices, &dc))
+        return fail(rc);
+    const RegView v = reg_view(r);
+    rest_edge_kernel<<<blocks_for(n_edges, 256), 256, 0, ctx->stream>>>(v, static_cast<const double*>(dc),
+                                                                         r->rest_len.as<double>());
+    if (n_vertices > 0)
+        rest_laplacian_kernel<<<blocks_for(n_vertices, 256), 256, 0, ctx->stream>>>(v, static_cast<const double*>(dc),
+                                                                                     r->rest_lap.as<double>());
+    ctx->launches += 2;
+    if (int rc = sync_and_check(ctx)) return fail(rc);  // host vectors above are released on return
+    *out = r;
+    return GVR_OK;
+}
+
+void gvr_regularizer_destroy(gvr_regularizer* r) {
+    if (!r) return;
+    cudaStreamSynchronize(r->ctx->stream);
+    Buf* bufs[] = {&r->edges, &r->rest_len, &r->adj_start, &r->adj, &r->rest_lap, &r->value};
+    for (Buf* b : bufs) b->release();
+    delete r;
+}
+
+int gvr_edge_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* centers, double weight, double* value,
+                 double* grad, int32_t accumulate) {
+    return reg_term(ctx, reg, centers, weight, value, grad, accumulate, false);
+}
+
+int gvr_laplacian_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* centers, double weight, double* value,
+                      double* grad, int32_t accumulate) {
+    return reg_term(ctx, reg, centers, weight, value, grad, accumulate, true);
 }
 
 }  // extern "C"

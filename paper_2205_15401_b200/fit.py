@@ -14,9 +14,11 @@ the GPU and the views sharded across ranks:
   the only collective of the render path)
   ADAM on [centers | attrs] (gvr_adam_step), identical on every rank.
 
-Differences from fit_shape: every view is used every iteration (the C5 config:
-32 views, no random batch sampling) and the edge / Laplacian regularisers are
-not applied (rgb + silhouette terms only).
+plus, when a ``ShapeRegularizer`` is given, the edge-length and uniform-Laplacian
+terms on the centres (fit.cpp:66-113, device kernels, weights of LossSpec).
+
+Difference from fit_shape: every view is used every iteration (the C5 config:
+32 views, no random batch sampling).
 """
 from __future__ import annotations
 
@@ -29,6 +31,71 @@ from .distributed import allreduce_gradients, shard_views
 from .render import (Context, DeviceScene, Tape, adam_step, backward_views_into, render_views_into,
                      scalar_loss_views_into)
 from .types import Camera, GaussianScene, GradFlags, SelectionConfig
+
+
+@dataclass
+class LossSpec:
+    """``gvr::LossSpec`` (fit.hpp:9-16)."""
+
+    rgb_weight: float = 1.0
+    silhouette_weight: float = 1.0
+    edge_weight: float = 0.0
+    laplacian_weight: float = 0.0
+
+    def validate(self) -> None:
+        """fit.cpp:10-18, same messages."""
+        from .types import ValidationError
+
+        if min(self.rgb_weight, self.silhouette_weight, self.edge_weight, self.laplacian_weight) < 0.0:
+            raise ValidationError("loss weights must be non-negative")
+        if self.rgb_weight == 0.0 and self.silhouette_weight == 0.0 and self.edge_weight == 0.0 and \
+                self.laplacian_weight == 0.0:
+            raise ValidationError("at least one loss weight must be positive")
+
+
+class ShapeRegularizer:
+    """``gvr::ShapeRegularizer`` (fit.hpp:50-60) on the device: neighbour graph,
+    rest edge lengths and rest Laplacian displacements (fit.cpp:44-64)."""
+
+    def __init__(self, ctx: Context, edges, rest_centers):
+        import ctypes
+
+        self.ctx = ctx
+        e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+        c = np.ascontiguousarray(rest_centers, dtype=np.float64).reshape(-1, 3)
+        self.n_vertices, self.n_edges = c.shape[0], e.shape[0]
+        h = ctypes.c_void_p()
+        ctx.check(ctx.lib.gvr_regularizer_create(ctx.handle, self.n_vertices, self.n_edges,
+                                                 e.ctypes.data if e.size else None, c.ctypes.data, ctypes.byref(h)))
+        self.handle = h
+
+    def _term(self, fn, centers, weight: float, grad, accumulate: bool):
+        from .render import _ptr
+
+        out = np.zeros(1)
+        c = np.ascontiguousarray(centers, dtype=np.float64) if isinstance(centers, np.ndarray) else centers
+        self.ctx.check(fn(self.ctx.handle, self.handle, _ptr(c), float(weight), _ptr(out), _ptr(grad),
+                          int(bool(accumulate))))
+        return float(out[0])
+
+    def edge_reg(self, centers, grad=None, weight: float = 1.0, accumulate: bool = False) -> float:
+        """``edge_reg`` (fit.cpp:66-85); grad [N, 3] receives weight * gradient."""
+        return self._term(self.ctx.lib.gvr_edge_reg, centers, weight, grad, accumulate)
+
+    def laplacian_reg(self, centers, grad=None, weight: float = 1.0, accumulate: bool = False) -> float:
+        """``laplacian_reg`` (fit.cpp:87-113)."""
+        return self._term(self.ctx.lib.gvr_laplacian_reg, centers, weight, grad, accumulate)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.gvr_regularizer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass
@@ -46,8 +113,13 @@ class Fitter:
 
     def __init__(self, ctx: Context, scene: GaussianScene, views: Sequence[Tuple[Camera, np.ndarray, np.ndarray]],
                  cfg: SelectionConfig = SelectionConfig(), rgb_weight: float = 1.0, silhouette_weight: float = 1.0,
-                 adam: AdamConfig = AdamConfig(), rank: int = 0, world: int = 1, device=None):
+                 adam: AdamConfig = AdamConfig(), rank: int = 0, world: int = 1, device=None,
+                 regularizer: Optional["ShapeRegularizer"] = None, edge_weight: float = 0.0,
+                 laplacian_weight: float = 0.0):
         import torch
+
+        LossSpec(rgb_weight, silhouette_weight, edge_weight, laplacian_weight).validate()
+        self.reg, self.edge_weight, self.laplacian_weight = regularizer, edge_weight, laplacian_weight
 
         self.torch = torch
         self.ctx = ctx
@@ -106,6 +178,10 @@ class Fitter:
             scalar_loss_views_into(self.ctx, tapes, tis, tas, w_img, w_alpha, losses)
             backward_views_into(self.ctx, tapes, GradFlags(), None, self.total)
             self.loss_acc += losses.sum()
+        if self.reg is not None and self.rank == 0:  # once per iteration (added before the rank sum)
+            for w, fn in ((self.edge_weight, self.reg.edge_reg), (self.laplacian_weight, self.reg.laplacian_reg)):
+                if w > 0.0:
+                    self.loss_acc += w * fn(self.centers, self.g_center.view(self.K, 3), w, accumulate=True)
 
     def step(self, group=None) -> None:
         """One fit_shape iteration: loss_and_grad, NCCL all-reduce, ADAM."""

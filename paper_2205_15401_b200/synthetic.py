@@ -64,6 +64,18 @@ def make_box_mesh(size=(1.0, 1.0, 1.0), divisions: int = 1, center=(0.0, 0.0, 0.
     return verts, np.concatenate(faces)
 
 
+def mesh_edges(faces) -> np.ndarray:
+    """Unique undirected edges (a < b) in std::set order (convert.cpp:39-51): [E, 2] int32."""
+    f = np.asarray(faces, dtype=np.int64)
+    e = np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]])
+    e = e[e[:, 0] != e[:, 1]]
+    a = np.minimum(e[:, 0], e[:, 1])
+    b = np.maximum(e[:, 0], e[:, 1])
+    n = int(max(a.max(), b.max())) + 1 if len(a) else 1
+    code = np.unique(a * n + b)
+    return np.stack([code // n, code % n], 1).astype(np.int32)
+
+
 def mesh_to_gaussians_isotropic(verts, faces, zeta: float, colors) -> GaussianScene:
     """``mesh_to_gaussians`` with flatten_rate = 1 (convert.cpp:90-130)."""
     nv = verts.shape[0]

@@ -126,6 +126,20 @@ def main() -> None:
     hs = random_frustum_scene(13, 200, 3, 8.0, 120.0)
     hs.centers[-1] = (0.0, 0.0, 300.0)
     save("sampler_random", hs, default_camera(48, 40.0), SelectionConfig(k_prime=12), 13, extra=sampler_extra)
+    regularizer_golden()
+
+
+def regularizer_golden() -> None:
+    """fit.cpp:44-113 on the bench box mesh (divisions 6) with jittered centres."""
+    verts, faces = synthetic.make_box_mesh((1.0, 1.0, 1.0), 6, (0.0, 0.0, 4.0))
+    edges = synthetic.mesh_edges(faces)
+    centers = verts + np.random.default_rng(14).normal(0.0, 0.01, verts.shape)
+    ev, eg, lv, lg = oracle.ref_shape_reg(edges, verts, centers)
+    path = os.path.join(HERE, "aux", "fit_regularizers.npz")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez_compressed(path, edges=edges, rest=verts, centers=centers, edge_value=ev, edge_grad=eg,
+                        laplacian_value=lv, laplacian_grad=lg)
+    print(f"fit_regularizers: V={len(verts)} E={len(edges)} edge={ev:.6e} laplacian={lv:.6e}")
 
 
 if __name__ == "__main__":

@@ -166,3 +166,23 @@ def test_port_sampler_equals_reference_random():
     de = rng.uniform(2, 6, (32, 28, 1))
     assert np.array_equal(oracle.port_shade_lambert(cam, n, al, de, [1.0, 2.0, -3.0], [0.9, 0.5, 0.1]),
                           oracle.ref_shade_lambert(cam, n, al, de, [1.0, 2.0, -3.0], [0.9, 0.5, 0.1]))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference build not present")
+def test_reference_regularizers_reproduce_golden():
+    """tests/golden/aux/fit_regularizers.npz was made by the reference build (fit.cpp:44-113)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "aux", "fit_regularizers.npz"))
+    ev, eg, lv, lg = oracle.ref_shape_reg(g["edges"], g["rest"], g["centers"])
+    assert ev == g["edge_value"] and lv == g["laplacian_value"]
+    assert np.array_equal(eg, g["edge_grad"]) and np.array_equal(lg, g["laplacian_grad"])
+
+
+def test_mesh_edges_of_the_box_mesh():
+    """mesh_edges (convert.cpp:39-51): unique sorted pairs; a closed box grid has E = 3V - 6."""
+    from paper_2205_15401_b200 import synthetic
+
+    verts, faces = synthetic.make_box_mesh((1.0, 1.0, 1.0), 6, (0.0, 0.0, 4.0))
+    e = synthetic.mesh_edges(faces)
+    assert np.all(e[:, 0] < e[:, 1])
+    assert len(np.unique(e[:, 0].astype(np.int64) * len(verts) + e[:, 1])) == len(e)
+    assert len(e) == 3 * len(verts) - 6
