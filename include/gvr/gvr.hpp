@@ -245,8 +245,8 @@ inline gvr_selection to_c(const SelectionConfig& s) {
 
 }  // namespace detail
 
-// grad.hpp:26-33. The device record of the forward; `traced` (Tape::traced) is
-// materialised on first use, `cam_scene` is not kept (it lives on the device).
+// grad.hpp:26-33. The device record of the forward; `traced` (Tape::traced) and
+// the camera-space scene (`cam_scene()`, Tape::cam_scene) are materialised on request.
 struct Tape {
     GaussianScene scene;
     Camera camera;
@@ -254,6 +254,19 @@ struct Tape {
     int threads = 0;
     std::shared_ptr<detail::SceneHandle> device_scene;
     std::shared_ptr<detail::TapeHandle> device_tape;
+
+    GaussianScene cam_scene() const {  // view_transform (scene.cpp:5-17) as the device computed it
+        const size_t k = scene.kernels.size();
+        std::vector<double> c(3 * k), s(9 * k);
+        detail::check(gvr_tape_cam_scene(detail::context(), device_tape->t, c.data(), s.data()));
+        GaussianScene out = scene;
+        for (size_t i = 0; i < k; ++i) {
+            out.kernels[i].center = Vec3(c[3 * i], c[3 * i + 1], c[3 * i + 2]);
+            for (int r = 0; r < 3; ++r)
+                for (int t = 0; t < 3; ++t) out.kernels[i].inv_cov(r, t) = s[9 * i + 3 * r + t];
+        }
+        return out;
+    }
 
     std::vector<std::vector<TracedKernel>> traced() const {
         const size_t p = static_cast<size_t>(camera.height) * camera.width, kp = cfg.k_prime;

@@ -15,7 +15,10 @@
  *   ForwardResult render_with_tape(scene, camera, cfg, threads)
  *                                      grad.hpp:41-42               gvr_render(tape)
  *   detail::render_core(..., traced_out, cam_scene_out)
- *                                      blender.hpp:53-56            gvr_render + gvr_tape_traced
+ *                                      blender.hpp:53-56            gvr_render + gvr_tape_traced +
+ *                                                                   gvr_tape_cam_scene
+ *   PixelKernelMap::dropped_behind_camera
+ *                                      tracer.hpp:39                gvr_tape_dropped_behind_camera
  *   RenderBuffers::weight_store        blender.hpp:24               gvr_render_outputs.topk_idx/topk_w
  *   GradientBundle backward(tape, d_image, d_alpha, flags)
  *                                      grad.hpp:53-54               gvr_backward
@@ -190,6 +193,12 @@ int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const gvr_camera*
  * Any pointer may be NULL. */
 int gvr_tape_traced(gvr_context* ctx, const gvr_tape* tape, int32_t* idx, double* l, double* q,
                     double* sigma);
+/* Tape::cam_scene (grad.hpp:29): the camera-space scene of the taped render
+ * (view_transform, scene.cpp:5-17; centers K*3, inv_cov K*9; either nullable). */
+int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* tape, double* centers, double* inv_cov);
+/* PixelKernelMap::dropped_behind_camera (tracer.hpp:39): kernels of the taped
+ * render with camera-space z <= 1e-4. Synchronises. */
+int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* tape, int32_t* count);
 /* Shape of the taped render. */
 int gvr_tape_shape(const gvr_tape* tape, int32_t* height, int32_t* width, int32_t* k_prime,
                    int32_t* attr_dim);

@@ -427,3 +427,12 @@ def ref_shape_reg(edges, rest, centers):
     vals, ge, gl = np.zeros(2), np.zeros_like(c), np.zeros_like(c)
     _ref_call("gvr_ref_shape_reg", r.shape[0], e.shape[0], _ptr(e, _ip), _ptr(r), _ptr(c), _ptr(vals), _ptr(ge), _ptr(gl))
     return vals[0], ge, vals[1], gl
+
+
+def ref_view_transform(scene, cam):
+    """Reference gvr::view_transform (scene.cpp:5-17): (centers [K,3], inv_cov [K,3,3])."""
+    c, s, a = _scene_arrays(scene)
+    oc, os_ = np.zeros((scene.size, 3)), np.zeros((scene.size, 3, 3))
+    _ref_call("gvr_ref_view_transform", scene.size, scene.attr_dim(), ctypes.c_double(scene.tau), _ptr(c), _ptr(s),
+              _ptr(a), _ptr(_cam17(cam)), _ptr(oc), _ptr(os_))
+    return oc, os_

@@ -418,4 +418,18 @@ int gvr_ref_shape_reg(int n_vertices, int n_edges, const int* edges, const doubl
     });
 }
 
+// gvr::view_transform (proj/src/scene.cpp:5-17): camera-space centers / inv_cov.
+int gvr_ref_view_transform(int k, int d, double tau, const double* centers, const double* inv_cov,
+                           const double* attr, const double* cam, double* out_centers, double* out_inv_cov) {
+    return guarded([&] {
+        const auto scene = make_scene(k, d, tau, centers, inv_cov, attr);
+        const auto cs = gvr::view_transform(scene, make_camera(cam));
+        for (int i = 0; i < k; ++i) {
+            for (int t = 0; t < 3; ++t) out_centers[3 * i + t] = cs.kernels[i].center[t];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) out_inv_cov[9 * i + 3 * r + c] = cs.kernels[i].inv_cov(r, c);
+        }
+    });
+}
+
 }  // extern "C"

@@ -63,6 +63,8 @@ EXPORTED_SYMBOLS = (
     "gvr_regularizer_destroy",
     "gvr_edge_reg",
     "gvr_laplacian_reg",
+    "gvr_tape_cam_scene",
+    "gvr_tape_dropped_behind_camera",
 )
 
 
@@ -154,6 +156,8 @@ def load() -> ctypes.CDLL:
         "gvr_render": (ctypes.c_int, [vp, vp, ctypes.POINTER(GvrCamera), ctypes.POINTER(GvrSelection), vp,
                                       ctypes.POINTER(GvrRenderOutputs)]),
         "gvr_tape_traced": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
+        "gvr_tape_cam_scene": (ctypes.c_int, [vp, vp, vp, vp]),
+        "gvr_tape_dropped_behind_camera": (ctypes.c_int, [vp, vp, ctypes.POINTER(i32)]),
         "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                                           ctypes.POINTER(i32)]),
         "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),

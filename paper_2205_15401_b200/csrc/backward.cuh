@@ -382,6 +382,19 @@ __global__ void expand_topk_kernel(long long P, int kp, const int* __restrict__ 
     if (out_w) out_w[o] = ok ? topk_w[o] : 0.0;
 }
 
+// Tape::cam_scene copy-out: the view-transformed centres and inverse
+// covariances (scene.cpp:5-17) exactly as the projection computed them.
+__global__ void cam_scene_kernel(int K, const Rec64* __restrict__ rec64, double* __restrict__ centers,
+                                 double* __restrict__ inv_cov) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const Rec64& r = rec64[k];
+    if (centers)
+        for (int t = 0; t < 3; ++t) centers[3ll * k + t] = r.m[t];
+    if (inv_cov)
+        for (int t = 0; t < 9; ++t) inv_cov[9ll * k + t] = r.s[t];
+}
+
 // Tape::traced copy-out: exact FP64 (l, q, sigma) of the taped selection.
 __global__ void traced_kernel(CameraP cam, int kp, const int* __restrict__ topk, const int* __restrict__ count,
                               const Rec64* __restrict__ rec64, int* __restrict__ out_idx, double* __restrict__ out_l,

@@ -1667,3 +1667,37 @@ int gvr_laplacian_reg(gvr_context* ctx, const gvr_regularizer* reg, const double
 }
 
 }  // extern "C"
+
+
+// ---------------------------------------------------------------- tape extras
+
+extern "C" {
+
+int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* t, double* centers, double* inv_cov) {
+    if (int rc = tape_ready(ctx, t)) return rc;
+    const int K = t->K;
+    if (K == 0) return GVR_OK;
+    void *dc = nullptr, *ds = nullptr;
+    bool hc = false, hs = false;
+    if (int rc = stage_out(ctx, ctx->scratch[0], centers, sizeof(double) * 3 * (size_t)K, &dc, &hc)) return rc;
+    if (int rc = stage_out(ctx, ctx->scratch[1], inv_cov, sizeof(double) * 9 * (size_t)K, &ds, &hs)) return rc;
+    cam_scene_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(K, t->rec64.as<Rec64>(), static_cast<double*>(dc),
+                                                                  static_cast<double*>(ds));
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (hc)
+        if (int rc = copy_out(ctx, centers, dc, sizeof(double) * 3 * (size_t)K, &host)) return rc;
+    if (hs)
+        if (int rc = copy_out(ctx, inv_cov, ds, sizeof(double) * 9 * (size_t)K, &host)) return rc;
+    return host ? sync_and_check(ctx) : GVR_OK;
+}
+
+int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* t, int32_t* count) {
+    if (!ctx || !t || !t->valid || !count) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    CUDA_TRY(ctx, cudaMemcpyAsync(t->h_flags, t->flags.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    *count = t->h_flags[0];
+    return GVR_OK;
+}
+
+}  // extern "C"

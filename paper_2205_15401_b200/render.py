@@ -249,6 +249,19 @@ class Tape:
                                                     _ptr(s)))
         return idx, l, q, s
 
+    def cam_scene(self):
+        """Tape::cam_scene (grad.hpp:29): camera-space centers [K, 3] and inv_cov [K, 3, 3]."""
+        k = self.scene.K
+        c, s = np.empty((k, 3)), np.empty((k, 3, 3))
+        self.ctx.check(self.ctx.lib.gvr_tape_cam_scene(self.ctx.handle, self.handle, _ptr(c), _ptr(s)))
+        return c, s
+
+    def dropped_behind_camera(self) -> int:
+        """PixelKernelMap::dropped_behind_camera (tracer.hpp:39)."""
+        out = ctypes.c_int32()
+        self.ctx.check(self.ctx.lib.gvr_tape_dropped_behind_camera(self.ctx.handle, self.handle, ctypes.byref(out)))
+        return int(out.value)
+
     def close(self) -> None:
         if self.handle:
             self.ctx.lib.gvr_tape_destroy(self.handle)

@@ -472,3 +472,24 @@ def test_gradcheck_kernels_behind_the_camera(ctx):
     cam = default_camera()
     report = gvr.gradcheck(scene, cam, SelectionConfig(), _random_loss(np.random.default_rng(65), cam), ctx=ctx)
     assert report.max_rel_err == 0.0
+
+
+def test_tape_cam_scene_is_the_reference_view_transform(ctx):
+    """Tape::cam_scene (grad.hpp:29) == view_transform (scene.cpp:5-17), bit for bit."""
+    if not oracle.ref_available():
+        pytest.skip("reference build not present")
+    scene = random_scene(77, 40)
+    cam = Camera(gvr.so3_exp([0.1, -0.2, 0.05]), np.array([0.1, -0.05, 0.3]), 30.0, 15.5, 15.5, 32, 32)
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    c, s = fr.tape.cam_scene()
+    rc, rs = oracle.ref_view_transform(scene, cam)
+    assert np.array_equal(c, rc) and np.array_equal(s, rs)
+
+
+def test_kernels_behind_the_camera_are_counted(ctx):
+    """test_tracer.cpp:185-201: a kernel behind the camera is dropped and counted."""
+    scene = GaussianScene(np.array([[0, 0, 4.0], [0, 0, -3.0]]), np.stack([np.eye(3)] * 2), np.ones((2, 3)), 1.0)
+    fr = gvr.render_with_tape(scene, default_camera(), ctx=ctx)
+    assert fr.tape.dropped_behind_camera() == 1
+    fr = gvr.render_with_tape(random_scene(78, 10), default_camera(), ctx=ctx)
+    assert fr.tape.dropped_behind_camera() == 0
