@@ -23,6 +23,9 @@
 #ifndef GVR_BLEND_MINB
 #define GVR_BLEND_MINB 1
 #endif
+#ifndef GVR_ONE_ORDER
+#define GVR_ONE_ORDER 1
+#endif
 #ifndef GVR_BWD_WAYS
 #define GVR_BWD_WAYS 2
 #endif

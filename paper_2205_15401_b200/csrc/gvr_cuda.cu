@@ -291,12 +291,18 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
         kern<<<tiles, NT, smem, ctx->stream>>>(fp);
     }
     LAUNCH_CHECK(ctx);
+#if !GVR_ONE_ORDER
     {
         StageTimer st(ctx, ST_RANGES);
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b, 0, 1,
                                                         fp.n_order_blend_all);
     }
     LAUNCH_CHECK(ctx);
+#else
+    (void)order_b;
+    (void)n_b;
+    (void)cost;
+#endif
     {
         const size_t smem = 28ull * KMAX * 64;
         auto kern = blend_kernel<KMAX>;
@@ -762,8 +768,13 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     // K3 over the non-empty tiles, longest list first
     {
         StageTimer st(ctx, ST_RANGES);
+#if GVR_ONE_ORDER  // one order (list length) for selection, blend and backward; then every other tile
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
+                                                        sched + 2 + 3 * (size_t)tiles);
+#else
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
                                                         nullptr);
+#endif
     }
     LAUNCH_CHECK(ctx);
     FwdParams fp;
@@ -778,7 +789,11 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.tiles_x = tiles_x;
     fp.tile_order = order_f;
     fp.n_order = sched;
+#if GVR_ONE_ORDER
+    fp.tile_order_blend = order_f;
+#else
     fp.tile_order_blend = sched + 2 + tiles;
+#endif
     fp.n_order_blend = sched + 2 + 3 * (size_t)tiles;  // all tiles: selected first, then cleared ones
     fp.n_order_blend_all = sched + 2 + 3 * (size_t)tiles;
     fp.bwd_cost = bwd_cost;
@@ -1031,10 +1046,15 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         const int btx = t->tiles_x, bty = t->tiles_y;
         const int tiles = btx * bty;
         int* sched = t->sched.as<int>();
+#if GVR_ONE_ORDER
+        int* order_b = sched + 2;  // the selection's order
+        bp.n_order = sched;
+#else
         int* order_b = sched + 2 + tiles;  // tiles by sum_p n_p^2, from the forward
+        bp.n_order = sched + 1;
+#endif
         bp.tiles_x = btx;
         bp.tile_order = order_b;
-        bp.n_order = sched + 1;
         bp.topk = t->topk.as<int>();
         bp.count = t->count.as<int>();
         bp.tape_t = t->tape_t.as<double>();
