@@ -36,8 +36,8 @@ struct BwdParams {
 // FP64-accurate argument; products and sums are FP64 (the gradient bar is
 // 1e-4 of a class-scaled floor, ~1e-7 of the largest gradient).
 template <int KMAX>
-__global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdParams p) {
-    constexpr int TILE = 8, NP = 64, PER = (KMAX + 3) / 4;
+__global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pixels_kernel(BwdParams p) {
+    constexpr int TILE = 8, NP = 64 / GVR_BWD_SPLIT, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]
     double* b_dl = reinterpret_cast<double*>(smem);  // l_k - l_0
@@ -47,11 +47,12 @@ __global__ void __launch_bounds__(256, GVR_BWD_MINB) backward_pixels_kernel(BwdP
     float* b_is = b_pk + KMAX * NP;                  // 1 / sigma_k
     int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
 
-    if ((int)blockIdx.x >= *p.n_order) return;
+    if ((int)(blockIdx.x / GVR_BWD_SPLIT) >= *p.n_order) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
-    const int tile = p.tile_order[blockIdx.x];
-    const int i = (tile / p.tiles_x) * TILE + g / TILE;
-    const int j = (tile % p.tiles_x) * TILE + g % TILE;
+    const int tile = p.tile_order[blockIdx.x / GVR_BWD_SPLIT];
+    const int gp = (blockIdx.x % GVR_BWD_SPLIT) * NP + g;  // pixel within the tile
+    const int i = (tile / p.tiles_x) * TILE + gp / TILE;
+    const int j = (tile % p.tiles_x) * TILE + gp % TILE;
     if (i >= p.cam.H || j >= p.cam.W) return;
     const long long pix = (long long)i * p.cam.W + j;
     const int n = p.count[pix];

@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
 //   W_k = exp(-tau sum_m e^{q_m} Phi((l_k - l_m)/sigma_m)) e^{q_k}
 // The sum is accumulated in FP64 and T(l_k) is taped for the backward.
 template <int KMAX>
-__global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p) {
-    constexpr int TILE = 8, NP = 64, PER = (KMAX + 3) / 4;
+__global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_kernel(FwdParams p) {
+    constexpr int TILE = 8, NP = 64 / GVR_BLEND_SPLIT, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
     double* b_dl = reinterpret_cast<double*>(smem);  // [slot][pixel] l - l0
     double* b_w = b_dl + KMAX * NP;                  // W_k
@@ -556,11 +556,12 @@ __global__ void __launch_bounds__(256, GVR_BLEND_MINB) blend_kernel(FwdParams p)
     float* b_is = b_pk + KMAX * NP;
     int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
 
-    if ((int)blockIdx.x >= *p.n_order_blend) return;
+    if ((int)(blockIdx.x / GVR_BLEND_SPLIT) >= *p.n_order_blend) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
-    const int tile = p.tile_order_blend[blockIdx.x];
-    const int i = (tile / p.tiles_x) * TILE + g / TILE;
-    const int j = (tile % p.tiles_x) * TILE + g % TILE;
+    const int tile = p.tile_order_blend[blockIdx.x / GVR_BLEND_SPLIT];
+    const int gp = (blockIdx.x % GVR_BLEND_SPLIT) * NP + g;  // pixel within the tile
+    const int i = (tile / p.tiles_x) * TILE + gp / TILE;
+    const int j = (tile % p.tiles_x) * TILE + gp % TILE;
     const bool inside = i < p.cam.H && j < p.cam.W;
     const long long pix = (long long)i * p.cam.W + j;
     const int kp = p.sel.kp;

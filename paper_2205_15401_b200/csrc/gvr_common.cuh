@@ -21,16 +21,22 @@
 #define GVR_SEL_MINB 3
 #endif
 #ifndef GVR_BLEND_MINB
-#define GVR_BLEND_MINB 1
+#define GVR_BLEND_MINB 12
 #endif
 #ifndef GVR_ONE_ORDER
 #define GVR_ONE_ORDER 1
+#endif
+#ifndef GVR_BLEND_SPLIT
+#define GVR_BLEND_SPLIT 4
+#endif
+#ifndef GVR_BWD_SPLIT
+#define GVR_BWD_SPLIT 4
 #endif
 #ifndef GVR_BWD_WAYS
 #define GVR_BWD_WAYS 2
 #endif
 #ifndef GVR_BWD_MINB
-#define GVR_BWD_MINB 4
+#define GVR_BWD_MINB 16
 #endif
 
 namespace gvrk {

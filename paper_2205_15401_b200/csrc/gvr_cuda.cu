@@ -304,11 +304,11 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     (void)cost;
 #endif
     {
-        const size_t smem = 28ull * KMAX * 64;
+        const size_t smem = 28ull * KMAX * (64 / GVR_BLEND_SPLIT);
         auto kern = blend_kernel<KMAX>;
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_BLEND);
-        kern<<<tiles, 256, smem, ctx->stream>>>(fp);
+        kern<<<tiles * GVR_BLEND_SPLIT, 256 / GVR_BLEND_SPLIT, smem, ctx->stream>>>(fp);
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
@@ -316,12 +316,12 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
 
 template <int KMAX>
 int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
-    const size_t smem = 36ull * KMAX * 64;
+    const size_t smem = 36ull * KMAX * (64 / GVR_BWD_SPLIT);
     auto kern = backward_pixels_kernel<KMAX>;
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
         StageTimer st(ctx, ST_BACKWARD);
-        kern<<<tiles, 256, smem, ctx->stream>>>(bp);
+        kern<<<tiles * GVR_BWD_SPLIT, 256 / GVR_BWD_SPLIT, smem, ctx->stream>>>(bp);
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
