@@ -82,13 +82,24 @@ __device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u,
 // The selection itself is exact and independent of the visiting order.
 // Returns the list length, or -1 when the tile overflowed its capacity (the
 // caller then streams every kernel, unsorted, with the same exact tests).
-__device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys) {
+// With smem_cap < count (<= p.cap) the list is left unsorted in global memory:
+// *sorted = false and the caller must not early-exit on it.
+__device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys,
+                                                int smem_cap = 0x7fffffff, const unsigned long long** list = nullptr,
+                                                bool* sorted = nullptr) {
     constexpr int NB = 256;
     __shared__ unsigned s_lo, s_hi;
     __shared__ int s_hist[NB];
     const int count = p.tile_count[tile];
     if (count > p.cap) return -1;
     const unsigned long long* src = p.tile_lists + (size_t)tile * p.cap;
+    if (list) *list = keys;
+    if (sorted) *sorted = true;
+    if (count > smem_cap) {
+        if (list) *list = src;
+        if (sorted) *sorted = false;
+        return count;
+    }
     if (threadIdx.x == 0) {
         s_lo = 0xffffffffu;
         s_hi = 0u;
@@ -341,7 +352,11 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     p.count[pix] = n;
 }
 
-constexpr int kWarpListCap = 512;  // per-warp compacted list capacity (entries)
+constexpr int kWarpListCap = 512;
+#ifndef GVR_SEL_LIST_SMEM
+#define GVR_SEL_LIST_SMEM 4096
+#endif
+constexpr int kSelListSmem = GVR_SEL_LIST_SMEM;  // sorted tile list entries kept in shared memory  // per-warp compacted list capacity (entries)
 
 // Exact order of two selection candidates (kernel ids a, b; l on the exact trace).
 __device__ __forceinline__ bool exact_less(int a, int b, const double* d, const Rec64* rec64) {
@@ -366,27 +381,33 @@ __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - 
 // comparison between keys within the FP32 bound is decided on the exact trace,
 // so the kept set is exactly the reference's.
 template <int KMAX>
-__global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParams p) {
+__global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp_kernel(FwdParams p) {
     constexpr int TILE = 8;
     __shared__ float sh_l[8][64];
     __shared__ int sh_i[8][64];
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-    if ((int)blockIdx.x >= *p.n_order) return;
+    // GVR_SEL_SPLIT CTAs per tile, each 8 / GVR_SEL_SPLIT warps (2x4 sub-blocks)
+    if ((int)(blockIdx.x / GVR_SEL_SPLIT) >= *p.n_order) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sb = (blockIdx.x % GVR_SEL_SPLIT) * (8 / GVR_SEL_SPLIT) + warp;  // sub-block of the tile
     const unsigned FULL = 0xffffffffu;
-    const int tile = p.tile_order[blockIdx.x];
-    const int listed = load_sorted_list(p, tile, keys);
+    const int tile = p.tile_order[blockIdx.x / GVR_SEL_SPLIT];
+    const int smem_cap = min(p.cap, kSelListSmem);
+    const unsigned long long* tl = keys;
+    bool sorted = true;
+    const int listed = load_sorted_list(p, tile, keys, smem_cap, &tl, &sorted);
     const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
+    const bool early = !overflow && sorted;  // the list is ordered by its depth bound
     const int start = 0;
     // Each warp owns a 2x4-pixel sub-block of the tile and first compacts the
     // tile list to the entries whose screen box meets the sub-block (stable, so
     // the depth order survives): its pixels then scan ~half the list. Lists
     // longer than kWarpListCap stay on the tile list.
-    const int sr0 = (tile / p.tiles_x) * TILE + (warp >> 1) * 2;
-    const int sc0 = (tile % p.tiles_x) * TILE + (warp & 1) * 4;
-    unsigned long long* wlist = keys + p.cap + warp * kWarpListCap;
-    const unsigned long long* list = keys;
+    const int sr0 = (tile / p.tiles_x) * TILE + (sb >> 1) * 2;
+    const int sc0 = (tile % p.tiles_x) * TILE + (sb & 1) * 4;
+    unsigned long long* wlist = keys + smem_cap + warp * kWarpListCap;
+    const unsigned long long* list = tl;
     int end = overflow ? p.K : listed;
     if (!overflow) {
         const float fr0 = (float)sr0, fr1 = (float)(sr0 + 1), fc0 = (float)sc0, fc1 = (float)(sc0 + 3);
@@ -396,7 +417,7 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
             bool hit = false;
             unsigned long long key = 0;
             if (e < listed) {
-                key = keys[e];
+                key = tl[e];
                 const float4 box = __ldg(reinterpret_cast<const float4*>(p.rec32 + (int)(key & 0xffffffffu)));
                 hit = box.x <= fr1 && box.y >= fr0 && box.z <= fc1 && box.w >= fc0;
             }
@@ -446,7 +467,7 @@ __global__ void __launch_bounds__(256, GVR_SEL_MINB) select_warp_kernel(FwdParam
             const bool valid = e < end;
             const int k = overflow ? (valid ? e : 0) : (int)(list[valid ? e : 0] & 0xffffffffu);
             // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
-            if (!overflow) {
+            if (early) {
                 const float zmin0 = float_from_order_bits((uint32_t)(list[base] >> 32));
                 if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
             }

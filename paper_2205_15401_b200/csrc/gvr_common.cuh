@@ -32,6 +32,9 @@
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
 #endif
+#ifndef GVR_SEL_SPLIT
+#define GVR_SEL_SPLIT 1
+#endif
 #ifndef GVR_BWD_WAYS
 #define GVR_BWD_WAYS 2
 #endif

@@ -278,10 +278,11 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     const size_t list_smem = sizeof(unsigned long long) * (size_t)fp.cap;
     if (KMAX <= 32) {
         auto kern = select_warp_kernel<KMAX>;
-        const size_t smem = list_smem + sizeof(unsigned long long) * 8 * kWarpListCap;  // + per-warp lists
+        const size_t smem = sizeof(unsigned long long) * (size_t)std::min(fp.cap, kSelListSmem) +
+                            sizeof(unsigned long long) * (8 / GVR_SEL_SPLIT) * kWarpListCap;  // + per-warp lists
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_SELECT);
-        kern<<<tiles, 256, smem, ctx->stream>>>(fp);
+        kern<<<tiles * GVR_SEL_SPLIT, 256 / GVR_SEL_SPLIT, smem, ctx->stream>>>(fp);
     } else {
         constexpr int NT = 64;
         const size_t smem = sizeof(Cand) * NT + 12ull * KMAX * NT + list_smem;
