@@ -432,6 +432,29 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             end = cnt;
         }
     }
+#if GVR_SEL_DYN
+    // dynamic pixel queue: the CTA's 64 pixels, heaviest sub-blocks first, are
+    // pulled by whichever warp is free (the CTA ends with its last pixel, not
+    // with its slowest warp)
+    __shared__ int sh_end[8], sh_sbo[8], sh_next;
+    if (lane == 0) sh_end[sb] = list == wlist ? end : -1;
+    if (threadIdx.x == 0) sh_next = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 8; ++a) sh_sbo[a] = a;
+        for (int a = 1; a < 8; ++a) {  // insertion sort by list length, descending (-1 = tile list: longest)
+            const int v = sh_sbo[a];
+            const int ev = sh_end[v] < 0 ? 0x7fffffff : sh_end[v];
+            int b = a - 1;
+            while (b >= 0 && (sh_end[sh_sbo[b]] < 0 ? 0x7fffffff : sh_end[sh_sbo[b]]) < ev) {
+                sh_sbo[b + 1] = sh_sbo[b];
+                --b;
+            }
+            sh_sbo[b + 1] = v;
+        }
+    }
+    __syncthreads();
+#endif
     const int kp = p.sel.kp;
     const Rec64* rec64 = p.rec64;
     const double log_eta = p.sel.log_eta;
@@ -444,10 +467,27 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     const bool exact_only = p.exact_only != 0;
     float cost = 0.0f;
 
+#if GVR_SEL_DYN
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(&sh_next, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= 64) break;
+        const int psb = sh_sbo[item >> 3], px = item & 7;
+        const int psr = (tile / p.tiles_x) * TILE + (psb >> 1) * 2;
+        const int psc = (tile % p.tiles_x) * TILE + (psb & 1) * 4;
+        const int i = psr + (px >> 2);
+        const int j = psc + (px & 3);
+        const int pe = sh_end[psb];
+        list = pe >= 0 ? keys + smem_cap + psb * kWarpListCap : tl;
+        end = pe >= 0 ? pe : (overflow ? p.K : listed);
+        if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
+#else
     for (int px = 0; px < 8; ++px) {
         const int i = sr0 + (px >> 2);
         const int j = sc0 + (px & 3);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
+#endif
         const long long pix = (long long)i * p.cam.W + j;
         double d[3];
         pixel_ray(p.cam, i, j, d);

@@ -35,6 +35,9 @@
 #ifndef GVR_SEL_SPLIT
 #define GVR_SEL_SPLIT 1
 #endif
+#ifndef GVR_SEL_DYN
+#define GVR_SEL_DYN 1
+#endif
 #ifndef GVR_BWD_WAYS
 #define GVR_BWD_WAYS 2
 #endif
