@@ -144,6 +144,12 @@ int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard);
  * trace and erfc (the reference's arithmetic, ~1e-15) instead of the FP32
  * closed-form pipeline. Slow; used by gradcheck's finite differences. */
 int gvr_context_set_precise(gvr_context* ctx, int on);
+/* Profiling hook (no reference counterpart): while on, renders record the SM
+ * cycles of each tile's selection CTA on the tape; read with gvr_tape_tile_cycles. */
+int gvr_context_set_tile_profile(gvr_context* ctx, int on);
+/* Per-tile selection cycles of a render made with the tile profile on
+ * (n = tiles_x * tiles_y of the tape; 0 for tiles with nothing to select). */
+int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* tape, int64_t* cycles, int64_t n);
 /* Per-tile candidate-list capacity (default 4096 entries of 8 B per 8x8 tile).
  * Tiles whose list overflows stream every kernel through the same exact tests
  * (slower, same results); a small value exercises that path in tests. */

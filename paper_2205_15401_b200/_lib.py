@@ -65,6 +65,8 @@ EXPORTED_SYMBOLS = (
     "gvr_laplacian_reg",
     "gvr_tape_cam_scene",
     "gvr_tape_dropped_behind_camera",
+    "gvr_context_set_tile_profile",
+    "gvr_tape_tile_cycles",
 )
 
 
@@ -158,6 +160,8 @@ def load() -> ctypes.CDLL:
         "gvr_tape_traced": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
         "gvr_tape_cam_scene": (ctypes.c_int, [vp, vp, vp, vp]),
         "gvr_tape_dropped_behind_camera": (ctypes.c_int, [vp, vp, ctypes.POINTER(i32)]),
+        "gvr_context_set_tile_profile": (ctypes.c_int, [vp, ctypes.c_int]),
+        "gvr_tape_tile_cycles": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64]),
         "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                                           ctypes.POINTER(i32)]),
         "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),

@@ -37,6 +37,9 @@ struct FwdParams {
     EntryRec* ent;  // [P*kp] traced selected entries (written by the blend)
     float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
     int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
+    unsigned* tile_done;     // [tiles] set (release) when the tile's selection is written; the blend,
+                             // launched as a programmatic dependent, waits per tile (nullable)
+    long long* tile_cycles;  // profiling hook: [tiles] SM cycles of the tile's selection CTA (nullable)
     int precise;     // verification mode: FP64 exact traces and erfc in the blend sums (gradcheck)
     int* nonfinite; // flag
 };
@@ -352,11 +355,14 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     p.count[pix] = n;
 }
 
-constexpr int kWarpListCap = 512;
-#ifndef GVR_SEL_LIST_SMEM
-#define GVR_SEL_LIST_SMEM 4096
+#ifndef GVR_SEL_WARP_LIST
+#define GVR_SEL_WARP_LIST 512
 #endif
-constexpr int kSelListSmem = GVR_SEL_LIST_SMEM;  // sorted tile list entries kept in shared memory  // per-warp compacted list capacity (entries)
+#ifndef GVR_SEL_LIST_SMEM
+#define GVR_SEL_LIST_SMEM 2048
+#endif
+constexpr int kWarpListCap = GVR_SEL_WARP_LIST;  // per-warp compacted list capacity (entries)
+constexpr int kSelListSmem = GVR_SEL_LIST_SMEM;  // sorted tile list entries kept in shared memory
 
 // Exact order of two selection candidates (kernel ids a, b; l on the exact trace).
 __device__ __forceinline__ bool exact_less(int a, int b, const double* d, const Rec64* rec64) {
@@ -388,7 +394,10 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
     // GVR_SEL_SPLIT CTAs per tile, each 8 / GVR_SEL_SPLIT warps (2x4 sub-blocks)
+    launch_dependents();  // the blend may fill the SMs this grid's tail leaves idle
     if ((int)(blockIdx.x / GVR_SEL_SPLIT) >= *p.n_order) return;
+    __shared__ long long sh_t0;  // profiling hook (kept out of registers)
+    if (p.tile_cycles && threadIdx.x == 0) sh_t0 = clock64();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sb = (blockIdx.x % GVR_SEL_SPLIT) * (8 / GVR_SEL_SPLIT) + warp;  // sub-block of the tile
     const unsigned FULL = 0xffffffffu;
@@ -436,13 +445,14 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     // dynamic pixel queue: the CTA's 64 pixels, heaviest sub-blocks first, are
     // pulled by whichever warp is free (the CTA ends with its last pixel, not
     // with its slowest warp)
-    __shared__ int sh_end[8], sh_sbo[8], sh_next;
-    if (lane == 0) sh_end[sb] = list == wlist ? end : -1;
+    constexpr int NSB = 8 / GVR_SEL_SPLIT;  // sub-blocks (= warps) of this CTA
+    __shared__ int sh_end[NSB], sh_sbo[NSB], sh_next;
+    if (lane == 0) sh_end[warp] = list == wlist ? end : -1;
     if (threadIdx.x == 0) sh_next = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int a = 0; a < 8; ++a) sh_sbo[a] = a;
-        for (int a = 1; a < 8; ++a) {  // insertion sort by list length, descending (-1 = tile list: longest)
+        for (int a = 0; a < NSB; ++a) sh_sbo[a] = a;
+        for (int a = 1; a < NSB; ++a) {  // insertion sort by list length, descending (-1 = tile list: longest)
             const int v = sh_sbo[a];
             const int ev = sh_end[v] < 0 ? 0x7fffffff : sh_end[v];
             int b = a - 1;
@@ -472,14 +482,15 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         int item = 0;
         if (lane == 0) item = atomicAdd(&sh_next, 1);
         item = __shfl_sync(FULL, item, 0);
-        if (item >= 64) break;
-        const int psb = sh_sbo[item >> 3], px = item & 7;
+        if (item >= NSB * 8) break;
+        const int pw = sh_sbo[item >> 3], px = item & 7;  // owning warp, pixel of its sub-block
+        const int psb = (blockIdx.x % GVR_SEL_SPLIT) * NSB + pw;
         const int psr = (tile / p.tiles_x) * TILE + (psb >> 1) * 2;
         const int psc = (tile % p.tiles_x) * TILE + (psb & 1) * 4;
         const int i = psr + (px >> 2);
         const int j = psc + (px & 3);
-        const int pe = sh_end[psb];
-        list = pe >= 0 ? keys + smem_cap + psb * kWarpListCap : tl;
+        const int pe = sh_end[pw];
+        list = pe >= 0 ? keys + smem_cap + pw * kWarpListCap : tl;
         end = pe >= 0 ? pe : (overflow ? p.K : listed);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
 #else
@@ -598,6 +609,16 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         cost += (float)(n * n);
     }
     if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
+    if (p.tile_done || p.tile_cycles) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (p.tile_cycles)  // profiling hook: the CTA's duration (its slowest warp)
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles + tile),
+                          (unsigned long long)(clock64() - sh_t0));
+            if (p.tile_done) red_add_release_gpu(p.tile_done + tile, 1u);  // one count per split CTA
+        }
+    }
 }
 
 // K3b closed-form blend (blender.cpp:27-53, 98-128). CTA = one 8x8 tile with
@@ -620,6 +641,12 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     if ((int)(blockIdx.x / GVR_BLEND_SPLIT) >= *p.n_order_blend) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
     const int tile = p.tile_order_blend[blockIdx.x / GVR_BLEND_SPLIT];
+    if (p.tile_done && (int)(blockIdx.x / GVR_BLEND_SPLIT) < *p.n_order) {
+        // started early (programmatic dependent of the selection): wait for this tile only
+        if (threadIdx.x == 0)
+            while (ld_acquire_gpu(p.tile_done + tile) < (unsigned)GVR_SEL_SPLIT) __nanosleep(100);
+        __syncthreads();
+    }
     const int gp = (blockIdx.x % GVR_BLEND_SPLIT) * NP + g;  // pixel within the tile
     const int i = (tile / p.tiles_x) * TILE + gp / TILE;
     const int j = (tile % p.tiles_x) * TILE + gp % TILE;

@@ -32,6 +32,9 @@
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
 #endif
+#ifndef GVR_PDL  // select -> blend per-tile hand-off with programmatic dependent launch
+#define GVR_PDL 1
+#endif
 #ifndef GVR_SEL_SPLIT
 #define GVR_SEL_SPLIT 1
 #endif
@@ -83,6 +86,19 @@ struct __align__(16) Rec64 {
 };
 
 // ---------------------------------------------------------------- exact FP64 (no contraction)
+
+// select -> blend per-tile hand-off (programmatic dependent launch)
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* a) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned* a, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+// let the next kernel of the stream (launched with programmatic stream
+// serialization) start while this grid's last wave runs
+__device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }

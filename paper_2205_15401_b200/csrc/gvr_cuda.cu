@@ -87,6 +87,7 @@ struct gvr_context {
     int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
     double guard = 0.02;
     bool precise = false;  // verification mode of the blend (gvr_context_set_precise)
+    bool tile_profile = false;  // record per-tile selection cycles (gvr_context_set_tile_profile)
     int tile_cap = 4096;  // per-tile candidate-list capacity
     bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
@@ -130,7 +131,7 @@ struct gvr_tape {
     // per kernel
     Buf rec32, rec64;
     // per-tile candidate lists
-    Buf tile_count, tile_lists;
+    Buf tile_count, tile_lists, tile_cycles;
     int cap = 0;
     Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
     // per pixel
@@ -309,7 +310,21 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
         auto kern = blend_kernel<KMAX>;
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_BLEND);
-        kern<<<tiles * GVR_BLEND_SPLIT, 256 / GVR_BLEND_SPLIT, smem, ctx->stream>>>(fp);
+        FwdParams bp = fp;
+        if (KMAX > 32) bp.tile_done = nullptr;  // the CTA selection does not hand off per tile
+        // with the per-tile hand-off the blend is a programmatic dependent of the
+        // selection: its CTAs start on the SMs the selection's last wave leaves idle
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(tiles * GVR_BLEND_SPLIT);
+        cfg.blockDim = dim3(256 / GVR_BLEND_SPLIT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = bp.tile_done ? 1 : 0;
+        CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, bp));
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
@@ -567,6 +582,12 @@ int gvr_context_set_precise(gvr_context* ctx, int on) {
     return GVR_OK;
 }
 
+int gvr_context_set_tile_profile(gvr_context* ctx, int on) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    ctx->tile_profile = on != 0;
+    return GVR_OK;
+}
+
 int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard) {
     if (!ctx || !(guard >= 0.0)) return GVR_ERR_RUNTIME;
     ctx->guard = guard;
@@ -722,7 +743,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     tape->cap = ctx->tile_cap;
     CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * (size_t)tiles));
     CUDA_TRY(ctx, tape->tile_lists.ensure(sizeof(unsigned long long) * (size_t)tiles * tape->cap));
-    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 3 * (size_t)tiles)));
+    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 4 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
     CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
@@ -740,7 +761,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
     CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 2 * sizeof(int), ctx->stream));
     CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * (size_t)tiles, ctx->stream));
-    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (size_t)tiles, ctx->stream));
+    // bwd_cost[tiles], n_all, tile_done[tiles] (contiguous)
+    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (2 * (size_t)tiles + 1), ctx->stream));
 
     if (K > 0) {
         // K1 projection + culling + binning into per-tile lists
@@ -816,6 +838,13 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.nonfinite = dflags + 1;
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     fp.precise = ctx->precise ? 1 : 0;
+    fp.tile_cycles = nullptr;
+    fp.tile_done = GVR_PDL ? reinterpret_cast<unsigned*>(sched + 3 + 3 * (size_t)tiles) : nullptr;
+    if (ctx->tile_profile) {
+        CUDA_TRY(ctx, tape->tile_cycles.ensure(sizeof(long long) * (size_t)tiles));
+        CUDA_TRY(ctx, cudaMemsetAsync(tape->tile_cycles.p, 0, sizeof(long long) * (size_t)tiles, ctx->stream));
+        fp.tile_cycles = tape->tile_cycles.as<long long>();
+    }
     int rc = GVR_OK;
     int* order_b = sched + 2 + tiles;
     if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
@@ -1711,6 +1740,16 @@ int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* t, double* centers, dou
     if (hs)
         if (int rc = copy_out(ctx, inv_cov, ds, sizeof(double) * 9 * (size_t)K, &host)) return rc;
     return host ? sync_and_check(ctx) : GVR_OK;
+}
+
+int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* t, int64_t* cycles, int64_t n) {
+    if (int rc = tape_ready(ctx, t)) return rc;
+    const int64_t tiles = (int64_t)t->tiles_x * t->tiles_y;
+    if (!cycles || n != tiles || t->tile_cycles.cap < sizeof(long long) * (size_t)tiles)
+        return set_err(ctx, GVR_ERR_RUNTIME, "tile_cycles: render with the tile profile on, n = tiles_x * tiles_y");
+    CUDA_TRY(ctx, cudaMemcpyAsync(cycles, t->tile_cycles.p, sizeof(long long) * (size_t)tiles, cudaMemcpyDefault,
+                                  ctx->stream));
+    return sync_and_check(ctx);
 }
 
 int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* t, int32_t* count) {

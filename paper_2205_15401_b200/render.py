@@ -121,6 +121,10 @@ class Context:
         """Verification mode: FP64 exact traces and erfc in the blend (gradcheck)."""
         self.check(self.lib.gvr_context_set_precise(self.handle, int(bool(on))))
 
+    def set_tile_profile(self, on: bool = True) -> None:
+        """Profiling hook: record per-tile selection cycles on each tape (Tape.tile_cycles)."""
+        self.check(self.lib.gvr_context_set_tile_profile(self.handle, int(bool(on))))
+
     def set_prefilter_guard(self, guard: float) -> None:
         self.check(self.lib.gvr_context_set_prefilter_guard(self.handle, float(guard)))
 
@@ -261,6 +265,15 @@ class Tape:
         out = ctypes.c_int32()
         self.ctx.check(self.ctx.lib.gvr_tape_dropped_behind_camera(self.ctx.handle, self.handle, ctypes.byref(out)))
         return int(out.value)
+
+    def tile_cycles(self) -> np.ndarray:
+        """[tiles_y, tiles_x] SM cycles of each 8x8 tile's selection CTA (needs Context.set_tile_profile)."""
+        h, w, _, _ = self.shape()
+        ty, tx = (h + 7) // 8, (w + 7) // 8
+        out = np.zeros((ty, tx), dtype=np.int64)
+        self.ctx.check(self.ctx.lib.gvr_tape_tile_cycles(self.ctx.handle, self.handle,
+                                                         out.ctypes.data_as(ctypes.c_void_p), out.size))
+        return out
 
     def close(self) -> None:
         if self.handle:
