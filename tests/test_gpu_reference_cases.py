@@ -188,3 +188,23 @@ def test_transmittance_is_non_increasing_and_in_unit_interval(ctx):
         cur = gvr.transmittance_at(fr, np.array([[t]]))[0, 0]
         assert 0.0 < cur <= 1.0 and cur <= prev + 1e-15
         prev = cur
+
+
+@pytest.mark.parametrize("k_prime", [8, 20, 32])
+def test_batch_merge_with_near_ties_matches_the_oracle(ctx, k_prime):
+    """Many candidates of one 32-candidate batch on the same ray with depths equal
+    or within FP32 resolution of each other: the warp batch merge must defer to the
+    exact (l, idx) order (fine_select, tracer.cpp:119-122) exactly like the oracle."""
+    import oracle
+    rng = np.random.default_rng(60 + k_prime)
+    triples = []
+    for _ in range(40):
+        base = float(rng.choice([5.0, 5.0 + 1e-7, 5.0 * (1 + 3e-7), 6.0, 7.25]))
+        triples.append((base * (1.0 + float(rng.integers(-2, 3)) * 1e-16), float(rng.uniform(-2.0, 0.0)), 0.5))
+    triples += [(float(l), float(rng.uniform(-2.0, 0.0)), 0.5) for l in rng.uniform(3.0, 9.0, 30)]
+    scene = axis_scene(triples)
+    cfg = SelectionConfig(k_prime=k_prime)
+    buf = gvr.render(scene, axis_camera(), cfg, ctx=ctx)
+    ref = oracle.port_render(scene, axis_camera(), cfg)
+    assert np.array_equal(buf.topk_idx, ref["topk_idx"])
+    assert (buf.topk_idx >= 0).sum() == k_prime
