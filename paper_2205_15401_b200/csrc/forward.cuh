@@ -377,6 +377,9 @@ constexpr float kKeyClose = 4.0e-7f;
 
 __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - b) <= kKeyClose * fabsf(b); }
 
+#ifndef GVR_SEL_CUNROLL  // list batches per compaction step (loads in flight together)
+#define GVR_SEL_CUNROLL 4
+#endif
 #ifndef GVR_SEL_BATCH_MIN  // eligible candidates per batch from which the batch merge is used (33: never)
 #define GVR_SEL_BATCH_MIN 10
 #endif
@@ -481,19 +484,29 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     if (!overflow) {
         const float fr0 = (float)sr0, fr1 = (float)(sr0 + 1), fc0 = (float)sc0, fc1 = (float)(sc0 + 3);
         int cnt = 0;
-        for (int base = 0; base < listed && cnt <= kWarpListCap; base += 32) {
-            const int e = base + lane;
-            bool hit = false;
-            unsigned long long key = 0;
-            if (e < listed) {
-                key = tl[e];
-                const float4 box = __ldg(reinterpret_cast<const float4*>(p.rec32 + (int)(key & 0xffffffffu)));
-                hit = box.x <= fr1 && box.y >= fr0 && box.z <= fc1 && box.w >= fc0;
+        // GVR_SEL_CUNROLL batches per step: their boxes' loads are in flight together
+        for (int base = 0; base < listed && cnt <= kWarpListCap; base += 32 * GVR_SEL_CUNROLL) {
+            unsigned long long key[GVR_SEL_CUNROLL];
+            float4 box[GVR_SEL_CUNROLL];
+#pragma unroll
+            for (int h = 0; h < GVR_SEL_CUNROLL; ++h) {
+                key[h] = 0ull;
+                const int e = base + 32 * h + lane;
+                if (e < listed) {
+                    key[h] = tl[e];
+                    box[h] = __ldg(reinterpret_cast<const float4*>(p.rec32 + (int)(key[h] & 0xffffffffu)));
+                }
             }
-            const unsigned b = __ballot_sync(FULL, hit);
-            const int off = cnt + __popc(b & ((1u << lane) - 1u));
-            if (hit && off < kWarpListCap) wlist[off] = key;
-            cnt += __popc(b);
+#pragma unroll
+            for (int h = 0; h < GVR_SEL_CUNROLL; ++h) {
+                const int e = base + 32 * h + lane;
+                const bool hit = e < listed && box[h].x <= fr1 && box[h].y >= fr0 && box[h].z <= fc1 &&
+                                 box[h].w >= fc0;
+                const unsigned b = __ballot_sync(FULL, hit);
+                const int off = cnt + __popc(b & ((1u << lane) - 1u));
+                if (hit && off < kWarpListCap) wlist[off] = key[h];
+                cnt += __popc(b);
+            }
         }
         __syncwarp();
         if (cnt <= kWarpListCap) {
