@@ -536,6 +536,21 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             sh_sbo[b + 1] = v;
         }
     }
+    // the tile's 64 rays (and their FP32 image-plane coordinates), once per CTA
+    __shared__ double sh_ray[64][3];
+    __shared__ float sh_uv[64][2];
+    for (int q = threadIdx.x; q < 64; q += blockDim.x) {
+        const int ri = (tile / p.tiles_x) * TILE + q / TILE, rj = (tile % p.tiles_x) * TILE + q % TILE;
+        if (ri < p.cam.H && rj < p.cam.W) {
+            double d[3];
+            pixel_ray(p.cam, ri, rj, d);
+            sh_ray[q][0] = d[0];
+            sh_ray[q][1] = d[1];
+            sh_ray[q][2] = d[2];
+            sh_uv[q][0] = (float)xdiv(xsub((double)ri, p.cam.oy), p.cam.focal);
+            sh_uv[q][1] = (float)xdiv(xsub((double)rj, p.cam.ox), p.cam.focal);
+        }
+    }
     __syncthreads();
 #endif
     const int kp = p.sel.kp;
@@ -566,19 +581,22 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         list = pe >= 0 ? keys + smem_cap + pw * kWarpListCap : tl;
         end = pe >= 0 ? pe : (overflow ? p.K : listed);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
+        const int q = ((psb >> 1) * 2 + (px >> 2)) * TILE + (psb & 1) * 4 + (px & 3);  // pixel within the tile
+        const double d[3] = {sh_ray[q][0], sh_ray[q][1], sh_ray[q][2]};
+        const float u = sh_uv[q][0], v = sh_uv[q][1];
 #else
     for (int px = 0; px < 8; ++px) {
         const int i = sr0 + (px >> 2);
         const int j = sc0 + (px & 3);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
-#endif
-        const long long pix = (long long)i * p.cam.W + j;
         double d[3];
         pixel_ray(p.cam, i, j, d);
-        const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
-                              2.0 * d[1] * d[2]};
         const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
         const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
+#endif
+        const long long pix = (long long)i * p.cam.W + j;
+        const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
+                              2.0 * d[1] * d[2]};
         const float fi = (float)i, fj = (float)j;
 
         float L = INFINITY;  // lane s < n: rank key of the s-th nearest
