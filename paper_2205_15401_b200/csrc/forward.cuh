@@ -745,8 +745,13 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     const int tile = p.tile_order_blend[blockIdx.x / GVR_BLEND_SPLIT];
     if (p.tile_done && (int)(blockIdx.x / GVR_BLEND_SPLIT) < *p.n_order) {
         // started early (programmatic dependent of the selection): wait for this tile only
-        if (threadIdx.x == 0)
-            while (ld_acquire_gpu(p.tile_done + tile) < (unsigned)GVR_SEL_SPLIT) __nanosleep(100);
+        if (threadIdx.x == 0) {
+            // bounded: a selection that never publishes (a bug) must fail the launch, not hang the device
+            for (unsigned spin = 0; ld_acquire_gpu(p.tile_done + tile) < (unsigned)GVR_SEL_SPLIT; ++spin) {
+                if (spin > (1u << 26)) __trap();
+                __nanosleep(100);
+            }
+        }
         __syncthreads();
     }
     const int gp = (blockIdx.x % GVR_BLEND_SPLIT) * NP + g;  // pixel within the tile
