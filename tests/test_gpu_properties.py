@@ -493,3 +493,25 @@ def test_kernels_behind_the_camera_are_counted(ctx):
     assert fr.tape.dropped_behind_camera() == 1
     fr = gvr.render_with_tape(random_scene(78, 10), default_camera(), ctx=ctx)
     assert fr.tape.dropped_behind_camera() == 0
+
+
+def test_tile_profile_hook(ctx):
+    """gvr_context_set_tile_profile: cycles on every tile with a selection; the
+    render's outputs do not change with the hook on."""
+    scene = random_scene(31, 40)
+    cam = default_camera(40, 20.0)
+    ref = gvr.render(scene, cam, ctx=ctx)
+    ctx.set_tile_profile(True)
+    try:
+        fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+        cyc = fr.tape.tile_cycles()
+    finally:
+        ctx.set_tile_profile(False)
+    assert cyc.shape == (5, 5)
+    selected = (fr.buffers.topk_idx[:, :, 0] >= 0).reshape(5, 8, 5, 8).any(axis=(1, 3))
+    assert np.all(cyc[selected] > 0)
+    assert np.array_equal(fr.buffers.topk_idx, ref.topk_idx)
+    assert np.array_equal(fr.buffers.image, ref.image)
+    fr2 = gvr.render_with_tape(scene, cam, ctx=ctx)
+    with pytest.raises(gvr.GvrRuntimeError, match="tile profile"):
+        fr2.tape.tile_cycles()
