@@ -171,6 +171,15 @@ void gvr_scene_destroy(gvr_scene* scene);
 /* Upload + validate (GaussianScene::validate, types.cpp:31-42). attr may be NULL when D == 0. */
 int gvr_scene_set(gvr_context* ctx, gvr_scene* scene, int32_t K, int32_t D, double tau,
                   const double* centers, const double* inv_cov, const double* attr);
+/* Same upload without the host synchronisation (fitting loops, graph capture):
+ * the validation runs on the device and its result is read by gvr_scene_check
+ * (the first error, with the gvr_scene_set message). Renders in between use the
+ * uploaded values as they are. Capturable when the scene buffers already have
+ * the size (one uncaptured call first) and the arrays are device pointers. */
+int gvr_scene_set_deferred(gvr_context* ctx, gvr_scene* scene, int32_t K, int32_t D, double tau,
+                           const double* centers, const double* inv_cov, const double* attr);
+/* Result of the last gvr_scene_set_deferred (synchronises; GVR_OK when none is pending). */
+int gvr_scene_check(gvr_context* ctx, gvr_scene* scene);
 int32_t gvr_scene_size(const gvr_scene* scene);
 int32_t gvr_scene_attr_dim(const gvr_scene* scene);
 

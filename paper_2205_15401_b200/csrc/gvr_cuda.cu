@@ -84,6 +84,7 @@ struct gvr_context {
     cudaStream_t own_stream = nullptr;
     std::string err;
     int64_t launches = 0;   // kernels of this library
+    int64_t capture_launch0 = 0;  // launches when the current capture began
     int64_t lib_calls = 0;  // CUB device-wide calls (scan, radix sort)
     double guard = 0.02;
     bool precise = false;  // verification mode of the blend (gvr_context_set_precise)
@@ -105,6 +106,7 @@ struct gvr_graph {
     gvr_context* ctx = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // kernels of this library captured (counted again on every replay)
 };
 
 struct gvr_scene {
@@ -113,7 +115,9 @@ struct gvr_scene {
     double tau = 1.0;
     uint64_t version = 0;
     bool valid = false;
+    bool check_pending = false;  // gvr_scene_set_deferred: validation result not read yet
     Buf centers, inv_cov, attr;
+    Buf vflag;  // deferred validation: first error (kernel << 2 | code), ~0 = none
 };
 
 struct gvr_tape {
@@ -352,6 +356,16 @@ int sync_and_check(gvr_context* ctx) {
 }
 
 // K0 on an uploaded scene (GaussianKernel::validate, types.cpp:17-29); one sync.
+int decode_validation(gvr_context* ctx, unsigned long long h) {
+    if (h == ~0ull) return GVR_OK;
+    const long long k = (long long)(h >> 2);
+    switch ((int)(h & 3)) {
+        case 1: return set_err(ctx, GVR_ERR_VALIDATION, "kernel has non-finite values (kernel %lld)", k);
+        case 2: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not symmetric (kernel %lld)", k);
+        default: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not positive-definite (kernel %lld)", k);
+    }
+}
+
 int validate_uploaded(gvr_context* ctx, gvr_scene* s) {
     const int K = s->K, D = s->D;
     if (K > 0) {
@@ -365,14 +379,7 @@ int validate_uploaded(gvr_context* ctx, gvr_scene* s) {
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, first, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
         if (int rc = sync_and_check(ctx)) return rc;
         std::memcpy(&h, ctx->h_flags + 2, sizeof h);
-        if (h != ~0ull) {
-            const long long k = (long long)(h >> 2);
-            switch ((int)(h & 3)) {
-                case 1: return set_err(ctx, GVR_ERR_VALIDATION, "kernel has non-finite values (kernel %lld)", k);
-                case 2: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not symmetric (kernel %lld)", k);
-                default: return set_err(ctx, GVR_ERR_VALIDATION, "inv_cov is not positive-definite (kernel %lld)", k);
-            }
-        }
+        return decode_validation(ctx, h);
     }
     return GVR_OK;
 }
@@ -536,6 +543,7 @@ int gvr_graph_begin(gvr_context* ctx) {
     if (int rc = sync_and_check(ctx)) return rc;
     CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     ctx->capturing = true;
+    ctx->capture_launch0 = ctx->launches;
     return GVR_OK;
 }
 
@@ -547,6 +555,7 @@ int gvr_graph_end(gvr_context* ctx, gvr_graph** out) {
     auto* gr = new gvr_graph();
     gr->ctx = ctx;
     gr->graph = g;
+    gr->launches = ctx->launches - ctx->capture_launch0;
     cudaError_t e = cudaGraphInstantiate(&gr->exec, g, 0);
     if (e != cudaSuccess) {
         cudaGraphDestroy(g);
@@ -560,6 +569,7 @@ int gvr_graph_end(gvr_context* ctx, gvr_graph** out) {
 int gvr_graph_launch(gvr_context* ctx, gvr_graph* g) {
     if (!ctx || !g || g->ctx != ctx) return GVR_ERR_RUNTIME;
     CUDA_TRY(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+    ctx->launches += g->launches;
     return GVR_OK;
 }
 
@@ -610,6 +620,7 @@ void gvr_scene_destroy(gvr_scene* s) {
     s->centers.release();
     s->inv_cov.release();
     s->attr.release();
+    s->vflag.release();
     delete s;
 }
 
@@ -638,6 +649,57 @@ int gvr_scene_set(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double t
     if (int rc = validate_uploaded(ctx, s)) return rc;
     s->valid = true;
     return GVR_OK;
+}
+
+int gvr_scene_set_deferred(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double tau, const double* centers,
+                           const double* inv_cov, const double* attr) {
+    if (!ctx || !s) return GVR_ERR_RUNTIME;
+    s->valid = false;
+    ++s->version;
+    if (K < 0 || D < 0) return set_err(ctx, GVR_ERR_VALIDATION, "scene sizes must be >= 0");
+    if (tau < 0.0 || !std::isfinite(tau)) return set_err(ctx, GVR_ERR_VALIDATION, "tau must be finite and >= 0");
+    if (K > 0 && (!centers || !inv_cov || (D > 0 && !attr)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "scene arrays must not be null");
+    const size_t need[4] = {sizeof(double) * 3 * (size_t)K, sizeof(double) * 9 * (size_t)K, sizeof(double) * (size_t)D * K,
+                            sizeof(unsigned long long)};
+    Buf* bufs[4] = {&s->centers, &s->inv_cov, &s->attr, &s->vflag};
+    for (int b = 0; b < 4; ++b) {
+        if (ctx->capturing && bufs[b]->cap < need[b])
+            return set_err(ctx, GVR_ERR_RUNTIME, "scene buffers must be sized by an uncaptured call first");
+        CUDA_TRY(ctx, bufs[b]->ensure(need[b]));
+    }
+    if (int rc = copy_in(ctx, s->centers.p, centers, need[0])) return rc;
+    if (int rc = copy_in(ctx, s->inv_cov.p, inv_cov, need[1])) return rc;
+    if (int rc = copy_in(ctx, s->attr.p, attr, need[2])) return rc;
+    s->K = K;
+    s->D = D;
+    s->tau = tau;
+    CUDA_TRY(ctx, cudaMemsetAsync(s->vflag.p, 0xff, sizeof(unsigned long long), ctx->stream));
+    if (K > 0) {
+        validate_scene_kernel<<<blocks_for(K, 256), 256, 0, ctx->stream>>>(
+            K, D, s->centers.as<double>(), s->inv_cov.as<double>(), s->attr.as<double>(),
+            s->vflag.as<unsigned long long>());
+        LAUNCH_CHECK(ctx);
+    }
+    s->valid = true;  // provisional: gvr_scene_check reports the validation result
+    s->check_pending = true;
+    return GVR_OK;
+}
+
+int gvr_scene_check(gvr_context* ctx, gvr_scene* s) {
+    if (!ctx || !s) return GVR_ERR_RUNTIME;
+    if (!s->check_pending) return s->valid ? GVR_OK : set_err(ctx, GVR_ERR_RUNTIME, "scene is not valid");
+    if (ctx->capturing)
+        return set_err(ctx, GVR_ERR_RUNTIME, "operation needs a host synchronisation; not allowed while capturing a graph");
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, s->vflag.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    unsigned long long h = 0;
+    std::memcpy(&h, ctx->h_flags + 2, sizeof h);
+    s->check_pending = false;
+    const int rc = decode_validation(ctx, h);
+    if (rc) s->valid = false;
+    return rc;
 }
 
 // ---------------------------------------------------------------- tape / forward

@@ -115,7 +115,7 @@ class Fitter:
                  cfg: SelectionConfig = SelectionConfig(), rgb_weight: float = 1.0, silhouette_weight: float = 1.0,
                  adam: AdamConfig = AdamConfig(), rank: int = 0, world: int = 1, device=None,
                  regularizer: Optional["ShapeRegularizer"] = None, edge_weight: float = 0.0,
-                 laplacian_weight: float = 0.0):
+                 laplacian_weight: float = 0.0, use_graph: bool = True):
         import torch
 
         LossSpec(rgb_weight, silhouette_weight, edge_weight, laplacian_weight).validate()
@@ -158,7 +158,14 @@ class Fitter:
         self.groups: List[Tuple[Tuple[float, float], list, list, list, list, object]] = [
             (w, cams, tis, tas, tapes, torch.zeros(len(cams), **f64)) for w, (cams, tis, tas, tapes) in groups.items()]
         self.loss_acc = torch.zeros(1, **f64)
+        self._lsum = [torch.zeros(1, **f64) for _ in self.groups]
         self.dscene = DeviceScene(ctx)
+        # the per-iteration device work (upload + validation, all views fwd + loss
+        # + bwd) is captured once into a CUDA graph and replayed: no host launch
+        # cost per view; the regularizers return host values, so they keep it eager
+        self.use_graph = use_graph and regularizer is None
+        self._graph = None
+        self._warm = False
         self.total = dict(d_center=self.g_center.view(self.K, 3),
                           d_attr=self.g_attr.view(self.K, self.D) if self.D > 0 else None)
         # torch work (accumulations, NCCL) on the context's stream, ordered with our kernels
@@ -167,17 +174,34 @@ class Fitter:
     def loss_and_grad(self) -> None:
         """Accumulate this rank's loss and gradients (device, asynchronous)."""
         with self.torch.cuda.stream(self.stream):
+            self._run_loss_and_grad()
+
+    def _run_loss_and_grad(self) -> None:
+        if not self.use_graph:
             self._loss_and_grad()
+            return
+        if self._graph is None:
+            if not self._warm:  # the first pass sizes every buffer (no allocation while capturing)
+                self._loss_and_grad()
+                self._warm = True
+                return
+            g = self.ctx.capture()
+            with g:
+                self._loss_and_grad()
+            self._graph = g
+        self._graph.launch()
 
     def _loss_and_grad(self) -> None:
-        self.dscene.set_raw(self.K, self.D, self.tau, self.centers, self.inv_cov, self.attr)
+        # deferred validation: no host synchronisation here; loss() reports it
+        self.dscene.set_raw(self.K, self.D, self.tau, self.centers, self.inv_cov, self.attr, deferred=True)
         self.grads.zero_()
         self.loss_acc.zero_()
-        for (w_img, w_alpha), cams, tis, tas, tapes, losses in self.groups:
+        for ((w_img, w_alpha), cams, tis, tas, tapes, losses), lsum in zip(self.groups, self._lsum):
             render_views_into(self.ctx, self.dscene, cams, self.cfg, tapes)
             scalar_loss_views_into(self.ctx, tapes, tis, tas, w_img, w_alpha, losses)
             backward_views_into(self.ctx, tapes, GradFlags(), None, self.total)
-            self.loss_acc += losses.sum()
+            self.torch.sum(losses, dim=0, keepdim=True, out=lsum)
+            self.loss_acc.add_(lsum)
         if self.reg is not None and self.rank == 0:  # once per iteration (added before the rank sum)
             for w, fn in ((self.edge_weight, self.reg.edge_reg), (self.laplacian_weight, self.reg.laplacian_reg)):
                 if w > 0.0:
@@ -186,7 +210,7 @@ class Fitter:
     def step(self, group=None) -> None:
         """One fit_shape iteration: loss_and_grad, NCCL all-reduce, ADAM."""
         with self.torch.cuda.stream(self.stream):
-            self._loss_and_grad()
+            self._run_loss_and_grad()
             allreduce_gradients([self.grads, self.loss_acc], group)
             self.step_count += 1
             adam_step(self.ctx, self.params, self.grads, self.m, self.v, self.step_count, self.adam.lr,
@@ -194,6 +218,7 @@ class Fitter:
 
     def loss(self) -> float:
         self.stream.synchronize()
+        self.dscene.check()  # the deferred validation of the last upload
         return float(self.loss_acc.item())
 
     def scene(self) -> GaussianScene:

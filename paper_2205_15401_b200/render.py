@@ -205,13 +205,20 @@ class DeviceScene:
     def set(self, scene: GaussianScene) -> "DeviceScene":
         return self.set_raw(scene.size, scene.attr_dim(), scene.tau, scene.centers, scene.inv_cov, scene.attr)
 
-    def set_raw(self, K: int, D: int, tau: float, centers, inv_cov, attr) -> "DeviceScene":
+    def set_raw(self, K: int, D: int, tau: float, centers, inv_cov, attr, deferred: bool = False) -> "DeviceScene":
+        """Upload from host or device arrays. ``deferred``: validate on the device
+        without synchronising (capturable); :meth:`check` reports the result."""
+        fn = self.ctx.lib.gvr_scene_set_deferred if deferred else self.ctx.lib.gvr_scene_set
         self.ctx.check(
-            self.ctx.lib.gvr_scene_set(self.ctx.handle, self.handle, int(K), int(D), float(tau), _ptr(centers),
-                                       _ptr(inv_cov), _ptr(attr) if D > 0 else None)
+            fn(self.ctx.handle, self.handle, int(K), int(D), float(tau), _ptr(centers), _ptr(inv_cov),
+               _ptr(attr) if D > 0 else None)
         )
         self.K, self.D, self.tau = int(K), int(D), float(tau)
         return self
+
+    def check(self) -> None:
+        """Raise the validation error of the last deferred upload, if any (synchronises)."""
+        self.ctx.check(self.ctx.lib.gvr_scene_check(self.ctx.handle, self.handle))
 
     def close(self) -> None:
         if self.handle:

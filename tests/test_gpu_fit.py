@@ -16,7 +16,7 @@ import paper_2205_15401_b200 as gvr
 from conftest import assert_grad_close
 from paper_2205_15401_b200 import synthetic
 from paper_2205_15401_b200.fit import AdamConfig, Fitter, make_fit_views
-from paper_2205_15401_b200.types import GaussianScene, SelectionConfig
+from paper_2205_15401_b200.types import GaussianScene, SelectionConfig, ValidationError
 
 pytestmark = pytest.mark.gpu
 
@@ -174,3 +174,42 @@ def test_fitter_adds_the_regularizer_terms(ctx):
     assert with_reg.loss() - plain.loss() == pytest.approx(0.3 * ev + 0.7 * lv, rel=1e-9)
     d = with_reg.g_center.cpu().numpy().reshape(-1, 3) - plain.g_center.cpu().numpy().reshape(-1, 3)
     np.testing.assert_allclose(d, 0.3 * eg + 0.7 * lg, rtol=1e-6, atol=1e-12)
+
+
+def test_graph_fitter_matches_eager(ctx):
+    """The captured iteration (deferred scene validation, all views in one CUDA
+    graph) follows the same trajectory as the eager one (FP64 atomic-order noise)."""
+    scene = gvr.make_bench_scene(1000)
+    target = scene.copy()
+    target.attr = np.tile([0.2, 0.6, 0.9], (scene.size, 1))
+    target.centers = target.centers * 1.01
+    views = _views(target, 5, 40)
+    eager = Fitter(ctx, scene, views, adam=AdamConfig(lr=0.01), use_graph=False)
+    graph = Fitter(ctx, scene, views, adam=AdamConfig(lr=0.01), use_graph=True)
+    for it in range(6):
+        eager.step()
+        graph.step()
+        assert graph._graph is not None or it == 0
+        assert graph.loss() == pytest.approx(eager.loss(), rel=1e-9)
+    np.testing.assert_allclose(graph.params.cpu().numpy(), eager.params.cpu().numpy(), rtol=1e-9, atol=1e-12)
+
+
+def test_deferred_scene_validation_reports_at_check(ctx):
+    import torch
+    scene = gvr.make_bench_scene(200)
+    dev = torch.device("cuda:0")
+    c = torch.tensor(scene.centers, device=dev)
+    s = torch.tensor(scene.inv_cov, device=dev)
+    a = torch.tensor(scene.attr, device=dev)
+    ds = gvr.DeviceScene(ctx)
+    ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)
+    ds.check()  # valid
+    s[7, 0, 1] += 1.0  # not symmetric
+    ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)
+    with pytest.raises(ValidationError, match=r"inv_cov is not symmetric \(kernel 7\)"):
+        ds.check()
+    s[7, 0, 1] -= 1.0
+    c[3, 2] = float("nan")
+    ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)
+    with pytest.raises(ValidationError, match=r"non-finite values \(kernel 3\)"):
+        ds.check()
