@@ -396,19 +396,40 @@ constexpr unsigned kKeyUlps = 8u;
 // first dropped position) lies within kKeyUlps of it: then it returns false and
 // the caller ranks the batch one candidate at a time on the exact trace.
 // Replaces ~35 warp instructions per eligible candidate with ~160 per batch.
+// Ascending bitonic sort of one 64-bit key per lane within groups of W lanes.
+template <int W>
+__device__ __forceinline__ unsigned long long bitonic_lanes(unsigned long long ck, int lane) {
+#pragma unroll
+    for (int size = 2; size <= W; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, ck, stride);
+            const bool asc = size == W || (lane & size) == 0;
+            const bool lower = (lane & stride) == 0;
+            ck = (lower == asc) ? (o < ck ? o : ck) : (o > ck ? o : ck);
+        }
+    }
+    return ck;
+}
+
 __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int k, bool me, int m, int kp, int lane,
                                             float* sl, int* si) {
     const unsigned FULL = 0xffffffffu;
     unsigned long long ck = me ? ((unsigned long long)float_order_bits(lk) << 32) | (unsigned)k : ~0ull;
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(FULL, ck, stride);
-            const bool asc = size == 32 || (lane & size) == 0;
-            const bool lower = (lane & stride) == 0;
-            ck = (lower == asc) ? (o < ck ? o : ck) : (o > ck ? o : ck);
+    if (m <= 16) {
+        // compact the eligible candidates to lanes 0..m-1 (staged in the upper
+        // half of the warp's list): a 16-lane sort (10 stages instead of 15)
+        const int r = __popc(__ballot_sync(FULL, me) & ((1u << lane) - 1u));
+        if (me) {
+            sl[32 + r] = lk;
+            si[32 + r] = k;
         }
+        __syncwarp();
+        ck = lane < m ? ((unsigned long long)float_order_bits(sl[32 + lane]) << 32) | (unsigned)si[32 + lane] : ~0ull;
+        __syncwarp();
+        ck = bitonic_lanes<16>(ck, lane);
+    } else {
+        ck = bitonic_lanes<32>(ck, lane);
     }
     const unsigned cu = (unsigned)(ck >> 32);  // lane r < m: key of the r-th smallest candidate
     const unsigned ku = float_order_bits(L);   // lane s < n: key of kept entry s (non-decreasing)
