@@ -144,6 +144,9 @@ int gvr_context_set_prefilter_guard(gvr_context* ctx, double guard);
  * trace and erfc (the reference's arithmetic, ~1e-15) instead of the FP32
  * closed-form pipeline. Slow; used by gradcheck's finite differences. */
 int gvr_context_set_precise(gvr_context* ctx, int on);
+/* Camera::validate (types.cpp:44-63) without a context or device (loaders,
+ * load_camera_json): GVR_OK or GVR_ERR_VALIDATION with the message in msg. */
+int gvr_camera_validate(const gvr_camera* camera, char* msg, int32_t msg_cap);
 /* Profiling hook (no reference counterpart): while on, renders record the SM
  * cycles of each tile's selection CTA on the tape; read with gvr_tape_tile_cycles. */
 int gvr_context_set_tile_profile(gvr_context* ctx, int on);

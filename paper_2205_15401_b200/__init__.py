@@ -42,4 +42,6 @@ from .render import (  # noqa: F401
 )
 from .synthetic import make_bench_camera, make_bench_scene, make_orbit_camera  # noqa: F401
 from .gradcheck import GradCheckEntry, GradCheckReport, gradcheck, so3_exp, so3_exp_gradient, so3_log  # noqa: F401
-from .scene_io import load_camera_json, load_scene_json  # noqa: F401
+from .scene_io import (  # noqa: F401
+    atomic_write_text, load_attrs_json, load_camera_json, load_scene_json, read_pfm, save_attrs_json,
+    save_camera_json, save_scene_json, validate_camera, write_pfm)

@@ -67,6 +67,7 @@ EXPORTED_SYMBOLS = (
     "gvr_tape_dropped_behind_camera",
     "gvr_context_set_tile_profile",
     "gvr_scene_set_deferred",
+    "gvr_camera_validate",
     "gvr_scene_check",
     "gvr_tape_tile_cycles",
 )
@@ -155,6 +156,7 @@ def load() -> ctypes.CDLL:
         "gvr_scene_set": (ctypes.c_int, [vp, vp, i32, i32, dp, vp, vp, vp]),
         "gvr_scene_set_deferred": (ctypes.c_int, [vp, vp, i32, i32, dp, vp, vp, vp]),
         "gvr_scene_check": (ctypes.c_int, [vp, vp]),
+        "gvr_camera_validate": (ctypes.c_int, [ctypes.POINTER(GvrCamera), ctypes.c_char_p, i32]),
         "gvr_scene_size": (i32, [vp]),
         "gvr_scene_attr_dim": (i32, [vp]),
         "gvr_tape_create": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),

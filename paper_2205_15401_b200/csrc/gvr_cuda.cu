@@ -177,13 +177,13 @@ int set_err(gvr_context* ctx, int code, const char* fmt, ...) {
     } while (0)
 
 // Camera::validate (types.cpp:44-63), same messages.
-int validate_camera(gvr_context* ctx, const gvr_camera* c) {
-    if (!c) return set_err(ctx, GVR_ERR_VALIDATION, "camera is null");
+const char* camera_error(const gvr_camera* c) {
+    if (!c) return "camera is null";
     for (int i = 0; i < 9; ++i)
-        if (!std::isfinite(c->rotation[i])) return set_err(ctx, GVR_ERR_VALIDATION, "camera extrinsics have non-finite values");
+        if (!std::isfinite(c->rotation[i])) return "camera extrinsics have non-finite values";
     for (int i = 0; i < 3; ++i)
         if (!std::isfinite(c->translation[i]))
-            return set_err(ctx, GVR_ERR_VALIDATION, "camera extrinsics have non-finite values");
+            return "camera extrinsics have non-finite values";
     const double* r = c->rotation;
     double worst = 0.0;
     for (int i = 0; i < 3; ++i)
@@ -192,16 +192,21 @@ int validate_camera(gvr_context* ctx, const gvr_camera* c) {
             for (int k = 0; k < 3; ++k) acc += r[3 * k + i] * r[3 * k + j];
             worst = std::fmax(worst, std::fabs(acc - (i == j ? 1.0 : 0.0)));
         }
-    if (worst > 1e-6) return set_err(ctx, GVR_ERR_VALIDATION, "camera rotation is not orthonormal");
+    if (worst > 1e-6) return "camera rotation is not orthonormal";
     const double det = r[0] * (r[4] * r[8] - r[5] * r[7]) - r[1] * (r[3] * r[8] - r[5] * r[6]) +
                        r[2] * (r[3] * r[7] - r[4] * r[6]);
-    if (std::fabs(det - 1.0) > 1e-6) return set_err(ctx, GVR_ERR_VALIDATION, "camera rotation determinant is not +1");
+    if (std::fabs(det - 1.0) > 1e-6) return "camera rotation determinant is not +1";
     if (!(c->focal > 0.0) || !std::isfinite(c->focal))
-        return set_err(ctx, GVR_ERR_VALIDATION, "camera focal length must be > 0");
-    if (c->height < 1 || c->width < 1) return set_err(ctx, GVR_ERR_VALIDATION, "camera image size must be at least 1x1");
+        return "camera focal length must be > 0";
+    if (c->height < 1 || c->width < 1) return "camera image size must be at least 1x1";
     if (!std::isfinite(c->ox) || !std::isfinite(c->oy))
-        return set_err(ctx, GVR_ERR_VALIDATION, "camera principal point has non-finite values");
-    return GVR_OK;
+        return "camera principal point has non-finite values";
+    return nullptr;
+}
+
+int validate_camera(gvr_context* ctx, const gvr_camera* c) {
+    const char* e = camera_error(c);
+    return e ? set_err(ctx, GVR_ERR_VALIDATION, "%s", e) : GVR_OK;
 }
 
 // SelectionConfig::validate (tracer.cpp:8-18), same messages.
@@ -590,6 +595,13 @@ int gvr_context_set_precise(gvr_context* ctx, int on) {
     if (!ctx) return GVR_ERR_RUNTIME;
     ctx->precise = on != 0;
     return GVR_OK;
+}
+
+int gvr_camera_validate(const gvr_camera* camera, char* msg, int32_t msg_cap) {
+    const char* e = camera_error(camera);
+    if (!e) return GVR_OK;
+    if (msg && msg_cap > 0) std::snprintf(msg, (size_t)msg_cap, "%s", e);
+    return GVR_ERR_VALIDATION;
 }
 
 int gvr_context_set_tile_profile(gvr_context* ctx, int on) {

@@ -149,3 +149,107 @@ def test_so3_chart_round_trip():
             e[i] = 1e-6
             num[i] = ((gvr_so3.so3_exp(w + e) - gvr_so3.so3_exp(w - e)) * dr).sum() / 2e-6
         assert np.allclose(g, num, rtol=1e-6, atol=1e-8)
+
+
+# ---------------------------------------------------------------- data formats (test_io.cpp)
+
+def _random_scene(seed, k):
+    from paper_2205_15401_b200.types import GaussianScene
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((k, 3, 3)))
+    s = q @ (rng.uniform(0.5, 9.0, (k, 3))[:, :, None] * np.transpose(q, (0, 2, 1)))
+    return GaussianScene(rng.normal(0, 1, (k, 3)) + [0, 0, 5], s, rng.uniform(0, 1, (k, 3)), float(rng.uniform(0.5, 2)))
+
+
+def test_scene_json_round_trip_is_exact(tmp_path):
+    """test_io.cpp:30-47 and :233-244 (identical bytes for the same scene)."""
+    import paper_2205_15401_b200 as gvr
+    scene = _random_scene(101, 7)
+    path = tmp_path / "scene.json"
+    gvr.save_scene_json(scene, path)
+    loaded = gvr.load_scene_json(path)
+    assert loaded.tau == scene.tau
+    assert np.array_equal(loaded.centers, scene.centers)
+    assert np.array_equal(loaded.inv_cov, scene.inv_cov)
+    assert np.array_equal(loaded.attr, scene.attr)
+    assert not (tmp_path / "scene.json.tmp").exists()
+    gvr.save_scene_json(scene, tmp_path / "b.json")
+    assert path.read_bytes() == (tmp_path / "b.json").read_bytes()
+
+
+@pytest.mark.skipif(not os.path.exists(_lib.LIB_PATH), reason="library not built")
+def test_camera_json_round_trip_is_exact_and_validated(tmp_path):
+    """test_io.cpp:49-70; the loader validates like Camera::validate (types.cpp:44-63)."""
+    import paper_2205_15401_b200 as gvr
+    from paper_2205_15401_b200.gradcheck import so3_exp
+    cam = gvr.Camera(so3_exp([0.3, -0.2, 0.9]), np.array([0.5, -1.0, 2.0]), 123.5, 31.25, 63.5, 128, 64)
+    path = tmp_path / "camera.json"
+    gvr.save_camera_json(cam, path)
+    loaded = gvr.load_camera_json(path)
+    assert np.array_equal(loaded.rotation, cam.rotation) and np.array_equal(loaded.translation, cam.translation)
+    assert (loaded.focal, loaded.ox, loaded.oy, loaded.height, loaded.width) == (123.5, 31.25, 63.5, 128, 64)
+    bad = gvr.Camera(np.diag([2.0, 1.0, 1.0]), np.zeros(3), 10.0, 1.0, 1.0, 4, 4)
+    gvr.save_camera_json(bad, path)
+    with pytest.raises(ValidationError, match="camera rotation is not orthonormal"):
+        gvr.load_camera_json(path)
+    gvr.save_camera_json(gvr.Camera(np.eye(3), np.zeros(3), -1.0, 1.0, 1.0, 4, 4), path)
+    with pytest.raises(ValidationError, match="camera focal length must be > 0"):
+        gvr.load_camera_json(path)
+
+
+def test_loading_rejects_missing_and_malformed_files(tmp_path):
+    """test_io.cpp:72-83."""
+    import paper_2205_15401_b200 as gvr
+    with pytest.raises(ValidationError, match="cannot open file"):
+        gvr.load_scene_json(tmp_path / "nope.json")
+    (tmp_path / "bad.json").write_text("{ not json")
+    with pytest.raises(ValidationError, match="invalid JSON"):
+        gvr.load_scene_json(tmp_path / "bad.json")
+    (tmp_path / "v2.json").write_text('{"version":2,"tau":1.0,"kernels":[]}')
+    with pytest.raises(ValidationError, match="unsupported format version"):
+        gvr.load_scene_json(tmp_path / "v2.json")
+
+
+def test_attrs_json_round_trip(tmp_path):
+    """test_io.cpp:85-100."""
+    import paper_2205_15401_b200 as gvr
+    from paper_2205_15401_b200.types import SampledAttributes
+    attrs = SampledAttributes(np.array([[0.1, 0.2, 0.3], [0.0, 0.0, 0.0]]), np.array([1.5, 0.0]),
+                              np.array([False, True]))
+    gvr.save_attrs_json(attrs, tmp_path / "attrs.json")
+    loaded = gvr.load_attrs_json(tmp_path / "attrs.json")
+    assert np.array_equal(loaded.attrs, attrs.attrs) and np.array_equal(loaded.support, attrs.support)
+    assert np.array_equal(loaded.masked, attrs.masked) and loaded.masked_count() == 1
+    (tmp_path / "bad.json").write_text('{"version":1,"attrs":[[1,2]],"support":[1,2],"masked":[false]}')
+    with pytest.raises(ValidationError, match="inconsistent attrs file"):
+        gvr.load_attrs_json(tmp_path / "bad.json")
+
+
+def test_pfm_round_trips_at_float_precision(tmp_path):
+    """test_io.cpp:213-231, plus the byte layout (image_io.cpp:124-157): header,
+    little-endian float32, rows bottom-up."""
+    import paper_2205_15401_b200 as gvr
+    rng = np.random.default_rng(103)
+    for ch in (1, 3):
+        img = rng.uniform(-5, 5, (9, 11, ch))
+        path = tmp_path / f"img{ch}.pfm"
+        gvr.write_pfm(img, path)
+        raw = path.read_bytes()
+        header = f"{'PF' if ch == 3 else 'Pf'}\n11 9\n-1.0\n".encode()
+        assert raw.startswith(header) and len(raw) == len(header) + 4 * img.size
+        first_row_on_disk = np.frombuffer(raw, "<f4", count=11 * ch, offset=len(header))
+        assert np.array_equal(first_row_on_disk, img[-1].reshape(-1).astype(np.float32))
+        loaded = gvr.read_pfm(path)
+        assert loaded.shape == img.shape
+        np.testing.assert_allclose(loaded, img, rtol=1e-7, atol=0)
+    with pytest.raises(ValidationError, match="write_pfm supports 1 or 3 channels"):
+        gvr.write_pfm(np.zeros((2, 2, 2)), tmp_path / "x.pfm")
+    (tmp_path / "be.pfm").write_bytes(b"PF\n1 1\n1.0\n" + b"\0" * 12)
+    with pytest.raises(ValidationError, match="big-endian PFM is not supported"):
+        gvr.read_pfm(tmp_path / "be.pfm")
+    (tmp_path / "short.pfm").write_bytes(b"PF\n2 2\n-1.0\n" + b"\0" * 12)
+    with pytest.raises(ValidationError, match="truncated PFM data"):
+        gvr.read_pfm(tmp_path / "short.pfm")
+    (tmp_path / "magic.pfm").write_bytes(b"P6\n2 2\n255\n")
+    with pytest.raises(ValidationError, match="not a PFM file"):
+        gvr.read_pfm(tmp_path / "magic.pfm")
