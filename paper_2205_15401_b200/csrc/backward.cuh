@@ -69,8 +69,20 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
     // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
     double peak_part = 0.0;
+#if GVR_BWD_IDS_FIRST
+    // ids first: the thread's id loads are independent, the record loads behind them overlap
+    int kq[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) kq[q] = sub + 4 * q < n ? p.topk[pix * p.kp + sub + 4 * q] : 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        if (s >= n) break;
+        const int k = kq[q];
+#else
     for (int s = sub; s < n; s += 4) {
         const int k = p.topk[pix * p.kp + s];
+#endif
         const EntryRec er = p.ent[pix * p.kp + s];  // traced by the forward
         const float pkf = er.pk;
         const double pk = (double)pkf;

@@ -32,6 +32,9 @@
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
 #endif
+#ifndef GVR_BWD_IDS_FIRST  // backward staging loop: entry ids loaded before the records
+#define GVR_BWD_IDS_FIRST 1
+#endif
 #ifndef GVR_PDL  // select -> blend per-tile hand-off with programmatic dependent launch
 #define GVR_PDL 1
 #endif
