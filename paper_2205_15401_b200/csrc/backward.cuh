@@ -62,8 +62,12 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     double d[3];
     pixel_ray(p.cam, i, j, d);
     const double tau = p.tau;
+    // d_image of the pixel in registers for D <= 4 (unrolled with constant
+    // indices: a runtime-indexed array would live in local memory)
     double dimg[4] = {0, 0, 0, 0};
-    for (int c = 0; c < p.D && c < 4; ++c) dimg[c] = p.d_image[pix * p.D + c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (c < p.D) dimg[c] = p.d_image[pix * p.D + c];
     const double l0 = p.ent[pix * p.kp].l;
 
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
@@ -90,14 +94,21 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         const double trans = p.tape_t[pix * p.kp + s];
         double dw = 0.0;
         if (p.D <= 4) {
-            for (int c = 0; c < p.D; ++c) dw += dimg[c] * p.attr[(long long)p.D * k + c];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < p.D) dw += dimg[c] * p.attr[(long long)p.D * k + c];
         } else {
             for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * k + c];
         }
         const double w = trans * pk;
         if (w != 0.0 || dw != 0.0) {
-            for (int c = 0; c < p.D; ++c)
-                atomicAdd(&p.d_attr[(long long)p.D * k + c], w * (p.D <= 4 ? dimg[c] : p.d_image[pix * p.D + c]));
+            if (p.D <= 4) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < p.D) atomicAdd(&p.d_attr[(long long)p.D * k + c], w * dimg[c]);
+            } else {
+                for (int c = 0; c < p.D; ++c) atomicAdd(&p.d_attr[(long long)p.D * k + c], w * p.d_image[pix * p.D + c]);
+            }
         }
         b_dl[s * NP + g] = er.l - l0;
         b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
