@@ -40,12 +40,11 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     constexpr int TILE = 8, NP = 64 / GVR_BWD_SPLIT, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]
-    double* b_dl = reinterpret_cast<double*>(smem);  // l_k - l_0
-    double* b_da = b_dl + KMAX * NP;                 // d_acc_k = -tau T_k d_w_k e^{q_k}
-    double* b_dt = b_da + KMAX * NP;                 // density path d_w_k T_k (grad.cpp:120)
-    float* b_pk = reinterpret_cast<float*>(b_dt + KMAX * NP);  // e^{q_k}
-    float* b_is = b_pk + KMAX * NP;                  // 1 / sigma_k
-    int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
+    // pairs read together are packed: one 16-byte and one 8-byte load per pair
+    double2* b_lda = reinterpret_cast<double2*>(smem);  // {l_k - l_0, d_acc_k = -tau T_k d_w_k e^{q_k}}
+    double* b_dt = reinterpret_cast<double*>(b_lda + KMAX * NP);  // density path d_w_k T_k (grad.cpp:120)
+    float2* b_pi = reinterpret_cast<float2*>(b_dt + KMAX * NP);   // {e^{q_k}, 1 / sigma_k}
+    int* b_id = reinterpret_cast<int*>(b_pi + KMAX * NP);
 
     if ((int)(blockIdx.x / GVR_BWD_SPLIT) >= *p.n_order) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
@@ -110,11 +109,9 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
                 for (int c = 0; c < p.D; ++c) atomicAdd(&p.d_attr[(long long)p.D * k + c], w * p.d_image[pix * p.D + c]);
             }
         }
-        b_dl[s * NP + g] = er.l - l0;
-        b_da[s * NP + g] = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
+        b_lda[s * NP + g] = make_double2(er.l - l0, (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0);
         b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
-        b_pk[s * NP + g] = pkf;
-        b_is[s * NP + g] = er.is;
+        b_pi[s * NP + g] = make_float2(pkf, er.is);
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
@@ -125,19 +122,21 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
 
     // entry-major pair terms + chain to camera space (grad.cpp:121-173)
     for (int e = sub; e < n; e += 4) {
-        const double dle = b_dl[e * NP + g];
-        const float ise = b_is[e * NP + g];
-        const double pke = (double)b_pk[e * NP + g];
-        const double dae = b_da[e * NP + g];
+        const double2 lde = b_lda[e * NP + g];
+        const double dle = lde.x, dae = lde.y;
+        const float2 pie = b_pi[e * NP + g];
+        const float ise = pie.y;
+        const double pke = (double)pie.x;
         const int kid = b_id[e * NP + g];
         double dpk = d_total + b_dt[e * NP + g];  // density path (grad.cpp:120)
         // branch-free pair terms, two independent accumulator sets (even / odd k)
         // so that consecutive pairs overlap instead of serialising on one chain
         double dpk2 = 0.0, dl = 0.0, dl2 = 0.0, dsg = 0.0, dsg2 = 0.0;
         auto pair = [&](int k, double& a_pk, double& a_l, double& a_sg) {
-            const double dak = b_da[k * NP + g];
-            const double dlk = b_dl[k * NP + g];
-            const float isk = b_is[k * NP + g];
+            const double2 ldk = b_lda[k * NP + g];
+            const double dak = ldk.y, dlk = ldk.x;
+            const float2 pik = b_pi[k * NP + g];
+            const float isk = pik.y;
             // pair (k, m = e): z1 = (l_k - l_e) / sigma_e ; pair (k = e, m = k): z2 = (l_e - l_k) / sigma_k
             const float dlf = (float)(dlk - dle);
             const float z1 = dlf * ise;
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
             const double gg = k != e ? dak * (double)(phi1 * ise) * pke : 0.0;
             a_l -= gg;
             a_sg -= gg * (double)z1;
-            if (k != e) a_l = fma(dae, (double)(b_pk[k * NP + g] * phi2 * isk), a_l);
+            if (k != e) a_l = fma(dae, (double)(pik.x * phi2 * isk), a_l);
         };
         int k = 0;
 #if GVR_BWD_WAYS == 4
