@@ -751,15 +751,22 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
 // in ascending (l, idx) order.
 //   W_k = exp(-tau sum_m e^{q_m} Phi((l_k - l_m)/sigma_m)) e^{q_k}
 // The sum is accumulated in FP64 and T(l_k) is taped for the backward.
+// Blend staging slot: the traced l with the FP32 peak and 1/sigma; after the
+// sort the first 8 bytes become the float pair (hi, lo) of l - l_0, so the pair
+// loop reads everything it needs about entry m with one 16-byte load.
+struct __align__(16) BlendSlot {
+    double l;
+    float pk, is;
+};
+
 template <int KMAX>
 __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_kernel(FwdParams p) {
     constexpr int TILE = 8, NP = 64 / GVR_BLEND_SPLIT, PER = (KMAX + 3) / 4;
     extern __shared__ __align__(16) unsigned char smem[];
-    double* b_dl = reinterpret_cast<double*>(smem);  // [slot][pixel] l - l0
-    double* b_w = b_dl + KMAX * NP;                  // W_k
-    float* b_pk = reinterpret_cast<float*>(b_w + KMAX * NP);
-    float* b_is = b_pk + KMAX * NP;
-    int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
+    BlendSlot* b_s = reinterpret_cast<BlendSlot*>(smem);  // [slot][pixel]
+    const float4* b_q = reinterpret_cast<const float4*>(smem);  // {hi, lo, pk, is} after the conversion
+    double* b_w = reinterpret_cast<double*>(b_s + KMAX * NP);  // W_k
+    int* b_id = reinterpret_cast<int*>(b_w + KMAX * NP);
 
     if ((int)(blockIdx.x / GVR_BLEND_SPLIT) >= *p.n_order_blend) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
@@ -815,10 +822,12 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
                 const Traced64 t = trace_fast(d, p.rec64[k]);
                 const double pk = exp(t.q);
                 const float pkf = (float)pk;
-                b_w[s * NP + g] = pk;    // FP64 peak until W overwrites it (alpha sum, after the sort)
-                b_dl[s * NP + g] = t.l;  // l for now; relative to the nearest after the sort
-                b_pk[s * NP + g] = pkf;
-                b_is[s * NP + g] = (float)sqrt(t.a);  // 1/sigma
+                b_w[s * NP + g] = pk;  // FP64 peak until W overwrites it (alpha sum, after the sort)
+                BlendSlot v;
+                v.l = t.l;  // l for now; relative to the nearest after the sort
+                v.pk = pkf;
+                v.is = (float)sqrt(t.a);  // 1/sigma
+                b_s[s * NP + g] = v;
                 b_id[s * NP + g] = k;
             }
         }
@@ -828,29 +837,24 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort;
         // keys closer than the fast-trace error are compared on exact l
         for (int s = 1; s < n; ++s) {
-            double ls = b_dl[s * NP + g];
+            BlendSlot vs = b_s[s * NP + g];
             int is = b_id[s * NP + g];
-            const float ps = b_pk[s * NP + g], ss = b_is[s * NP + g];
             const double ws = b_w[s * NP + g];
             int t = s - 1;
             while (t >= 0) {
-                double lt = b_dl[t * NP + g];
+                BlendSlot vt = b_s[t * NP + g];
                 int it = b_id[t * NP + g];
-                const bool less = key_less(ls, is, lt, it, d, p.rec64);
-                b_dl[t * NP + g] = lt;  // possibly upgraded to exact
+                const bool less = key_less(vs.l, is, vt.l, it, d, p.rec64);
+                b_s[t * NP + g] = vt;  // possibly upgraded to exact
                 b_id[t * NP + g] = it;
                 if (!less) break;
-                b_dl[(t + 1) * NP + g] = lt;
+                b_s[(t + 1) * NP + g] = vt;
                 b_id[(t + 1) * NP + g] = it;
-                b_pk[(t + 1) * NP + g] = b_pk[t * NP + g];
-                b_is[(t + 1) * NP + g] = b_is[t * NP + g];
                 b_w[(t + 1) * NP + g] = b_w[t * NP + g];
                 --t;
             }
-            b_dl[(t + 1) * NP + g] = ls;
+            b_s[(t + 1) * NP + g] = vs;
             b_id[(t + 1) * NP + g] = is;
-            b_pk[(t + 1) * NP + g] = ps;
-            b_is[(t + 1) * NP + g] = ss;
             b_w[(t + 1) * NP + g] = ws;
         }
     }
@@ -860,17 +864,17 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     for (int s = sub; s < n; s += 4) peak_part += b_w[s * NP + g];
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
     peak_part += __shfl_xor_sync(grp, peak_part, 2, 4);
-    const double l0 = b_dl[g];
+    const double l0 = b_s[g].l;
     __syncwarp(grp);
     // l_k - l_0 as an unevaluated float pair hi + lo (replaces the double in place):
     // hi_k - hi_m is exact whenever the pair's z is moderate (Sterbenz), so the
     // argument z = (l_k - l_m) / sigma_m keeps ~1e-7 relative accuracy in FP32.
-    float2* b_hl = reinterpret_cast<float2*>(b_dl);
     for (int s = sub; s < n; s += 4) {
-        const double lval = b_dl[s * NP + g];
+        const BlendSlot v = b_s[s * NP + g];
+        const double lval = v.l;
         const double dl = lval - l0;
         const float hi = (float)dl;
-        b_hl[s * NP + g] = make_float2(hi, (float)(dl - (double)hi));
+        reinterpret_cast<float2*>(&b_s[s * NP + g].l)[0] = make_float2(hi, (float)(dl - (double)hi));
         if (!p.presorted) {
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
@@ -878,8 +882,8 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         // tape the traced entry for the backward and the sampler
         EntryRec er;
         er.l = lval;
-        er.pk = b_pk[s * NP + g];
-        er.is = b_is[s * NP + g];
+        er.pk = v.pk;
+        er.is = v.is;
         p.ent[pix * kp + s] = er;
     }
     __syncwarp(grp);
@@ -902,21 +906,21 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         }
     }
     for (int k = sub; k < n && !p.precise; k += 4) {
-        const float2 hk = b_hl[k * NP + g];
+        const float4 hk = b_q[k * NP + g];
         // sum_m e^{q_m} Phi(z_km): non-negative FP32 terms, Kahan-compensated
         // (error ~2^-24 of the sum, below the 6e-8 of the Phi approximation)
         float sum = 0.0f, comp = 0.0f;
         for (int m = 0; m < n; ++m) {
-            const float2 hm = b_hl[m * NP + g];
-            const float z = ((hk.x - hm.x) + (hk.y - hm.y)) * b_is[m * NP + g];
-            const float y = fmaf(b_pk[m * NP + g], fast_normal_cdf(z), -comp);
+            const float4 hm = b_q[m * NP + g];  // {hi, lo, pk, 1/sigma}
+            const float z = ((hk.x - hm.x) + (hk.y - hm.y)) * hm.w;
+            const float y = fmaf(hm.z, fast_normal_cdf(z), -comp);
             const float t = sum + y;
             comp = (t - sum) - y;
             sum = t;
         }
         const double acc = (double)sum - (double)comp;
         const double trans = exp(-p.tau * acc);
-        const double wd = trans * (double)b_pk[k * NP + g];
+        const double wd = trans * (double)hk.z;
         p.tape_t[pix * kp + k] = trans;
         b_w[k * NP + g] = wd;
         if (p.topk_w) p.topk_w[pix * kp + k] = wd;
@@ -944,7 +948,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             for (int k = 0; k < n; ++k) {
                 const double wd = b_w[k * NP + g];
                 wsum += wd;
-                const float2 h = b_hl[k * NP + g];
+                const float4 h = b_q[k * NP + g];
                 wld += wd * (l0 + ((double)h.x + (double)h.y));
             }
             const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
@@ -964,7 +968,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             p.image[o] = xadd(k == 0 ? 0.0 : p.image[o], xmul(wd, p.attr[(long long)p.D * kid + c]));
         }
         wsum += wd;
-        const float2 h = b_hl[k * NP + g];
+        const float4 h = b_q[k * NP + g];
         wld += wd * (l0 + ((double)h.x + (double)h.y));
     }
     const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
