@@ -112,6 +112,8 @@ struct Camera {
     double oy = 0.0;
     int height = 1;
     int width = 1;
+
+    void validate() const;  // types.cpp:44-63 (gvr_camera_validate: no device needed)
 };
 
 enum class ChannelSemantics : std::uint8_t { Color, Alpha, Normal, Feature };
@@ -238,6 +240,16 @@ inline gvr_camera to_c(const Camera& cam) {
     c.width = cam.width;
     return c;
 }
+
+}  // namespace detail
+
+inline void Camera::validate() const {
+    const gvr_camera c = detail::to_c(*this);
+    char msg[256] = {0};
+    if (gvr_camera_validate(&c, msg, static_cast<int32_t>(sizeof msg)) != GVR_OK) throw ValidationError(msg);
+}
+
+namespace detail {
 
 inline gvr_selection to_c(const SelectionConfig& s) {
     return gvr_selection{s.eta, s.k_prime, s.coarse_enabled ? 1 : 0, s.coarse_downsample};

@@ -177,6 +177,28 @@ inline int run_all() {
         ::doctest::detail::report(doctest_thrown_, __FILE__, __LINE__, "throws " #type ": " #expr); \
     } while (0)
 
+#define CHECK_THROWS_WITH_AS(expr, msg, type)                                               \
+    do {                                                                                    \
+        bool doctest_thrown_ = false;                                                       \
+        try {                                                                               \
+            (void)(expr);                                                                   \
+        } catch (const type& doctest_e_) {                                                  \
+            doctest_thrown_ = std::string(doctest_e_.what()) == std::string(msg);           \
+        } catch (...) {                                                                     \
+        }                                                                                   \
+        ::doctest::detail::report(doctest_thrown_, __FILE__, __LINE__, "throws " #type " with " #msg ": " #expr); \
+    } while (0)
+#define CHECK_NOTHROW(expr)                                                                 \
+    do {                                                                                    \
+        bool doctest_ok_ = true;                                                            \
+        try {                                                                               \
+            (void)(expr);                                                                   \
+        } catch (...) {                                                                     \
+            doctest_ok_ = false;                                                            \
+        }                                                                                   \
+        ::doctest::detail::report(doctest_ok_, __FILE__, __LINE__, "nothrow: " #expr);      \
+    } while (0)
+
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main() { return ::doctest::detail::run_all(); }
 #endif

@@ -174,6 +174,25 @@ TEST_CASE("scene validation catches broken kernels") {  // test_scene.cpp:156-18
     }
 }
 
+TEST_CASE("camera validation") {  // test_scene.cpp:83-89 (non-orthonormal rotation), types.cpp:44-63
+    Camera cam = default_camera();
+    CHECK_NOTHROW(cam.validate());
+    cam.rotation(0, 0) = 2.0;
+    CHECK_THROWS_WITH_AS(cam.validate(), "camera rotation is not orthonormal", ValidationError);
+    cam = default_camera();
+    cam.rotation(0, 0) = -1.0;  // reflection: orthonormal, det = -1
+    CHECK_THROWS_WITH_AS(cam.validate(), "camera rotation determinant is not +1", ValidationError);
+    cam = default_camera();
+    cam.focal = 0.0;
+    CHECK_THROWS_AS(cam.validate(), ValidationError);
+    cam = default_camera();
+    cam.height = 0;
+    CHECK_THROWS_AS(cam.validate(), ValidationError);
+    cam = default_camera();
+    cam.translation[1] = std::nan("");
+    CHECK_THROWS_AS(cam.validate(), ValidationError);
+}
+
 TEST_CASE("selection config validation") {  // test_tracer.cpp:252-259
     GaussianScene scene;
     scene.kernels.push_back(isotropic(0, 0, 4, 1.0, VecX{0, 0, 0}));
