@@ -788,8 +788,9 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     const bool inside = i < p.cam.H && j < p.cam.W;
     const long long pix = (long long)i * p.cam.W + j;
     const int kp = p.sel.kp;
-    // tiles without any selection (or not visited: other shards, empty lists) are cleared
-    const bool visited = p.bwd_cost[tile] > 0.0f;
+    // tiles after the selected ones in the order (other shards, empty lists) are
+    // cleared; a selected tile has a count for every pixel
+    const bool visited = (int)(blockIdx.x / GVR_BLEND_SPLIT) < *p.n_order;
     const int n = inside && visited ? p.count[pix] : 0;
     if (n == 0) {
         if (inside && sub == 0) {
