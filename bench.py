@@ -593,6 +593,7 @@ def run_ours(args):
                        "step": "render_with_tape -> ScalarLoss (device) -> backward, inputs resident in HBM"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks, "c3": c3, "c4": c4, "c5": c5,
             "gpu_launches": launches, "graph": not args.no_graph,
+            "step_ms_stats": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
             "loss": float(loss.item()),
         }
         print(json.dumps(line), flush=True)
