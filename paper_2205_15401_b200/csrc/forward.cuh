@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             // bounded: a selection that never publishes (a bug) must fail the launch, not hang the device
             for (unsigned spin = 0; ld_acquire_gpu(p.tile_done + tile) < (unsigned)GVR_SEL_SPLIT; ++spin) {
                 if (spin > (1u << 26)) __trap();
-                __nanosleep(100);
+                __nanosleep(GVR_PDL_SLEEP_NS);
             }
         }
         __syncthreads();

@@ -35,6 +35,9 @@
 #ifndef GVR_BWD_IDS_FIRST  // backward staging loop: entry ids loaded before the records
 #define GVR_BWD_IDS_FIRST 1
 #endif
+#ifndef GVR_PDL_SLEEP_NS  // back-off of a blend CTA waiting for its tile's selection
+#define GVR_PDL_SLEEP_NS 100
+#endif
 #ifndef GVR_PDL  // select -> blend per-tile hand-off with programmatic dependent launch
 #define GVR_PDL 1
 #endif
