@@ -181,7 +181,8 @@ int gvr_scene_set(gvr_context* ctx, gvr_scene* scene, int32_t K, int32_t D, doub
  * the size (one uncaptured call first) and the arrays are device pointers. */
 int gvr_scene_set_deferred(gvr_context* ctx, gvr_scene* scene, int32_t K, int32_t D, double tau,
                            const double* centers, const double* inv_cov, const double* attr);
-/* Result of the last gvr_scene_set_deferred (synchronises; GVR_OK when none is pending). */
+/* Result of the last gvr_scene_set_deferred (synchronises; re-read on every call,
+ * so a captured upload is re-validated by every replay; GVR_OK after gvr_scene_set). */
 int gvr_scene_check(gvr_context* ctx, gvr_scene* scene);
 int32_t gvr_scene_size(const gvr_scene* scene);
 int32_t gvr_scene_attr_dim(const gvr_scene* scene);

@@ -115,7 +115,7 @@ struct gvr_scene {
     double tau = 1.0;
     uint64_t version = 0;
     bool valid = false;
-    bool check_pending = false;  // gvr_scene_set_deferred: validation result not read yet
+    bool deferred = false;  // last upload by gvr_scene_set_deferred: gvr_scene_check reads the device flag
     Buf centers, inv_cov, attr;
     Buf vflag;  // deferred validation: first error (kernel << 2 | code), ~0 = none
 };
@@ -643,6 +643,7 @@ int gvr_scene_set(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double t
                   const double* inv_cov, const double* attr) {
     if (!ctx || !s) return GVR_ERR_RUNTIME;
     s->valid = false;
+    s->deferred = false;
     ++s->version;
     if (K < 0 || D < 0) return set_err(ctx, GVR_ERR_VALIDATION, "scene sizes must be >= 0");
     // GaussianScene::validate order: tau first, then kernels (types.cpp:31-42)
@@ -667,6 +668,7 @@ int gvr_scene_set_deferred(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D,
                            const double* inv_cov, const double* attr) {
     if (!ctx || !s) return GVR_ERR_RUNTIME;
     s->valid = false;
+    s->deferred = false;
     ++s->version;
     if (K < 0 || D < 0) return set_err(ctx, GVR_ERR_VALIDATION, "scene sizes must be >= 0");
     if (tau < 0.0 || !std::isfinite(tau)) return set_err(ctx, GVR_ERR_VALIDATION, "tau must be finite and >= 0");
@@ -694,13 +696,14 @@ int gvr_scene_set_deferred(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D,
         LAUNCH_CHECK(ctx);
     }
     s->valid = true;  // provisional: gvr_scene_check reports the validation result
-    s->check_pending = true;
+    s->deferred = true;
     return GVR_OK;
 }
 
 int gvr_scene_check(gvr_context* ctx, gvr_scene* s) {
     if (!ctx || !s) return GVR_ERR_RUNTIME;
-    if (!s->check_pending) return s->valid ? GVR_OK : set_err(ctx, GVR_ERR_RUNTIME, "scene is not valid");
+    // the flag is re-read on every check: a captured upload re-validates on every replay
+    if (!s->deferred) return s->valid ? GVR_OK : set_err(ctx, GVR_ERR_RUNTIME, "scene is not valid");
     if (ctx->capturing)
         return set_err(ctx, GVR_ERR_RUNTIME, "operation needs a host synchronisation; not allowed while capturing a graph");
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, s->vflag.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -708,9 +711,8 @@ int gvr_scene_check(gvr_context* ctx, gvr_scene* s) {
     if (int rc = sync_and_check(ctx)) return rc;
     unsigned long long h = 0;
     std::memcpy(&h, ctx->h_flags + 2, sizeof h);
-    s->check_pending = false;
     const int rc = decode_validation(ctx, h);
-    if (rc) s->valid = false;
+    s->valid = rc == GVR_OK;
     return rc;
 }
 

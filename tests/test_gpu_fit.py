@@ -213,3 +213,29 @@ def test_deferred_scene_validation_reports_at_check(ctx):
     ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)
     with pytest.raises(ValidationError, match=r"non-finite values \(kernel 3\)"):
         ds.check()
+
+
+def test_deferred_validation_is_rechecked_after_graph_replays(ctx):
+    """A captured deferred upload validates on every replay; check() reads the latest."""
+    import torch
+    scene = gvr.make_bench_scene(200)
+    dev = torch.device("cuda:0")
+    c = torch.tensor(scene.centers, device=dev)
+    s = torch.tensor(scene.inv_cov, device=dev)
+    a = torch.tensor(scene.attr, device=dev)
+    ds = gvr.DeviceScene(ctx)
+    ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)  # sizes the buffers
+    ds.check()
+    stream = torch.cuda.ExternalStream(int(ctx.lib.gvr_context_stream(ctx.handle)), device=dev)
+    with torch.cuda.stream(stream):
+        with ctx.capture() as g:
+            ds.set_raw(scene.size, 3, 1.0, c, s, a, deferred=True)
+        g.launch()
+        ds.check()
+        c[5, 0] = float("inf")
+        g.launch()
+        with pytest.raises(ValidationError, match=r"non-finite values \(kernel 5\)"):
+            ds.check()
+        c[5, 0] = 0.0
+        g.launch()
+        ds.check()
