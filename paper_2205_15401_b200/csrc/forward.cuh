@@ -44,7 +44,8 @@ struct FwdParams {
     int* nonfinite; // flag
 };
 
-// FP32 centre-relative classification of q against ln(eta).
+// FP32 centre-relative classification of q against ln(eta), and the FP32
+// depth key of the certain accepts.
 // With dt = ((i-Oy)/F, (j-Ox)/F, 1), delta = m - z dt = (z/F)(c_i - i, c_j - j, 0)
 // is formed without cancellation from the integer and fractional parts of the
 // projected centre, and (the line minimum is parametrisation independent)
@@ -52,28 +53,57 @@ struct FwdParams {
 // Division-free, with a guard band g on q and a relative slack on the
 // delta.S.delta * A term (FP32 cancellation):
 //   returns 0: q <= ln(eta) for certain      (reject)
-//           2: q >  ln(eta) for certain      (eligible)
-//           1: inside the band               (decide with the exact FP64 trace)
+//           2: q >  ln(eta) for certain      (eligible; *key set)
+//           1: inside the band, or a key     (decide with the exact FP64 trace)
+//              whose error bound is not met
+// Depth key: the minimiser along dt is t* = z + B'/A (m = z dt + delta, B' =
+// dt.S.delta), so l = |dt| t* = nrm (z + (z/F) c), c = (di sd0 + dj sd1) / A
+// with (di, dj) = (c_i - i, c_j - j) in pixels. In FP32 the key is within
+// 6 units of 2^-24 |l| of the exact l (z: 1, c: <= 2 by the checked bound
+// below, fma + product: 2, nrm: 1), so keys more than kKeyClose apart order
+// like the exact keys and closer ones are decided on the exact trace.
 struct QClass {
     float c_rej, c_acc;   // 2(-ln eta + g), 2(-ln eta - g)
     float slack_lo, slack_hi;  // 1 -/+ relative slack
+    float f, inv_f;       // F, 1 / F
 };
 
-__device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u, float v, const QClass& qc) {
-    if (r.zf < 0.0f) return 1;  // unusual geometry: exact path only
+__device__ __forceinline__ int classify_key(const Rec32& r, int i, int j, float u, float v, float nrm,
+                                            const QClass& qc, float* key) {
+    if (r.z < 0.0f) return 1;  // unusual geometry: exact path only
+    const float zf = r.z * qc.inv_f;
     const float di = (float)(r.ci_int - i) + r.ci_frac;
     const float dj = (float)(r.cj_int - j) + r.cj_frac;
-    const float dx = r.zf * di, dy = r.zf * dj;
+    const float dx = zf * di, dy = zf * dj;
     const float sd0 = fmaf(r.s00, u, fmaf(r.s01, v, r.s02));
     const float sd1 = fmaf(r.s01, u, fmaf(r.s11, v, r.s12));
     const float sd2 = fmaf(r.s02, u, fmaf(r.s12, v, r.s22));
     const float A = fmaf(u, sd0, fmaf(v, sd1, sd2));
-    const float B = fmaf(dx, sd0, dy * sd1);
+    const float Bp = fmaf(di, sd0, dj * sd1);
+    const float B = zf * Bp;
     const float dsd = fmaf(dx, fmaf(r.s00, dx, 2.0f * r.s01 * dy), r.s11 * dy * dy);
     const float bb = B * B;
     if (fmaf(dsd * qc.slack_lo, A, -bb) > qc.c_rej * A) return 0;
-    if (fmaf(dsd * qc.slack_hi, A, -bb) < qc.c_acc * A) return 2;
-    return 1;
+    if (!(fmaf(dsd * qc.slack_hi, A, -bb) < qc.c_acc * A)) return 1;
+    if (key) {
+        const float rA = 1.0f / A;
+        const float c = Bp * rA;
+        // error of c (each FP32 rounding of S, (u, v), (di, dj), the sums and the
+        // quotient; 8 units of 2^-24 of the unsigned sums) must stay within 2
+        // units of 2^-24 of F + c >= F / 2: (Babs + |c| Aabs) / A <= F / 8
+        const float a0 = fabsf(r.s00 * u) + fabsf(r.s01 * v) + fabsf(r.s02);
+        const float a1 = fabsf(r.s01 * u) + fabsf(r.s11 * v) + fabsf(r.s12);
+        const float a2 = fabsf(r.s02 * u) + fabsf(r.s12 * v) + fabsf(r.s22);
+        const float babs = (fabsf(di) + 1.0f) * a0 + (fabsf(dj) + 1.0f) * a1;
+        const float aabs = fabsf(u) * a0 + fabsf(v) * a1 + a2;
+        if (!(fmaf(fabsf(c), aabs, babs) * rA <= 0.125f * qc.f) || !(fabsf(c) <= 0.5f * qc.f)) return 1;
+        *key = nrm * fmaf(zf, c, r.z);
+    }
+    return 2;
+}
+
+__device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u, float v, const QClass& qc) {
+    return classify_key(r, i, j, u, v, 1.0f, qc, nullptr);
 }
 
 // Loads a tile's candidate list into shared memory in ascending order of a
@@ -170,13 +200,18 @@ struct __align__(16) Cand {
     int pad[3];
 };
 
-// Fast FP64 peak distance l = d.(S m) / d.S.d (the reference's b/a with S
-// symmetric), contracted FMAs: within a few ulps (~1e-15 relative) of the
-// reference-order l of trace_exact. dd = (d0^2, d1^2, d2^2, 2 d0 d1, 2 d0 d2, 2 d1 d2).
-__device__ __forceinline__ double fast_l(const Rec64& r, const double* d, const double* dd) {
-    const double a = fma(r.s[0], dd[0], fma(r.s[4], dd[1], fma(r.s[8], dd[2],
-                         fma(r.s[1], dd[3], fma(r.s[2], dd[4], r.s[5] * dd[5])))));
-    const double b = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2]));
+// Fast FP64 peak distance l = b / a with the reference's a = d.Sd and
+// b = (m.Sd + d.Sm) / 2 (full S), contracted FMAs: within a few ulps (~1e-15
+// relative) of the reference-order l of trace_exact. Keys of the CTA selection
+// (K' > 32).
+__device__ __forceinline__ double fast_l(const Rec64& r, const double* d) {
+    const double* s = r.s;
+    const double sd0 = fma(s[0], d[0], fma(s[1], d[1], s[2] * d[2]));
+    const double sd1 = fma(s[3], d[0], fma(s[4], d[1], s[5] * d[2]));
+    const double sd2 = fma(s[6], d[0], fma(s[7], d[1], s[8] * d[2]));
+    const double a = fma(d[0], sd0, fma(d[1], sd1, d[2] * sd2));
+    const double b = 0.5 * (fma(r.m[0], sd0, fma(r.m[1], sd1, r.m[2] * sd2)) +
+                            fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2])));
     double rc;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(a));
     rc = rc * fma(-a, rc, 2.0);  // Newton: ~2^-40
@@ -266,8 +301,6 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
 
     double d[3];
     pixel_ray(p.cam, inside ? i : 0, inside ? j : 0, d);
-    const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
-                          2.0 * d[1] * d[2]};
     const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
     const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
     const float fi = (float)i, fj = (float)j;
@@ -277,6 +310,8 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
     qc.slack_lo = p.prefilter_c1;
     qc.slack_hi = 2.0f - p.prefilter_c1;
+    qc.f = (float)p.cam.focal;
+    qc.inv_f = (float)(1.0 / p.cam.focal);
     const bool exact_only = p.exact_only != 0;
     const double log_eta = p.sel.log_eta;
     const Rec64* rec64 = p.rec64;
@@ -321,7 +356,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
                     lk = t.l;
                     k |= kExact;
                 } else {
-                    lk = fast_l(rec64[k], d, dd);
+                    lk = fast_l(rec64[k], d);
                 }
                 if (n < kp) {
                     s_l[n * NT + tid] = lk;
@@ -370,10 +405,10 @@ __device__ __forceinline__ bool exact_less(int a, int b, const double* d, const 
     return la < lb || (la == lb && a < b);
 }
 
-// FP32 rank keys: lf = (float)fast l. |lf - l_exact| <= 2^-24 |l| + 1e-11 |l|, so two
-// keys farther apart than kKeyClose |l| order like the exact keys; closer ones
-// are compared on the exact trace.
-constexpr float kKeyClose = 4.0e-7f;
+// FP32 rank keys (classify_key, or the exact l rounded to FP32): within 7 units
+// of 2^-24 |l| of the exact l, so two keys farther apart than kKeyClose |l|
+// order like the exact keys; closer ones are compared on the exact trace.
+constexpr float kKeyClose = 9.5367431640625e-7f;  // 2^-20 = 16 units of 2^-24
 
 __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - b) <= kKeyClose * fabsf(b); }
 
@@ -384,9 +419,9 @@ __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - 
 #define GVR_SEL_BATCH_MIN 10
 #endif
 // Keys within kKeyUlps units in the last place of each other are "close" for the
-// batch merge: 8 ulps >= 8 * 2^-24 |l| > 4 x the FP32 key error, so keys farther
-// apart order like the exact keys.
-constexpr unsigned kKeyUlps = 8u;
+// batch merge: 16 ulps >= 16 * 2^-24 |l| > the sum of two keys' errors (<= 14
+// units), so keys farther apart order like the exact keys.
+constexpr unsigned kKeyUlps = 16u;
 
 // Batch merge of one 32-candidate batch into the kept list (warp-wide): bitonic
 // sort of the eligible candidates by (FP32 key, id), binary-search ranks of
@@ -557,9 +592,10 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             sh_sbo[b + 1] = v;
         }
     }
-    // the tile's 64 rays (and their FP32 image-plane coordinates), once per CTA
+    // the tile's 64 rays (FP64, exact path) and their FP32 image-plane
+    // coordinates and |dt| (pre-filter and depth keys), once per CTA
     __shared__ double sh_ray[64][3];
-    __shared__ float sh_uv[64][2];
+    __shared__ float4 sh_uvn[64];
     for (int q = threadIdx.x; q < 64; q += blockDim.x) {
         const int ri = (tile / p.tiles_x) * TILE + q / TILE, rj = (tile % p.tiles_x) * TILE + q % TILE;
         if (ri < p.cam.H && rj < p.cam.W) {
@@ -568,8 +604,9 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             sh_ray[q][0] = d[0];
             sh_ray[q][1] = d[1];
             sh_ray[q][2] = d[2];
-            sh_uv[q][0] = (float)xdiv(xsub((double)ri, p.cam.oy), p.cam.focal);
-            sh_uv[q][1] = (float)xdiv(xsub((double)rj, p.cam.ox), p.cam.focal);
+            const double u = xdiv(xsub((double)ri, p.cam.oy), p.cam.focal);
+            const double v = xdiv(xsub((double)rj, p.cam.ox), p.cam.focal);
+            sh_uvn[q] = make_float4((float)u, (float)v, (float)sqrt(u * u + v * v + 1.0), 0.0f);
         }
     }
     __syncthreads();
@@ -583,6 +620,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
     qc.slack_lo = p.prefilter_c1;
     qc.slack_hi = 2.0f - p.prefilter_c1;
+    qc.f = (float)p.cam.focal;
+    qc.inv_f = (float)(1.0 / p.cam.focal);
     const bool exact_only = p.exact_only != 0;
     float cost = 0.0f;
 
@@ -603,8 +642,9 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         end = pe >= 0 ? pe : (overflow ? p.K : listed);
         if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
         const int q = ((psb >> 1) * 2 + (px >> 2)) * TILE + (psb & 1) * 4 + (px & 3);  // pixel within the tile
-        const double d[3] = {sh_ray[q][0], sh_ray[q][1], sh_ray[q][2]};
-        const float u = sh_uv[q][0], v = sh_uv[q][1];
+        const double* d = sh_ray[q];  // read only on the exact path
+        const float4 uvn = sh_uvn[q];
+        const float u = uvn.x, v = uvn.y, nrm = uvn.z;
 #else
     for (int px = 0; px < 8; ++px) {
         const int i = sr0 + (px >> 2);
@@ -614,10 +654,9 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         pixel_ray(p.cam, i, j, d);
         const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
         const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
+        const float nrm = (float)sqrt((double)u * u + (double)v * v + 1.0);
 #endif
         const long long pix = (long long)i * p.cam.W + j;
-        const double dd[6] = {d[0] * d[0], d[1] * d[1], d[2] * d[2], 2.0 * d[0] * d[1], 2.0 * d[0] * d[2],
-                              2.0 * d[1] * d[2]};
         const float fi = (float)i, fj = (float)j;
 
         float L = INFINITY;  // lane s < n: rank key of the s-th nearest
@@ -636,16 +675,17 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             }
             const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
             const float4 box = __ldg(rp);        // top, bottom, left, right
-            const float4 zrec = __ldg(rp + 1);   // zmin, zf, ci_frac, cj_frac
+            const float4 zrec = __ldg(rp + 1);   // zmin, z, ci_frac, cj_frac
             // zmin <= l for any kernel that can pass eta: a candidate whose bound is
             // past the worst kept key cannot enter the full list (skip the tests)
             const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w &&
                                 !(zrec.x > worst + 2.0f * kKeyClose * fabsf(worst));
             int cls = 0;
+            float lk = INFINITY;
             if (in_box) {
                 Rec32 r;
                 r.zmin = zrec.x;
-                r.zf = zrec.y;
+                r.z = zrec.y;
                 r.ci_frac = zrec.z;
                 r.cj_frac = zrec.w;
                 const float4 c2 = __ldg(rp + 2), c3 = __ldg(rp + 3);
@@ -657,19 +697,17 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
                 r.s11 = c3.y;
                 r.s12 = c3.z;
                 r.s22 = c3.w;
-                cls = classify_q(r, i, j, u, v, qc);
+                cls = classify_key(r, i, j, u, v, nrm, qc, &lk);
             }
-            float lk = INFINITY;
             if (cls != 0) {
                 if (exact_only || cls == 1) {
-                    const Traced64 t = trace_exact(d, rec64[k]);
+                    const double dr[3] = {d[0], d[1], d[2]};
+                    const Traced64 t = trace_exact(dr, rec64[k]);
                     if (t.q > log_eta) {  // fine_select threshold (tracer.cpp:117-118)
                         lk = (float)t.l;
                     } else {
                         cls = 0;
                     }
-                } else {
-                    lk = (float)fast_l(rec64[k], d, dd);
                 }
                 // cannot enter a full list
                 if (cls != 0 && lk > worst + 2.0f * kKeyClose * fabsf(worst)) cls = 0;

@@ -77,10 +77,11 @@ struct __align__(16) Rec32 {
     // and cell rounding), rounded outward: contains every pixel centre whose ray
     // meets the eta-ellipsoid, i.e. every pixel where q > ln(eta) is possible.
     float top, bottom, left, right;
-    float zmin, zf;            // zmin = conservative lower bound of l; zf = z / F
+    float zmin, z;             // zmin = conservative lower bound of l; z = camera-space depth
+                               // (FP32; < 0: unusual geometry, exact FP64 path only)
     float ci_frac, cj_frac;
     int ci_int, cj_int;        // screen centre (row, col) = int + frac
-    float s00, s01, s02, s11, s12, s22;
+    float s00, s01, s02, s11, s12, s22;  // S' = R S R^T, off-diagonals symmetrised (S + S^T) / 2
 };
 
 // Per-kernel FP64 camera-space record for the exact trace (128 B).
@@ -184,21 +185,24 @@ __device__ __forceinline__ Traced64 trace_exact(const double* d, const Rec64& r)
 
 __device__ __forceinline__ double sigma_of(double a) { return xdiv(1.0, __dsqrt_rn(a)); }
 
-// The same trace with contracted FMAs and the symmetric upper triangle of S:
-// ~1e-15 relative of trace_exact (q: ~1e-13, cancellation in v). Used where
-// values feed tolerance-checked arithmetic (blend, backward), never decisions.
+// The same trace with contracted FMAs (same formulas as the reference: a = d.Sd,
+// b = (m.Sd + d.Sm) / 2 with the full S, so asymmetric S within the validation
+// tolerance is treated like the reference does): ~1e-15 relative of trace_exact
+// (q: ~1e-13, cancellation in v). Used where values feed tolerance-checked
+// arithmetic (blend, backward), never decisions.
 __device__ __forceinline__ Traced64 trace_fast(const double* d, const Rec64& r) {
-    const double s00 = r.s[0], s01 = r.s[1], s02 = r.s[2], s11 = r.s[4], s12 = r.s[5], s22 = r.s[8];
-    const double sd0 = fma(s00, d[0], fma(s01, d[1], s02 * d[2]));
-    const double sd1 = fma(s01, d[0], fma(s11, d[1], s12 * d[2]));
-    const double sd2 = fma(s02, d[0], fma(s12, d[1], s22 * d[2]));
+    const double* s = r.s;
+    const double sd0 = fma(s[0], d[0], fma(s[1], d[1], s[2] * d[2]));
+    const double sd1 = fma(s[3], d[0], fma(s[4], d[1], s[5] * d[2]));
+    const double sd2 = fma(s[6], d[0], fma(s[7], d[1], s[8] * d[2]));
     const double a = fma(d[0], sd0, fma(d[1], sd1, d[2] * sd2));
-    const double b = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2]));
+    const double b = 0.5 * (fma(r.m[0], sd0, fma(r.m[1], sd1, r.m[2] * sd2)) +
+                            fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2])));
     const double l = b / a;
     const double v0 = fma(-l, d[0], r.m[0]), v1 = fma(-l, d[1], r.m[1]), v2 = fma(-l, d[2], r.m[2]);
-    const double sv0 = fma(s00, v0, fma(s01, v1, s02 * v2));
-    const double sv1 = fma(s01, v0, fma(s11, v1, s12 * v2));
-    const double sv2 = fma(s02, v0, fma(s12, v1, s22 * v2));
+    const double sv0 = fma(s[0], v0, fma(s[1], v1, s[2] * v2));
+    const double sv1 = fma(s[3], v0, fma(s[4], v1, s[5] * v2));
+    const double sv2 = fma(s[6], v0, fma(s[7], v1, s[8] * v2));
     double q = -0.5 * fma(v0, sv0, fma(v1, sv1, v2 * sv2));
     if (q > 0.0) q = 0.0;
     return Traced64{l, q, a};

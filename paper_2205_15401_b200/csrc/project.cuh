@@ -178,11 +178,12 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     const double f = c.focal;
     const double z = r.m[2];
     Rec32 q;
+    // quadratic forms (and so l and q) depend only on the symmetric part of S'
     q.s00 = (float)r.s[0];
-    q.s01 = (float)r.s[1];
-    q.s02 = (float)r.s[2];
+    q.s01 = (float)(0.5 * (r.s[1] + r.s[3]));
+    q.s02 = (float)(0.5 * (r.s[2] + r.s[6]));
     q.s11 = (float)r.s[4];
-    q.s12 = (float)r.s[5];
+    q.s12 = (float)(0.5 * (r.s[5] + r.s[7]));
     q.s22 = (float)r.s[8];
     q.top = q.left = 1.0f;
     q.bottom = q.right = 0.0f;  // empty box
@@ -191,7 +192,7 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     if (z <= kBehindCameraEps) {
         // behind the camera: dropped (tracer.cpp:52-56, blender.cpp:86)
         atomicAdd(p.dropped_behind, 1);
-        q.zf = -1.0f;
+        q.z = -1.0f;
         q.ci_int = q.cj_int = 0;
         q.ci_frac = q.cj_frac = 0.0f;
         p.rec32[k] = q;
@@ -214,10 +215,10 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     if (zmin > 0.0) q.zmin = __double2float_rd(zmin - 1e-12 * zmin);
 
     // Centre-relative FP32 pre-filter data; unusual geometry (near-plane
-    // straddlers, far off-axis centres) bypasses the pre-filter (zf < 0).
-    q.zf = (float)(z / f);
+    // straddlers, far off-axis centres) bypasses the pre-filter (z < 0).
+    q.z = (float)z;
     if (straddles || fabs(ci) > 1e7 || fabs(cj) > 1e7) {
-        q.zf = -1.0f;
+        q.z = -1.0f;
         q.ci_int = q.cj_int = 0;
         q.ci_frac = q.cj_frac = 0.0f;
     } else {
