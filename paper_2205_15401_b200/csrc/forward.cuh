@@ -415,6 +415,9 @@ __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - 
 #ifndef GVR_SEL_CUNROLL  // list batches per compaction step (loads in flight together)
 #define GVR_SEL_CUNROLL 4
 #endif
+#ifndef GVR_SEL_FIRST_FAST  // a pixel's first batch merge skips the kept-list ranks
+#define GVR_SEL_FIRST_FAST 1
+#endif
 #ifndef GVR_SEL_BATCH_MIN  // eligible candidates per batch from which the batch merge is used (33: never)
 #define GVR_SEL_BATCH_MIN 10
 #endif
@@ -467,6 +470,21 @@ __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int
         ck = bitonic_lanes<32>(ck, lane);
     }
     const unsigned cu = (unsigned)(ck >> 32);  // lane r < m: key of the r-th smallest candidate
+#if GVR_SEL_FIRST_FAST
+    if (n == 0) {
+        // nothing kept yet (a pixel's first eligible batch): the sorted
+        // candidates are the merged order; only their adjacency is checked
+        const unsigned nxt = __shfl_down_sync(FULL, cu, 1);
+        const bool bad = lane + 1 < min(m, kp + 1) && nxt - cu <= kKeyUlps;
+        if (__any_sync(FULL, bad)) return false;
+        if (lane < min(m, kp)) {
+            sl[lane] = float_from_order_bits(cu);
+            si[lane] = (int)(unsigned)ck;
+        }
+        __syncwarp();
+        return true;
+    }
+#endif
     const unsigned ku = float_order_bits(L);   // lane s < n: key of kept entry s (non-decreasing)
     // below: kept entries at or before the candidate (ties: kept first); above: candidates before the kept entry
     int below = 0, above = 0;
