@@ -124,13 +124,13 @@ const char* gvr_last_error(const gvr_context* ctx);
 int gvr_context_set_stream(gvr_context* ctx, void* cuda_stream);
 void* gvr_context_stream(gvr_context* ctx);
 int gvr_context_synchronize(gvr_context* ctx);
-/* Instrumentation: kernels of this library launched since creation, and
- * device-wide CUB calls (exclusive scan, radix sort) issued. */
+/* Instrumentation: kernels of this library launched since creation; calls into
+ * device-wide libraries (none on the render path: always 0). */
 int64_t gvr_context_launch_count(const gvr_context* ctx);
 int64_t gvr_context_library_call_count(const gvr_context* ctx);
 /* Per-stage device time via CUDA events around each launch (off by default).
- * Stages: 0 project, 1 scan, 2 emit, 3 sort, 4 ranges/tile ordering,
- * 5 select, 6 blend, 7 loss, 8 backward, 9 object-space. Enabling resets the
+ * Stages: 0 project + bin count, 1 (unused), 2 bin emit, 3 (unused), 4 tile
+ * order + list layout, 5 select, 6 blend, 7 loss, 8 backward, 9 object-space. Enabling resets the
  * accumulators. */
 int gvr_context_enable_timing(gvr_context* ctx, int on);
 int gvr_context_stage_times(gvr_context* ctx, double* ms, int64_t* count, int n);
@@ -153,10 +153,13 @@ int gvr_context_set_tile_profile(gvr_context* ctx, int on);
 /* Per-tile selection cycles of a render made with the tile profile on
  * (n = tiles_x * tiles_y of the tape; 0 for tiles with nothing to select). */
 int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* tape, int64_t* cycles, int64_t n);
-/* Per-tile candidate-list capacity (default 4096 entries of 8 B per 8x8 tile).
- * Tiles whose list overflows stream every kernel through the same exact tests
- * (slower, same results); a small value exercises that path in tests. */
+/* Test hook: caps the tile-list pool at `cap` entries (8 B each; 0 = automatic
+ * sizing). Lists that do not fit stream every kernel through the same exact
+ * tests (slower, same results); a small value exercises that path in tests. */
 int gvr_context_set_tile_capacity(gvr_context* ctx, int cap);
+/* Test hook: tile lists longer than n entries (default and maximum 2048) are
+ * sorted in global memory instead of shared memory. Results must not change. */
+int gvr_context_set_list_smem(gvr_context* ctx, int n);
 
 /* ---- CUDA graphs ----------------------------------------------------------
  * Capture a sequence of calls on the context stream (e.g. gvr_render +
@@ -191,8 +194,8 @@ int32_t gvr_scene_attr_dim(const gvr_scene* scene);
 int gvr_tape_create(gvr_context* ctx, gvr_tape** out);
 void gvr_tape_destroy(gvr_tape* tape);
 
-/* render_with_tape: view transform, projection + culling, 16x16 tile binning,
- * fused trace / top-K' selection / closed-form blend. The tape records the
+/* render_with_tape: view transform, projection + culling, 8x8 tile binning
+ * (count pass, scan, emit), trace / top-K' selection, closed-form blend. The tape records the
  * per-pixel selection for gvr_backward and references `scene`, which must not be
  * re-set before the backward (checked). `out` may be NULL. */
 int gvr_render(gvr_context* ctx, const gvr_scene* scene, const gvr_camera* camera,
@@ -218,6 +221,11 @@ int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* tape, double* centers, 
 /* PixelKernelMap::dropped_behind_camera (tracer.hpp:39): kernels of the taped
  * render with camera-space z <= 1e-4. Synchronises. */
 int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* tape, int32_t* count);
+/* Tile-list layout of the taped render (no reference counterpart; synchronises):
+ * stats[0] listed (tile, kernel) entries, [1] longest tile list, [2] tiles whose
+ * list did not fit the pool (streamed: every kernel, no early exit), [3] lists
+ * longer than the shared-memory stage (sorted in global memory), [4] pool capacity. */
+int gvr_tape_list_stats(gvr_context* ctx, const gvr_tape* tape, int64_t* stats);
 /* Shape of the taped render. */
 int gvr_tape_shape(const gvr_tape* tape, int32_t* height, int32_t* width, int32_t* k_prime,
                    int32_t* attr_dim);

@@ -70,6 +70,8 @@ EXPORTED_SYMBOLS = (
     "gvr_camera_validate",
     "gvr_scene_check",
     "gvr_tape_tile_cycles",
+    "gvr_tape_list_stats",
+    "gvr_context_set_list_smem",
 )
 
 
@@ -168,6 +170,8 @@ def load() -> ctypes.CDLL:
         "gvr_tape_dropped_behind_camera": (ctypes.c_int, [vp, vp, ctypes.POINTER(i32)]),
         "gvr_context_set_tile_profile": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_tape_tile_cycles": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64]),
+        "gvr_tape_list_stats": (ctypes.c_int, [vp, vp, vp]),
+        "gvr_context_set_list_smem": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                                           ctypes.POINTER(i32)]),
         "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),

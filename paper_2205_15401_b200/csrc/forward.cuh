@@ -16,9 +16,12 @@ struct FwdParams {
     int tiles_x;
     const int* tile_order;  // tiles by list length, longest first (LPT); first *n_order valid
     const int* n_order;
-    const int* tile_count;                 // [tiles] list lengths (may exceed cap)
-    const unsigned long long* tile_lists;  // [tiles * cap] (order(zmin) << 32 | id), unsorted
-    int cap;
+    const int* tile_count;           // [tiles] list lengths
+    const int* tile_off;             // [tiles] list offset in the pool; -1: not listed (pool overflow:
+                                     // the tile streams every kernel through the same exact tests)
+    const unsigned long long* pool;  // tile lists (order(zmin) << 32 | id), unsorted within a list
+    unsigned long long* sorted_pool; // same offsets: sorted copies of lists too long for shared memory
+    int list_smem;                   // lists up to this length are sorted in shared memory (<= kSelListSmem)
     int K;
     const int* tile_order_blend;  // tiles by sum_p n_p^2 (from the selection), then the tiles with no
     const int* n_order_blend;     // selection (cleared by the blend); first *n_order_blend valid
@@ -113,26 +116,21 @@ __device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u,
 // lower bound, so keys[e] >> 32 is non-decreasing along the list and bounds the
 // zmin (hence the l) of every entry at or after e -- all the early exit needs.
 // The selection itself is exact and independent of the visiting order.
-// Returns the list length, or -1 when the tile overflowed its capacity (the
+// Returns the list length, or -1 when the tile's list did not fit the pool (the
 // caller then streams every kernel, unsorted, with the same exact tests).
-// With smem_cap < count (<= p.cap) the list is left unsorted in global memory:
-// *sorted = false and the caller must not early-exit on it.
+// Lists longer than smem_cap are sorted into the tile's slot of the global
+// sorted pool instead of shared memory; *list points at the sorted list.
 __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys,
-                                                int smem_cap = 0x7fffffff, const unsigned long long** list = nullptr,
-                                                bool* sorted = nullptr) {
+                                                int smem_cap, const unsigned long long** list) {
     constexpr int NB = 256;
     __shared__ unsigned s_lo, s_hi;
     __shared__ int s_hist[NB];
     const int count = p.tile_count[tile];
-    if (count > p.cap) return -1;
-    const unsigned long long* src = p.tile_lists + (size_t)tile * p.cap;
-    if (list) *list = keys;
-    if (sorted) *sorted = true;
-    if (count > smem_cap) {
-        if (list) *list = src;
-        if (sorted) *sorted = false;
-        return count;
-    }
+    const int off = p.tile_off[tile];
+    if (off < 0) return count > 0 ? -1 : 0;
+    const unsigned long long* src = p.pool + off;
+    if (count > smem_cap) keys = p.sorted_pool + off;
+    *list = keys;
     if (threadIdx.x == 0) {
         s_lo = 0xffffffffu;
         s_hi = 0u;
@@ -192,6 +190,11 @@ __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, un
     __syncthreads();
     return count;
 }
+
+#ifndef GVR_SEL_LIST_SMEM
+#define GVR_SEL_LIST_SMEM 2048
+#endif
+constexpr int kSelListSmem = GVR_SEL_LIST_SMEM;  // sorted tile list entries kept in shared memory
 
 // Per-warp candidate chunk entry.
 struct __align__(16) Cand {
@@ -292,7 +295,8 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     const int i = (tile / p.tiles_x) * TILE + tid / TILE;
     const int j = (tile % p.tiles_x) * TILE + tid % TILE;
     const bool inside = i < p.cam.H && j < p.cam.W;
-    const int listed = load_sorted_list(p, tile, keys);
+    const unsigned long long* tl = keys;
+    const int listed = load_sorted_list(p, tile, keys, p.list_smem, &tl);
     const bool overflow = listed < 0;  // stream every kernel, unsorted
     const int start = 0;
     const int end = overflow ? p.K : listed;
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         if (__all_sync(0xffffffffu, done)) break;
         const int e = base + lane;
         if (e < end) {
-            const int k = overflow ? e : (int)(keys[e] & 0xffffffffu);
+            const int k = overflow ? e : (int)(tl[e] & 0xffffffffu);
             chunk[lane].r = p.rec32[k];
             chunk[lane].k = k;
         }
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         for (int c0 = 0; c0 < cnt && !done; c0 += 4) {
             // early exit: every later candidate has l >= zmin > worst kept (+ key error)
             if (!overflow &&
-                (double)float_from_order_bits((uint32_t)(keys[base + c0] >> 32)) > wl + 1e-11 * fabs(wl)) {
+                (double)float_from_order_bits((uint32_t)(tl[base + c0] >> 32)) > wl + 1e-11 * fabs(wl)) {
                 done = true;
                 break;
             }
@@ -393,11 +397,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
 #ifndef GVR_SEL_WARP_LIST
 #define GVR_SEL_WARP_LIST 512
 #endif
-#ifndef GVR_SEL_LIST_SMEM
-#define GVR_SEL_LIST_SMEM 2048
-#endif
 constexpr int kWarpListCap = GVR_SEL_WARP_LIST;  // per-warp compacted list capacity (entries)
-constexpr int kSelListSmem = GVR_SEL_LIST_SMEM;  // sorted tile list entries kept in shared memory
 
 // Exact order of two selection candidates (kernel ids a, b; l on the exact trace).
 __device__ __forceinline__ bool exact_less(int a, int b, const double* d, const Rec64* rec64) {
@@ -539,12 +539,11 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     const int sb = (blockIdx.x % GVR_SEL_SPLIT) * (8 / GVR_SEL_SPLIT) + warp;  // sub-block of the tile
     const unsigned FULL = 0xffffffffu;
     const int tile = p.tile_order[blockIdx.x / GVR_SEL_SPLIT];
-    const int smem_cap = min(p.cap, kSelListSmem);
+    const int smem_cap = kSelListSmem;  // shared-memory layout; p.list_smem decides where a list is sorted
     const unsigned long long* tl = keys;
-    bool sorted = true;
-    const int listed = load_sorted_list(p, tile, keys, smem_cap, &tl, &sorted);
+    const int listed = load_sorted_list(p, tile, keys, p.list_smem, &tl);
     const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
-    const bool early = !overflow && sorted;  // the list is ordered by its depth bound
+    const bool early = !overflow;  // the list is ordered by its depth bound
     const int start = 0;
     // Each warp owns a 2x4-pixel sub-block of the tile and first compacts the
     // tile list to the entries whose screen box meets the sub-block (stable, so
@@ -1051,17 +1050,82 @@ __global__ void clear_empty_tiles_kernel(CameraP cam, int Dc, int tiles_x, const
     count[pix] = 0;
 }
 
+// Tile-list layout (blockDim.x == 1024): exclusive scan of the per-tile counts
+// in tile order into pool offsets. Lists that would end past pool_cap get
+// offset -1 (streamed by the selection, counted as overflow). stats: [0] total
+// entries, [1] longest list, [2] overflowed tiles, [3] lists longer than
+// smem_cap (sorted in the global sorted pool).
+__device__ void list_offsets(int tiles, const int* __restrict__ count, int* __restrict__ tile_off, int pool_cap,
+                             int smem_cap, int* __restrict__ stats) {
+    __shared__ long long s_warp[32];
+    __shared__ int s_max, s_over, s_long;
+    if (threadIdx.x == 0) s_max = s_over = s_long = 0;
+    const int chunk = (tiles + 1023) / 1024;
+    const int t0 = min(tiles, (int)threadIdx.x * chunk), t1 = min(tiles, t0 + chunk);
+    long long run = 0;
+    int mx = 0;
+    for (int t = t0; t < t1; ++t) {
+        run += count[t];
+        mx = max(mx, count[t]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (lane == 0) atomicMax(&s_max, mx);
+    if (warp == 0) {
+        long long w = s_warp[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;  // exclusive
+        if (lane == 31) stats[0] = (int)min(wi, (long long)0x7fffffff);
+    }
+    __syncthreads();
+    long long off = s_warp[warp] + incl - run;
+    int over = 0, lng = 0;
+    for (int t = t0; t < t1; ++t) {
+        const int c = count[t];
+        const bool fits = c > 0 && off + c <= (long long)pool_cap;
+        tile_off[t] = fits ? (int)off : -1;
+        over += c > 0 && !fits;
+        lng += fits && c > smem_cap;
+        off += c;
+    }
+    if (over) atomicAdd(&s_over, over);
+    if (lng) atomicAdd(&s_long, lng);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        stats[1] = s_max;
+        stats[2] = s_over;
+        stats[3] = s_long;
+    }
+}
+
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
 // log-spaced cost buckets, descending). Zero-cost tiles and tiles of other
 // shards (t % nshards != shard) are dropped; *n_out receives the number kept.
-// Cost = icost[t] (list length) or fcost[t].
+// Cost = icost[t] (list length) or fcost[t]. With tile_off, the tile-list
+// offsets are laid out first (list_offsets; icost = the list lengths).
 __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
                                                            const float* __restrict__ fcost, int* __restrict__ order,
                                                            int* __restrict__ n_out, int shard, int nshards,
-                                                           int* __restrict__ n_all_out) {
+                                                           int* __restrict__ n_all_out, int* __restrict__ tile_off = nullptr,
+                                                           int pool_cap = 0, int smem_cap = 0,
+                                                           int* __restrict__ stats = nullptr) {
     __shared__ int hist[256];
     __shared__ int offs[256];
     __shared__ int s_tail;
+    if (tile_off) list_offsets(tiles, icost, tile_off, pool_cap, smem_cap, stats);
     for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     auto bucket_of = [&](int t) -> int {

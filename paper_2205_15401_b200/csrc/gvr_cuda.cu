@@ -15,6 +15,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -68,6 +69,10 @@ bool is_device_ptr(const void* ptr) {
 
 }  // namespace
 
+// Tape flags buffer (ints): [0] dropped_behind, [1] nonfinite, [2..3] loss (double),
+// [kListStats .. +3] tile-list stats of the last render (list_offsets).
+constexpr int kListStats = 8;
+
 enum Stage {
     ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
 };
@@ -89,7 +94,8 @@ struct gvr_context {
     double guard = 0.02;
     bool precise = false;  // verification mode of the blend (gvr_context_set_precise)
     bool tile_profile = false;  // record per-tile selection cycles (gvr_context_set_tile_profile)
-    int tile_cap = 4096;  // per-tile candidate-list capacity
+    int list_smem = kSelListSmem;  // test hook: longest list sorted in shared memory
+    long long pool_override = 0;  // tile-list pool capacity in entries (test hook); 0 = automatic
     bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
@@ -135,8 +141,9 @@ struct gvr_tape {
     // per kernel
     Buf rec32, rec64;
     // per-tile candidate lists
-    Buf tile_count, tile_lists, tile_cycles;
-    int cap = 0;
+    Buf tile_count, tile_off, tile_fill, pool, sorted_pool, tile_cycles;
+    long long pool_hint = 0;  // entries the last observed render listed (grow-only sizing)
+    bool profiled = false;    // the last render recorded tile cycles
     Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
     // per pixel
     Buf topk, count, image, alpha, depth, topk_w, tape_t, ent;
@@ -285,10 +292,10 @@ unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads -
 
 template <int KMAX>
 int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
-    const size_t list_smem = sizeof(unsigned long long) * (size_t)fp.cap;
+    const size_t list_smem = sizeof(unsigned long long) * (size_t)kSelListSmem;
     if (KMAX <= 32) {
         auto kern = select_warp_kernel<KMAX>;
-        const size_t smem = sizeof(unsigned long long) * (size_t)std::min(fp.cap, kSelListSmem) +
+        const size_t smem = sizeof(unsigned long long) * (size_t)kSelListSmem +
                             sizeof(unsigned long long) * (8 / GVR_SEL_SPLIT) * kWarpListCap;  // + per-warp lists
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_SELECT);
@@ -586,8 +593,14 @@ void gvr_graph_destroy(gvr_graph* g) {
 }
 
 int gvr_context_set_tile_capacity(gvr_context* ctx, int cap) {
-    if (!ctx || cap < 1 || cap > (1 << 20)) return GVR_ERR_RUNTIME;
-    ctx->tile_cap = cap;
+    if (!ctx || cap < 0) return GVR_ERR_RUNTIME;
+    ctx->pool_override = cap;
+    return GVR_OK;
+}
+
+int gvr_context_set_list_smem(gvr_context* ctx, int n) {
+    if (!ctx || n < 0) return GVR_ERR_RUNTIME;
+    ctx->list_smem = std::min(n, kSelListSmem);
     return GVR_OK;
 }
 
@@ -727,6 +740,7 @@ int gvr_tape_create(gvr_context* ctx, gvr_tape** out) {
         delete t;
         return set_err(ctx, GVR_ERR_RUNTIME, "tape allocation failed");
     }
+    std::memset(t->h_flags, 0, 64);
     *out = t;
     return GVR_OK;
 }
@@ -734,7 +748,8 @@ int gvr_tape_create(gvr_context* ctx, gvr_tape** out) {
 void gvr_tape_destroy(gvr_tape* t) {
     if (!t) return;
     cudaStreamSynchronize(t->ctx->stream);
-    Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_lists, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
+    Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_off, &t->tile_fill, &t->pool, &t->sorted_pool,
+                   &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags};
     for (Buf* b : bufs) b->release();
@@ -814,11 +829,26 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
 
     CUDA_TRY(ctx, tape->rec32.ensure(sizeof(Rec32) * (size_t)(K > 0 ? K : 1)));
     CUDA_TRY(ctx, tape->rec64.ensure(sizeof(Rec64) * (size_t)(K > 0 ? K : 1)));
-    // Per-tile candidate-list capacity: lists beyond it are streamed (every
-    // kernel, exact tests, no early exit) instead of failing.
-    tape->cap = ctx->tile_cap;
-    CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * (size_t)tiles));
-    CUDA_TRY(ctx, tape->tile_lists.ensure(sizeof(unsigned long long) * (size_t)tiles * tape->cap));
+    // Tile lists live in one pool laid out by a count pass + scan. Its size is
+    // not known on the host before the render, so the pool is sized from an
+    // estimate and from the totals of earlier renders on this tape (grow-only);
+    // lists that do not fit are streamed (every kernel, exact tests, no early
+    // exit) and counted (gvr_tape_list_stats); host-synchronous renders grow
+    // the pool and re-render instead.
+    {
+        tape->pool_hint = std::max<long long>(tape->pool_hint, tape->h_flags[kListStats]);
+        const long long est = std::max<long long>(1 << 18, (4LL * K + 64LL * tiles) / nshards);
+        const long long want = std::max(est, tape->pool_hint + tape->pool_hint / 4);
+        if (!ctx->capturing || tape->pool.cap == 0)
+            CUDA_TRY(ctx, tape->pool.ensure(sizeof(unsigned long long) * (size_t)want));
+        if (!ctx->capturing || tape->sorted_pool.cap == 0)
+            CUDA_TRY(ctx, tape->sorted_pool.ensure(sizeof(unsigned long long) * (size_t)want));
+    }
+    const long long pool_cap = std::min<long long>(
+        {(long long)(tape->pool.cap / sizeof(unsigned long long)), (long long)(tape->sorted_pool.cap / sizeof(unsigned long long)),
+         0x7fffffffLL, ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL});
+    CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * 2 * (size_t)tiles));
+    CUDA_TRY(ctx, tape->tile_off.ensure(sizeof(int) * (size_t)tiles));
     CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 4 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
@@ -836,7 +866,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     int* order_f = sched + 2;
     float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
     CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 2 * sizeof(int), ctx->stream));
-    CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * (size_t)tiles, ctx->stream));
+    int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts: one memset
+    CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
     // bwd_cost[tiles], n_all, tile_done[tiles] (contiguous)
     CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (2 * (size_t)tiles + 1), ctx->stream));
 
@@ -854,8 +885,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         pp.rec32 = tape->rec32.as<Rec32>();
         pp.rec64 = tape->rec64.as<Rec64>();
         pp.tile_count = tile_count;
-        pp.tile_lists = tape->tile_lists.as<unsigned long long>();
-        pp.cap = tape->cap;
+        pp.shard = shard;
+        pp.nshards = nshards;
         pp.dropped_behind = dflags;
         {
             StageTimer st(ctx, ST_PROJECT);
@@ -869,13 +900,33 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         StageTimer st(ctx, ST_RANGES);
 #if GVR_ONE_ORDER  // one order (list length) for selection, blend and backward; then every other tile
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
-                                                        sched + 2 + 3 * (size_t)tiles);
+                                                        sched + 2 + 3 * (size_t)tiles, tape->tile_off.as<int>(),
+                                                        (int)pool_cap, ctx->list_smem, dflags + kListStats);
 #else
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
-                                                        nullptr);
+                                                        nullptr, tape->tile_off.as<int>(), (int)pool_cap, ctx->list_smem,
+                                                        dflags + kListStats);
 #endif
     }
     LAUNCH_CHECK(ctx);
+    if (K > 0) {
+        // K2 emit: fill the laid-out tile lists
+        EmitParams ep;
+        ep.K = K;
+        ep.rec32 = tape->rec32.as<Rec32>();
+        ep.H = H;
+        ep.W = W;
+        ep.tile = tile;
+        ep.tiles_x = tiles_x;
+        ep.tile_off = tape->tile_off.as<int>();
+        ep.tile_fill = tile_fill;
+        ep.pool = tape->pool.as<unsigned long long>();
+        {
+            StageTimer st(ctx, ST_EMIT);
+            emit_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(ep);
+        }
+        LAUNCH_CHECK(ctx);
+    }
     FwdParams fp;
     fp.cam = cp;
     fp.sel = sp;
@@ -897,8 +948,10 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.n_order_blend_all = sched + 2 + 3 * (size_t)tiles;
     fp.bwd_cost = bwd_cost;
     fp.tile_count = tile_count;
-    fp.tile_lists = tape->tile_lists.as<unsigned long long>();
-    fp.cap = tape->cap;
+    fp.tile_off = tape->tile_off.as<int>();
+    fp.pool = tape->pool.as<unsigned long long>();
+    fp.sorted_pool = tape->sorted_pool.as<unsigned long long>();
+    fp.list_smem = ctx->list_smem;
     fp.K = K;
     fp.rec32 = tape->rec32.as<Rec32>();
     fp.rec64 = tape->rec64.as<Rec64>();
@@ -916,6 +969,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.precise = ctx->precise ? 1 : 0;
     fp.tile_cycles = nullptr;
     fp.tile_done = GVR_PDL ? reinterpret_cast<unsigned*>(sched + 3 + 3 * (size_t)tiles) : nullptr;
+    tape->profiled = ctx->tile_profile;
     if (ctx->tile_profile) {
         CUDA_TRY(ctx, tape->tile_cycles.ensure(sizeof(long long) * (size_t)tiles));
         CUDA_TRY(ctx, cudaMemsetAsync(tape->tile_cycles.p, 0, sizeof(long long) * (size_t)tiles, ctx->stream));
@@ -933,6 +987,9 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     if (rc) return rc;
 
     tape->valid = true;
+    if (!ctx->capturing)  // sizing hint for the next render (read without a sync: a stale value is harmless)
+        CUDA_TRY(ctx, cudaMemcpyAsync(tape->h_flags + kListStats, dflags + kListStats, 4 * sizeof(int),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
 
     if (out) {
         bool host = false;
@@ -985,6 +1042,12 @@ extern "C" int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const 
     if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
     if (!host) return GVR_OK;
     if (int rc = sync_and_check(ctx)) return rc;
+    if (tape->h_flags[kListStats + 2] > 0 && ctx->pool_override == 0) {
+        // some tile lists did not fit the pool: size it from this render's total and render again
+        tape->pool_hint = std::max<long long>(tape->pool_hint, tape->h_flags[kListStats]);
+        if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
+        if (int rc = sync_and_check(ctx)) return rc;
+    }
     return check_finite(ctx, tape);
 }
 
@@ -1821,11 +1884,23 @@ int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* t, double* centers, dou
 int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* t, int64_t* cycles, int64_t n) {
     if (int rc = tape_ready(ctx, t)) return rc;
     const int64_t tiles = (int64_t)t->tiles_x * t->tiles_y;
-    if (!cycles || n != tiles || t->tile_cycles.cap < sizeof(long long) * (size_t)tiles)
+    if (!cycles || n != tiles || !t->profiled || t->tile_cycles.cap < sizeof(long long) * (size_t)tiles)
         return set_err(ctx, GVR_ERR_RUNTIME, "tile_cycles: render with the tile profile on, n = tiles_x * tiles_y");
     CUDA_TRY(ctx, cudaMemcpyAsync(cycles, t->tile_cycles.p, sizeof(long long) * (size_t)tiles, cudaMemcpyDefault,
                                   ctx->stream));
     return sync_and_check(ctx);
+}
+
+int gvr_tape_list_stats(gvr_context* ctx, const gvr_tape* t, int64_t* stats) {
+    if (!ctx || !t || !t->valid || !stats) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
+    CUDA_TRY(ctx, cudaMemcpyAsync(t->h_flags + kListStats, t->flags.as<int>() + kListStats, 4 * sizeof(int),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    for (int i = 0; i < 4; ++i) stats[i] = t->h_flags[kListStats + i];
+    stats[4] = std::min<long long>((long long)(t->pool.cap / sizeof(unsigned long long)),
+                                   ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL);
+    return GVR_OK;
 }
 
 int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* t, int32_t* count) {

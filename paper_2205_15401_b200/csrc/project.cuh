@@ -135,9 +135,8 @@ struct ProjectParams {
     int tiles_x, tiles_y;
     Rec32* rec32;
     Rec64* rec64;
-    int* tile_count;                 // [tiles] list lengths (zeroed before the launch)
-    unsigned long long* tile_lists;  // [tiles * cap] (order(zmin) << 32 | id), unsorted
-    int cap;                         // per-tile list capacity
+    int* tile_count;  // [tiles] list lengths (zeroed before the launch)
+    int shard, nshards;  // only tiles t with t % nshards == shard are binned (C4 tile sharding)
     int* dropped_behind;
 };
 
@@ -148,6 +147,20 @@ struct BinJob {
     int tr0 = 0, tc0 = 0, ntc = 1;
     unsigned long long key = 0;
 };
+
+// Tile rectangle of kernel k's box as a binning job (emit pass: from its record).
+__device__ __forceinline__ BinJob job_from_record(const Rec32& q, int k, int H, int W, int tile) {
+    BinJob job;
+    int tr0, tr1, tc0, tc1;
+    if (box_tiles(q, H, W, tile, tr0, tr1, tc0, tc1)) {
+        job.key = ((unsigned long long)float_order_bits(q.zmin) << 32) | (unsigned)k;
+        job.tr0 = tr0;
+        job.tc0 = tc0;
+        job.ntc = tc1 - tc0 + 1;
+        job.nt = (tr1 - tr0 + 1) * job.ntc;
+    }
+    return job;
+}
 
 __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     BinJob job;
@@ -296,23 +309,17 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
         q.bottom = __double2float_ru(fmin(bottom + mb, 1.0e30));
         q.left = __double2float_rd(fmax(left - ml, -1.0e30));
         q.right = __double2float_ru(fmin(right + mr, 1.0e30));
-        int tr0, tr1, tc0, tc1;
-        if (box_tiles(q, c.H, c.W, p.tile, tr0, tr1, tc0, tc1)) {
-            job.key = ((unsigned long long)float_order_bits(q.zmin) << 32) | (unsigned)k;
-            job.tr0 = tr0;
-            job.tc0 = tc0;
-            job.ntc = tc1 - tc0 + 1;
-            job.nt = (tr1 - tr0 + 1) * job.ntc;
-        }
+        job = job_from_record(q, k, c.H, c.W, p.tile);  // the emit pass recomputes the same rectangle
     }
     p.rec32[k] = q;
     return job;
 }
 
-// K1. Binning: every kernel appends (depth key, id) to the list of every tile
-// its box overlaps. Appends are warp-aggregated: lanes that hit the same tile
-// in the same round (neighbouring kernels usually do) share one atomicAdd on
-// the tile's counter, and four rounds of returned atomics are kept in flight.
+// K1. Projection + binning count pass: every kernel adds one to the counter of
+// every tile (of this shard) its box overlaps. The adds are warp-aggregated:
+// lanes that hit the same tile in the same round (neighbouring kernels usually
+// do) share one reduction on the tile's counter. The counts size the tile lists
+// (exclusive scan in order_tiles_kernel), which emit_kernel then fills.
 __global__ void project_kernel(ProjectParams p) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     BinJob job;
@@ -321,25 +328,57 @@ __global__ void project_kernel(ProjectParams p) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     for (int it0 = 0; __any_sync(FULL, it0 < job.nt); it0 += 4) {
-        int t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int it = it0 + u;
+            int t = it < job.nt ? (job.tr0 + it / job.ntc) * p.tiles_x + job.tc0 + it % job.ntc : -1;
+            if (t >= 0 && t % p.nshards != p.shard) t = -1;
+            const unsigned mk = __match_any_sync(FULL, t);
+            if (t >= 0 && (mk & lt) == 0) atomicAdd(p.tile_count + t, __popc(mk));
+        }
+    }
+}
+
+struct EmitParams {
+    int K;
+    const Rec32* rec32;
+    int H, W, tile, tiles_x;
+    const int* tile_off;        // [tiles] list offsets in the pool; -1: not listed (other shard / overflow)
+    int* tile_fill;             // [tiles] append cursors (zeroed before the launch)
+    unsigned long long* pool;   // tile lists, (order(zmin) << 32 | id), unsorted within a list
+};
+
+// K2. Binning emit pass: appends (depth key, id) to the list of every tile the
+// kernel's box overlaps (same rectangle as the count pass, recomputed from the
+// record), warp-aggregated returned atomics, four rounds in flight.
+__global__ void emit_kernel(EmitParams p) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    BinJob job;
+    if (k < p.K) job = job_from_record(p.rec32[k], k, p.H, p.W, p.tile);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int it0 = 0; __any_sync(FULL, it0 < job.nt); it0 += 4) {
+        int t[4], off[4], base[4];
         unsigned mk[4];
-        int base[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int it = it0 + u;
             t[u] = it < job.nt ? (job.tr0 + it / job.ntc) * p.tiles_x + job.tc0 + it % job.ntc : -1;
+            off[u] = t[u] >= 0 ? p.tile_off[t[u]] : -1;
+            if (off[u] < 0) t[u] = -1;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) mk[u] = __match_any_sync(FULL, t[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             base[u] = 0;
-            if (t[u] >= 0 && (mk[u] & lt) == 0) base[u] = atomicAdd(p.tile_count + t[u], __popc(mk[u]));
+            if (t[u] >= 0 && (mk[u] & lt) == 0) base[u] = atomicAdd(p.tile_fill + t[u], __popc(mk[u]));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int pos = __shfl_sync(FULL, base[u], __ffs(mk[u]) - 1) + __popc(mk[u] & lt);
-            if (t[u] >= 0 && pos < p.cap) p.tile_lists[(size_t)t[u] * p.cap + pos] = job.key;
+            if (t[u] >= 0) p.pool[(size_t)off[u] + pos] = job.key;
         }
     }
 }

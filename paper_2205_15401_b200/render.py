@@ -114,8 +114,12 @@ class Context:
         return Graph(self)
 
     def set_tile_capacity(self, cap: int) -> None:
-        """Test hook: per-tile candidate-list capacity (overflowing tiles stream every kernel)."""
+        """Test hook: tile-list pool capacity in entries, 0 = automatic (tiles whose list does not fit stream every kernel)."""
         self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
+
+    def set_list_smem(self, n: int) -> None:
+        """Test hook: tile lists longer than n (<= 2048) are sorted in global memory."""
+        self.check(self.lib.gvr_context_set_list_smem(self.handle, int(n)))
 
     def set_precise(self, on: bool = True) -> None:
         """Verification mode: FP64 exact traces and erfc in the blend (gradcheck)."""
@@ -273,6 +277,15 @@ class Tape:
         self.ctx.check(self.ctx.lib.gvr_tape_dropped_behind_camera(self.ctx.handle, self.handle, ctypes.byref(out)))
         return int(out.value)
 
+    def list_stats(self) -> dict:
+        """Tile-list layout of the taped render (gvr_tape_list_stats): listed entries, longest
+        list, tiles that overflowed the pool (streamed), lists sorted in global memory, pool capacity."""
+        out = np.zeros(5, dtype=np.int64)
+        self.ctx.check(self.ctx.lib.gvr_tape_list_stats(self.ctx.handle, self.handle,
+                                                        out.ctypes.data_as(ctypes.c_void_p)))
+        return {"entries": int(out[0]), "max_list": int(out[1]), "overflow_tiles": int(out[2]),
+                "global_sorted_tiles": int(out[3]), "pool_capacity": int(out[4])}
+
     def tile_cycles(self) -> np.ndarray:
         """[tiles_y, tiles_x] SM cycles of each 8x8 tile's selection CTA (needs Context.set_tile_profile)."""
         h, w, _, _ = self.shape()
@@ -334,8 +347,9 @@ def render_into(ctx: Context, dscene: DeviceScene, camera: Camera, cfg: Selectio
 
 
 def render_with_tape(scene, camera: Camera, cfg: SelectionConfig = SelectionConfig(), threads: int = 0, *,
-                     weights: bool = True, ctx: Optional[Context] = None) -> ForwardResult:
-    """``gvr::render_with_tape`` (grad.cpp:38-47): render and keep the tape for backward."""
+                     weights: bool = True, ctx: Optional[Context] = None, shard=(0, 1)) -> ForwardResult:
+    """``gvr::render_with_tape`` (grad.cpp:38-47): render and keep the tape for backward.
+    ``shard=(r, n)``: only tiles with index % n == r (C4 tile sharding; the rest stay empty)."""
     del threads
     ctx = ctx or default_context()
     dscene = _as_device_scene(scene, ctx)
@@ -348,7 +362,7 @@ def render_with_tape(scene, camera: Camera, cfg: SelectionConfig = SelectionConf
     tidx = np.empty((h, w, kp), dtype=np.int32) if weights else None
     tw = np.empty((h, w, kp)) if weights else None
     tape = Tape(ctx)
-    render_into(ctx, dscene, camera, cfg, tape, image, alpha, depth, tidx, tw)
+    render_into(ctx, dscene, camera, cfg, tape, image, alpha, depth, tidx, tw, shard=shard)
     tape.host_scene = scene if isinstance(scene, GaussianScene) else None
     return ForwardResult(RenderBuffers(image, alpha, depth, tidx, tw), tape)
 

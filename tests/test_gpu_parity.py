@@ -74,16 +74,38 @@ def test_forward_deterministic(ctx):
 
 
 def test_tile_list_overflow_path(golden, ctx):
-    """Tiles whose candidate list exceeds the capacity stream every kernel with
-    the same exact tests: outputs are bit-identical."""
-    a = gvr.render(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+    """Tiles whose candidate list does not fit the list pool stream every kernel
+    with the same exact tests: outputs are bit-identical."""
+    a = gvr.render_with_tape(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+    assert a.tape.list_stats()["overflow_tiles"] == 0
     ctx.set_tile_capacity(8)
     try:
-        b = gvr.render(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+        b = gvr.render_with_tape(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+        st = b.tape.list_stats()
     finally:
-        ctx.set_tile_capacity(4096)
-    assert np.array_equal(a.topk_idx, b.topk_idx)
-    assert np.array_equal(a.image, b.image)
+        ctx.set_tile_capacity(0)
+    if st["entries"] > 8:
+        assert st["overflow_tiles"] > 0
+    assert np.array_equal(a.buffers.topk_idx, b.buffers.topk_idx)
+    assert np.array_equal(a.buffers.image, b.buffers.image)
+
+
+def test_lists_sorted_in_global_memory(golden, ctx):
+    """Lists longer than the shared-memory stage are depth-sorted in the global
+    sorted pool (same bucket order, same early exit): bit-identical outputs."""
+    a = gvr.render_with_tape(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+    ctx.set_list_smem(1)
+    try:
+        b = gvr.render_with_tape(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+        st = b.tape.list_stats()
+    finally:
+        ctx.set_list_smem(2048)
+    assert st["overflow_tiles"] == 0
+    if st["max_list"] > 1:
+        assert st["global_sorted_tiles"] > 0
+    assert np.array_equal(a.buffers.topk_idx, b.buffers.topk_idx)
+    assert np.array_equal(a.buffers.image, b.buffers.image)
+    assert np.array_equal(a.buffers.topk_w, b.buffers.topk_w)
 
 
 def test_graph_replay_matches_eager(ctx):
