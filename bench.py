@@ -601,8 +601,35 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run
+    with N ranks (one process per GPU). Under torchrun WORLD_SIZE must equal N."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+            sys.exit(2)
+        return
+    if args.gpus <= 1 or args.impl == "reference":  # the reference arm runs on rank 0 only
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -221,6 +221,10 @@ int gvr_tape_cam_scene(gvr_context* ctx, const gvr_tape* tape, double* centers, 
 /* PixelKernelMap::dropped_behind_camera (tracer.hpp:39): kernels of the taped
  * render with camera-space z <= 1e-4. Synchronises. */
 int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* tape, int32_t* count);
+/* validate_finite (blender.cpp:132-134) for a render whose outputs stayed on the
+ * device: GVR_ERR_VALIDATION "image contains non-finite values" when any image,
+ * alpha or depth value of the taped render is not finite. Synchronises. */
+int gvr_tape_check_finite(gvr_context* ctx, gvr_tape* tape);
 /* Tile-list layout of the taped render (no reference counterpart; synchronises):
  * stats[0] listed (tile, kernel) entries, [1] longest tile list, [2] tiles whose
  * list did not fit the pool (streamed: every kernel, no early exit), [3] lists
@@ -254,6 +258,13 @@ int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* tape, const double* d_im
  * is the 1-based step count used for the bias corrections. */
 int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
                   int64_t step, double lr, double beta1, double beta2, double eps);
+
+/* As gvr_adam_step, with fit_shape's divergence rule (fit.cpp:246-250): when the
+ * device scalar *loss is not finite, or *diverged is already set, nothing is
+ * updated and *diverged (device int32) is set to 1. */
+int gvr_adam_step_guarded(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
+                          int64_t step, double lr, double beta1, double beta2, double eps, const double* loss,
+                          int32_t* diverged);
 
 /* ---- sampler and render-path helpers -------------------------------------- */
 /* gvr::sample_attributes (sampler.hpp:23-25, sampler.cpp:11-51): render (as

@@ -72,6 +72,8 @@ EXPORTED_SYMBOLS = (
     "gvr_tape_tile_cycles",
     "gvr_tape_list_stats",
     "gvr_context_set_list_smem",
+    "gvr_tape_check_finite",
+    "gvr_adam_step_guarded",
 )
 
 
@@ -172,6 +174,9 @@ def load() -> ctypes.CDLL:
         "gvr_tape_tile_cycles": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64]),
         "gvr_tape_list_stats": (ctypes.c_int, [vp, vp, vp]),
         "gvr_context_set_list_smem": (ctypes.c_int, [vp, ctypes.c_int]),
+        "gvr_tape_check_finite": (ctypes.c_int, [vp, vp]),
+        "gvr_adam_step_guarded": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp,
+                                                 vp, vp]),
         "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                                           ctypes.POINTER(i32)]),
         "gvr_scalar_loss": (ctypes.c_int, [vp, vp, vp, vp, dp, dp, vp, vp, vp]),

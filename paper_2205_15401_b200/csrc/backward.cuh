@@ -381,9 +381,16 @@ __global__ void axpy_kernel(long long n, const double* __restrict__ src, double*
 // AdamState::update (fit.cpp:20-42), bias corrections from the host in FP64.
 __global__ void adam_kernel(long long n, double* __restrict__ params, const double* __restrict__ grads,
                             double* __restrict__ m, double* __restrict__ v, double lr, double beta1, double beta2,
-                            double eps, double bc1, double bc2) {
+                            double eps, double bc1, double bc2, const double* __restrict__ loss = nullptr,
+                            int* __restrict__ diverged = nullptr) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
+    // fit_shape (fit.cpp:246-250): a non-finite loss ends the fit before the update;
+    // the device flag latches, so every later update is skipped as well
+    if (diverged && (*diverged || !isfinite(*loss))) {
+        if (i == 0) *diverged = 1;
+        return;
+    }
     const double g = grads[i];
     const double mi = beta1 * m[i] + (1.0 - beta1) * g;
     const double vi = beta2 * v[i] + (1.0 - beta2) * g * g;

@@ -998,6 +998,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             }
             for (; k < n; ++k) img = xadd(img, xmul(b_w[k * NP + g], p.attr[(long long)p.D * b_id[k * NP + g] + sub]));
             p.image[pix * p.Dc + sub] = img;
+            if (!isfinite(img)) atomicExch(p.nonfinite, 1);
         } else if (sub == 3) {
             if (p.D == 0) p.image[pix * p.Dc] = 0.0;
             double wsum = 0.0, wld = 0.0;
@@ -1030,7 +1031,9 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     const double depth = wsum > 1e-12 ? wld / wsum : 0.0;
     p.alpha[pix] = alpha;
     p.depth[pix] = depth;
-    if (!isfinite(alpha) || !isfinite(depth) || !isfinite(wsum)) atomicExch(p.nonfinite, 1);
+    bool bad = !isfinite(alpha) || !isfinite(depth) || !isfinite(wsum);
+    for (int c = 0; c < p.D && n > 0; ++c) bad = bad || !isfinite(p.image[pix * p.Dc + c]);
+    if (bad) atomicExch(p.nonfinite, 1);
 }
 
 // Tiles whose pixels selected nothing (zero blend cost) are not visited by the

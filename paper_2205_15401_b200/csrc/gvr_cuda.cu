@@ -535,17 +535,26 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
 
 // ---------------------------------------------------------------- ADAM (fit.cpp:20-42)
 
-int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
-                  int64_t step, double lr, double beta1, double beta2, double eps) {
+int gvr_adam_step_guarded(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
+                          int64_t step, double lr, double beta1, double beta2, double eps, const double* loss,
+                          int32_t* diverged) {
     if (!ctx || step < 1 || n < 0) return GVR_ERR_RUNTIME;
     if (n == 0) return GVR_OK;
     if (!is_device_ptr(params) || !is_device_ptr(grads) || !is_device_ptr(m) || !is_device_ptr(v))
         return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step needs device pointers");
+    if ((loss == nullptr) != (diverged == nullptr) || (loss && (!is_device_ptr(loss) || !is_device_ptr(diverged))))
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step_guarded needs device loss and diverged pointers");
     const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
     const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
-    adam_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, params, grads, m, v, lr, beta1, beta2, eps, bc1, bc2);
+    adam_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, params, grads, m, v, lr, beta1, beta2, eps, bc1, bc2,
+                                                             loss, diverged);
     LAUNCH_CHECK(ctx);
     return GVR_OK;
+}
+
+int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
+                  int64_t step, double lr, double beta1, double beta2, double eps) {
+    return gvr_adam_step_guarded(ctx, params, grads, m, v, n, step, lr, beta1, beta2, eps, nullptr, nullptr);
 }
 
 // ---------------------------------------------------------------- CUDA graphs
@@ -1055,6 +1064,7 @@ extern "C" {
 
 int gvr_tape_traced(gvr_context* ctx, const gvr_tape* t, int32_t* idx, double* l, double* q, double* sigma) {
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     const long long P = (long long)t->H * t->W;
     const int kp = t->cfg.k_prime;
     const size_t n = (size_t)P * kp;
@@ -1094,6 +1104,7 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
                             bool* host_out) {
     *host_out = false;
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!target_image || !target_alpha) return set_err(ctx, GVR_ERR_RUNTIME, "targets must not be null");
     const long long P = (long long)t->H * t->W;
     const int Dc = t->D > 1 ? t->D : 1;
@@ -1162,6 +1173,7 @@ int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* t, const double* d_image
 static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
                          const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate) {
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
         return set_err(ctx, GVR_ERR_RUNTIME, "the scene changed after the forward render");
     const gvr_scene* scene = t->scene;
@@ -1670,6 +1682,7 @@ int gvr_backward_views(gvr_context* ctx, int32_t n_views, gvr_tape* const* tapes
     };
     for (int v = 0; v < n_views; ++v) {
         if (!tapes[v] || !tapes[v]->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape %d is not valid", v);
+        if (tapes[v]->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
         if (!tapes[v]->has_upstream)
             return set_err(ctx, GVR_ERR_RUNTIME, "tape %d has no upstream gradient (gvr_scalar_loss_views first)", v);
         if (outs && !dev_ok(outs + v)) return set_err(ctx, GVR_ERR_RUNTIME, "gvr_backward_views needs device outputs");
@@ -1889,6 +1902,15 @@ int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* t, int64_t* cycles, i
     CUDA_TRY(ctx, cudaMemcpyAsync(cycles, t->tile_cycles.p, sizeof(long long) * (size_t)tiles, cudaMemcpyDefault,
                                   ctx->stream));
     return sync_and_check(ctx);
+}
+
+int gvr_tape_check_finite(gvr_context* ctx, gvr_tape* t) {
+    if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
+    if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
+    CUDA_TRY(ctx, cudaMemcpyAsync(t->h_flags + 1, t->flags.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    return check_finite(ctx, t);
 }
 
 int gvr_tape_list_stats(gvr_context* ctx, const gvr_tape* t, int64_t* stats) {

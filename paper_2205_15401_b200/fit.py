@@ -158,6 +158,7 @@ class Fitter:
         self.groups: List[Tuple[Tuple[float, float], list, list, list, list, object]] = [
             (w, cams, tis, tas, tapes, torch.zeros(len(cams), **f64)) for w, (cams, tis, tas, tapes) in groups.items()]
         self.loss_acc = torch.zeros(1, **f64)
+        self._diverged = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._lsum = [torch.zeros(1, **f64) for _ in self.groups]
         self.dscene = DeviceScene(ctx)
         # the per-iteration device work (upload + validation, all views fwd + loss
@@ -214,12 +215,25 @@ class Fitter:
             allreduce_gradients([self.grads, self.loss_acc], group)
             self.step_count += 1
             adam_step(self.ctx, self.params, self.grads, self.m, self.v, self.step_count, self.adam.lr,
-                      self.adam.beta1, self.adam.beta2, self.adam.eps)
+                      self.adam.beta1, self.adam.beta2, self.adam.eps, loss=self.loss_acc, diverged=self._diverged)
 
     def loss(self) -> float:
+        """Loss of the last loss_and_grad / step (synchronises). Raises ValidationError
+        like the reference's render would: invalid parameters (deferred scene
+        validation) or non-finite render outputs (blender.cpp:132-134)."""
         self.stream.synchronize()
         self.dscene.check()  # the deferred validation of the last upload
+        for group in self.groups:
+            for tape in group[4]:
+                tape.check_finite()
         return float(self.loss_acc.item())
+
+    @property
+    def diverged(self) -> bool:
+        """FitReport::diverged (fit.cpp:248): a step saw a non-finite loss; the
+        parameters stay as they were before it (every later update is skipped)."""
+        self.stream.synchronize()
+        return bool(self._diverged.item())
 
     def scene(self) -> GaussianScene:
         return GaussianScene(self.centers.cpu().numpy().copy(), self.inv_cov.cpu().numpy().copy(),

@@ -277,6 +277,11 @@ class Tape:
         self.ctx.check(self.ctx.lib.gvr_tape_dropped_behind_camera(self.ctx.handle, self.handle, ctypes.byref(out)))
         return int(out.value)
 
+    def check_finite(self) -> None:
+        """validate_finite (blender.cpp:132-134) of a render with device outputs:
+        raises ValidationError("image contains non-finite values")."""
+        self.ctx.check(self.ctx.lib.gvr_tape_check_finite(self.ctx.handle, self.handle))
+
     def list_stats(self) -> dict:
         """Tile-list layout of the taped render (gvr_tape_list_stats): listed entries, longest
         list, tiles that overflowed the pool (streamed), lists sorted in global memory, pool capacity."""
@@ -412,10 +417,18 @@ def backward_into(tape: Tape, d_image, d_alpha, flags: GradFlags = GradFlags(), 
 
 
 def adam_step(ctx: Context, params, grads, m, v, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
-              eps: float = 1e-8) -> None:
-    """``AdamState::update`` (fit.cpp:20-42) on device tensors (FP64, same length)."""
-    ctx.check(ctx.lib.gvr_adam_step(ctx.handle, _ptr(params), _ptr(grads), _ptr(m), _ptr(v), int(params.numel()),
-                                    int(step), float(lr), float(beta1), float(beta2), float(eps)))
+              eps: float = 1e-8, loss=None, diverged=None) -> None:
+    """``AdamState::update`` (fit.cpp:20-42) on device tensors (FP64, same length).
+    With ``loss`` (device FP64 scalar) and ``diverged`` (device int32 flag), the update
+    follows fit_shape's divergence rule (fit.cpp:246-250): a non-finite loss skips it
+    and latches the flag."""
+    if loss is None:
+        ctx.check(ctx.lib.gvr_adam_step(ctx.handle, _ptr(params), _ptr(grads), _ptr(m), _ptr(v), int(params.numel()),
+                                        int(step), float(lr), float(beta1), float(beta2), float(eps)))
+        return
+    ctx.check(ctx.lib.gvr_adam_step_guarded(ctx.handle, _ptr(params), _ptr(grads), _ptr(m), _ptr(v),
+                                            int(params.numel()), int(step), float(lr), float(beta1), float(beta2),
+                                            float(eps), _ptr(loss), _ptr(diverged)))
 
 
 def backward(tape, d_image, d_alpha, flags: GradFlags = GradFlags()) -> GradientBundle:

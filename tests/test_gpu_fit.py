@@ -239,3 +239,57 @@ def test_deferred_validation_is_rechecked_after_graph_replays(ctx):
         c[5, 0] = 0.0
         g.launch()
         ds.check()
+
+
+def test_device_render_reports_non_finite_outputs(ctx):
+    """validate_finite (blender.cpp:132-134) for renders into device buffers:
+    Tape.check_finite raises the reference's message (image channels included).
+    A deferred upload renders the values as they are, so a NaN attribute reaches
+    the image while the geometry (alpha, depth) stays finite."""
+    import torch
+    dev = torch.device("cuda:0")
+    scene = gvr.make_bench_scene(200)
+    cam = gvr.make_bench_camera(32)
+    attr = torch.tensor(scene.attr, device=dev)
+    attr[:, 1] = float("nan")
+    ds = gvr.DeviceScene(ctx)
+    ds.set_raw(scene.size, 3, scene.tau, torch.tensor(scene.centers, device=dev),
+               torch.tensor(scene.inv_cov, device=dev), attr, deferred=True)
+    tape = gvr.Tape(ctx)
+    img = torch.empty((32, 32, 3), dtype=torch.float64, device=dev)
+    alpha = torch.empty((32, 32, 1), dtype=torch.float64, device=dev)
+    gvr.render_into(ctx, ds, cam, SelectionConfig(), tape, img, alpha)
+    assert torch.isfinite(alpha).all() and not torch.isfinite(img).all()
+    with pytest.raises(ValidationError, match="image contains non-finite values"):
+        tape.check_finite()
+    ok = gvr.Tape(ctx)
+    gvr.render_into(ctx, gvr.DeviceScene(ctx).set(scene), cam, SelectionConfig(), ok, img)
+    ok.check_finite()
+
+
+def test_objects_of_another_context_are_rejected(ctx):
+    other = gvr.Context(0)
+    fr = gvr.render_with_tape(gvr.make_bench_scene(200), gvr.make_bench_camera(24), ctx=other)
+    with pytest.raises(gvr.GvrRuntimeError, match="another context"):
+        ctx.check(ctx.lib.gvr_backward(ctx.handle, fr.tape.handle, None, None, None, None))
+    with pytest.raises(gvr.GvrRuntimeError, match="another context"):
+        ctx.check(ctx.lib.gvr_tape_traced(ctx.handle, fr.tape.handle, None, None, None, None))
+
+
+def test_fitter_stops_updating_after_a_non_finite_loss(ctx):
+    """fit_shape (fit.cpp:246-250): a non-finite loss ends the fit before the
+    update -- the device ADAM step is skipped and the divergence latches."""
+    target = gvr.make_bench_scene(300)
+    views = make_fit_views(target, 2, 32, ctx=ctx)
+    start = target.copy()
+    start.attr[:] = 1e200  # finite image, overflowing loss
+    fitter = Fitter(ctx, start, views, adam=AdamConfig(lr=0.01))
+    p0 = fitter.params.cpu().numpy().copy()
+    fitter.step()
+    fitter.step()
+    assert fitter.diverged
+    assert not np.isfinite(fitter.loss())
+    assert np.array_equal(fitter.params.cpu().numpy(), p0)
+    healthy = Fitter(ctx, target, views, adam=AdamConfig(lr=0.01))
+    healthy.step()
+    assert not healthy.diverged
