@@ -153,9 +153,11 @@ int gvr_context_set_tile_profile(gvr_context* ctx, int on);
 /* Per-tile selection cycles of a render made with the tile profile on
  * (n = tiles_x * tiles_y of the tape; 0 for tiles with nothing to select). */
 int gvr_tape_tile_cycles(gvr_context* ctx, const gvr_tape* tape, int64_t* cycles, int64_t n);
-/* Test hook: caps the tile-list pool at `cap` entries (8 B each; 0 = automatic
- * sizing). Lists that do not fit stream every kernel through the same exact
- * tests (slower, same results); a small value exercises that path in tests. */
+/* Test hook: caps the tile-list pool and the backward's mask rectangles at `cap`
+ * entries (8 B each; 0 = automatic sizing). Lists that do not fit stream every
+ * kernel through the same exact tests (slower, same selection); kernels without a
+ * mask rectangle take the backward's atomic fallback (same gradients within
+ * rounding, not bit-deterministic). A small value exercises both paths in tests. */
 int gvr_context_set_tile_capacity(gvr_context* ctx, int cap);
 /* Test hook: tile lists longer than n entries (default and maximum 2048) are
  * sorted in global memory instead of shared memory. Results must not change. */
@@ -228,7 +230,9 @@ int gvr_tape_check_finite(gvr_context* ctx, gvr_tape* tape);
 /* Tile-list layout of the taped render (no reference counterpart; synchronises):
  * stats[0] listed (tile, kernel) entries, [1] longest tile list, [2] tiles whose
  * list did not fit the pool (streamed: every kernel, no early exit), [3] lists
- * longer than the shared-memory stage (sorted in global memory), [4] pool capacity. */
+ * longer than the shared-memory stage (sorted in global memory), [4] pool capacity,
+ * [5] backward mask-rectangle tiles requested, [6] mask capacity (kernels beyond it
+ * take the non-deterministic atomic fallback). */
 int gvr_tape_list_stats(gvr_context* ctx, const gvr_tape* tape, int64_t* stats);
 /* Shape of the taped render. */
 int gvr_tape_shape(const gvr_tape* tape, int32_t* height, int32_t* width, int32_t* k_prime,

@@ -21,9 +21,54 @@ struct BwdParams {
     const double* attr;     // [K*D]
     const double* d_image;  // [P*D]
     const double* d_alpha;  // [P]
+    const int4* kinfo;           // [K] mask rectangle of each kernel (project_kernel)
+    const unsigned long long* masks;  // per (kernel, tile): pixels of the tile that selected the kernel
+    const int* slot_off;              // per (kernel, tile): first record of its pixels (appearance_kernel)
+    double4* bent;                    // records, 2 x 32 B: {d_l, d_q, d_sigma, W} {ray, pixel}
+    // fallback for kernels without a mask rectangle (mask pool full): FP64 atomics
     double* acc;            // [K*9] camera space: dm(3), dS upper (00 01 02 11 12 22)
-    double* d_attr;         // [K*D]
+    double* attr_fb;        // [K*D]
 };
+
+// Chain of one selected entry to camera space (grad.cpp:150-170): with a = d.Sd,
+// l = d.Sm / a, v = m - l d, sigma = a^-1/2:
+//   dm = (d_l / a) S d - d_q S v
+//   dS = (d_l / a)(0.5 (m d^T + d m^T) - l d d^T) - 0.5 d_q v v^T - 0.5 sigma^3 d_sigma d d^T
+// dS as its upper triangle (00 01 02 11 12 22).
+__device__ __forceinline__ void chain_entry(const Rec64& r, const double* d, double dl, double dq, double dsg,
+                                            double* dm, double* ds) {
+    double sd[3], v[3], sv[3];
+    const double s00 = r.s[0], s01 = r.s[1], s02 = r.s[2], s11 = r.s[4], s12 = r.s[5], s22 = r.s[8];
+    sd[0] = fma(s00, d[0], fma(s01, d[1], s02 * d[2]));
+    sd[1] = fma(s01, d[0], fma(s11, d[1], s12 * d[2]));
+    sd[2] = fma(s02, d[0], fma(s12, d[1], s22 * d[2]));
+    const double a = fma(d[0], sd[0], fma(d[1], sd[1], d[2] * sd[2]));
+    const double ia = 1.0 / a;
+    const double l = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2])) * ia;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) v[t] = fma(-l, d[t], r.m[t]);
+    sv[0] = fma(s00, v[0], fma(s01, v[1], s02 * v[2]));
+    sv[1] = fma(s01, v[0], fma(s11, v[1], s12 * v[2]));
+    sv[2] = fma(s02, v[0], fma(s12, v[1], s22 * v[2]));
+    const double scale = dl * ia;
+    const double d_a = -0.5 * ia * sqrt(ia) * dsg;  // -0.5 sigma^3 d_sigma, sigma = a^-1/2
+#pragma unroll
+    for (int t = 0; t < 3; ++t) dm[t] = scale * sd[t] - dq * sv[t];
+    const int rr[6] = {0, 0, 0, 1, 1, 2};
+    const int cc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+        const int a0 = rr[t], a1 = cc[t];
+        const double ddt = d[a0] * d[a1];
+        ds[t] = scale * (0.5 * (r.m[a0] * d[a1] + d[a0] * r.m[a1]) - l * ddt) - 0.5 * dq * (v[a0] * v[a1]) + d_a * ddt;
+    }
+}
+
+// Entry of a kernel without a mask rectangle (the mask pool was full): FP64
+// atomics into camera-space accumulators, consumed by the gather (rare; kept
+// out of line so it costs the hot loop no registers).
+__device__ __noinline__ void backward_fallback(const Rec64* rec, double* acc, double* attr_fb, const double* dimg, int D,
+                                               const double* d, double dl, double dq, double dsg, double w);
 
 // Per pixel (grad.cpp:75-174). CTA = one 8x8 tile, 4 threads per pixel (256
 // threads): the pixel's entries are split 4 ways in every pass, which cuts the
@@ -99,16 +144,6 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         } else {
             for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * k + c];
         }
-        const double w = trans * pk;
-        if (w != 0.0 || dw != 0.0) {
-            if (p.D <= 4) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c < p.D) atomicAdd(&p.d_attr[(long long)p.D * k + c], w * dimg[c]);
-            } else {
-                for (int c = 0; c < p.D; ++c) atomicAdd(&p.d_attr[(long long)p.D * k + c], w * p.d_image[pix * p.D + c]);
-            }
-        }
         b_lda[s * NP + g] = make_double2(er.l - l0, (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0);
         b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
         b_pi[s * NP + g] = make_float2(pkf, er.is);
@@ -174,56 +209,54 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         dl += dl2;
         dsg += dsg2;
         const double dq = dpk * pke;
-        if (dl == 0.0 && dq == 0.0 && dsg == 0.0) continue;
-
-        const Rec64 r = p.rec64[kid];
-        double sd[3], v[3], sv[3];
-        const double s00 = r.s[0], s01 = r.s[1], s02 = r.s[2], s11 = r.s[4], s12 = r.s[5], s22 = r.s[8];
-        sd[0] = fma(s00, d[0], fma(s01, d[1], s02 * d[2]));
-        sd[1] = fma(s01, d[0], fma(s11, d[1], s12 * d[2]));
-        sd[2] = fma(s02, d[0], fma(s12, d[1], s22 * d[2]));
-        const double a = fma(d[0], sd[0], fma(d[1], sd[1], d[2] * sd[2]));
-        const double l = fma(d[0], r.sm[0], fma(d[1], r.sm[1], d[2] * r.sm[2])) / a;
-#pragma unroll
-        for (int t = 0; t < 3; ++t) v[t] = fma(-l, d[t], r.m[t]);
-        sv[0] = fma(s00, v[0], fma(s01, v[1], s02 * v[2]));
-        sv[1] = fma(s01, v[0], fma(s11, v[1], s12 * v[2]));
-        sv[2] = fma(s02, v[0], fma(s12, v[1], s22 * v[2]));
-        const double scale = dl / a;
-        const double sigma = 1.0 / sqrt(a);
-        const double d_a = -0.5 * sigma * sigma * sigma * dsg;
-        double* acc = p.acc + 9ll * kid;
-        // dm = (d_l/a) S d - d_q S v
-#pragma unroll
-        for (int t = 0; t < 3; ++t) atomicAdd(acc + t, scale * sd[t] - dq * sv[t]);
-        // dS = (d_l/a)(0.5 (m d^T + d m^T) - l d d^T) - 0.5 d_q v v^T + d_a d d^T  (upper triangle)
-        const int rr[6] = {0, 0, 0, 1, 1, 2};
-        const int cc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-            const int a0 = rr[t], a1 = cc[t];
-            const double ddt = d[a0] * d[a1];
-            const double val = scale * (0.5 * (r.m[a0] * d[a1] + d[a0] * r.m[a1]) - l * ddt) -
-                               0.5 * dq * (v[a0] * v[a1]) + d_a * ddt;
-            atomicAdd(acc + 3 + t, val);
+        const double w = p.tape_t[pix * p.kp + e] * pke;  // W_e (the forward's weight)
+        const int4 ki = p.kinfo[kid];
+        if (ki.x >= 0) {
+            // deterministic path: the entry's adjoints go to its record in the
+            // kernel's block: the slot's first record + the pixel's rank in the mask
+            const int slot = ki.x + (i / TILE - (ki.y >> 16)) * ki.z + (j / TILE - (ki.y & 0xffff));
+            const int bit = (i % TILE) * TILE + j % TILE;
+            const int rec = p.slot_off[slot] + __popcll(p.masks[slot] & ((1ull << bit) - 1ull));
+            p.bent[2ll * rec] = make_double4(dl, dq, dsg, w);
+            p.bent[2ll * rec + 1] = make_double4(d[0], d[1], d[2], __longlong_as_double((pix << 32) | (unsigned)kid));
+            continue;
         }
+        backward_fallback(p.rec64 + kid, p.acc + 9ll * kid, p.attr_fb + (long long)p.D * kid,
+                          p.d_image + pix * p.D, p.D, d, dl, dq, dsg, w);
     }
 }
 
-struct ObjParams {
-    int K;
-    CameraP cam;
-    const double* acc;      // [K*9]
-    const double* centers;  // object space
-    const double* inv_cov;  // object space
-    double* d_center;       // [K*3]
-    double* d_inv_cov;      // [K*9]
-    double* d_rt;           // [12] = d_rotation(9) d_translation(3), accumulated
-};
+__device__ __noinline__ void backward_fallback(const Rec64* rec, double* acc, double* attr_fb, const double* dimg, int D,
+                                               const double* d, double dl, double dq, double dsg, double w) {
+    if (w != 0.0)
+        for (int c = 0; c < D; ++c) atomicAdd(attr_fb + c, w * dimg[c]);
+    if (dl == 0.0 && dq == 0.0 && dsg == 0.0) return;
+    double dmv[3], dsv[6];
+    chain_entry(*rec, d, dl, dq, dsg, dmv, dsv);
+    for (int t = 0; t < 3; ++t) atomicAdd(acc + t, dmv[t]);
+    for (int t = 0; t < 6; ++t) atomicAdd(acc + 3 + t, dsv[t]);
+}
 
-// K5: camera -> object space once per kernel (grad.cpp:184-197):
-// d_center = R^T dm, d_inv_cov = R^T dS R, d_T = sum dm, d_R = sum dm m^T + 2 dS R S.
-constexpr int kObjThreads = 128;
+// Position of the r-th (0-based) set bit of m (r < popc(m)): popc binary search.
+__device__ __forceinline__ int select_bit64(unsigned long long m, int r) {
+    unsigned w = (unsigned)m;
+    int pos = 0, c = __popc(w);
+    if (r >= c) {
+        r -= c;
+        w = (unsigned)(m >> 32);
+        pos = 32;
+    }
+#pragma unroll
+    for (int width = 16; width >= 1; width >>= 1) {
+        c = __popc(w & ((1u << width) - 1u));
+        if (r >= c) {
+            r -= c;
+            w >>= width;
+            pos += width;
+        }
+    }
+    return pos;
+}
 
 // Block-contiguous rows of `width` doubles staged through shared memory so the
 // global side is coalesced 16-byte traffic (rows are 24 / 72 bytes apart).
@@ -251,92 +284,336 @@ __device__ __forceinline__ void stage_rows_out(double* __restrict__ dst, const d
     }
 }
 
-__global__ void __launch_bounds__(kObjThreads) object_space_kernel(ObjParams p) {
-    __shared__ __align__(16) double s_acc[kObjThreads * 9];
-    __shared__ __align__(16) double s_cov[kObjThreads * 9];
-    __shared__ __align__(16) double s_ctr[kObjThreads * 3];
-    const int k0 = blockIdx.x * kObjThreads;
-    const int count = min(kObjThreads, p.K - k0);
-    stage_rows_in(s_acc, p.acc, k0, count, 9);
+__device__ __forceinline__ void prefetch_l1(const void* ptr, int offset = 0) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(ptr) + offset));
+}
+
+// Position of the j-th (0-based) set bit of m (j < popc(m)).
+__device__ __forceinline__ int select_bit32(unsigned m, int j) {
+    int pos = 0;
+#pragma unroll
+    for (int width = 16; width >= 1; width >>= 1) {
+        const int c = __popc(m & ((1u << width) - 1u));
+        if (j >= c) {
+            j -= c;
+            m >>= width;
+            pos += width;
+        }
+    }
+    return pos;
+}
+
+// ---------------------------------------------------------------- deterministic backward layout
+// Kernel k's selected (pixel, entry) pairs are the set bits of its mask
+// rectangle (set by the blend). Records are laid out in kernel order, and
+// inside a kernel in (tile row-major, pixel) order: an exclusive scan of the
+// per-kernel counts (K4a/b/c: counts + CTA sums, CTA-sum scan, offsets), so
+// the layout is a pure function of the selection.
+constexpr int kScanThreads = 256;
+
+struct AppParams {
+    int K;
+    const int4* kinfo;
+    const unsigned long long* masks;
+    const int* count;  // [K] records of each kernel (the blend's counts)
+    int* cta_sum;    // [ceil(K / kScanThreads)] then exclusive offsets (in place)
+    int* slot_off;   // [mask slots] first record of each (kernel, tile)
+    int2* app;       // [K] {first record, count}
+    int* total;      // records of the render
+};
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* total) {
+    __shared__ int s_warp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        int w = lane < nw ? s_warp[lane] : 0, wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < nw) s_warp[lane] = wi - w;
+        if (lane == nw - 1) s_warp[31] = wi;  // nw <= 31 for blocks <= 992 threads
+    }
+    __syncthreads();
+    const int out = s_warp[warp] + incl - v;
+    if (total) *total = s_warp[31];
+    __syncthreads();
+    return out;
+}
+
+__global__ void __launch_bounds__(kScanThreads) count_kernel(AppParams p) {
+    const int k = blockIdx.x * kScanThreads + threadIdx.x;
+    const int c = k < p.K ? p.count[k] : 0;  // counted by the blend
+    int tot;
+    block_exclusive_scan(c, &tot);
+    if (threadIdx.x == 0) p.cta_sum[blockIdx.x] = tot;
+}
+
+// exclusive scan of the CTA sums in place (one CTA of 1024 threads, chunks per thread)
+__global__ void __launch_bounds__(1024) cta_scan_kernel(AppParams p, int n) {
+    const int chunk = (n + 1023) / 1024;
+    const int t0 = min(n, (int)threadIdx.x * chunk), t1 = min(n, t0 + chunk);
+    int run = 0;
+    for (int t = t0; t < t1; ++t) run += p.cta_sum[t];
+    int tot;
+    int off = block_exclusive_scan(run, &tot);
+    for (int t = t0; t < t1; ++t) {
+        const int v = p.cta_sum[t];
+        p.cta_sum[t] = off;
+        off += v;
+    }
+    if (threadIdx.x == 0) *p.total = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
+    const int k = blockIdx.x * kScanThreads + threadIdx.x;
+    const int c = k < p.K ? p.count[k] : 0;
+    const int off = p.cta_sum[blockIdx.x] + block_exclusive_scan(c, nullptr);
+    if (k >= p.K) return;
+    p.app[k] = make_int2(off, c);
+    if (c > 0) {
+        const int4 ki = p.kinfo[k];
+        int run = off;
+        for (int t = 0; t < ki.w; ++t) {
+            p.slot_off[ki.x + t] = run;
+            run += __popcll(p.masks[ki.x + t]);
+        }
+    }
+}
+
+constexpr int kRecThreads = 128;
+
+// K5a: one thread per record (grid-stride over 32-record windows, one warp per
+// window): the entry's chain to camera space (chain_entry) and its attribute
+// term, then a segmented reduction of the window by kernel (shfl_down over
+// equal keys: a fixed tree given the layout). The first lane of each kernel's
+// piece writes it to pieces[k + window] -- injective, because records are in
+// kernel order, so a kernel's pieces are consecutive in window order.
+struct GatherParams {
+    int K, D, nv;           // nv = 9 + D values per piece
+    CameraP cam;
+    const int4* kinfo;
+    const int2* app;        // [K] {first record, count}
+    const int* total;       // records of the render
+    const double4* bent;    // records, 2 x 32 B: {d_l, d_q, d_sigma, W} {ray, pixel << 32 | kernel}
+    const Rec64* rec64;
+    const double* d_image;  // [P*D]
+    double* pieces;         // [(K + windows) * nv]
+    double* acc;            // fallback accumulators (consumed and re-zeroed by K5b)
+    double* attr_fb;
+    const double* centers;  // object space
+    const double* inv_cov;
+    double* d_center;       // [K*3]
+    double* d_inv_cov;      // [K*9]
+    double* d_attr;         // [K*D]
+    double* rt_part;        // [gridDim.x * 12] then [groups * 12]
+    unsigned* tickets;      // [1 + groups], zero between launches (reset by the last CTAs)
+    double* d_rt;           // [12] d_rotation (9), d_translation (3)
+};
+
+__global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
+    // per warp: the window's record values [32][nv], summed per kernel piece by
+    // one lane each, rows in record order
+    extern __shared__ __align__(16) double s_rows[];
+    const int lane = threadIdx.x & 31;
+    double* rows = s_rows + (threadIdx.x >> 5) * 32 * p.nv;
+    __shared__ int s_keys[kRecThreads / 32][32];
+    int* keys = s_keys[threadIdx.x >> 5];
+    const int n_rec = *p.total;
+    const int windows = (n_rec + 31) >> 5;
+    const int wstride = (gridDim.x * blockDim.x) >> 5;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < windows; w += wstride) {
+        const int r = 32 * w + lane;
+        const bool valid = r < n_rec;
+        int k = -1;
+        if (valid) {
+            const double4 b = p.bent[2ll * r];
+            const double4 ray = p.bent[2ll * r + 1];
+            const long long bits = __double_as_longlong(ray.w);
+            k = (int)(bits & 0xffffffffll);
+            const long long pix = bits >> 32;
+            double* row = rows + lane * p.nv;
+            // upstream image gradient loads issued before the chain (D <= 4 unrolled)
+            double di[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) di[c] = c < p.D ? p.d_image[pix * p.D + c] : 0.0;
+            double v[9];
+            const double d[3] = {ray.x, ray.y, ray.z};
+            chain_entry(p.rec64[k], d, b.x, b.y, b.z, v, v + 3);
+#pragma unroll
+            for (int u = 0; u < 9; ++u) row[u] = v[u];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < p.D) row[9 + c] = b.w * di[c];
+            for (int c = 4; c < p.D; ++c) row[9 + c] = b.w * p.d_image[pix * p.D + c];
+        }
+        keys[lane] = k;
+        const int kprev = __shfl_up_sync(0xffffffffu, k, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || kprev != k));
+        const int nvalid = min(32, n_rec - 32 * w);
+        __syncwarp();
+        // piece sums: (piece, value) tasks over the lanes, each summing its rows
+        // in record order
+        const int npieces = __popc(heads);
+        for (int task = lane; task < npieces * p.nv; task += 32) {
+            const int j = task / p.nv, u = task - j * p.nv;
+            const int start = select_bit32(heads, j);
+            const int end = j + 1 < npieces ? select_bit32(heads, j + 1) : nvalid;
+            double acc = 0.0;
+            for (int q = start; q < end; ++q) acc += rows[q * p.nv + u];
+            p.pieces[(long long)(keys[start] + w) * p.nv + u] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+// K5b: per kernel, its pieces summed in window order, then camera -> object
+// space (grad.cpp:184-197):
+//   d_center = R^T dm, d_inv_cov = R^T dS R, d_T = sum dm, d_R = sum dm m^T + 2 dS R S.
+// d_R, d_T: CTA partial in kernel order -> group of kRtGroup CTAs -> total,
+// each in a fixed order (tickets: the last CTA of a level reduces it).
+constexpr int kFinishThreads = 128, kRtGroup = 32;
+
+__global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) {
+    __shared__ double s_part[kFinishThreads / 32][12];
+    __shared__ bool s_last;
+    // object-space rows staged through shared memory (coalesced 16-byte traffic)
+    __shared__ __align__(16) double s_cov[kFinishThreads * 9];
+    __shared__ __align__(16) double s_ctr[kFinishThreads * 3];
+    const int k0 = blockIdx.x * kFinishThreads;
+    const int count = min(kFinishThreads, p.K - k0);
     stage_rows_in(s_cov, p.inv_cov, k0, count, 9);
     stage_rows_in(s_ctr, p.centers, k0, count, 3);
     __syncthreads();
-    const int t0 = threadIdx.x;
-    const int k = k0 + t0;
-    double part[12], dc[3] = {0.0, 0.0, 0.0}, dcov[9];
+    const int k = k0 + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double part[12];
 #pragma unroll
     for (int t = 0; t < 12; ++t) part[t] = 0.0;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) dcov[t] = 0.0;
     if (k < p.K) {
-        const double* a = s_acc + 9 * t0;
-        const double dm[3] = {a[0], a[1], a[2]};
-        const double ds[9] = {a[3], a[4], a[5], a[4], a[6], a[7], a[5], a[7], a[8]};
-        const double* R = p.cam.R;
+        const int2 ap = p.app[k];
+        const int4 ki = p.kinfo[k];
+        double c9[9];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) dc[r] = R[r] * dm[0] + R[3 + r] * dm[1] + R[6 + r] * dm[2];
-        // T1 = dS R; out = R^T T1 (symmetric: compute upper, mirror)
-        double t1[9];
+        for (int u = 0; u < 9; ++u) c9[u] = 0.0;
+        if (ap.y > 0) {
+            const int w0 = ap.x >> 5, w1 = (ap.x + ap.y - 1) >> 5;
+            for (int w = w0; w <= w1; ++w) {
+                const double* src = p.pieces + (long long)(k + w) * p.nv;
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) t1[3 * r + c] = ds[3 * r] * R[c] + ds[3 * r + 1] * R[3 + c] + ds[3 * r + 2] * R[6 + c];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = r; c < 3; ++c) {
-                const double val = R[r] * t1[c] + R[3 + r] * t1[3 + c] + R[6 + r] * t1[6 + c];
-                dcov[3 * r + c] = val;
-                dcov[3 * c + r] = val;
+                for (int u = 0; u < 9; ++u) c9[u] += src[u];
             }
-        // d_R += dm m_obj^T + 2 (dS R) S_obj
-        const double* mo = s_ctr + 3 * t0;
-        const double* so = s_cov + 9 * t0;
+            for (int c = 0; c < p.D; ++c) {
+                double a = 0.0;
+                for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 9 + c];
+                p.d_attr[(long long)p.D * k + c] = a;
+            }
+        } else if (ki.x < 0 && ki.w > 0) {  // fallback accumulators (no mask rectangle): consume, re-zero
+#pragma unroll
+            for (int u = 0; u < 9; ++u) {
+                c9[u] = p.acc[9ll * k + u];
+                p.acc[9ll * k + u] = 0.0;
+            }
+            for (int c = 0; c < p.D; ++c) {
+                p.d_attr[(long long)p.D * k + c] = p.attr_fb[(long long)p.D * k + c];
+                p.attr_fb[(long long)p.D * k + c] = 0.0;
+            }
+        } else {
+            for (int c = 0; c < p.D; ++c) p.d_attr[(long long)p.D * k + c] = 0.0;
+        }
+        const double* R = p.cam.R;
+        const double dsf[9] = {c9[3], c9[4], c9[5], c9[4], c9[6], c9[7], c9[5], c9[7], c9[8]};
+        double dc[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dc[r] = R[r] * c9[0] + R[3 + r] * c9[1] + R[6 + r] * c9[2];
+        double t1[9];  // dS R
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-                part[3 * r + c] = dm[r] * mo[c] +
-                                  2.0 * (t1[3 * r] * so[c] + t1[3 * r + 1] * so[3 + c] + t1[3 * r + 2] * so[6 + c]);
+                t1[3 * r + c] = dsf[3 * r] * R[c] + dsf[3 * r + 1] * R[3 + c] + dsf[3 * r + 2] * R[6 + c];
+        double dcov[9];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) part[9 + t] = dm[t];
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int rr = r < c ? r : c, cc = r < c ? c : r;  // symmetric: the upper value, mirrored
+                dcov[3 * r + c] = R[rr] * t1[cc] + R[3 + rr] * t1[3 + cc] + R[6 + rr] * t1[6 + cc];
+            }
+        double mo[3], so[9];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) mo[t] = s_ctr[3 * threadIdx.x + t];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) so[t] = s_cov[9 * threadIdx.x + t];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                part[3 * r + c] = c9[r] * mo[c] + 2.0 * (t1[3 * r] * so[c] + t1[3 * r + 1] * so[3 + c] +
+                                                         t1[3 * r + 2] * so[6 + c]);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) part[9 + t] = c9[t];
+        __syncwarp(__activemask());
+#pragma unroll
+        for (int t = 0; t < 3; ++t) s_ctr[3 * threadIdx.x + t] = dc[t];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s_cov[9 * threadIdx.x + t] = dcov[t];
     }
-    __syncthreads();  // the staging rows are reused for the outputs
-#pragma unroll
-    for (int t = 0; t < 9; ++t) s_acc[9 * t0 + t] = dcov[t];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) s_ctr[3 * t0 + t] = dc[t];
     __syncthreads();
-    stage_rows_out(p.d_inv_cov, s_acc, k0, count, 9);
     stage_rows_out(p.d_center, s_ctr, k0, count, 3);
-    // block reduction of the 12 camera-gradient components: a 16-value
-    // butterfly (each step halves the values a lane carries), then lane 2v
-    // holds the warp total of value v
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double a[16];
+    stage_rows_out(p.d_inv_cov, s_cov, k0, count, 9);
+    // fixed-order block reduction: shfl_down tree per warp, warps in order
 #pragma unroll
-    for (int t = 0; t < 16; ++t) a[t] = t < 12 ? part[t] : 0.0;
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int half = 8, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
-        const bool hi = lane & bit;
+        for (int t = 0; t < 12; ++t) part[t] += __shfl_down_sync(0xffffffffu, part[t], o);
+    if (lane == 0)
 #pragma unroll
-        for (int t = 0; t < half; ++t) {
-            const double send = hi ? a[t] : a[t + half];
-            const double keep = hi ? a[t + half] : a[t];
-            a[t] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
-        }
-    }
-    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-    __shared__ double red[32][12];
-    const int v = lane >> 1;
-    if (!(lane & 1) && v < 12) red[warp][v] = a[0];
+        for (int t = 0; t < 12; ++t) s_part[warp][t] = part[t];
     __syncthreads();
     if (threadIdx.x < 12) {
-        double acc = 0.0;
-        const int nw = (blockDim.x + 31) / 32;
-        for (int w = 0; w < nw; ++w) acc += red[w][threadIdx.x];
-        if (acc != 0.0) atomicAdd(p.d_rt + threadIdx.x, acc);
+        double v = 0.0;
+        for (int w2 = 0; w2 < kFinishThreads / 32; ++w2) v += s_part[w2][threadIdx.x];
+        p.rt_part[12ll * blockIdx.x + threadIdx.x] = v;
     }
+    __threadfence();
+    __syncthreads();
+    const int ngroups = (gridDim.x + kRtGroup - 1) / kRtGroup;
+    const int group = blockIdx.x / kRtGroup;
+    const int gsize = min(kRtGroup, (int)gridDim.x - group * kRtGroup);
+    if (threadIdx.x == 0) s_last = atomicAdd(p.tickets + 1 + group, 1u) == (unsigned)gsize - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double* gpart = p.rt_part + 12ll * gridDim.x;
+    if (threadIdx.x < 12) {
+        double v = 0.0;
+        for (int c = group * kRtGroup; c < group * kRtGroup + gsize; ++c) v += __ldcg(p.rt_part + 12ll * c + threadIdx.x);
+        gpart[12 * group + threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) p.tickets[1 + group] = 0u;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(p.tickets, 1u) == (unsigned)ngroups - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < 12) {
+        double v = 0.0;
+        for (int g2 = 0; g2 < ngroups; ++g2) v += __ldcg(gpart + 12 * g2 + threadIdx.x);
+        p.d_rt[threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) p.tickets[0] = 0u;
 }
 
 // ScalarLoss::value (grad.cpp:201-216) on device: d = w (x - target), loss += w d^2 / 2.

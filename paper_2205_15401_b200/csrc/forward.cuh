@@ -45,6 +45,9 @@ struct FwdParams {
     long long* tile_cycles;  // profiling hook: [tiles] SM cycles of the tile's selection CTA (nullable)
     int precise;     // verification mode: FP64 exact traces and erfc in the blend sums (gradcheck)
     int* nonfinite; // flag
+    const int4* kinfo;          // [K] mask rectangles (project_kernel)
+    unsigned long long* masks;  // (kernel, tile) pixel masks for the backward
+    int* kcount;                // [K] selected pixels per kernel (zeroed by project_kernel)
 };
 
 // FP32 centre-relative classification of q against ln(eta), and the FP32
@@ -934,6 +937,16 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         if (!p.presorted) {
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
+        }
+        {
+            // the pixel's bit in the kernel's (kernel, tile) mask: the backward's
+            // per-kernel record order (order-independent OR)
+            const int4 ki = p.kinfo[b_id[s * NP + g] & ~kExact];
+            if (ki.x >= 0) {
+                const int slot = ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff));
+                atomicOr(p.masks + slot, 1ull << ((i % 8) * 8 + j % 8));
+                atomicAdd(p.kcount + (b_id[s * NP + g] & ~kExact), 1);
+            }
         }
         // tape the traced entry for the backward and the sampler
         EntryRec er;

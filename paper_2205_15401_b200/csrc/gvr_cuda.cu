@@ -70,8 +70,9 @@ bool is_device_ptr(const void* ptr) {
 }  // namespace
 
 // Tape flags buffer (ints): [0] dropped_behind, [1] nonfinite, [2..3] loss (double),
-// [kListStats .. +3] tile-list stats of the last render (list_offsets).
-constexpr int kListStats = 8;
+// [kListStats .. +3] tile-list stats of the last render (list_offsets),
+// [kMaskTotal] mask-rectangle tiles requested by the last render (project_kernel).
+constexpr int kListStats = 8, kMaskTotal = 12;
 
 enum Stage {
     ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
@@ -149,7 +150,10 @@ struct gvr_tape {
     Buf topk, count, image, alpha, depth, topk_w, tape_t, ent;
     Buf d_image, d_alpha;
     // gradients
-    Buf acc, d_attr, d_center, d_inv_cov, d_rt;
+    Buf acc, attr_fb, d_attr, d_center, d_inv_cov, d_rt;
+    // deterministic backward: per-kernel mask rectangles (render), entry adjoints, CTA partials
+    Buf kinfo, masks, slot_off, app, bent, pieces, kcount, rt_part, tickets;
+    long long mask_hint = 0;
     // host copy-out staging
     Buf stage_i, stage_w;
     // [0] dropped_behind (int), [1] nonfinite (int), [2..3] loss (double); pinned mirror
@@ -356,6 +360,14 @@ int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
         kern<<<tiles * GVR_BWD_SPLIT, 256 / GVR_BWD_SPLIT, smem, ctx->stream>>>(bp);
     }
     LAUNCH_CHECK(ctx);
+    return GVR_OK;
+}
+
+// Grow-only buffer whose contents must start at zero (cleared when reallocated).
+int ensure_zeroed(gvr_context* ctx, Buf& b, size_t bytes) {
+    const void* before = b.p;
+    CUDA_TRY(ctx, b.ensure(bytes));
+    if (b.p != before) CUDA_TRY(ctx, cudaMemsetAsync(b.p, 0, b.cap, ctx->stream));
     return GVR_OK;
 }
 
@@ -760,7 +772,8 @@ void gvr_tape_destroy(gvr_tape* t) {
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_off, &t->tile_fill, &t->pool, &t->sorted_pool,
                    &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
-                   &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags};
+                   &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags, &t->attr_fb, &t->kinfo,
+                   &t->masks, &t->slot_off, &t->app, &t->bent, &t->pieces, &t->kcount, &t->rt_part, &t->tickets};
     for (Buf* b : bufs) b->release();
     if (t->h_flags) cudaFreeHost(t->h_flags);
     delete t;
@@ -856,6 +869,20 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     const long long pool_cap = std::min<long long>(
         {(long long)(tape->pool.cap / sizeof(unsigned long long)), (long long)(tape->sorted_pool.cap / sizeof(unsigned long long)),
          0x7fffffffLL, ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL});
+    // mask rectangles of the deterministic backward: one 8-byte pixel mask per
+    // (kernel, tile of its box), sized like the pool (estimate / earlier totals)
+    {
+        tape->mask_hint = std::max<long long>(tape->mask_hint, tape->h_flags[kMaskTotal]);
+        const long long est = std::max<long long>(1 << 18, 4LL * K + 64LL * tiles);
+        const long long want = std::max(est, tape->mask_hint + tape->mask_hint / 4);
+        if (!ctx->capturing || tape->masks.cap == 0) {
+            CUDA_TRY(ctx, tape->masks.ensure(sizeof(unsigned long long) * (size_t)want));
+        }
+        CUDA_TRY(ctx, tape->kinfo.ensure(sizeof(int4) * (size_t)(K > 0 ? K : 1)));
+        CUDA_TRY(ctx, tape->kcount.ensure(sizeof(int) * ((size_t)(K > 0 ? K : 1) + (K + kScanThreads - 1) / kScanThreads + 1)));
+    }
+    const long long mask_cap = std::min<long long>({(long long)(tape->masks.cap / sizeof(unsigned long long)), 0x7fffffffLL,
+                                                    ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL});
     CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * 2 * (size_t)tiles));
     CUDA_TRY(ctx, tape->tile_off.ensure(sizeof(int) * (size_t)tiles));
     CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 4 * (size_t)tiles)));
@@ -874,7 +901,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     int* sched = tape->sched.as<int>();
     int* order_f = sched + 2;
     float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
-    CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 2 * sizeof(int), ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 16 * sizeof(int), ctx->stream));
     int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts: one memset
     CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
     // bwd_cost[tiles], n_all, tile_done[tiles] (contiguous)
@@ -896,6 +923,11 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         pp.tile_count = tile_count;
         pp.shard = shard;
         pp.nshards = nshards;
+        pp.kinfo = tape->kinfo.as<int4>();
+        pp.masks = tape->masks.as<unsigned long long>();
+        pp.mask_total = dflags + kMaskTotal;
+        pp.mask_cap = (int)mask_cap;
+        pp.kcount = tape->kcount.as<int>();
         pp.dropped_behind = dflags;
         {
             StageTimer st(ctx, ST_PROJECT);
@@ -974,6 +1006,9 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.tape_t = tape->tape_t.as<double>();
     fp.ent = tape->ent.as<EntryRec>();
     fp.nonfinite = dflags + 1;
+    fp.kinfo = tape->kinfo.as<int4>();
+    fp.masks = tape->masks.as<unsigned long long>();
+    fp.kcount = tape->kcount.as<int>();
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     fp.precise = ctx->precise ? 1 : 0;
     fp.tile_cycles = nullptr;
@@ -997,7 +1032,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
 
     tape->valid = true;
     if (!ctx->capturing)  // sizing hint for the next render (read without a sync: a stale value is harmless)
-        CUDA_TRY(ctx, cudaMemcpyAsync(tape->h_flags + kListStats, dflags + kListStats, 4 * sizeof(int),
+        CUDA_TRY(ctx, cudaMemcpyAsync(tape->h_flags + kListStats, dflags + kListStats, 5 * sizeof(int),
                                       cudaMemcpyDeviceToHost, ctx->stream));
 
     if (out) {
@@ -1051,9 +1086,12 @@ extern "C" int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const 
     if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
     if (!host) return GVR_OK;
     if (int rc = sync_and_check(ctx)) return rc;
-    if (tape->h_flags[kListStats + 2] > 0 && ctx->pool_override == 0) {
-        // some tile lists did not fit the pool: size it from this render's total and render again
+    if ((tape->h_flags[kListStats + 2] > 0 && ctx->pool_override == 0) ||
+        ((long long)tape->h_flags[kMaskTotal] > (long long)(tape->masks.cap / sizeof(unsigned long long)) &&
+         ctx->pool_override == 0)) {
+        // some tile lists / mask rectangles did not fit: size them from this render's totals and render again
         tape->pool_hint = std::max<long long>(tape->pool_hint, tape->h_flags[kListStats]);
+        tape->mask_hint = std::max<long long>(tape->mask_hint, tape->h_flags[kMaskTotal]);
         if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
         if (int rc = sync_and_check(ctx)) return rc;
     }
@@ -1206,14 +1244,27 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     const int through_t = flags ? flags->through_transmittance : 1;
     const int through_rho = flags ? flags->through_density : 1;
 
-    CUDA_TRY(ctx, t->acc.ensure(sizeof(double) * 9 * (size_t)(K > 0 ? K : 1)));
+    const long long P_kp = P * t->cfg.k_prime;
+    const unsigned finish_grid = (unsigned)std::max<long long>(1, (K + kFinishThreads - 1) / kFinishThreads);
+    const unsigned rt_groups = (finish_grid + kRtGroup - 1) / kRtGroup;
+    const long long scan_ctas = std::max<long long>(1, (K + kScanThreads - 1) / kScanThreads);
+    const long long windows = (P_kp + 31) / 32;
+    // fallback accumulators and tickets are zero between backwards (the gather
+    // re-zeroes what it consumed): cleared only when (re)allocated
+    if (int rc = ensure_zeroed(ctx, t->acc, sizeof(double) * 9 * (size_t)(K > 0 ? K : 1))) return rc;
+    if (int rc = ensure_zeroed(ctx, t->attr_fb, sizeof(double) * (size_t)(D > 0 ? D : 1) * (K > 0 ? K : 1))) return rc;
+    if (int rc = ensure_zeroed(ctx, t->tickets, sizeof(unsigned) * (2 + (size_t)rt_groups))) return rc;
+    CUDA_TRY(ctx, t->rt_part.ensure(sizeof(double) * 12 * ((size_t)finish_grid + rt_groups)));
+    CUDA_TRY(ctx, t->pieces.ensure(sizeof(double) * (9 + (size_t)D) * ((size_t)K + windows + 1)));
+
+    CUDA_TRY(ctx, t->bent.ensure(2 * sizeof(double4) * (size_t)(P_kp > 0 ? P_kp : 1)));
+    CUDA_TRY(ctx, t->app.ensure(sizeof(int2) * (size_t)(K > 0 ? K : 1)));
+    CUDA_TRY(ctx, t->slot_off.ensure(sizeof(int) * (t->masks.cap / sizeof(unsigned long long) + 1)));
     CUDA_TRY(ctx, t->d_attr.ensure(sizeof(double) * (size_t)(D > 0 ? D : 1) * (K > 0 ? K : 1)));
     CUDA_TRY(ctx, t->d_center.ensure(sizeof(double) * 3 * (size_t)(K > 0 ? K : 1)));
     CUDA_TRY(ctx, t->d_inv_cov.ensure(sizeof(double) * 9 * (size_t)(K > 0 ? K : 1)));
     CUDA_TRY(ctx, t->d_rt.ensure(sizeof(double) * 12));
-    CUDA_TRY(ctx, cudaMemsetAsync(t->acc.p, 0, sizeof(double) * 9 * (size_t)K, ctx->stream));
-    CUDA_TRY(ctx, cudaMemsetAsync(t->d_attr.p, 0, sizeof(double) * (size_t)D * K, ctx->stream));
-    CUDA_TRY(ctx, cudaMemsetAsync(t->d_rt.p, 0, sizeof(double) * 12, ctx->stream));
+    if (K == 0) CUDA_TRY(ctx, cudaMemsetAsync(t->d_rt.p, 0, sizeof(double) * 12, ctx->stream));
 
     if (K > 0) {
         BwdParams bp;
@@ -1244,9 +1295,32 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.attr = scene->attr.as<double>();
         bp.d_image = di;
         bp.d_alpha = da;
+        bp.kinfo = t->kinfo.as<int4>();
+        bp.masks = t->masks.as<unsigned long long>();
+        bp.slot_off = t->slot_off.as<int>();
+        bp.bent = t->bent.as<double4>();
         bp.acc = t->acc.as<double>();
-        bp.d_attr = t->d_attr.as<double>();
+        bp.attr_fb = t->attr_fb.as<double>();
         const int kp = t->cfg.k_prime;
+        unsigned* rec_total = t->tickets.as<unsigned>() + 1 + rt_groups;
+        AppParams ap;
+        ap.K = K;
+        ap.kinfo = t->kinfo.as<int4>();
+        ap.masks = t->masks.as<unsigned long long>();
+        ap.count = t->kcount.as<int>();
+        ap.cta_sum = t->kcount.as<int>() + K;
+        ap.slot_off = t->slot_off.as<int>();
+        ap.app = t->app.as<int2>();
+        ap.total = reinterpret_cast<int*>(rec_total);
+        {
+            // K4a-c: record layout (per-kernel counts from the blend's masks, scan, offsets)
+            StageTimer st(ctx, ST_OBJECT);
+            count_kernel<<<(unsigned)scan_ctas, kScanThreads, 0, ctx->stream>>>(ap);
+            cta_scan_kernel<<<1, 1024, 0, ctx->stream>>>(ap, (int)scan_ctas);
+            offsets_kernel<<<(unsigned)scan_ctas, kScanThreads, 0, ctx->stream>>>(ap);
+        }
+        ctx->launches += 2;
+        LAUNCH_CHECK(ctx);
         int rc;
         if (kp <= 8) rc = launch_backward<8>(ctx, bp, btx * bty);
         else if (kp <= 16) rc = launch_backward<16>(ctx, bp, btx * bty);
@@ -1257,19 +1331,36 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         else rc = launch_backward<64>(ctx, bp, btx * bty);
         if (rc) return rc;
 
-        ObjParams op;
-        op.K = K;
-        op.cam = t->camp;
-        op.acc = t->acc.as<double>();
-        op.centers = scene->centers.as<double>();
-        op.inv_cov = scene->inv_cov.as<double>();
-        op.d_center = t->d_center.as<double>();
-        op.d_inv_cov = t->d_inv_cov.as<double>();
-        op.d_rt = t->d_rt.as<double>();
+        GatherParams gp;
+        gp.K = K;
+        gp.D = D;
+        gp.nv = 9 + D;
+        gp.cam = t->camp;
+        gp.kinfo = t->kinfo.as<int4>();
+        gp.app = t->app.as<int2>();
+        gp.total = reinterpret_cast<const int*>(rec_total);
+        gp.bent = t->bent.as<double4>();
+        gp.rec64 = t->rec64.as<Rec64>();
+        gp.d_image = di;
+        gp.pieces = t->pieces.as<double>();
+        gp.acc = t->acc.as<double>();
+        gp.attr_fb = t->attr_fb.as<double>();
+        gp.centers = scene->centers.as<double>();
+        gp.inv_cov = scene->inv_cov.as<double>();
+        gp.d_center = t->d_center.as<double>();
+        gp.d_inv_cov = t->d_inv_cov.as<double>();
+        gp.d_attr = t->d_attr.as<double>();
+        gp.rt_part = t->rt_part.as<double>();
+        gp.tickets = t->tickets.as<unsigned>();
+        gp.d_rt = t->d_rt.as<double>();
         {
             StageTimer st(ctx, ST_OBJECT);
-            object_space_kernel<<<blocks_for(K, kObjThreads), kObjThreads, 0, ctx->stream>>>(op);
+            const size_t rsmem = sizeof(double) * kRecThreads * (size_t)gp.nv;
+            CUDA_TRY(ctx, cudaFuncSetAttribute(records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+            records_kernel<<<148 * 16, kRecThreads, rsmem, ctx->stream>>>(gp);
+            finish_kernel<<<finish_grid, kFinishThreads, 0, ctx->stream>>>(gp);
         }
+        ++ctx->launches;
         LAUNCH_CHECK(ctx);
     }
     if (out && accumulate) {
@@ -1916,12 +2007,14 @@ int gvr_tape_check_finite(gvr_context* ctx, gvr_tape* t) {
 int gvr_tape_list_stats(gvr_context* ctx, const gvr_tape* t, int64_t* stats) {
     if (!ctx || !t || !t->valid || !stats) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
     if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
-    CUDA_TRY(ctx, cudaMemcpyAsync(t->h_flags + kListStats, t->flags.as<int>() + kListStats, 4 * sizeof(int),
+    CUDA_TRY(ctx, cudaMemcpyAsync(t->h_flags + kListStats, t->flags.as<int>() + kListStats, 5 * sizeof(int),
                                   cudaMemcpyDeviceToHost, ctx->stream));
     if (int rc = sync_and_check(ctx)) return rc;
     for (int i = 0; i < 4; ++i) stats[i] = t->h_flags[kListStats + i];
     stats[4] = std::min<long long>((long long)(t->pool.cap / sizeof(unsigned long long)),
                                    ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL);
+    stats[5] = t->h_flags[kMaskTotal];
+    stats[6] = (long long)(t->masks.cap / sizeof(unsigned long long));
     return GVR_OK;
 }
 

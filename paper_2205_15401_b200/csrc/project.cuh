@@ -138,6 +138,12 @@ struct ProjectParams {
     int* tile_count;  // [tiles] list lengths (zeroed before the launch)
     int shard, nshards;  // only tiles t with t % nshards == shard are binned (C4 tile sharding)
     int* dropped_behind;
+    // backward bookkeeping: one 64-bit pixel mask per (kernel, tile of its box rectangle)
+    int4* kinfo;                 // [K] {mask base (-1: no room), tr0 << 16 | tc0, tiles per row, tiles}
+    unsigned long long* masks;   // [mask_cap], zeroed here for every allocated rectangle
+    int* mask_total;             // rectangle tiles requested (bump allocator, zeroed before the launch)
+    int* kcount;                 // [K] zeroed here (the blend counts each kernel's selected pixels)
+    int mask_cap;
 };
 
 // K1: view transform (scene.cpp:5-17), coarse screen box (tracer.cpp:37-113) in
@@ -327,6 +333,26 @@ __global__ void project_kernel(ProjectParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
+    {
+        // mask rectangle of the kernel (deterministic backward): one warp-aggregated
+        // bump allocation, then the kernel zeroes its own masks
+        int incl = job.nt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int base = 0;
+        if (lane == 31 && incl > 0) base = atomicAdd(p.mask_total, incl);
+        base = __shfl_sync(FULL, base, 31) + incl - job.nt;
+        if (k < p.K) {
+            const bool fits = base >= 0 && (long long)base + job.nt <= (long long)p.mask_cap;
+            p.kinfo[k] = make_int4(job.nt > 0 && fits ? base : -1, (job.tr0 << 16) | job.tc0, job.ntc, job.nt);
+            p.kcount[k] = 0;
+            if (fits)
+                for (int t = 0; t < job.nt; ++t) p.masks[base + t] = 0ull;
+        }
+    }
     for (int it0 = 0; __any_sync(FULL, it0 < job.nt); it0 += 4) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {

@@ -285,11 +285,12 @@ class Tape:
     def list_stats(self) -> dict:
         """Tile-list layout of the taped render (gvr_tape_list_stats): listed entries, longest
         list, tiles that overflowed the pool (streamed), lists sorted in global memory, pool capacity."""
-        out = np.zeros(5, dtype=np.int64)
+        out = np.zeros(7, dtype=np.int64)
         self.ctx.check(self.ctx.lib.gvr_tape_list_stats(self.ctx.handle, self.handle,
                                                         out.ctypes.data_as(ctypes.c_void_p)))
         return {"entries": int(out[0]), "max_list": int(out[1]), "overflow_tiles": int(out[2]),
-                "global_sorted_tiles": int(out[3]), "pool_capacity": int(out[4])}
+                "global_sorted_tiles": int(out[3]), "pool_capacity": int(out[4]),
+                "mask_tiles": int(out[5]), "mask_capacity": int(out[6])}
 
     def tile_cycles(self) -> np.ndarray:
         """[tiles_y, tiles_x] SM cycles of each 8x8 tile's selection CTA (needs Context.set_tile_profile)."""

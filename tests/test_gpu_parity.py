@@ -88,6 +88,35 @@ def test_tile_list_overflow_path(golden, ctx):
         assert st["overflow_tiles"] > 0
     assert np.array_equal(a.buffers.topk_idx, b.buffers.topk_idx)
     assert np.array_equal(a.buffers.image, b.buffers.image)
+    # the same cap leaves kernels without a mask rectangle: the backward's atomic fallback
+    ctx.set_tile_capacity(8)
+    try:
+        c = gvr.render_with_tape(golden.scene, golden.camera, golden.cfg, ctx=ctx)
+        gb = gvr.backward(c, golden["d_image"], golden["d_alpha"], golden.flags)
+    finally:
+        ctx.set_tile_capacity(0)
+    for key in ("d_attr", "d_center", "d_inv_cov", "d_rotation", "d_translation"):
+        assert_grad_close(getattr(gb, key), golden[key], what=f"fallback {key}")
+
+
+def test_backward_is_bit_deterministic(ctx):
+    """test_grad.cpp:279-296: repeated backwards give bit-identical bundles (the
+    per-kernel gather sums every gradient in one fixed order)."""
+    scene = gvr.make_bench_scene(100000)
+    cam = gvr.make_orbit_camera(0.7, 0.3, 4.0, (0, 0, 4), 256, 256, 1.6 * 256)
+    rng = np.random.default_rng(9)
+    bundles = []
+    for _ in range(3):
+        fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+        st = fr.tape.list_stats()
+        assert st["mask_tiles"] <= st["mask_capacity"]
+        di = rng.uniform(-1, 1, fr.buffers.image.shape) if not bundles else di
+        da = rng.uniform(-1, 1, fr.buffers.alpha.shape) if not bundles else da
+        bundles.append(gvr.backward(fr, di, da))
+        bundles.append(gvr.backward(fr, di, da))
+    for b in bundles[1:]:
+        for key in ("d_center", "d_inv_cov", "d_attr", "d_rotation", "d_translation"):
+            assert np.array_equal(getattr(b, key), getattr(bundles[0], key)), key
 
 
 def test_lists_sorted_in_global_memory(golden, ctx):
