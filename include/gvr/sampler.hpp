@@ -1,0 +1,5 @@
+// gvr/sampler.hpp — the reference header of the same name (/root/reference/proj/include/gvr/sampler.hpp),
+// served by the GPU drop-in: every declaration lives in gvr/gvr.hpp.
+#pragma once
+
+#include "gvr.hpp"

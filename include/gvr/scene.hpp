@@ -1,0 +1,5 @@
+// gvr/scene.hpp — the reference header of the same name (/root/reference/proj/include/gvr/scene.hpp),
+// served by the GPU drop-in: every declaration lives in gvr/gvr.hpp.
+#pragma once
+
+#include "gvr.hpp"

@@ -331,6 +331,47 @@ int gvr_edge_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* cen
 int gvr_laplacian_reg(gvr_context* ctx, const gvr_regularizer* reg, const double* centers, double weight,
                       double* value, double* grad, int32_t accumulate);
 
+/* ---- building blocks of the reference API (C++ drop-in, include/gvr/) ------
+ * One device launch per call; all pointers host or device; synchronising. */
+/* trace_kernel (tracer.hpp:45, tracer.cpp:20-35) for n (ray, kernel) pairs:
+ * dirs[n*3], centers[n*3], inv_cov[n*9] -> l, q, sigma [n] (nullable), bit-exact.
+ * GVR_ERR_VALIDATION "trace_kernel: D^T inv_cov D <= 0 (inv_cov not positive-definite)". */
+int gvr_trace_pairs(gvr_context* ctx, int64_t n, const double* dirs, const double* centers, const double* inv_cov,
+                    double* l, double* q, double* sigma);
+/* view_transform (scene.hpp:10, scene.cpp:5-17): camera validated first; bit-exact. */
+int gvr_view_transform(gvr_context* ctx, int32_t K, const double* centers, const double* inv_cov,
+                       const gvr_camera* camera, double* out_centers, double* out_inv_cov);
+/* pixel_ray / generate_rays (scene.hpp:13-16, scene.cpp:19-33): dirs[n*3] of the
+ * pixels (rows[i], cols[i]), or of every pixel row-major when rows == cols == NULL
+ * (n = height * width). */
+int gvr_pixel_rays(gvr_context* ctx, const gvr_camera* camera, int64_t n, const int32_t* rows, const int32_t* cols,
+                   double* dirs);
+/* coarse_select (tracer.hpp:49, tracer.cpp:37-113) on a camera-space scene: per
+ * kernel the pixel box it is pushed into, boxes[K*4] = {row_lo, row_hi, col_lo,
+ * col_hi} ({1, 0, 1, 0} = not pushed), and PixelKernelMap::dropped_behind_camera;
+ * the cells (ds x ds) of the box are the kernel's cells. Config validated first. */
+int gvr_coarse_select_boxes(gvr_context* ctx, int32_t K, const double* cam_centers, const double* cam_inv_cov,
+                            const gvr_camera* camera, const gvr_selection* cfg, int32_t* boxes, int32_t* dropped);
+/* fine_select / blend order (tracer.cpp:115-127): the entries with q > ln(eta)
+ * (all when eta is outside (0, 1)) sorted by (l, idx); order[m] = input positions.
+ * n <= 2048 per call. */
+int gvr_ray_sort(gvr_context* ctx, int32_t n, const int32_t* idx, const double* l, const double* q, double eta,
+                 int32_t* order, int32_t* m_out);
+/* blend (blender.hpp:33, blender.cpp:27-53) of one ray (n <= 2048): weights in
+ * ascending (l, idx) order (out_idx, out_w [n]) and alpha (FP64 erfc / exp). */
+int gvr_blend_ray(gvr_context* ctx, int32_t n, const int32_t* idx, const double* l, const double* q,
+                  const double* sigma, double tau, int32_t* out_idx, double* out_w, double* alpha);
+/* transmittance_at (blender.hpp:29, blender.cpp:19-25) of one ray's entries at nt depths. */
+int gvr_transmittance_ray(gvr_context* ctx, int32_t n, const double* l, const double* q, const double* sigma,
+                          double tau, int32_t nt, const double* t, double* out);
+/* normalized_weights (blender.hpp:36, blender.cpp:55-62): w / max(sum w, eps). */
+int gvr_normalized_weights_ray(gvr_context* ctx, int32_t n, const double* w, double eps, double* out);
+/* ScalarLoss::value (grad.hpp:68, grad.cpp:201-216) on caller buffers:
+ * loss = sum w_i (x - t)^2 / 2 over image then alpha; d_image / d_alpha nullable. */
+int gvr_scalar_loss_buffers(gvr_context* ctx, int64_t n_img, const double* image, const double* target_image,
+                            int64_t n_alpha, const double* alpha, const double* target_alpha, double w_image,
+                            double w_alpha, double* loss, double* d_image, double* d_alpha);
+
 #ifdef __cplusplus
 }
 #endif

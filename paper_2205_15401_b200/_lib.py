@@ -74,6 +74,15 @@ EXPORTED_SYMBOLS = (
     "gvr_context_set_list_smem",
     "gvr_tape_check_finite",
     "gvr_adam_step_guarded",
+    "gvr_trace_pairs",
+    "gvr_view_transform",
+    "gvr_pixel_rays",
+    "gvr_coarse_select_boxes",
+    "gvr_ray_sort",
+    "gvr_blend_ray",
+    "gvr_transmittance_ray",
+    "gvr_normalized_weights_ray",
+    "gvr_scalar_loss_buffers",
 )
 
 
@@ -175,6 +184,17 @@ def load() -> ctypes.CDLL:
         "gvr_tape_list_stats": (ctypes.c_int, [vp, vp, vp]),
         "gvr_context_set_list_smem": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_tape_check_finite": (ctypes.c_int, [vp, vp]),
+        "gvr_trace_pairs": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
+        "gvr_view_transform": (ctypes.c_int, [vp, i32, vp, vp, ctypes.POINTER(GvrCamera), vp, vp]),
+        "gvr_pixel_rays": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), ctypes.c_int64, vp, vp, vp]),
+        "gvr_coarse_select_boxes": (ctypes.c_int, [vp, i32, vp, vp, ctypes.POINTER(GvrCamera),
+                                                   ctypes.POINTER(GvrSelection), vp, ctypes.POINTER(i32)]),
+        "gvr_ray_sort": (ctypes.c_int, [vp, i32, vp, vp, vp, dp, vp, ctypes.POINTER(i32)]),
+        "gvr_blend_ray": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, dp, vp, vp, vp]),
+        "gvr_transmittance_ray": (ctypes.c_int, [vp, i32, vp, vp, vp, dp, i32, vp, vp]),
+        "gvr_normalized_weights_ray": (ctypes.c_int, [vp, i32, vp, dp, vp]),
+        "gvr_scalar_loss_buffers": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, ctypes.c_int64, vp, vp, dp, dp, vp, vp,
+                                                   vp]),
         "gvr_adam_step_guarded": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp,
                                                  vp, vp]),
         "gvr_tape_shape": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),

@@ -13,7 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgvr_cuda.so")
 SOURCES = ["gvr_cuda.cu"]
-DEPS = ["gvr_cuda.cu", "gvr_common.cuh", "project.cuh", "forward.cuh", "backward.cuh", "sampler.cuh", "fit.cuh"]
+DEPS = ["gvr_cuda.cu", "gvr_common.cuh", "project.cuh", "forward.cuh", "backward.cuh", "sampler.cuh", "fit.cuh",
+        "blocks.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -47,6 +48,37 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+REF_TESTS = ("test_scene", "test_tracer", "test_blender", "test_grad")
+REF_TEST_DIR = os.path.join(ROOT, "tests", "cpp", "_build")
+
+
+def build_reference_suites(verbose: bool = False) -> list:
+    """The reference's own hot-path test suites (/root/reference/proj/tests/
+    test_{scene,tracer,blender,grad}.cpp), compiled UNMODIFIED against the C++
+    drop-in (include/gvr/*.hpp -> libgvr_cuda.so), with Eigen and doctest from
+    the repo's test shims (oracle/shim). Only where /root/reference exists (this
+    container); the binaries travel to the GPU box with the tree and are run by
+    tests/test_gpu_reference_suites.py. Returns the binaries built."""
+    src = "/root/reference/proj/tests"
+    if not os.path.isdir(src):
+        return []
+    os.makedirs(REF_TEST_DIR, exist_ok=True)
+    out = []
+    for t in REF_TESTS:
+        exe = os.path.join(REF_TEST_DIR, "ref_" + t)
+        cpp = os.path.join(src, t + ".cpp")
+        deps = [cpp, os.path.join(ROOT, "include", "gvr", "gvr.hpp"), os.path.join(ROOT, "include", "gvr_cuda.h")]
+        if _stale(exe, deps):
+            cmd = ["g++", "-std=c++20", "-O2", "-DGVR_WITH_EIGEN", f"-I{ROOT}/include", f"-I{ROOT}/oracle/shim",
+                   f"-I{src}", cpp, f"-L{HERE}", "-lgvr_cuda", "-Wl,-rpath,$ORIGIN/../../../paper_2205_15401_b200",
+                   "-o", exe]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.run(cmd, check=True)
+        out.append(exe)
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Checker only: the C port always; the reference build when /root/reference exists."""
     odir = os.path.join(ROOT, "oracle")
@@ -57,4 +89,5 @@ def build_oracle(verbose: bool = False) -> None:
 
 if __name__ == "__main__":
     build_cuda(force="--force" in sys.argv, verbose=True)
+    build_reference_suites(verbose=True)
     build_oracle(verbose=True)

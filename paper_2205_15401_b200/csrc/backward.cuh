@@ -616,12 +616,14 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
     if (threadIdx.x == 0) p.tickets[0] = 0u;
 }
 
-// ScalarLoss::value (grad.cpp:201-216) on device: d = w (x - target), loss += w d^2 / 2.
+// ScalarLoss::value (grad.cpp:201-216) on device: d = w (x - target), loss = sum w d^2 / 2.
+// Deterministic: a fixed grid-stride partition, per-block partials in a fixed
+// tree, and the last block (ticket) sums the partials in block order.
 __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const double* __restrict__ image,
                                    const double* __restrict__ t_image, const double* __restrict__ alpha,
                                    const double* __restrict__ t_alpha, double w_image, double w_alpha,
                                    double* __restrict__ d_image, double* __restrict__ d_alpha,
-                                   double* __restrict__ loss) {
+                                   double* __restrict__ loss, double* __restrict__ part_out, unsigned* ticket) {
     double part = 0.0;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_img + n_alpha;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -639,13 +641,32 @@ __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const dou
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     __shared__ double red[32];
+    __shared__ bool s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) red[warp] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
         double v = 0.0;
         for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) v += red[w];
-        atomicAdd(loss, v);
+        part_out[blockIdx.x] = v;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last block: partials in block order (lane-strided, then a fixed tree)
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += __ldcg(part_out + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) tot += red[w];
+        *loss = tot;
+        *ticket = 0u;
     }
 }
 

@@ -12,6 +12,7 @@
 #include "forward.cuh"
 #include "project.cuh"
 #include "sampler.cuh"
+#include "blocks.cuh"
 
 #include <cuda_runtime.h>
 
@@ -152,7 +153,7 @@ struct gvr_tape {
     // gradients
     Buf acc, attr_fb, d_attr, d_center, d_inv_cov, d_rt;
     // deterministic backward: per-kernel mask rectangles (render), entry adjoints, CTA partials
-    Buf kinfo, masks, slot_off, app, bent, pieces, kcount, rt_part, tickets;
+    Buf kinfo, masks, slot_off, app, bent, pieces, kcount, rt_part, tickets, loss_part;
     long long mask_hint = 0;
     // host copy-out staging
     Buf stage_i, stage_w;
@@ -221,11 +222,17 @@ int validate_camera(gvr_context* ctx, const gvr_camera* c) {
 }
 
 // SelectionConfig::validate (tracer.cpp:8-18), same messages.
-int validate_cfg(gvr_context* ctx, const gvr_selection* s) {
+int validate_cfg_ref(gvr_context* ctx, const gvr_selection* s) {
     if (!s) return set_err(ctx, GVR_ERR_VALIDATION, "selection config is null");
     if (!(s->eta > 0.0 && s->eta < 1.0)) return set_err(ctx, GVR_ERR_VALIDATION, "selection eta must be in (0, 1)");
     if (s->k_prime < 1) return set_err(ctx, GVR_ERR_VALIDATION, "selection k_prime must be >= 1");
     if (s->coarse_downsample < 1) return set_err(ctx, GVR_ERR_VALIDATION, "coarse downsample must be >= 1");
+    return GVR_OK;
+}
+
+// ... plus the render path's K' limit.
+int validate_cfg(gvr_context* ctx, const gvr_selection* s) {
+    if (int rc = validate_cfg_ref(ctx, s)) return rc;
     if (s->k_prime > kMaxKPrime)
         return set_err(ctx, GVR_ERR_RUNTIME, "k_prime %d exceeds the CUDA backend limit of %d", s->k_prime, kMaxKPrime);
     return GVR_OK;
@@ -773,7 +780,8 @@ void gvr_tape_destroy(gvr_tape* t) {
                    &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags, &t->attr_fb, &t->kinfo,
-                   &t->masks, &t->slot_off, &t->app, &t->bent, &t->pieces, &t->kcount, &t->rt_part, &t->tickets};
+                   &t->masks, &t->slot_off, &t->app, &t->bent, &t->pieces, &t->kcount, &t->rt_part, &t->tickets,
+                   &t->loss_part};
     for (Buf* b : bufs) b->release();
     if (t->h_flags) cudaFreeHost(t->h_flags);
     delete t;
@@ -909,7 +917,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
 
     if (K > 0) {
         // K1 projection + culling + binning into per-tile lists
-        ProjectParams pp;
+        ProjectParams pp{};
         pp.K = K;
         pp.centers = scene->centers.as<double>();
         pp.inv_cov = scene->inv_cov.as<double>();
@@ -968,7 +976,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         }
         LAUNCH_CHECK(ctx);
     }
-    FwdParams fp;
+    FwdParams fp{};
     fp.cam = cp;
     fp.sel = sp;
     fp.D = D;
@@ -1163,6 +1171,8 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
         ta = talpha;
     }
     double* dloss = reinterpret_cast<double*>(t->flags.as<int>() + 2);
+    // block partials (<= 148 * 8) + the last-block ticket (zero between launches)
+    if (int rc = ensure_zeroed(ctx, t->loss_part, sizeof(double) * 148 * 8 + 16)) return rc;
     CUDA_TRY(ctx, cudaMemsetAsync(dloss, 0, sizeof(double), ctx->stream));
     const int threads = 256;
     const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), 148 * 8);
@@ -1171,7 +1181,8 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
         scalar_loss_kernel<<<blocks, threads, 0, ctx->stream>>>(n_img, P, t->image.as<double>(), ti,
                                                                 t->alpha.as<double>(), ta, w_image, w_alpha,
                                                                 t->d_image.as<double>(), t->d_alpha.as<double>(),
-                                                                dloss);
+                                                                dloss, t->loss_part.as<double>(),
+                                                                t->loss_part.as<unsigned>() + 2 * 148 * 8);
     }
     LAUNCH_CHECK(ctx);
     t->has_upstream = true;
@@ -1267,7 +1278,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     if (K == 0) CUDA_TRY(ctx, cudaMemsetAsync(t->d_rt.p, 0, sizeof(double) * 12, ctx->stream));
 
     if (K > 0) {
-        BwdParams bp;
+        BwdParams bp{};
         bp.cam = t->camp;
         bp.kp = t->cfg.k_prime;
         bp.D = D;
@@ -1303,7 +1314,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.attr_fb = t->attr_fb.as<double>();
         const int kp = t->cfg.k_prime;
         unsigned* rec_total = t->tickets.as<unsigned>() + 1 + rt_groups;
-        AppParams ap;
+        AppParams ap{};
         ap.K = K;
         ap.kinfo = t->kinfo.as<int4>();
         ap.masks = t->masks.as<unsigned long long>();
@@ -1331,7 +1342,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         else rc = launch_backward<64>(ctx, bp, btx * bty);
         if (rc) return rc;
 
-        GatherParams gp;
+        GatherParams gp{};
         gp.K = K;
         gp.D = D;
         gp.nv = 9 + D;
@@ -2024,6 +2035,306 @@ int gvr_tape_dropped_behind_camera(gvr_context* ctx, const gvr_tape* t, int32_t*
     if (int rc = sync_and_check(ctx)) return rc;
     *count = t->h_flags[0];
     return GVR_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- building blocks (C++ drop-in)
+
+namespace {
+
+CameraP camera_params(const gvr_camera* camera) {
+    CameraP cp;
+    std::memcpy(cp.R, camera->rotation, sizeof cp.R);
+    std::memcpy(cp.T, camera->translation, sizeof cp.T);
+    cp.focal = camera->focal;
+    cp.ox = camera->ox;
+    cp.oy = camera->oy;
+    cp.H = camera->height;
+    cp.W = camera->width;
+    return cp;
+}
+
+// device copies of up to four host-or-device inputs (freed with the guard)
+struct Tmp {
+    Buf b[8];
+    ~Tmp() {
+        for (Buf& x : b) x.release();
+    }
+};
+
+int in_dev(gvr_context* ctx, Buf& buf, const void* src, size_t bytes, const void** dev) {
+    return stage_in(ctx, buf, src, bytes, dev);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gvr_trace_pairs(gvr_context* ctx, int64_t n, const double* dirs, const double* centers, const double* inv_cov,
+                    double* l, double* q, double* sigma) {
+    if (!ctx || n < 0 || (n > 0 && (!dirs || !centers || !inv_cov)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (n == 0) return GVR_OK;
+    if (ctx->capturing) return set_err(ctx, GVR_ERR_RUNTIME, "gvr_trace_pairs synchronises; not capturable");
+    Tmp t;
+    const void *dd, *dc, *ds;
+    if (int rc = in_dev(ctx, t.b[0], dirs, sizeof(double) * 3 * (size_t)n, &dd)) return rc;
+    if (int rc = in_dev(ctx, t.b[1], centers, sizeof(double) * 3 * (size_t)n, &dc)) return rc;
+    if (int rc = in_dev(ctx, t.b[2], inv_cov, sizeof(double) * 9 * (size_t)n, &ds)) return rc;
+    CUDA_TRY(ctx, t.b[3].ensure(sizeof(double) * 3 * (size_t)n + sizeof(unsigned long long)));
+    double* out = t.b[3].as<double>();
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(out + 3 * n);
+    CUDA_TRY(ctx, cudaMemsetAsync(bad, 0xff, sizeof *bad, ctx->stream));
+    trace_pairs_kernel<<<blocks_for(n, 128), 128, 0, ctx->stream>>>(
+        n, static_cast<const double*>(dd), static_cast<const double*>(dc), static_cast<const double*>(ds), out,
+        out + n, out + 2 * n, bad);
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    int rc;
+    if ((rc = copy_out(ctx, l, out, sizeof(double) * n, &host))) return rc;
+    if ((rc = copy_out(ctx, q, out + n, sizeof(double) * n, &host))) return rc;
+    if ((rc = copy_out(ctx, sigma, out + 2 * n, sizeof(double) * n, &host))) return rc;
+    unsigned long long hbad = 0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags + 2, bad, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((rc = sync_and_check(ctx))) return rc;
+    std::memcpy(&hbad, ctx->h_flags + 2, sizeof hbad);
+    if (hbad != ~0ull)
+        return set_err(ctx, GVR_ERR_VALIDATION, "trace_kernel: D^T inv_cov D <= 0 (inv_cov not positive-definite)");
+    return GVR_OK;
+}
+
+int gvr_view_transform(gvr_context* ctx, int32_t K, const double* centers, const double* inv_cov,
+                       const gvr_camera* camera, double* out_centers, double* out_inv_cov) {
+    if (!ctx || K < 0 || (K > 0 && (!centers || !inv_cov))) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (int rc = validate_camera(ctx, camera)) return rc;  // view_transform validates the camera (scene.cpp:6)
+    if (K == 0) return GVR_OK;
+    Tmp t;
+    const void *dc, *ds;
+    if (int rc = in_dev(ctx, t.b[0], centers, sizeof(double) * 3 * (size_t)K, &dc)) return rc;
+    if (int rc = in_dev(ctx, t.b[1], inv_cov, sizeof(double) * 9 * (size_t)K, &ds)) return rc;
+    CUDA_TRY(ctx, t.b[2].ensure(sizeof(double) * 12 * (size_t)K));
+    double* out = t.b[2].as<double>();
+    view_transform_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(K, camera_params(camera),
+                                                                        static_cast<const double*>(dc),
+                                                                        static_cast<const double*>(ds), out,
+                                                                        out + 3 * (size_t)K);
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    int rc;
+    if ((rc = copy_out(ctx, out_centers, out, sizeof(double) * 3 * (size_t)K, &host))) return rc;
+    if ((rc = copy_out(ctx, out_inv_cov, out + 3 * (size_t)K, sizeof(double) * 9 * (size_t)K, &host))) return rc;
+    return sync_and_check(ctx);
+}
+
+int gvr_pixel_rays(gvr_context* ctx, const gvr_camera* camera, int64_t n, const int32_t* rows, const int32_t* cols,
+                   double* dirs) {
+    if (!ctx || !camera || !dirs || n < 0 || (!rows) != (!cols)) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (!rows && n != (int64_t)camera->height * camera->width)
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_pixel_rays: n must be height * width without rows / cols");
+    if (n == 0) return GVR_OK;
+    Tmp t;
+    const void *dr = nullptr, *dcl = nullptr;
+    if (rows) {
+        if (int rc = in_dev(ctx, t.b[0], rows, sizeof(int32_t) * (size_t)n, &dr)) return rc;
+        if (int rc = in_dev(ctx, t.b[1], cols, sizeof(int32_t) * (size_t)n, &dcl)) return rc;
+    }
+    CUDA_TRY(ctx, t.b[2].ensure(sizeof(double) * 3 * (size_t)n));
+    pixel_rays_kernel<<<blocks_for(n, 128), 128, 0, ctx->stream>>>(camera_params(camera), n,
+                                                                    static_cast<const int*>(dr),
+                                                                    static_cast<const int*>(dcl), t.b[2].as<double>());
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (int rc = copy_out(ctx, dirs, t.b[2].p, sizeof(double) * 3 * (size_t)n, &host)) return rc;
+    return sync_and_check(ctx);
+}
+
+int gvr_coarse_select_boxes(gvr_context* ctx, int32_t K, const double* cam_centers, const double* cam_inv_cov,
+                            const gvr_camera* camera, const gvr_selection* cfg, int32_t* boxes, int32_t* dropped) {
+    if (!ctx || !camera || K < 0 || (K > 0 && (!cam_centers || !cam_inv_cov || !boxes)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (int rc = validate_cfg_ref(ctx, cfg)) return rc;  // coarse_select validates the config (tracer.cpp:39)
+    if (dropped) *dropped = 0;
+    if (K == 0) return GVR_OK;
+    Tmp t;
+    const void *dc, *ds;
+    if (int rc = in_dev(ctx, t.b[0], cam_centers, sizeof(double) * 3 * (size_t)K, &dc)) return rc;
+    if (int rc = in_dev(ctx, t.b[1], cam_inv_cov, sizeof(double) * 9 * (size_t)K, &ds)) return rc;
+    CUDA_TRY(ctx, t.b[2].ensure(sizeof(Rec32) * (size_t)K));
+    CUDA_TRY(ctx, t.b[3].ensure(sizeof(Rec64) * (size_t)K));
+    CUDA_TRY(ctx, t.b[4].ensure(sizeof(int4) * (size_t)K + sizeof(int)));
+    int* ddrop = reinterpret_cast<int*>(t.b[4].as<int4>() + K);
+    CUDA_TRY(ctx, cudaMemsetAsync(ddrop, 0, sizeof(int), ctx->stream));
+    gvr_camera ident = *camera;  // the scene is already in camera space: identity extrinsics, exact
+    for (int i = 0; i < 9; ++i) ident.rotation[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    for (int i = 0; i < 3; ++i) ident.translation[i] = 0.0;
+    ProjectParams pp{};
+    pp.K = K;
+    pp.centers = static_cast<const double*>(dc);
+    pp.inv_cov = static_cast<const double*>(ds);
+    pp.cam = camera_params(&ident);
+    pp.sel.eta = cfg->eta;
+    pp.sel.log_eta = std::log(cfg->eta);
+    pp.sel.chi = 2.0 * std::log(1.0 / cfg->eta);
+    pp.sel.kp = cfg->k_prime;
+    pp.sel.coarse = 1;
+    pp.sel.ds = cfg->coarse_downsample;
+    pp.tile = kFwdTile;
+    pp.rec32 = t.b[2].as<Rec32>();
+    pp.rec64 = t.b[3].as<Rec64>();
+    pp.dropped_behind = ddrop;
+    pp.ref_box = t.b[4].as<int4>();
+    coarse_box_kernel<<<blocks_for(K, 128), 128, 0, ctx->stream>>>(pp);
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (int rc = copy_out(ctx, boxes, t.b[4].p, sizeof(int4) * (size_t)K, &host)) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags, ddrop, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    if (dropped) *dropped = ctx->h_flags[0];
+    return GVR_OK;
+}
+
+int gvr_ray_sort(gvr_context* ctx, int32_t n, const int32_t* idx, const double* l, const double* q, double eta,
+                 int32_t* order, int32_t* m_out) {
+    if (!ctx || n < 0 || !order || !m_out || (n > 0 && (!idx || !l))) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    const bool filter = eta > 0.0 && eta < 1.0;
+    if (filter && n > 0 && !q) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (n > kRaySortMax)
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_ray_sort: at most %d entries per call", kRaySortMax);
+    *m_out = 0;
+    if (n == 0) return GVR_OK;
+    Tmp t;
+    const void *di, *dl, *dq = nullptr;
+    if (int rc = in_dev(ctx, t.b[0], idx, sizeof(int32_t) * (size_t)n, &di)) return rc;
+    if (int rc = in_dev(ctx, t.b[1], l, sizeof(double) * (size_t)n, &dl)) return rc;
+    if (filter)
+        if (int rc = in_dev(ctx, t.b[2], q, sizeof(double) * (size_t)n, &dq)) return rc;
+    CUDA_TRY(ctx, t.b[3].ensure(sizeof(int32_t) * ((size_t)n + 1)));
+    int* dorder = t.b[3].as<int>();
+    ray_sort_kernel<<<1, 1024, 0, ctx->stream>>>(n, static_cast<const int*>(di), static_cast<const double*>(dl),
+                                                 static_cast<const double*>(dq), filter ? std::log(eta) : 0.0,
+                                                 filter ? 1 : 0, dorder, dorder + n);
+    LAUNCH_CHECK(ctx);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_flags, dorder + n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = sync_and_check(ctx)) return rc;
+    const int m = ctx->h_flags[0];
+    *m_out = m;
+    bool host = false;
+    if (int rc = copy_out(ctx, order, dorder, sizeof(int32_t) * (size_t)m, &host)) return rc;
+    return sync_and_check(ctx);
+}
+
+int gvr_blend_ray(gvr_context* ctx, int32_t n, const int32_t* idx, const double* l, const double* q,
+                  const double* sigma, double tau, int32_t* out_idx, double* out_w, double* alpha) {
+    if (!ctx || n < 0 || (n > 0 && (!idx || !l || !q || !sigma || !out_idx || !out_w)) || !alpha)
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (n > kRaySortMax)
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_blend_ray: at most %d entries per call", kRaySortMax);
+    Tmp t;
+    const void *di, *dl, *dq, *dsg;
+    if (int rc = in_dev(ctx, t.b[0], idx, sizeof(int32_t) * (size_t)n, &di)) return rc;
+    if (int rc = in_dev(ctx, t.b[1], l, sizeof(double) * (size_t)n, &dl)) return rc;
+    if (int rc = in_dev(ctx, t.b[2], q, sizeof(double) * (size_t)n, &dq)) return rc;
+    if (int rc = in_dev(ctx, t.b[3], sigma, sizeof(double) * (size_t)n, &dsg)) return rc;
+    CUDA_TRY(ctx, t.b[4].ensure(sizeof(int32_t) * ((size_t)n + 1)));
+    CUDA_TRY(ctx, t.b[5].ensure(sizeof(double) * ((size_t)n + 1)));
+    int* dorder = t.b[4].as<int>();
+    double* dw = t.b[5].as<double>();
+    if (n > 0) {
+        ray_sort_kernel<<<1, 1024, 0, ctx->stream>>>(n, static_cast<const int*>(di), static_cast<const double*>(dl),
+                                                     nullptr, 0.0, 0, dorder, dorder + n);
+        LAUNCH_CHECK(ctx);
+    }
+    blend_ray_kernel<<<blocks_for(n > 0 ? n : 1, 128), 128, 0, ctx->stream>>>(
+        n, dorder, static_cast<const double*>(dl), static_cast<const double*>(dq), static_cast<const double*>(dsg), tau,
+        dw, dw + n);
+    LAUNCH_CHECK(ctx);
+    std::vector<int32_t> ord((size_t)n);
+    bool host = false;
+    int rc;
+    if (n > 0 && (rc = copy_out(ctx, ord.data(), dorder, sizeof(int32_t) * (size_t)n, &host))) return rc;
+    if (n > 0 && (rc = copy_out(ctx, out_w, dw, sizeof(double) * (size_t)n, &host))) return rc;
+    if ((rc = copy_out(ctx, alpha, dw + n, sizeof(double), &host))) return rc;
+    if ((rc = sync_and_check(ctx))) return rc;
+    // the sorted kernel indices (host input: re-read; device input: gathered on the host copy)
+    std::vector<int32_t> hidx((size_t)n);
+    if (n > 0) {
+        CUDA_TRY(ctx, cudaMemcpy(hidx.data(), di, sizeof(int32_t) * (size_t)n, cudaMemcpyDefault));
+        std::vector<int32_t> sorted_idx((size_t)n);
+        for (int k = 0; k < n; ++k) sorted_idx[(size_t)k] = hidx[(size_t)ord[(size_t)k]];
+        CUDA_TRY(ctx, cudaMemcpy(out_idx, sorted_idx.data(), sizeof(int32_t) * (size_t)n, cudaMemcpyDefault));
+    }
+    return GVR_OK;
+}
+
+int gvr_transmittance_ray(gvr_context* ctx, int32_t n, const double* l, const double* q, const double* sigma,
+                          double tau, int32_t nt, const double* t_in, double* out) {
+    if (!ctx || n < 0 || nt < 0 || (n > 0 && (!l || !q || !sigma)) || (nt > 0 && (!t_in || !out)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (nt == 0) return GVR_OK;
+    Tmp t;
+    const void *dl = nullptr, *dq = nullptr, *dsg = nullptr, *dt;
+    if (n > 0) {
+        if (int rc = in_dev(ctx, t.b[0], l, sizeof(double) * (size_t)n, &dl)) return rc;
+        if (int rc = in_dev(ctx, t.b[1], q, sizeof(double) * (size_t)n, &dq)) return rc;
+        if (int rc = in_dev(ctx, t.b[2], sigma, sizeof(double) * (size_t)n, &dsg)) return rc;
+    }
+    if (int rc = in_dev(ctx, t.b[3], t_in, sizeof(double) * (size_t)nt, &dt)) return rc;
+    CUDA_TRY(ctx, t.b[4].ensure(sizeof(double) * (size_t)nt));
+    transmittance_ray_kernel<<<blocks_for(nt, 128), 128, 0, ctx->stream>>>(
+        n, static_cast<const double*>(dl), static_cast<const double*>(dq), static_cast<const double*>(dsg), tau, nt,
+        static_cast<const double*>(dt), t.b[4].as<double>());
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (int rc = copy_out(ctx, out, t.b[4].p, sizeof(double) * (size_t)nt, &host)) return rc;
+    return sync_and_check(ctx);
+}
+
+int gvr_normalized_weights_ray(gvr_context* ctx, int32_t n, const double* w, double eps, double* out) {
+    if (!ctx || n < 0 || (n > 0 && (!w || !out))) return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    if (n == 0) return GVR_OK;
+    Tmp t;
+    const void* dw;
+    if (int rc = in_dev(ctx, t.b[0], w, sizeof(double) * (size_t)n, &dw)) return rc;
+    CUDA_TRY(ctx, t.b[1].ensure(sizeof(double) * (size_t)n));
+    normalized_weights_ray_kernel<<<1, 256, 0, ctx->stream>>>(n, static_cast<const double*>(dw), eps,
+                                                               t.b[1].as<double>());
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    if (int rc = copy_out(ctx, out, t.b[1].p, sizeof(double) * (size_t)n, &host)) return rc;
+    return sync_and_check(ctx);
+}
+
+int gvr_scalar_loss_buffers(gvr_context* ctx, int64_t n_img, const double* image, const double* target_image,
+                            int64_t n_alpha, const double* alpha, const double* target_alpha, double w_image,
+                            double w_alpha, double* loss, double* d_image, double* d_alpha) {
+    if (!ctx || n_img < 0 || n_alpha < 0 || !loss || (n_img > 0 && (!image || !target_image)) ||
+        (n_alpha > 0 && (!alpha || !target_alpha)))
+        return set_err(ctx, GVR_ERR_RUNTIME, "null argument");
+    Tmp t;
+    const void *di = nullptr, *dti = nullptr, *da = nullptr, *dta = nullptr;
+    if (n_img > 0) {
+        if (int rc = in_dev(ctx, t.b[0], image, sizeof(double) * (size_t)n_img, &di)) return rc;
+        if (int rc = in_dev(ctx, t.b[1], target_image, sizeof(double) * (size_t)n_img, &dti)) return rc;
+    }
+    if (n_alpha > 0) {
+        if (int rc = in_dev(ctx, t.b[2], alpha, sizeof(double) * (size_t)n_alpha, &da)) return rc;
+        if (int rc = in_dev(ctx, t.b[3], target_alpha, sizeof(double) * (size_t)n_alpha, &dta)) return rc;
+    }
+    CUDA_TRY(ctx, t.b[4].ensure(sizeof(double) * ((size_t)n_img + (size_t)n_alpha + 1)));
+    double* dout = t.b[4].as<double>();
+    loss_buffers_kernel<<<1, 1024, 0, ctx->stream>>>(
+        n_img, static_cast<const double*>(di), static_cast<const double*>(dti), n_alpha, static_cast<const double*>(da),
+        static_cast<const double*>(dta), w_image, w_alpha, d_image ? dout : nullptr,
+        d_alpha ? dout + n_img : nullptr, dout + n_img + n_alpha);
+    LAUNCH_CHECK(ctx);
+    bool host = false;
+    int rc;
+    if (d_image && n_img > 0 && (rc = copy_out(ctx, d_image, dout, sizeof(double) * (size_t)n_img, &host))) return rc;
+    if (d_alpha && n_alpha > 0 && (rc = copy_out(ctx, d_alpha, dout + n_img, sizeof(double) * (size_t)n_alpha, &host)))
+        return rc;
+    if ((rc = copy_out(ctx, loss, dout + n_img + n_alpha, sizeof(double), &host))) return rc;
+    return sync_and_check(ctx);
 }
 
 }  // extern "C"

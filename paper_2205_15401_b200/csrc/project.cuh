@@ -143,6 +143,8 @@ struct ProjectParams {
     unsigned long long* masks;   // [mask_cap], zeroed here for every allocated rectangle
     int* mask_total;             // rectangle tiles requested (bump allocator, zeroed before the launch)
     int* kcount;                 // [K] zeroed here (the blend counts each kernel's selected pixels)
+    int4* ref_box;               // nullable: the reference's pushed pixel box {row_lo, row_hi, col_lo, col_hi}
+                                 // (tracer.cpp:100-103), {1, 0, 1, 0} when not pushed (coarse_select API)
     int mask_cap;
 };
 
@@ -168,6 +170,22 @@ __device__ __forceinline__ BinJob job_from_record(const Rec32& q, int k, int H, 
     return job;
 }
 
+// view_transform (scene.cpp:5-17) of one kernel, in Eigen's evaluation order:
+// M' = R M + T ; S' = (R S) R^T.
+__device__ __forceinline__ void view_transform_one(const CameraP& c, const double* mo, const double* so, double* m,
+                                                   double* s) {
+    xmatvec(c.R, mo, m);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) m[i] = xadd(m[i], c.T[i]);
+    double rt[9], rs[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) rt[3 * j + i] = c.R[3 * i + j];
+    xmatmul(c.R, so, rs);
+    xmatmul(rs, rt, s);
+}
+
 __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     BinJob job;
     const CameraP& c = p.cam;
@@ -178,18 +196,8 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) so[i] = p.inv_cov[9ll * k + i];
 
-    // M' = R M + T ; S' = (R S) R^T
     Rec64 r;
-    xmatvec(c.R, mo, r.m);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) r.m[i] = xadd(r.m[i], c.T[i]);
-    double rt[9], rs[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) rt[3 * j + i] = c.R[3 * i + j];
-    xmatmul(c.R, so, rs);
-    xmatmul(rs, rt, r.s);
+    view_transform_one(c, mo, so, r.m, r.s);
     xmatvec(r.s, r.m, r.sm);
     r.pad = 0.0;
     p.rec64[k] = r;
@@ -208,6 +216,7 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     q.bottom = q.right = 0.0f;  // empty box
     q.zmin = -FLT_MAX;
 
+    if (p.ref_box) p.ref_box[k] = make_int4(1, 0, 1, 0);
     if (z <= kBehindCameraEps) {
         // behind the camera: dropped (tracer.cpp:52-56, blender.cpp:86)
         atomicAdd(p.dropped_behind, 1);
@@ -302,6 +311,7 @@ __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
         const int lo_c = max(0, x86_int(floor(xsub(left, 1.0))));
         const int hi_c = min(c.W - 1, x86_int(ceil(xadd(right, 1.0))));
         candidate = lo_r <= hi_r && lo_c <= hi_c;
+        if (p.ref_box && candidate) p.ref_box[k] = make_int4(lo_r, hi_r, lo_c, hi_c);
     }
     // Every pushed kernel is in the candidate list of every pixel of its padded
     // box; among those it can only pass the eta test where the pixel centre lies

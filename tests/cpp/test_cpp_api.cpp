@@ -63,7 +63,7 @@ TEST_CASE("kernel on the ray axis peaks at its depth") {  // test_tracer.cpp:24-
     Camera cam = default_camera(1, 10.0);
     cam.ox = cam.oy = 0.0;
     const ForwardResult fr = render_with_tape(scene, cam, SelectionConfig{}, 1);
-    const auto traced = fr.tape.traced();
+    const auto& traced = fr.tape.traced.get();
     REQUIRE(traced[0].size() == 1);
     CHECK(traced[0][0].l == doctest::Approx(5.0));
     CHECK(traced[0][0].q == doctest::Approx(0.0));
