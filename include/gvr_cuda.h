@@ -116,6 +116,10 @@ typedef struct {
     double* d_translation; /* 3 */
 } gvr_gradients;
 
+/* SHA-256 prefix of the sources the library was built from (build.py:
+ * source_hash); the Python loader refuses a library that does not match. */
+const char* gvr_build_hash(void);
+
 /* ---- context: device, stream, scratch arenas ---------------------------- */
 int gvr_context_create(int device, gvr_context** out);
 void gvr_context_destroy(gvr_context* ctx);

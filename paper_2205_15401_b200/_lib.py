@@ -83,6 +83,7 @@ EXPORTED_SYMBOLS = (
     "gvr_transmittance_ray",
     "gvr_normalized_weights_ray",
     "gvr_scalar_loss_buffers",
+    "gvr_build_hash",
 )
 
 
@@ -144,6 +145,19 @@ def load() -> ctypes.CDLL:
             f"{LIB_PATH} is missing: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')"
         )
     lib = ctypes.CDLL(LIB_PATH)
+    lib.gvr_build_hash.restype = ctypes.c_char_p
+    lib.gvr_build_hash.argtypes = []
+    if "GVR_LIB_PATH" not in os.environ:  # A/B experiment builds are loaded on purpose
+        from . import build as _build
+
+        try:
+            want = _build.source_hash()
+        except OSError:  # sources not shipped next to the library
+            want = None
+        got = lib.gvr_build_hash().decode()
+        if want is not None and got != want:
+            raise ImportError(f"{LIB_PATH} was built from other sources (hash {got}, sources {want}): rebuild it "
+                              "(python -c 'import __graft_entry__ as g; g.build()')")
     vp, i32, dp = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
     sig = {
         "gvr_context_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),

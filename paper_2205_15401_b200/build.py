@@ -38,10 +38,28 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def source_hash() -> str:
+    """SHA-256 (first 16 hex digits) of every CUDA source and the C ABI header:
+    embedded in libgvr_cuda.so (gvr_build_hash) and checked at load time, so a
+    stale library cannot silently stand in for the sources next to it."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "gvr_cuda.h")]:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "gvr_cuda.h")]
-    if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
+    stale = force or _stale(LIB, deps)
+    if not stale:  # same mtimes, other sources (e.g. a checkout): the embedded hash decides
+        with open(LIB, "rb") as fh:
+            stale = source_hash().encode() not in fh.read()
+    if stale:
+        cmd = [_nvcc(), *NVCC_FLAGS, f"-DGVR_SOURCE_HASH=\"{source_hash()}\"",
+               *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

@@ -438,6 +438,11 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
 
 extern "C" {
 
+#ifndef GVR_SOURCE_HASH
+#define GVR_SOURCE_HASH "unknown"
+#endif
+const char* gvr_build_hash(void) { return GVR_SOURCE_HASH; }
+
 int gvr_context_create(int device, gvr_context** out) {
     if (!out) return GVR_ERR_RUNTIME;
     *out = nullptr;

@@ -106,33 +106,6 @@ def mesh_to_gaussians_isotropic(verts, faces, zeta: float, colors) -> GaussianSc
     return GaussianScene(verts.copy(), inv_cov, attr, 1.0)
 
 
-def pointcloud_to_gaussians(points, colors=None, zeta: float = 0.5, neighbors: int = 3) -> GaussianScene:
-    """``pointcloud_to_gaussians`` (convert.cpp:132-180): isotropic kernels with
-    sigma = (d/2)^2 / ln(1/zeta), d = mean distance to the m nearest points."""
-    pts = np.asarray(points, dtype=np.float64)
-    n = pts.shape[0]
-    if n <= neighbors:
-        raise ValueError("point cloud needs more points than requested neighbors")
-    diff = pts[:, None, :] - pts[None, :, :]
-    sq = diff * diff
-    d2 = (sq[..., 0] + sq[..., 1]) + sq[..., 2]
-    np.fill_diagonal(d2, np.inf)
-    near = np.sort(np.partition(d2, neighbors - 1, axis=1)[:, :neighbors], axis=1)
-    mean_dist = np.zeros(n)
-    for m in range(neighbors):
-        mean_dist += np.sqrt(near[:, m])
-    mean_dist /= neighbors
-    if np.any(mean_dist == 0.0):
-        raise ValueError("duplicate points give zero neighbor distance")
-    half = mean_dist / 2.0
-    sigma = half * half / math.log(1.0 / zeta)
-    inv_cov = np.zeros((n, 3, 3))
-    for d in range(3):
-        inv_cov[:, d, d] = 1.0 / sigma
-    attr = np.ones((n, 3)) if colors is None else np.asarray(colors, dtype=np.float64).copy()
-    return GaussianScene(pts.copy(), inv_cov, attr, 1.0)
-
-
 def make_cuboid_scene(size, min_kernels: int, zeta: float, color, center) -> GaussianScene:
     """shapes.cpp:108-116: smallest div with 6 div^2 + 2 >= min_kernels."""
     div = 1
