@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-slots", type=int, default=4, help="contexts the end-to-end steps are pipelined over")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured graph")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 multi-view batch measurement")
     ap.add_argument("--c3-views", type=int, default=64, help="C3 batch size (views over all ranks)")
@@ -379,6 +380,95 @@ def measure_c5(args, ctx, stream, dev, rank, world):
             "loss_first": first, "loss_last": last}
 
 
+def measure_e2e(args, ctx, stream, dev, scene, cam, cfg, ti_h, ta_h, flush, world):
+    """End to end through the C ABI with HOST buffers: every step uploads its
+    inputs (the scene arrays and the loss targets) from pinned host memory and
+    reads back image / alpha / depth, the loss and the whole GradientBundle.
+    Steps are pipelined over --e2e-slots contexts in asynchronous host-buffer mode
+    (gvr_context_set_async): step i's copies run on the copy engines under step
+    i-1's kernels; a step's outputs are consumed (context synchronised, deferred
+    scene validation and non-finite checks read) before its slot is reused.
+    Timed on the host clock around the whole loop (both contexts drained)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_15401_b200 as gvr
+
+    H = W = IMAGE
+    K = scene.size
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    h_c, h_s, h_a = pin(scene.centers), pin(scene.inv_cov), pin(scene.attr)
+    h_ti, h_ta = pin(ti_h), pin(ta_h)
+    slots = []
+    ns = max(1, args.e2e_slots)
+    for _ in range(ns):
+        c = gvr.Context(ctx.device)
+        c.set_async(True)
+        out = dict(img=torch.empty((H, W, 3), dtype=torch.float64).pin_memory(),
+                   alpha=torch.empty((H, W, 1), dtype=torch.float64).pin_memory(),
+                   depth=torch.empty((H, W, 1), dtype=torch.float64).pin_memory(),
+                   loss=torch.zeros(1, dtype=torch.float64).pin_memory(),
+                   gc=torch.empty((K, 3), dtype=torch.float64).pin_memory(),
+                   gs=torch.empty((K, 3, 3), dtype=torch.float64).pin_memory(),
+                   ga=torch.empty((K, 3), dtype=torch.float64).pin_memory(),
+                   gr=torch.empty((3, 3), dtype=torch.float64).pin_memory(),
+                   gt=torch.empty(3, dtype=torch.float64).pin_memory())
+        slots.append((c, gvr.DeviceScene(c), gvr.Tape(c), out))
+
+    def enqueue(slot):
+        c, sc, tp, o = slot
+        sc.set_raw(K, 3, scene.tau, h_c, h_s, h_a)  # H2D + device validation (deferred)
+        gvr.render_into(c, sc, cam, cfg, tp, o["img"], o["alpha"], o["depth"])  # D2H image/alpha/depth
+        gvr.scalar_loss_into(tp, h_ti, h_ta, 1.0, 1.0, o["loss"])  # H2D targets, D2H loss
+        gvr.backward_into(tp, None, None, gvr.GradFlags(), o["gc"], o["gs"], o["ga"], o["gr"], o["gt"])  # D2H
+
+    def consume(slot):
+        c, sc, tp, o = slot
+        c.synchronize()
+        sc.check()  # GaussianScene::validate of this step's upload
+        tp.check_finite()  # validate_finite of this step's render
+        return float(o["loss"][0])
+
+    for i in range(2 * ns):  # warm-up (sizes every buffer)
+        enqueue(slots[i % ns])
+        consume(slots[i % ns])
+    e_steps = max(6, min(args.steps, 40))
+    torch.cuda.synchronize(dev)
+    flush.zero_()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(e_steps):
+        if i >= ns:
+            consume(slots[i % ns])
+        enqueue(slots[i % ns])
+    for i in range(max(0, e_steps - ns), e_steps):
+        consume(slots[i % ns])
+    e_ms = (time.perf_counter() - t0) * 1e3
+    te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # the same calls synchronous, one step at a time (no pipelining), for reference
+    c0 = slots[0]
+    c0[0].set_async(False)
+    s_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    for _ in range(s_steps):
+        enqueue(c0)
+    sync_ms = (time.perf_counter() - t1) * 1e3 / s_steps
+    h2d = 8 * (K * 15) + 8 * (H * W * 4)
+    d2h = 8 * (H * W * 5) + 8 * (K * 15 + 12) + 8
+    return {"value": world * e_steps / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": e_steps, "ms_per_step": float(te.item()) / e_steps,
+            "synchronous_ms_per_step": sync_ms, "slots": ns,
+            "path": "per step: gvr_scene_set(pinned host) -> gvr_render(host image/alpha/depth) -> "
+                    "gvr_scalar_loss(host targets, host loss) -> gvr_backward(host GradientBundle); "
+                    f"asynchronous host-buffer mode, steps round-robin over {ns} contexts, each step's results "
+                    "consumed (synchronised + validated) before its context is reused; host wall clock"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -518,50 +608,7 @@ def run_ours(args):
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_c, h_s, h_a = pin(scene.centers), pin(scene.inv_cov), pin(scene.attr)
-        h_ti, h_ta = pin(ti_h), pin(ta_h)
-        h_img = torch.empty((H, W, 3), dtype=torch.float64).pin_memory()
-        h_alpha = torch.empty((H, W, 1), dtype=torch.float64).pin_memory()
-        h_depth = torch.empty((H, W, 1), dtype=torch.float64).pin_memory()
-        h_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
-        h_gc = torch.empty((K, 3), dtype=torch.float64).pin_memory()
-        h_gs = torch.empty((K, 3, 3), dtype=torch.float64).pin_memory()
-        h_ga = torch.empty((K, 3), dtype=torch.float64).pin_memory()
-        h_gr = torch.empty((3, 3), dtype=torch.float64).pin_memory()
-        h_gt = torch.empty(3, dtype=torch.float64).pin_memory()
-        escene = gvr.DeviceScene(ctx)
-        etape = gvr.Tape(ctx)
-
-        def e2e_step():
-            escene.set_raw(K, 3, scene.tau, h_c, h_s, h_a)  # H2D + device validation
-            gvr.render_into(ctx, escene, cam, cfg, etape, h_img, h_alpha, h_depth)  # D2H buffers
-            gvr.scalar_loss_into(etape, h_ti, h_ta, 1.0, 1.0, h_loss)  # H2D targets, D2H loss
-            gvr.backward_into(etape, None, None, gvr.GradFlags(), h_gc, h_gs, h_ga, h_gr, h_gt)  # D2H bundle
-
-        for _ in range(3):
-            e2e_step()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e_steps = max(5, min(args.steps, 30))
-        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e_steps)]
-        for a, b in eev:
-            flush.zero_()
-            a.record(stream)
-            e2e_step()
-            b.record(stream)
-        torch.cuda.synchronize(dev)
-        e_ms = sum(a.elapsed_time(b) for a, b in eev)
-        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = 8 * (K * 15) + 8 * (H * W * 4)
-        d2h = 8 * (H * W * 5) + 8 * (K * 15 + 12) + 8
-        e2e = {"value": world * e_steps / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": e_steps,
-               "path": "gvr_scene_set(host) -> gvr_render(host image/alpha/depth) -> gvr_scalar_loss(host targets, "
-                       "host loss) -> gvr_backward(host GradientBundle)"}
+        e2e = measure_e2e(args, ctx, stream, dev, scene, cam, cfg, ti_h, ta_h, flush, world)
 
     # ---------------- C3 multi-view batch (configs[2])
     c3 = None

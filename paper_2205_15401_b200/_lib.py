@@ -84,6 +84,7 @@ EXPORTED_SYMBOLS = (
     "gvr_normalized_weights_ray",
     "gvr_scalar_loss_buffers",
     "gvr_build_hash",
+    "gvr_context_set_async",
 )
 
 
@@ -198,6 +199,7 @@ def load() -> ctypes.CDLL:
         "gvr_tape_list_stats": (ctypes.c_int, [vp, vp, vp]),
         "gvr_context_set_list_smem": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_tape_check_finite": (ctypes.c_int, [vp, vp]),
+        "gvr_context_set_async": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_trace_pairs": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
         "gvr_view_transform": (ctypes.c_int, [vp, i32, vp, vp, ctypes.POINTER(GvrCamera), vp, vp]),
         "gvr_pixel_rays": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), ctypes.c_int64, vp, vp, vp]),

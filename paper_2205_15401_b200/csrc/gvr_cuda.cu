@@ -99,6 +99,7 @@ struct gvr_context {
     int list_smem = kSelListSmem;  // test hook: longest list sorted in shared memory
     long long pool_override = 0;  // tile-list pool capacity in entries (test hook); 0 = automatic
     bool capturing = false;  // stream capture in progress: no host syncs, no allocations, no timers
+    bool async = false;      // host-buffer calls enqueue their copies and return (gvr_context_set_async)
     Buf flags;  // [0] dropped_behind (int), [1] nonfinite (int), [2..3] first_error (u64), [4..5] loss (double)
     int* h_flags = nullptr;  // pinned mirror (64 B)
     Buf scratch[4];           // staging of host inputs / outputs of the helper entry points
@@ -637,6 +638,13 @@ int gvr_context_set_list_smem(gvr_context* ctx, int n) {
     return GVR_OK;
 }
 
+int gvr_context_set_async(gvr_context* ctx, int on) {
+    if (!ctx) return GVR_ERR_RUNTIME;
+    if (int rc = sync_and_check(ctx)) return rc;
+    ctx->async = on != 0;
+    return GVR_OK;
+}
+
 int gvr_context_set_precise(gvr_context* ctx, int on) {
     if (!ctx) return GVR_ERR_RUNTIME;
     ctx->precise = on != 0;
@@ -688,6 +696,7 @@ int32_t gvr_scene_attr_dim(const gvr_scene* s) { return s ? s->D : 0; }
 int gvr_scene_set(gvr_context* ctx, gvr_scene* s, int32_t K, int32_t D, double tau, const double* centers,
                   const double* inv_cov, const double* attr) {
     if (!ctx || !s) return GVR_ERR_RUNTIME;
+    if (ctx->async) return gvr_scene_set_deferred(ctx, s, K, D, tau, centers, inv_cov, attr);
     s->valid = false;
     s->deferred = false;
     ++s->version;
@@ -1097,7 +1106,7 @@ extern "C" int gvr_render_shard(gvr_context* ctx, const gvr_scene* scene, const 
                                 int32_t nshards) {
     bool host = false;
     if (int rc = render_impl(ctx, scene, camera, cfg, tape, out, shard, nshards, &host)) return rc;
-    if (!host) return GVR_OK;
+    if (!host || ctx->async) return GVR_OK;  // async: gvr_context_synchronize + gvr_tape_check_finite
     if (int rc = sync_and_check(ctx)) return rc;
     if ((tape->h_flags[kListStats + 2] > 0 && ctx->pool_override == 0) ||
         ((long long)tape->h_flags[kMaskTotal] > (long long)(tape->masks.cap / sizeof(unsigned long long)) &&
@@ -1207,7 +1216,7 @@ extern "C" int gvr_scalar_loss(gvr_context* ctx, gvr_tape* t, const double* targ
     if (int rc = scalar_loss_impl(ctx, t, target_image, target_alpha, w_image, w_alpha, loss_out, d_image_out,
                                   d_alpha_out, &host))
         return rc;
-    return host ? sync_and_check(ctx) : GVR_OK;
+    return host && !ctx->async ? sync_and_check(ctx) : GVR_OK;
 }
 
 extern "C" {
@@ -1401,7 +1410,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         if ((rc = copy_out(ctx, out->d_attr, t->d_attr.p, sizeof(double) * (size_t)D * K, &host))) return rc;
         if ((rc = copy_out(ctx, out->d_rotation, t->d_rt.p, sizeof(double) * 9, &host))) return rc;
         if ((rc = copy_out(ctx, out->d_translation, t->d_rt.as<double>() + 9, sizeof(double) * 3, &host))) return rc;
-        if (host) return sync_and_check(ctx);
+        if (host && !ctx->async) return sync_and_check(ctx);
     }
     return GVR_OK;
 }

@@ -117,6 +117,12 @@ class Context:
         """Test hook: tile-list pool capacity in entries, 0 = automatic (tiles whose list does not fit stream every kernel)."""
         self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
 
+    def set_async(self, on: bool = True) -> None:
+        """Host-buffer calls enqueue their copies and return (gvr_context_set_async):
+        synchronize() before reading results; scene validation and the non-finite
+        check are then read with DeviceScene.check() / Tape.check_finite()."""
+        self.check(self.lib.gvr_context_set_async(self.handle, int(bool(on))))
+
     def set_list_smem(self, n: int) -> None:
         """Test hook: tile lists longer than n (<= 2048) are sorted in global memory."""
         self.check(self.lib.gvr_context_set_list_smem(self.handle, int(n)))

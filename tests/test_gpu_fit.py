@@ -293,3 +293,40 @@ def test_fitter_stops_updating_after_a_non_finite_loss(ctx):
     healthy = Fitter(ctx, target, views, adam=AdamConfig(lr=0.01))
     healthy.step()
     assert not healthy.diverged
+
+
+def test_async_host_buffer_mode_matches_synchronous_calls():
+    """gvr_context_set_async: host-buffer calls return before their copies finish;
+    after synchronize the outputs equal the synchronous calls' bit for bit, and
+    the deferred checks report an invalid upload."""
+    import torch
+    scene = gvr.make_bench_scene(2000)
+    cam = gvr.make_bench_camera(64)
+    rng = np.random.default_rng(2)
+    ti = torch.tensor(rng.uniform(0, 1, (64, 64, 3))).pin_memory()
+    ta = torch.tensor(rng.uniform(0, 1, (64, 64, 1))).pin_memory()
+    results = []
+    for mode in (False, True):
+        c = gvr.Context(0)
+        c.set_async(mode)
+        ds = gvr.DeviceScene(c).set_raw(scene.size, 3, scene.tau, torch.tensor(scene.centers).pin_memory(),
+                                        torch.tensor(scene.inv_cov).pin_memory(), torch.tensor(scene.attr).pin_memory())
+        tp = gvr.Tape(c)
+        img = torch.empty((64, 64, 3), dtype=torch.float64).pin_memory()
+        loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+        gc = torch.empty((scene.size, 3), dtype=torch.float64).pin_memory()
+        gvr.render_into(c, ds, cam, SelectionConfig(), tp, img)
+        gvr.scalar_loss_into(tp, ti, ta, 1.0, 1.0, loss)
+        gvr.backward_into(tp, None, None, gvr.GradFlags(), gc)
+        c.synchronize()
+        ds.check()
+        tp.check_finite()
+        results.append((img.clone(), loss.clone(), gc.clone()))
+        if mode:
+            bad = scene.inv_cov.copy()
+            bad[3, 0, 1] += 1.0
+            ds.set_raw(scene.size, 3, scene.tau, scene.centers, bad, scene.attr)  # returns: validated later
+            with pytest.raises(ValidationError, match=r"not symmetric \(kernel 3\)"):
+                ds.check()
+    for a, b in zip(results[0], results[1]):
+        assert torch.equal(a, b)
