@@ -24,7 +24,9 @@ struct BwdParams {
     const int4* kinfo;           // [K] mask rectangle of each kernel (project_kernel)
     const unsigned long long* masks;  // per (kernel, tile): pixels of the tile that selected the kernel
     const int* slot_off;              // per (kernel, tile): first record of its pixels (appearance_kernel)
-    double4* bent;                    // records, 2 x 32 B: {d_l, d_q, d_sigma, W} {ray, pixel}
+    double4* bent;                    // records {d_l, d_q, d_sigma, W}
+    int2* bkey;                       // records' {pixel, kernel}
+    double4* rays;                    // [P] the pixel's ray (pixel_ray), for the record pass
     // fallback for kernels without a mask rectangle (mask pool full): FP64 atomics
     double* acc;            // [K*9] camera space: dm(3), dS upper (00 01 02 11 12 22)
     double* attr_fb;        // [K*D]
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
 
     double d[3];
     pixel_ray(p.cam, i, j, d);
+    if (sub == 0) p.rays[pix] = make_double4(d[0], d[1], d[2], 0.0);
     const double tau = p.tau;
     // d_image of the pixel in registers for D <= 4 (unrolled with constant
     // indices: a runtime-indexed array would live in local memory)
@@ -217,8 +220,8 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
             const int slot = ki.x + (i / TILE - (ki.y >> 16)) * ki.z + (j / TILE - (ki.y & 0xffff));
             const int bit = (i % TILE) * TILE + j % TILE;
             const int rec = p.slot_off[slot] + __popcll(p.masks[slot] & ((1ull << bit) - 1ull));
-            p.bent[2ll * rec] = make_double4(dl, dq, dsg, w);
-            p.bent[2ll * rec + 1] = make_double4(d[0], d[1], d[2], __longlong_as_double((pix << 32) | (unsigned)kid));
+            p.bent[rec] = make_double4(dl, dq, dsg, w);
+            p.bkey[rec] = make_int2((int)pix, kid);
             continue;
         }
         backward_fallback(p.rec64 + kid, p.acc + 9ll * kid, p.attr_fb + (long long)p.D * kid,
@@ -405,7 +408,9 @@ struct GatherParams {
     const int4* kinfo;
     const int2* app;        // [K] {first record, count}
     const int* total;       // records of the render
-    const double4* bent;    // records, 2 x 32 B: {d_l, d_q, d_sigma, W} {ray, pixel << 32 | kernel}
+    const double4* bent;    // records {d_l, d_q, d_sigma, W}
+    const int2* bkey;       // records' {pixel, kernel}
+    const double4* rays;    // [P] pixel rays (K4)
     const Rec64* rec64;
     const double* d_image;  // [P*D]
     double* pieces;         // [(K + windows) * nv]
@@ -437,11 +442,11 @@ __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
         const bool valid = r < n_rec;
         int k = -1;
         if (valid) {
-            const double4 b = p.bent[2ll * r];
-            const double4 ray = p.bent[2ll * r + 1];
-            const long long bits = __double_as_longlong(ray.w);
-            k = (int)(bits & 0xffffffffll);
-            const long long pix = bits >> 32;
+            const int2 key = p.bkey[r];
+            const double4 b = p.bent[r];
+            k = key.y;
+            const long long pix = key.x;
+            const double4 ray = p.rays[pix];
             double* row = rows + lane * p.nv;
             // upstream image gradient loads issued before the chain (D <= 4 unrolled)
             double di[4];
@@ -469,9 +474,19 @@ __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
             const int j = task / p.nv, u = task - j * p.nv;
             const int start = select_bit32(heads, j);
             const int end = j + 1 < npieces ? select_bit32(heads, j + 1) : nvalid;
-            double acc = 0.0;
-            for (int q = start; q < end; ++q) acc += rows[q * p.nv + u];
-            p.pieces[(long long)(keys[start] + w) * p.nv + u] = acc;
+            // four interleaved partial sums (records q = start + 4i + r), combined in a fixed order
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int q = start;
+            for (; q + 4 <= end; q += 4) {
+                a0 += rows[q * p.nv + u];
+                a1 += rows[(q + 1) * p.nv + u];
+                a2 += rows[(q + 2) * p.nv + u];
+                a3 += rows[(q + 3) * p.nv + u];
+            }
+            if (q < end) a0 += rows[q * p.nv + u];
+            if (q + 1 < end) a1 += rows[(q + 1) * p.nv + u];
+            if (q + 2 < end) a2 += rows[(q + 2) * p.nv + u];
+            p.pieces[(long long)(keys[start] + w) * p.nv + u] = (a0 + a1) + (a2 + a3);
         }
         __syncwarp();
     }

@@ -154,7 +154,7 @@ struct gvr_tape {
     // gradients
     Buf acc, attr_fb, d_attr, d_center, d_inv_cov, d_rt;
     // deterministic backward: per-kernel mask rectangles (render), entry adjoints, CTA partials
-    Buf kinfo, masks, slot_off, app, bent, pieces, kcount, rt_part, tickets, loss_part;
+    Buf kinfo, masks, slot_off, app, bent, bkey, rays, pieces, kcount, rt_part, tickets, loss_part;
     long long mask_hint = 0;
     // host copy-out staging
     Buf stage_i, stage_w;
@@ -794,7 +794,7 @@ void gvr_tape_destroy(gvr_tape* t) {
                    &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags, &t->attr_fb, &t->kinfo,
-                   &t->masks, &t->slot_off, &t->app, &t->bent, &t->pieces, &t->kcount, &t->rt_part, &t->tickets,
+                   &t->masks, &t->slot_off, &t->app, &t->bent, &t->bkey, &t->rays, &t->pieces, &t->kcount, &t->rt_part, &t->tickets,
                    &t->loss_part};
     for (Buf* b : bufs) b->release();
     if (t->h_flags) cudaFreeHost(t->h_flags);
@@ -1282,7 +1282,9 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     CUDA_TRY(ctx, t->rt_part.ensure(sizeof(double) * 12 * ((size_t)finish_grid + rt_groups)));
     CUDA_TRY(ctx, t->pieces.ensure(sizeof(double) * (9 + (size_t)D) * ((size_t)K + windows + 1)));
 
-    CUDA_TRY(ctx, t->bent.ensure(2 * sizeof(double4) * (size_t)(P_kp > 0 ? P_kp : 1)));
+    CUDA_TRY(ctx, t->bent.ensure(sizeof(double4) * (size_t)(P_kp > 0 ? P_kp : 1)));
+    CUDA_TRY(ctx, t->bkey.ensure(sizeof(int2) * (size_t)(P_kp > 0 ? P_kp : 1)));
+    CUDA_TRY(ctx, t->rays.ensure(sizeof(double4) * (size_t)(P > 0 ? P : 1)));
     CUDA_TRY(ctx, t->app.ensure(sizeof(int2) * (size_t)(K > 0 ? K : 1)));
     CUDA_TRY(ctx, t->slot_off.ensure(sizeof(int) * (t->masks.cap / sizeof(unsigned long long) + 1)));
     CUDA_TRY(ctx, t->d_attr.ensure(sizeof(double) * (size_t)(D > 0 ? D : 1) * (K > 0 ? K : 1)));
@@ -1324,6 +1326,8 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.masks = t->masks.as<unsigned long long>();
         bp.slot_off = t->slot_off.as<int>();
         bp.bent = t->bent.as<double4>();
+        bp.bkey = t->bkey.as<int2>();
+        bp.rays = t->rays.as<double4>();
         bp.acc = t->acc.as<double>();
         bp.attr_fb = t->attr_fb.as<double>();
         const int kp = t->cfg.k_prime;
@@ -1365,6 +1369,8 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         gp.app = t->app.as<int2>();
         gp.total = reinterpret_cast<const int*>(rec_total);
         gp.bent = t->bent.as<double4>();
+        gp.bkey = t->bkey.as<int2>();
+        gp.rays = t->rays.as<double4>();
         gp.rec64 = t->rec64.as<Rec64>();
         gp.d_image = di;
         gp.pieces = t->pieces.as<double>();
