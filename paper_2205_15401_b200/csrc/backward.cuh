@@ -318,7 +318,7 @@ struct AppParams {
     int K;
     const int4* kinfo;
     const unsigned long long* masks;
-    const int* count;  // [K] records of each kernel (the blend's counts)
+    int* count;      // [K] records of each kernel (count_kernel)
     int* cta_sum;    // [ceil(K / kScanThreads)] then exclusive offsets (in place)
     int* slot_off;   // [mask slots] first record of each (kernel, tile)
     int2* app;       // [K] {first record, count}
@@ -356,7 +356,13 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* total) {
 
 __global__ void __launch_bounds__(kScanThreads) count_kernel(AppParams p) {
     const int k = blockIdx.x * kScanThreads + threadIdx.x;
-    const int c = k < p.K ? p.count[k] : 0;  // counted by the blend
+    int c = 0;  // the kernel's selected pixels: the bits of its masks (set by the blend)
+    if (k < p.K) {
+        const int4 ki = p.kinfo[k];
+        if (ki.x >= 0)
+            for (int t = 0; t < ki.w; ++t) c += __popcll(p.masks[ki.x + t]);
+        p.count[k] = c;
+    }
     int tot;
     block_exclusive_scan(c, &tot);
     if (threadIdx.x == 0) p.cta_sum[blockIdx.x] = tot;

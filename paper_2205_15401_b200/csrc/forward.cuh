@@ -802,6 +802,19 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     }
 }
 
+// The pixel's bit in each selected kernel's (kernel, tile) mask: the backward's
+// per-kernel record order (order-independent OR). Entries s = sub, sub + 4, ...
+__device__ __forceinline__ void mark_selection(const FwdParams& p, const int* b_id, int n, int sub, int g, int np,
+                                               int i, int j) {
+    for (int s = sub; s < n; s += 4) {
+        const int4 ki = p.kinfo[b_id[s * np + g] & ~kExact];
+        if (ki.x >= 0) {
+            const int slot = ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff));
+            atomicOr(p.masks + slot, 1ull << ((i % 8) * 8 + j % 8));
+        }
+    }
+}
+
 // K3b closed-form blend (blender.cpp:27-53, 98-128). CTA = one 8x8 tile with
 // 4 threads per pixel (256 threads): entries are re-traced (exact FP64) and the
 // O(n^2) transmittance sums split 4 ways; the ordered attribute/depth sums are
@@ -938,16 +951,6 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
         }
-        {
-            // the pixel's bit in the kernel's (kernel, tile) mask: the backward's
-            // per-kernel record order (order-independent OR)
-            const int4 ki = p.kinfo[b_id[s * NP + g] & ~kExact];
-            if (ki.x >= 0) {
-                const int slot = ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff));
-                atomicOr(p.masks + slot, 1ull << ((i % 8) * 8 + j % 8));
-                atomicAdd(p.kcount + (b_id[s * NP + g] & ~kExact), 1);
-            }
-        }
         // tape the traced entry for the backward and the sampler
         EntryRec er;
         er.l = lval;
@@ -1026,8 +1029,10 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             p.depth[pix] = depth;
             if (!isfinite(alpha) || !isfinite(depth) || !isfinite(wsum)) atomicExch(p.nonfinite, 1);
         }
+        mark_selection(p, b_id, n, sub, g, NP, i, j);
         return;
     }
+    mark_selection(p, b_id, n, sub, g, NP, i, j);
     if (sub != 0) return;
     double wsum = 0.0, wld = 0.0;
     for (int k = 0; k < n; ++k) {
