@@ -302,8 +302,13 @@ def _timed(fn, steps, stream, dev, world, flush=None):
 def measure_c4(args, ctx, stream, dev, rank, world):
     """C4 (BASELINE.json configs[3]): one 1024x1024 view of make_bench_scene(1e6)
     (1,003,688 kernels), fwd + ScalarLoss + bwd, image tiles dealt round-robin to
-    the ranks (gvr_render_shard: tile % N == rank); the partial gradients of the
-    ranks are summed with one NCCL all-reduce. One step = one whole render."""
+    the ranks (gvr_render_shard: tile % N == rank; each rank bins only its own
+    tiles). Gradients leave the backward packed as one row of 9 + D = 12 FP64 per
+    kernel (gvr_backward_packed) and are summed by ONE NCCL reduce-scatter (each
+    rank ends up owning K/N kernels' gradients: 12 x 8 B x K x (N-1)/N sent per
+    rank) plus a 12-value all-reduce for d_R / d_T. One step = one whole render.
+    At N = 1 the per-rank compute of shard (0, n) is also timed for n = 2, 4, 8
+    (the work one rank of an n-GPU run does, without the collective)."""
     import torch
     import torch.distributed as dist
 
@@ -315,6 +320,8 @@ def measure_c4(args, ctx, stream, dev, rank, world):
     cam = synthetic.make_bench_camera(S)
     cfg = gvr.SelectionConfig()
     K = scene.size
+    nv = 9 + 3
+    Kp = -(-K // world) * world  # rows padded to a multiple of the ranks
     dscene = gvr.DeviceScene(ctx)
     dscene.set_raw(K, 3, scene.tau, torch.from_numpy(scene.centers).to(dev), torch.from_numpy(scene.inv_cov).to(dev),
                    torch.from_numpy(scene.attr).to(dev))
@@ -324,26 +331,40 @@ def measure_c4(args, ctx, stream, dev, rank, world):
     ta = torch.tensor(rng.uniform(0, 1, (S, S, 1)), device=dev)
     img = torch.empty((S, S, 3), dtype=torch.float64, device=dev)
     loss = torch.zeros(1, dtype=torch.float64, device=dev)
-    grads = torch.zeros(K * 15 + 12, dtype=torch.float64, device=dev)
-    g_c, g_s, g_a = grads[:3 * K].view(K, 3), grads[3 * K:12 * K].view(K, 3, 3), grads[12 * K:15 * K].view(K, 3)
-    g_r, g_t = grads[15 * K:15 * K + 9].view(3, 3), grads[15 * K + 9:]
+    packed = torch.zeros((Kp, nv), dtype=torch.float64, device=dev)
+    mine = torch.empty((Kp // world, nv), dtype=torch.float64, device=dev)
+    d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
+
+    def run(shard, nshards, collective):
+        gvr.render_into(ctx, dscene, cam, cfg, tape, img, shard=(shard, nshards))
+        gvr.scalar_loss_into(tape, ti, ta, 1.0, 1.0, loss)
+        gvr.backward_packed_into(tape, None, None, gvr.GradFlags(), packed, d_rt)
+        if collective and world > 1:
+            dist.reduce_scatter_tensor(mine, packed, op=dist.ReduceOp.SUM)
+            dist.all_reduce(d_rt, op=dist.ReduceOp.SUM)
 
     def step():
-        gvr.render_into(ctx, dscene, cam, cfg, tape, img, shard=(rank, world))
-        gvr.scalar_loss_into(tape, ti, ta, 1.0, 1.0, loss)
-        gvr.backward_into(tape, None, None, gvr.GradFlags(), g_c, g_s, g_a, g_r, g_t)
-        if world > 1:
-            dist.all_reduce(grads, op=dist.ReduceOp.SUM)
+        run(rank, world, True)
 
     for _ in range(max(args.warmup, 3)):
         step()
     steps = max(3, min(args.steps, 10))
     n0 = ctx.launch_count
     ms = _timed(step, steps, stream, dev, world) / steps
-    return {"workload": f"C4: 1024x1024 view of make_bench_scene(1e6) ({K} kernels), fwd+bwd, image tiles "
-                        f"round-robin over {world} rank(s), NCCL all-reduce of the partial gradients",
-            "value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "steps": steps,
-            "gpu_launches": ctx.launch_count - n0}
+    out = {"workload": f"C4: 1024x1024 view of make_bench_scene(1e6) ({K} kernels), fwd+bwd, image tiles "
+                       f"round-robin over {world} rank(s), packed gradients summed by one NCCL reduce-scatter",
+           "value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "steps": steps,
+           "gpu_launches": ctx.launch_count - n0,
+           "collective_bytes_per_rank": (8 * nv * Kp * (world - 1) // world + 8 * 12) if world > 1 else 0}
+    if world == 1:
+        per_rank = {}
+        for n in (2, 4, 8):
+            for _ in range(2):
+                run(0, n, False)
+            per_rank[str(n)] = _timed(lambda: run(0, n, False), steps, stream, dev, 1) / steps
+        out["per_rank_compute_ms_of_n_shards"] = per_rank
+        out["reduce_scatter_bytes_per_rank_at_n"] = {str(n): 8 * nv * K * (n - 1) // n for n in (2, 4, 8)}
+    return out
 
 
 def measure_c5(args, ctx, stream, dev, rank, world):

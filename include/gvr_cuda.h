@@ -269,6 +269,14 @@ int gvr_backward(gvr_context* ctx, gvr_tape* tape, const double* d_image, const 
 int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* tape, const double* d_image, const double* d_alpha,
                             const gvr_grad_flags* flags, const gvr_gradients* out);
 
+/* As gvr_backward, with the per-kernel gradients written as one DEVICE row per
+ * kernel, packed[K*(9+D)] = [d_center(3) | d_inv_cov upper triangle (00 01 02 11
+ * 12 22) | d_attr(D)], and d_rt[12] = [d_rotation(9) | d_translation(3)] (device):
+ * the layout a multi-GPU reduction sums (tile-sharded C4: one reduce-scatter of
+ * 9+D doubles per kernel instead of 15). */
+int gvr_backward_packed(gvr_context* ctx, gvr_tape* tape, const double* d_image, const double* d_alpha,
+                        const gvr_grad_flags* flags, double* packed, double* d_rt);
+
 /* ---- fitting helpers ------------------------------------------------------ */
 /* AdamState::update (fit.cpp:20-42) on device arrays of n parameters; `step`
  * is the 1-based step count used for the bias corrections. */

@@ -24,6 +24,8 @@ from .render import (  # noqa: F401
     adam_step,
     backward,
     backward_into,
+    backward_packed_into,
+    unpack_gradients,
     backward_views_into,
     render_views_into,
     scalar_loss_views_into,

@@ -85,6 +85,7 @@ EXPORTED_SYMBOLS = (
     "gvr_scalar_loss_buffers",
     "gvr_build_hash",
     "gvr_context_set_async",
+    "gvr_backward_packed",
 )
 
 
@@ -200,6 +201,7 @@ def load() -> ctypes.CDLL:
         "gvr_context_set_list_smem": (ctypes.c_int, [vp, ctypes.c_int]),
         "gvr_tape_check_finite": (ctypes.c_int, [vp, vp]),
         "gvr_context_set_async": (ctypes.c_int, [vp, ctypes.c_int]),
+        "gvr_backward_packed": (ctypes.c_int, [vp, vp, vp, vp, ctypes.POINTER(GvrGradFlags), vp, vp]),
         "gvr_trace_pairs": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
         "gvr_view_transform": (ctypes.c_int, [vp, i32, vp, vp, ctypes.POINTER(GvrCamera), vp, vp]),
         "gvr_pixel_rays": (ctypes.c_int, [vp, ctypes.POINTER(GvrCamera), ctypes.c_int64, vp, vp, vp]),

@@ -427,6 +427,8 @@ struct GatherParams {
     double* d_center;       // [K*3]
     double* d_inv_cov;      // [K*9]
     double* d_attr;         // [K*D]
+    double* packed;         // nullable: instead of d_center / d_inv_cov / d_attr, rows of nv values
+                            // [d_center(3) | d_inv_cov upper (00 01 02 11 12 22) | d_attr(D)] (multi-GPU)
     double* rt_part;        // [gridDim.x * 12] then [groups * 12]
     unsigned* tickets;      // [1 + groups], zero between launches (reset by the last CTAs)
     double* d_rt;           // [12] d_rotation (9), d_translation (3)
@@ -537,7 +539,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
             for (int c = 0; c < p.D; ++c) {
                 double a = 0.0;
                 for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 9 + c];
-                p.d_attr[(long long)p.D * k + c] = a;
+                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = a;
+                else p.d_attr[(long long)p.D * k + c] = a;
             }
         } else if (ki.x < 0 && ki.w > 0) {  // fallback accumulators (no mask rectangle): consume, re-zero
 #pragma unroll
@@ -546,11 +549,16 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
                 p.acc[9ll * k + u] = 0.0;
             }
             for (int c = 0; c < p.D; ++c) {
-                p.d_attr[(long long)p.D * k + c] = p.attr_fb[(long long)p.D * k + c];
+                const double a = p.attr_fb[(long long)p.D * k + c];
+                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = a;
+                else p.d_attr[(long long)p.D * k + c] = a;
                 p.attr_fb[(long long)p.D * k + c] = 0.0;
             }
         } else {
-            for (int c = 0; c < p.D; ++c) p.d_attr[(long long)p.D * k + c] = 0.0;
+            for (int c = 0; c < p.D; ++c) {
+                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = 0.0;
+                else p.d_attr[(long long)p.D * k + c] = 0.0;
+            }
         }
         const double* R = p.cam.R;
         const double dsf[9] = {c9[3], c9[4], c9[5], c9[4], c9[6], c9[7], c9[5], c9[7], c9[8]};
@@ -584,15 +592,27 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
                                                          t1[3 * r + 2] * so[6 + c]);
 #pragma unroll
         for (int t = 0; t < 3; ++t) part[9 + t] = c9[t];
-        __syncwarp(__activemask());
 #pragma unroll
         for (int t = 0; t < 3; ++t) s_ctr[3 * threadIdx.x + t] = dc[t];
 #pragma unroll
         for (int t = 0; t < 9; ++t) s_cov[9 * threadIdx.x + t] = dcov[t];
+        if (p.packed) {
+            double* row = p.packed + (long long)k * p.nv;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) row[t] = dc[t];
+            row[3] = dcov[0];
+            row[4] = dcov[1];
+            row[5] = dcov[2];
+            row[6] = dcov[4];
+            row[7] = dcov[5];
+            row[8] = dcov[8];
+        }
     }
     __syncthreads();
-    stage_rows_out(p.d_center, s_ctr, k0, count, 3);
-    stage_rows_out(p.d_inv_cov, s_cov, k0, count, 9);
+    if (!p.packed) {
+        stage_rows_out(p.d_center, s_ctr, k0, count, 3);
+        stage_rows_out(p.d_inv_cov, s_cov, k0, count, 9);
+    }
     // fixed-order block reduction: shfl_down tree per warp, warps in order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)

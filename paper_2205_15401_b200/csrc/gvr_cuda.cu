@@ -435,7 +435,8 @@ __global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
 }  // namespace
 
 static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
-                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate);
+                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate,
+                         double* packed = nullptr, double* packed_rt = nullptr);
 
 extern "C" {
 
@@ -1231,10 +1232,19 @@ int gvr_backward_accumulate(gvr_context* ctx, gvr_tape* t, const double* d_image
     return backward_impl(ctx, t, d_image, d_alpha, flags, out, true);
 }
 
+int gvr_backward_packed(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
+                        const gvr_grad_flags* flags, double* packed, double* d_rt) {
+    if (!ctx || !t) return GVR_ERR_RUNTIME;
+    if (!packed || !d_rt || !is_device_ptr(packed) || !is_device_ptr(d_rt))
+        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_backward_packed needs device outputs");
+    return backward_impl(ctx, t, d_image, d_alpha, flags, nullptr, false, packed, d_rt);
+}
+
 }  // extern "C"
 
 static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, const double* d_alpha,
-                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate) {
+                         const gvr_grad_flags* flags, const gvr_gradients* out, bool accumulate, double* packed,
+                         double* packed_rt) {
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
     if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
@@ -1381,9 +1391,10 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         gp.d_center = t->d_center.as<double>();
         gp.d_inv_cov = t->d_inv_cov.as<double>();
         gp.d_attr = t->d_attr.as<double>();
+        gp.packed = packed;
         gp.rt_part = t->rt_part.as<double>();
         gp.tickets = t->tickets.as<unsigned>();
-        gp.d_rt = t->d_rt.as<double>();
+        gp.d_rt = packed_rt ? packed_rt : t->d_rt.as<double>();
         {
             StageTimer st(ctx, ST_OBJECT);
             const size_t rsmem = sizeof(double) * kRecThreads * (size_t)gp.nv;

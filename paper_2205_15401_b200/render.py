@@ -423,6 +423,33 @@ def backward_into(tape: Tape, d_image, d_alpha, flags: GradFlags = GradFlags(), 
     ctx.check(fn(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f), ctypes.byref(g)))
 
 
+def backward_packed_into(tape: Tape, d_image, d_alpha, flags: GradFlags, packed, d_rt) -> None:
+    """``gvr_backward_packed``: per-kernel rows [d_center | d_inv_cov upper | d_attr]
+    (device [K, 9 + D]) and d_rt = [d_rotation | d_translation] (device [12])."""
+    ctx = tape.ctx
+    f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
+    ctx.check(ctx.lib.gvr_backward_packed(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f),
+                                          _ptr(packed), _ptr(d_rt)))
+
+
+def unpack_gradients(packed, d_rt, D: int):
+    """Split packed rows back into (d_center [K,3], d_inv_cov [K,3,3] symmetric,
+    d_attr [K,D], d_rotation [3,3], d_translation [3]) (torch or numpy)."""
+    c = packed[:, 0:3]
+    u = packed[:, 3:9]
+    rows = [[u[:, 0], u[:, 1], u[:, 2]], [u[:, 1], u[:, 3], u[:, 4]], [u[:, 2], u[:, 4], u[:, 5]]]
+    try:
+        import torch
+
+        if isinstance(packed, torch.Tensor):
+            inv = torch.stack([torch.stack(r, dim=1) for r in rows], dim=1)
+            return c, inv, packed[:, 9:9 + D], d_rt[:9].reshape(3, 3), d_rt[9:12]
+    except ImportError:
+        pass
+    inv = np.stack([np.stack(r, axis=1) for r in rows], axis=1)
+    return c, inv, packed[:, 9:9 + D], d_rt[:9].reshape(3, 3), d_rt[9:12]
+
+
 def adam_step(ctx: Context, params, grads, m, v, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
               eps: float = 1e-8, loss=None, diverged=None) -> None:
     """``AdamState::update`` (fit.cpp:20-42) on device tensors (FP64, same length).

@@ -330,3 +330,23 @@ def test_async_host_buffer_mode_matches_synchronous_calls():
                 ds.check()
     for a, b in zip(results[0], results[1]):
         assert torch.equal(a, b)
+
+
+def test_packed_backward_equals_the_gradient_bundle(ctx):
+    """gvr_backward_packed rows unpack to gvr_backward's bundle bit for bit."""
+    import torch
+    scene = gvr.make_bench_scene(3000)
+    cam = gvr.make_orbit_camera(0.4, 0.3, 4.0, (0, 0, 4), 96, 96, 150.0)
+    rng = np.random.default_rng(8)
+    fr = gvr.render_with_tape(scene, cam, ctx=ctx)
+    di = rng.uniform(-1, 1, fr.buffers.image.shape)
+    da = rng.uniform(-1, 1, fr.buffers.alpha.shape)
+    g = gvr.backward(fr, di, da)
+    dev = torch.device("cuda:0")
+    packed = torch.zeros((scene.size, 12), dtype=torch.float64, device=dev)
+    d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
+    gvr.backward_packed_into(fr.tape, torch.tensor(di, device=dev), torch.tensor(da, device=dev), gvr.GradFlags(),
+                             packed, d_rt)
+    c, s, a, r, t = gvr.unpack_gradients(packed.cpu().numpy(), d_rt.cpu().numpy(), 3)
+    for got, want in ((c, g.d_center), (s, g.d_inv_cov), (a, g.d_attr), (r, g.d_rotation), (t, g.d_translation)):
+        assert np.array_equal(got, want)

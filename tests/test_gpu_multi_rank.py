@@ -46,11 +46,14 @@ def _c4_rank(rank, world):
     ctx = gvr.Context(0)
     fr = gvr.render_with_tape(scene, cam, ctx=ctx, shard=(rank, world))
     gvr.scalar_loss(fr.tape, gvr.ScalarLoss(ti, ta), want_grads=False)
-    g = gvr.backward(fr, None, None)
-    parts = [torch.from_numpy(np.ascontiguousarray(getattr(g, k))) for k in
-             ("d_center", "d_inv_cov", "d_attr", "d_rotation", "d_translation")]
-    allreduce_gradients(parts)
-    return fr.buffers, [p.numpy() for p in parts]
+    # the bench's C4 path: packed rows (gvr_backward_packed), summed across ranks
+    dev = torch.device("cuda:0")
+    packed = torch.zeros((scene.size, 12), dtype=torch.float64, device=dev)
+    d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
+    gvr.backward_packed_into(fr.tape, None, None, gvr.GradFlags(), packed, d_rt)
+    allreduce_gradients([packed, d_rt])
+    parts = gvr.unpack_gradients(packed.cpu().numpy(), d_rt.cpu().numpy(), 3)
+    return fr.buffers, [np.ascontiguousarray(p) for p in parts]
 
 
 def _fit_run(rank, world, steps=3):
