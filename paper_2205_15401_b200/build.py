@@ -66,7 +66,54 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+NLOHMANN = None
+for _cand in [os.path.join(p, "include", "cudnn_frontend", "thirdparty", "nlohmann") for p in sys.path if p] + [
+        "/usr/include/nlohmann"]:
+    if os.path.exists(os.path.join(_cand, "json.hpp")):
+        NLOHMANN = _cand
+        break
+CLI = os.path.join(HERE, "gvr")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The `gvr` command-line tool (paper_2205_15401_b200/cli/gvr_main.cpp) over the
+    C++ drop-in; JSON through nlohmann::json (header shipped with the Python env)."""
+    src = os.path.join(HERE, "cli", "gvr_main.cpp")
+    deps = [src, LIB] + [os.path.join(ROOT, "include", "gvr", f) for f in ("gvr.hpp", "scene_io.hpp", "image_io.hpp")]
+    if NLOHMANN is None:
+        raise RuntimeError("nlohmann/json.hpp not found: the CLI needs it")
+    if _stale(CLI, deps):
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", f"-I{ROOT}/include", f"-I{NLOHMANN}", src, f"-L{HERE}",
+               "-lgvr_cuda", "-Wl,-rpath,$ORIGIN", "-o", CLI]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return CLI
+
+
 REF_TESTS = ("test_scene", "test_tracer", "test_blender", "test_grad")
+CLI_DATA = os.path.join(ROOT, "tests", "cpp", "_build", "cli_data")
+
+
+def write_cli_data() -> str:
+    """JSON inputs of the reference's CLI tests (tests/data/{test,gradcheck,texture}_
+    {scene,camera}.json), re-serialised from the committed golden vectors (the
+    same doubles; tests/golden/make_golden.py read them from the reference)."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    from paper_2205_15401_b200 import scene_io
+    from paper_2205_15401_b200.types import Camera, GaussianScene
+
+    os.makedirs(CLI_DATA, exist_ok=True)
+    for name in ("test", "gradcheck", "texture"):
+        g = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_scene.npz"))
+        scene_io.save_scene_json(GaussianScene(g["centers"], g["inv_cov"], g["attr"], float(g["tau"])),
+                                 os.path.join(CLI_DATA, f"{name}_scene.json"))
+        c = g["camera"]
+        scene_io.save_camera_json(Camera(c[:9].reshape(3, 3), c[9:12], c[12], c[13], c[14], int(c[15]), int(c[16])),
+                                  os.path.join(CLI_DATA, f"{name}_camera.json"))
+    return CLI_DATA
 REF_TEST_DIR = os.path.join(ROOT, "tests", "cpp", "_build")
 
 
@@ -94,6 +141,20 @@ def build_reference_suites(verbose: bool = False) -> list:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.run(cmd, check=True)
         out.append(exe)
+    # the CLI suite (test_cli.cpp) against the `gvr` tool
+    if NLOHMANN is not None and os.path.exists(CLI):
+        write_cli_data()
+        exe = os.path.join(REF_TEST_DIR, "ref_test_cli")
+        cpp = os.path.join(src, "test_cli.cpp")
+        deps = [cpp] + [os.path.join(ROOT, "include", "gvr", f) for f in ("gvr.hpp", "scene_io.hpp", "image_io.hpp")]
+        if _stale(exe, deps):
+            cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", f"-I{ROOT}/oracle/shim", f"-I{NLOHMANN}",
+                   f'-DGVR_CLI_PATH="{CLI}"', f'-DGVR_TEST_DATA="{CLI_DATA}"', cpp, f"-L{HERE}", "-lgvr_cuda",
+                   "-Wl,-rpath,$ORIGIN/../../../paper_2205_15401_b200", "-o", exe]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.run(cmd, check=True)
+        out.append(exe)
     return out
 
 
@@ -107,5 +168,6 @@ def build_oracle(verbose: bool = False) -> None:
 
 if __name__ == "__main__":
     build_cuda(force="--force" in sys.argv, verbose=True)
+    build_cli(verbose=True)
     build_reference_suites(verbose=True)
     build_oracle(verbose=True)
