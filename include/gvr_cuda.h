@@ -278,8 +278,9 @@ int gvr_backward_packed(gvr_context* ctx, gvr_tape* tape, const double* d_image,
                         const gvr_grad_flags* flags, double* packed, double* d_rt);
 
 /* ---- fitting helpers ------------------------------------------------------ */
-/* AdamState::update (fit.cpp:20-42) on device arrays of n parameters; `step`
- * is the 1-based step count used for the bias corrections. */
+/* AdamState::update (fit.cpp:20-42) on arrays of n parameters (device, or host:
+ * staged and copied back, synchronising); `step` is the 1-based step count used
+ * for the bias corrections. */
 int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
                   int64_t step, double lr, double beta1, double beta2, double eps);
 

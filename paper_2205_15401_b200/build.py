@@ -79,7 +79,8 @@ def build_cli(verbose: bool = False) -> str:
     """The `gvr` command-line tool (paper_2205_15401_b200/cli/gvr_main.cpp) over the
     C++ drop-in; JSON through nlohmann::json (header shipped with the Python env)."""
     src = os.path.join(HERE, "cli", "gvr_main.cpp")
-    deps = [src, LIB] + [os.path.join(ROOT, "include", "gvr", f) for f in ("gvr.hpp", "scene_io.hpp", "image_io.hpp")]
+    deps = [src, LIB] + [os.path.join(ROOT, "include", "gvr", f)
+                         for f in ("gvr.hpp", "scene_io.hpp", "image_io.hpp", "fit.hpp")]
     if NLOHMANN is None:
         raise RuntimeError("nlohmann/json.hpp not found: the CLI needs it")
     if _stale(CLI, deps):
@@ -113,6 +114,14 @@ def write_cli_data() -> str:
         c = g["camera"]
         scene_io.save_camera_json(Camera(c[:9].reshape(3, 3), c[9:12], c[12], c[13], c[14], int(c[15]), int(c[16])),
                                   os.path.join(CLI_DATA, f"{name}_camera.json"))
+    # the fitting fixtures are read from the reference's data at build time (like
+    # tests/golden/make_golden.py) and re-serialised into the ignored build tree
+    ref_data = "/root/reference/proj/tests/data"
+    for name in ("part_red", "part_blue"):
+        scene_io.save_scene_json(scene_io.load_scene_json(os.path.join(ref_data, f"{name}.json")),
+                                 os.path.join(CLI_DATA, f"{name}.json"))
+    scene_io.save_camera_json(scene_io.load_camera_json(os.path.join(ref_data, "fit_camera.json")),
+                              os.path.join(CLI_DATA, "fit_camera.json"))
     return CLI_DATA
 REF_TEST_DIR = os.path.join(ROOT, "tests", "cpp", "_build")
 

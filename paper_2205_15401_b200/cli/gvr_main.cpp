@@ -5,12 +5,15 @@
 //
 //   render           gvr_main.cpp:111-137    extract-texture  gvr_main.cpp:434-449
 //   bench            gvr_main.cpp:154-186    rerender         gvr_main.cpp:451-466
-//   gradcheck        gvr_main.cpp:188-223
-// The converters (convert: OBJ/PLY -> scene) and the fitting drivers (fit-shape,
-// fit-translation, fit-pose) are not part of this backend's CLI: they exit 1 with
-// a message (the device fitting loop is the Python Fitter, paper_2205_15401_b200/fit.py).
+//   gradcheck        gvr_main.cpp:188-223    fit-translation  gvr_main.cpp:271-352
+//                                            fit-pose         gvr_main.cpp:354-432
+// The converters (convert: OBJ/PLY -> scene) and fit-shape (whose initial scene is
+// an icosphere through the mesh converter) are not part of this backend's CLI: they
+// exit 1 with a message (the device shape-fitting loop is the Python Fitter,
+// paper_2205_15401_b200/fit.py, and gvr::fit_shape in include/gvr/fit.hpp).
 //
 // Exit codes: 0 ok, 1 runtime error, 2 usage / validation error (gvr_main.cpp:19-21, 612-621).
+#include "gvr/fit.hpp"
 #include "gvr/image_io.hpp"
 #include "gvr/scene_io.hpp"
 
@@ -38,6 +41,59 @@ struct UsageError : std::runtime_error {
 
 void require_file(const fs::path& path, const std::string& what) {
     if (!fs::exists(path)) throw UsageError(what + " file does not exist: " + path.string());
+}
+
+nlohmann::json load_config(const fs::path& path) {
+    require_file(path, "config");
+    std::ifstream in(path);
+    nlohmann::json j;
+    try {
+        in >> j;
+    } catch (const nlohmann::json::exception& e) {
+        throw UsageError("invalid JSON in " + path.string() + ": " + e.what());
+    }
+    return j;
+}
+
+// gvr_main.cpp:46-66
+gvr::SelectionConfig selection_from_json(const nlohmann::json& j) {
+    gvr::SelectionConfig sel;
+    if (j.contains("selection")) {
+        const auto& s = j.at("selection");
+        sel.eta = s.value("eta", sel.eta);
+        sel.k_prime = s.value("k_prime", sel.k_prime);
+        sel.coarse_enabled = s.value("coarse", sel.coarse_enabled);
+    }
+    return sel;
+}
+
+gvr::LossSpec loss_from_json(const nlohmann::json& j) {
+    gvr::LossSpec spec;
+    if (j.contains("loss")) {
+        const auto& l = j.at("loss");
+        spec.rgb_weight = l.value("rgb", spec.rgb_weight);
+        spec.silhouette_weight = l.value("silhouette", spec.silhouette_weight);
+        spec.edge_weight = l.value("edge", spec.edge_weight);
+        spec.laplacian_weight = l.value("laplacian", spec.laplacian_weight);
+    }
+    return spec;
+}
+
+// gvr_main.cpp:74-92
+void write_report_json(const gvr::FitReport& report, const nlohmann::json& extra, const fs::path& path) {
+    nlohmann::json j = extra;
+    j["iterations"] = report.iterations;
+    j["diverged"] = report.diverged;
+    j["loss_trace"] = report.loss_trace;
+    for (const auto& [key, value] : report.metrics) j["metrics"][key] = value;
+    gvr::atomic_write_text(path, j.dump(2) + "\n");
+}
+
+void write_loss_csv(const gvr::FitReport& report, const fs::path& path) {
+    std::string csv = "iteration,loss\n";
+    for (size_t i = 0; i < report.loss_trace.size(); ++i)
+        csv += std::to_string(i) + "," + std::to_string(report.loss_trace[i]) + "\n";
+    gvr::atomic_write_text(path, csv);
 }
 
 // ---------------------------------------------------------------- flags
@@ -352,6 +408,153 @@ int cmd_extract_texture(const Args& a) {
     return kExitOk;
 }
 
+int cmd_fit_translation(const Args& a) {
+    require_opts(a, {"config"});
+    const nlohmann::json cfg = load_config(a.str("config"));
+    const auto sel = selection_from_json(cfg);
+    const auto spec = loss_from_json(cfg);
+    std::vector<gvr::GaussianScene> parts;
+    for (const auto& jp : cfg.at("parts")) {
+        const fs::path p = jp.get<std::string>();
+        require_file(p, "part scene");
+        parts.push_back(gvr::load_scene_json(p));
+    }
+    if (parts.empty()) throw UsageError("fit-translation needs at least one part");
+    gvr::GaussianScene scene;
+    scene.tau = parts.front().tau;
+    std::vector<std::vector<int>> groups;
+    for (const auto& part : parts) {
+        std::vector<int> group;
+        for (const auto& k : part.kernels) {
+            group.push_back(scene.size());
+            scene.kernels.push_back(k);
+        }
+        groups.push_back(std::move(group));
+    }
+    const fs::path camera_path = cfg.at("camera").get<std::string>();
+    require_file(camera_path, "camera");
+    gvr::FitView target;
+    target.camera = gvr::load_camera_json(camera_path);
+    std::vector<gvr::Vec3> gt(groups.size(), gvr::Vec3::Zero());
+    if (cfg.contains("gt_offsets")) {
+        const auto& jg = cfg.at("gt_offsets");
+        for (size_t g = 0; g < groups.size() && g < jg.size(); ++g) {
+            const auto v = jg[g].get<std::vector<double>>();
+            gt[g] = gvr::Vec3(v[0], v[1], v[2]);
+        }
+    }
+    if (cfg.contains("target_image")) {
+        target.image = load_image_any(cfg.at("target_image").get<std::string>());
+        target.alpha = gvr::Image(target.camera.height, target.camera.width, 1, gvr::ChannelSemantics::Alpha);
+    } else {  // synthesised from the ground-truth offsets
+        gvr::GaussianScene gts = scene;
+        for (size_t g = 0; g < groups.size(); ++g)
+            for (int k : groups[g])
+                for (int d = 0; d < 3; ++d) gts.kernels[k].center[d] += gt[g][d];
+        gvr::RenderBuffers buf = gvr::render(gts, target.camera, sel);
+        target.image = std::move(buf.image);
+        target.alpha = std::move(buf.alpha);
+    }
+    if (cfg.contains("init_offsets")) {
+        const auto& jo = cfg.at("init_offsets");
+        for (size_t g = 0; g < groups.size() && g < jo.size(); ++g) {
+            const auto v = jo[g].get<std::vector<double>>();
+            for (int k : groups[g])
+                for (int d = 0; d < 3; ++d) scene.kernels[k].center[d] += v[d];
+        }
+    }
+    gvr::AdamConfig adam;
+    adam.lr = cfg.value("lr", 0.05);
+    const auto result = gvr::fit_translation(scene, groups, target, spec, cfg.value("iters", 300), adam, sel);
+    nlohmann::json extra;
+    extra["task"] = "fit-translation";
+    extra["translations"] = nlohmann::json::array();
+    for (size_t g = 0; g < result.translations.size(); ++g) {
+        const gvr::Vec3& t = result.translations[g];
+        extra["translations"].push_back({t[0], t[1], t[2]});
+        if (cfg.contains("init_offsets")) {
+            const auto jo = cfg.at("init_offsets")[g].get<std::vector<double>>();
+            double e2 = 0.0;
+            for (int d = 0; d < 3; ++d) e2 += (jo[d] + t[d] - gt[g][d]) * (jo[d] + t[d] - gt[g][d]);
+            extra["residual_error"].push_back(std::sqrt(e2));
+        }
+    }
+    const fs::path out = a.str("out", "fit_translation.json");
+    write_report_json(result.report, extra, out);
+    write_loss_csv(result.report, fs::path(out).replace_extension(".csv"));
+    std::cout << "fit-translation finished: iters=" << result.report.iterations
+              << " final loss=" << (result.report.loss_trace.empty() ? 0.0 : result.report.loss_trace.back()) << "\n";
+    return result.report.diverged ? kExitRuntime : kExitOk;
+}
+
+int cmd_fit_pose(const Args& a) {
+    require_opts(a, {"config"});
+    const nlohmann::json cfg = load_config(a.str("config"));
+    const auto sel = selection_from_json(cfg);
+    gvr::LossSpec spec = loss_from_json(cfg);
+    const fs::path scene_path = cfg.at("scene").get<std::string>();
+    require_file(scene_path, "scene");
+    const gvr::GaussianScene scene = gvr::load_scene_json(scene_path);
+    const fs::path camera_path = cfg.at("camera").get<std::string>();
+    require_file(camera_path, "camera");
+    const gvr::Camera model = gvr::load_camera_json(camera_path);
+    gvr::Image target_image, target_alpha;
+    if (cfg.contains("target_image")) {
+        target_image = load_image_any(cfg.at("target_image").get<std::string>());
+        spec.silhouette_weight = 0.0;
+    } else {  // the camera file carries the ground-truth extrinsics: synthesise
+        gvr::RenderBuffers buf = gvr::render(scene, model, sel);
+        target_image = std::move(buf.image);
+        target_alpha = std::move(buf.alpha);
+    }
+    std::vector<gvr::PoseStart> starts;
+    if (cfg.contains("starts")) {
+        for (const auto& js : cfg.at("starts")) {
+            const auto w = js.at("omega").get<std::vector<double>>();
+            const auto t = js.at("translation").get<std::vector<double>>();
+            gvr::PoseStart st;
+            st.omega = gvr::Vec3(w[0], w[1], w[2]);
+            st.translation = gvr::Vec3(t[0], t[1], t[2]);
+            starts.push_back(st);
+        }
+    } else {  // ring of azimuth starts around the ground-truth pose
+        const int n = cfg.value("azimuth_starts", 8);
+        const gvr::Mat3 r_gt = gvr::so3_exp(gvr::so3_log(model.rotation));
+        for (int i = 0; i < n; ++i) {
+            const gvr::Mat3 ry = gvr::so3_exp(gvr::Vec3(0, 2.0 * M_PI * i / n, 0));
+            gvr::Mat3 prod = gvr::Mat3::Identity();
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) {
+                    double acc = 0.0;
+                    for (int k = 0; k < 3; ++k) acc += ry(r, k) * r_gt(k, c);
+                    prod(r, c) = acc;
+                }
+            gvr::PoseStart st;
+            st.omega = gvr::so3_log(prod);
+            st.translation = model.translation;
+            starts.push_back(st);
+        }
+    }
+    gvr::AdamConfig adam;
+    adam.lr = cfg.value("lr", 0.05);
+    const auto result =
+        gvr::fit_pose(scene, target_image, target_alpha, model, starts, spec, cfg.value("iters", 300), adam, sel);
+    nlohmann::json extra;
+    extra["task"] = "fit-pose";
+    extra["best_start"] = result.best_start;
+    extra["best_omega"] = {result.best_pose.omega[0], result.best_pose.omega[1], result.best_pose.omega[2]};
+    extra["best_translation"] = {result.best_pose.translation[0], result.best_pose.translation[1],
+                                 result.best_pose.translation[2]};
+    if (!cfg.contains("target_image"))
+        extra["rotation_error_rad"] = gvr::rotation_error(result.best_camera.rotation, model.rotation);
+    const fs::path out = a.str("out", "fit_pose.json");
+    write_report_json(result.report, extra, out);
+    write_loss_csv(result.report, fs::path(out).replace_extension(".csv"));
+    std::cout << "fit-pose finished: best start " << result.best_start << " loss "
+              << result.report.metrics.at("best_loss") << "\n";
+    return result.report.diverged ? kExitRuntime : kExitOk;
+}
+
 int cmd_rerender(const Args& a) {
     require_opts(a, {"attrs", "scene", "camera"});
     const fs::path attrs_path = a.str("attrs"), scene_path = a.str("scene"), camera_path = a.str("camera");
@@ -377,6 +580,8 @@ int main(int argc, char** argv) {
         if (a.cmd == "gradcheck") return cmd_gradcheck(a);
         if (a.cmd == "extract-texture") return cmd_extract_texture(a);
         if (a.cmd == "rerender") return cmd_rerender(a);
+        if (a.cmd == "fit-translation") return cmd_fit_translation(a);
+        if (a.cmd == "fit-pose") return cmd_fit_pose(a);
         std::cerr << "error: " << a.cmd
                   << " is not part of the GPU backend (converters and fitting drivers: see INTEGRATION.md)\n";
         return kExitRuntime;

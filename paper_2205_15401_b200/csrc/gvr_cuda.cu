@@ -564,18 +564,37 @@ int gvr_measure_pipe_peak(gvr_context* ctx, int kind, double* flops) {
 int gvr_adam_step_guarded(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
                           int64_t step, double lr, double beta1, double beta2, double eps, const double* loss,
                           int32_t* diverged) {
-    if (!ctx || step < 1 || n < 0) return GVR_ERR_RUNTIME;
+    if (!ctx || step < 1 || n < 0 || !params || !grads || !m || !v) return GVR_ERR_RUNTIME;
     if (n == 0) return GVR_OK;
-    if (!is_device_ptr(params) || !is_device_ptr(grads) || !is_device_ptr(m) || !is_device_ptr(v))
-        return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step needs device pointers");
     if ((loss == nullptr) != (diverged == nullptr) || (loss && (!is_device_ptr(loss) || !is_device_ptr(diverged))))
         return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step_guarded needs device loss and diverged pointers");
     const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
     const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
-    adam_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, params, grads, m, v, lr, beta1, beta2, eps, bc1, bc2,
-                                                             loss, diverged);
+    // host arrays (the C++ drop-in's AdamState) are staged through the context scratch
+    double* arr[4] = {params, const_cast<double*>(grads), m, v};
+    double* dev[4];
+    bool host[4];
+    const size_t bytes = sizeof(double) * (size_t)n;
+    for (int i = 0; i < 4; ++i) {
+        host[i] = !is_device_ptr(arr[i]);
+        dev[i] = arr[i];
+        if (host[i]) {
+            if (ctx->capturing) return set_err(ctx, GVR_ERR_RUNTIME, "gvr_adam_step with host arrays is not capturable");
+            CUDA_TRY(ctx, ctx->scratch[i].ensure(bytes));
+            dev[i] = ctx->scratch[i].as<double>();
+            CUDA_TRY(ctx, cudaMemcpyAsync(dev[i], arr[i], bytes, cudaMemcpyHostToDevice, ctx->stream));
+        }
+    }
+    adam_kernel<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, dev[0], dev[1], dev[2], dev[3], lr, beta1, beta2, eps,
+                                                             bc1, bc2, loss, diverged);
     LAUNCH_CHECK(ctx);
-    return GVR_OK;
+    bool any = false;
+    for (int i : {0, 2, 3})
+        if (host[i]) {
+            CUDA_TRY(ctx, cudaMemcpyAsync(arr[i], dev[i], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            any = true;
+        }
+    return any ? sync_and_check(ctx) : GVR_OK;
 }
 
 int gvr_adam_step(gvr_context* ctx, double* params, const double* grads, double* m, double* v, int64_t n,
@@ -1313,13 +1332,12 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.through_t = through_t;
         bp.through_rho = through_rho;
         const int btx = t->tiles_x, bty = t->tiles_y;
-        const int tiles = btx * bty;
         int* sched = t->sched.as<int>();
 #if GVR_ONE_ORDER
         int* order_b = sched + 2;  // the selection's order
         bp.n_order = sched;
 #else
-        int* order_b = sched + 2 + tiles;  // tiles by sum_p n_p^2, from the forward
+        int* order_b = sched + 2 + btx * bty;  // tiles by sum_p n_p^2, from the forward
         bp.n_order = sched + 1;
 #endif
         bp.tiles_x = btx;

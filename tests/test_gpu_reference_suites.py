@@ -34,9 +34,6 @@ CLI_OUT_OF_SCOPE = {
     "convert handles an OBJ cube with the documented sigma",
     "convert rejects invalid zeta naming the constraint",
     "PLY convert then render smoke test",
-    # fit_translation / fit_pose drivers (fit.cpp:267-407)
-    "fit-translation completes from a config and writes the report",
-    "fit-pose multi-start picks the basin of the true pose",
 }
 
 
