@@ -345,8 +345,11 @@ def test_packed_backward_equals_the_gradient_bundle(ctx):
     dev = torch.device("cuda:0")
     packed = torch.zeros((scene.size, 12), dtype=torch.float64, device=dev)
     d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
-    gvr.backward_packed_into(fr.tape, torch.tensor(di, device=dev), torch.tensor(da, device=dev), gvr.GradFlags(),
-                             packed, d_rt)
+    tdi, tda = torch.tensor(di, device=dev), torch.tensor(da, device=dev)
+    torch.cuda.synchronize()  # torch's stream is not the context's: inputs ready before the backward
+    gvr.backward_packed_into(fr.tape, tdi, tda, gvr.GradFlags(), packed, d_rt)
+    ctx.synchronize()
+    assert np.abs(g.d_center).max() > 0.0
     c, s, a, r, t = gvr.unpack_gradients(packed.cpu().numpy(), d_rt.cpu().numpy(), 3)
     for got, want in ((c, g.d_center), (s, g.d_inv_cov), (a, g.d_attr), (r, g.d_rotation), (t, g.d_translation)):
         assert np.array_equal(got, want)

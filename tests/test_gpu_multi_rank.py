@@ -50,7 +50,10 @@ def _c4_rank(rank, world):
     dev = torch.device("cuda:0")
     packed = torch.zeros((scene.size, 12), dtype=torch.float64, device=dev)
     d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()  # torch's stream is not the context's
     gvr.backward_packed_into(fr.tape, None, None, gvr.GradFlags(), packed, d_rt)
+    ctx.synchronize()
+    assert float(packed.abs().max()) > 0.0
     allreduce_gradients([packed, d_rt])
     parts = gvr.unpack_gradients(packed.cpu().numpy(), d_rt.cpu().numpy(), 3)
     return fr.buffers, [np.ascontiguousarray(p) for p in parts]

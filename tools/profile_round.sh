@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-c3 --no-c4 --no-c5 > gpurun_out/launches_bench.log 2>&1
-for k in select_warp_kernel blend_kernel backward_pixels_kernel; do
+for k in select_warp_kernel blend_kernel backward_pixels_kernel records_kernel finish_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
       -o gpurun_out/full_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-c3 --no-c4 --no-c5 > gpurun_out/full_$k.log 2>&1
 done
