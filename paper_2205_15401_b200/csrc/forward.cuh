@@ -804,14 +804,11 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
 
 // The pixel's bit in each selected kernel's (kernel, tile) mask: the backward's
 // per-kernel record order (order-independent OR). Entries s = sub, sub + 4, ...
-__device__ __forceinline__ void mark_selection(const FwdParams& p, const int* b_id, int n, int sub, int g, int np,
+__device__ __forceinline__ void mark_selection(const FwdParams& p, const int* b_slot, int n, int sub, int g, int np,
                                                int i, int j) {
     for (int s = sub; s < n; s += 4) {
-        const int4 ki = p.kinfo[b_id[s * np + g] & ~kExact];
-        if (ki.x >= 0) {
-            const int slot = ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff));
-            atomicOr(p.masks + slot, 1ull << ((i % 8) * 8 + j % 8));
-        }
+        const int slot = b_slot[s * np + g];
+        if (slot >= 0) atomicOr(p.masks + slot, 1ull << ((i % 8) * 8 + j % 8));
     }
 }
 
@@ -838,6 +835,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     const float4* b_q = reinterpret_cast<const float4*>(smem);  // {hi, lo, pk, is} after the conversion
     double* b_w = reinterpret_cast<double*>(b_s + KMAX * NP);  // W_k
     int* b_id = reinterpret_cast<int*>(b_w + KMAX * NP);
+    int* b_slot = b_id + KMAX * NP;  // the entry's (kernel, tile) mask slot, -1: none (selection order)
 
     if ((int)(blockIdx.x / GVR_BLEND_SPLIT) >= *p.n_order_blend) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
@@ -901,6 +899,10 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
                 v.is = (float)sqrt(t.a);  // 1/sigma
                 b_s[s * NP + g] = v;
                 b_id[s * NP + g] = k;
+                // the kernel's mask slot for this tile (its record was loaded with the trace's)
+                const int4 ki = p.kinfo[k];
+                b_slot[s * NP + g] =
+                    ki.x >= 0 ? ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff)) : -1;
             }
         }
     }
@@ -1029,10 +1031,10 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
             p.depth[pix] = depth;
             if (!isfinite(alpha) || !isfinite(depth) || !isfinite(wsum)) atomicExch(p.nonfinite, 1);
         }
-        mark_selection(p, b_id, n, sub, g, NP, i, j);
+        mark_selection(p, b_slot, n, sub, g, NP, i, j);
         return;
     }
-    mark_selection(p, b_id, n, sub, g, NP, i, j);
+    mark_selection(p, b_slot, n, sub, g, NP, i, j);
     if (sub != 0) return;
     double wsum = 0.0, wld = 0.0;
     for (int k = 0; k < n; ++k) {

@@ -334,7 +334,7 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
     (void)cost;
 #endif
     {
-        const size_t smem = 28ull * KMAX * (64 / GVR_BLEND_SPLIT);
+        const size_t smem = 32ull * KMAX * (64 / GVR_BLEND_SPLIT);
         auto kern = blend_kernel<KMAX>;
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_BLEND);
