@@ -32,7 +32,7 @@ namespace {
 // Forward tile = 8x8 pixels = one default coarse cell (64 threads, 2 warps):
 // small CTAs balance the very uneven per-tile work and keep 8 CTAs per SM.
 constexpr int kFwdTile = 8;
-constexpr int kMaxKPrime = 64;
+constexpr int kMaxKPrime = 128;
 
 struct Buf {
     void* p = nullptr;
@@ -1069,7 +1069,9 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     else if (kp <= 24) rc = launch_forward<24>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     else if (kp <= 32) rc = launch_forward<32>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     else if (kp <= 48) rc = launch_forward<48>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else rc = launch_forward<64>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 64) rc = launch_forward<64>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else if (kp <= 96) rc = launch_forward<96>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    else rc = launch_forward<128>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
     if (rc) return rc;
 
     tape->valid = true;
@@ -1385,7 +1387,9 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         else if (kp <= 24) rc = launch_backward<24>(ctx, bp, btx * bty);
         else if (kp <= 32) rc = launch_backward<32>(ctx, bp, btx * bty);
         else if (kp <= 48) rc = launch_backward<48>(ctx, bp, btx * bty);
-        else rc = launch_backward<64>(ctx, bp, btx * bty);
+        else if (kp <= 64) rc = launch_backward<64>(ctx, bp, btx * bty);
+        else if (kp <= 96) rc = launch_backward<96>(ctx, bp, btx * bty);
+        else rc = launch_backward<128>(ctx, bp, btx * bty);
         if (rc) return rc;
 
         GatherParams gp{};

@@ -176,3 +176,31 @@ def test_graph_replay_matches_eager(ctx):
     assert torch.allclose(loss, eager_loss, rtol=1e-14, atol=0)
     assert torch.allclose(gc, eager_gc, rtol=1e-12, atol=1e-15)
     torch.cuda.set_stream(torch.cuda.default_stream(dev))
+
+
+@pytest.mark.parametrize("kp", [80, 128])
+def test_large_k_prime_matches_the_oracle(ctx, kp):
+    """K' beyond the warp selection (CTA selection + sorting blend), up to the
+    backend's 128: bit-exact selection, tolerance parity of outputs and gradients."""
+    import oracle
+    from paper_2205_15401_b200.types import Camera, GaussianScene, SelectionConfig
+
+    rng = np.random.default_rng(kp)
+    k = 220
+    centers = np.stack([rng.uniform(-0.4, 0.4, k), rng.uniform(-0.4, 0.4, k), rng.uniform(3.0, 6.0, k)], 1)
+    inv_cov = np.stack([np.eye(3) / rng.uniform(0.2, 0.5) ** 2 for _ in range(k)])
+    scene = GaussianScene(centers, inv_cov, rng.uniform(0, 1, (k, 3)), 0.3)
+    cam = Camera(np.eye(3), np.zeros(3), 20.0, 11.5, 11.5, 24, 24)
+    cfg = SelectionConfig(k_prime=kp)
+    fr = gvr.render_with_tape(scene, cam, cfg, ctx=ctx)
+    o = oracle.port_render(scene, cam, cfg, threads=0)
+    assert (fr.buffers.topk_idx >= 0).sum(axis=2).max() > 64  # the case is really beyond 64
+    assert np.array_equal(fr.buffers.topk_idx, o["topk_idx"])
+    for key in ("image", "alpha", "depth", "topk_w"):
+        assert_close_rel(getattr(fr.buffers, key), o[key], what=f"kp{kp} {key}")
+    di = rng.uniform(-1, 1, fr.buffers.image.shape)
+    da = rng.uniform(-1, 1, fr.buffers.alpha.shape)
+    g = gvr.backward(fr, di, da)
+    go = oracle.port_backward(scene, cam, cfg, di, da, threads=0)
+    for key in ("d_center", "d_inv_cov", "d_attr", "d_rotation", "d_translation"):
+        assert_grad_close(getattr(g, key), go[key], what=f"kp{kp} {key}")
