@@ -20,6 +20,7 @@ tensors / any object exposing ``data_ptr()`` (device-resident; no copy).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 from dataclasses import dataclass
@@ -55,6 +56,42 @@ def _ptr(x) -> Optional[int]:
     if hasattr(x, "data_ptr"):
         return int(x.data_ptr())
     raise TypeError(f"unsupported buffer type {type(x)!r}")
+
+
+def _cuda_tensors(bufs):
+    out = []
+    for b in bufs:
+        if isinstance(b, (list, tuple)):
+            out += _cuda_tensors(b)
+        elif isinstance(b, dict):
+            out += _cuda_tensors(list(b.values()))
+        elif b is not None and getattr(b, "is_cuda", False):
+            out.append(b)
+    return out
+
+
+@contextlib.contextmanager
+def _stream_order(ctx: "Context", *bufs):
+    """Stream ordering for CUDA tensor arguments: the context's stream waits for
+    torch's current stream before the call (inputs written by torch are ready)
+    and torch's current stream waits for the context's stream after it (outputs
+    are ready for torch). Asynchronous (events); nothing to do when torch already
+    runs on the context's stream (bench.py, Fitter) or no tensor is on the GPU."""
+    if not _cuda_tensors(bufs):
+        yield
+        return
+    import torch
+
+    cur = torch.cuda.current_stream()
+    ext = ctx.torch_stream()
+    if cur.cuda_stream == ext.cuda_stream:
+        yield
+        return
+    ext.wait_stream(cur)
+    try:
+        yield
+    finally:
+        cur.wait_stream(ext)
 
 
 class Context:
@@ -116,6 +153,17 @@ class Context:
     def set_tile_capacity(self, cap: int) -> None:
         """Test hook: tile-list pool capacity in entries, 0 = automatic (tiles whose list does not fit stream every kernel)."""
         self.check(self.lib.gvr_context_set_tile_capacity(self.handle, int(cap)))
+
+    def torch_stream(self):
+        """The context's stream as a torch stream (cached)."""
+        st = getattr(self, "_torch_stream", None)
+        ptr = int(self.lib.gvr_context_stream(self.handle) or 0)
+        if st is None or st.cuda_stream != ptr:
+            import torch
+
+            st = torch.cuda.ExternalStream(ptr, device=torch.device(f"cuda:{self.device}"))
+            self._torch_stream = st
+        return st
 
     def set_async(self, on: bool = True) -> None:
         """Host-buffer calls enqueue their copies and return (gvr_context_set_async):
@@ -219,10 +267,11 @@ class DeviceScene:
         """Upload from host or device arrays. ``deferred``: validate on the device
         without synchronising (capturable); :meth:`check` reports the result."""
         fn = self.ctx.lib.gvr_scene_set_deferred if deferred else self.ctx.lib.gvr_scene_set
-        self.ctx.check(
-            fn(self.ctx.handle, self.handle, int(K), int(D), float(tau), _ptr(centers), _ptr(inv_cov),
-               _ptr(attr) if D > 0 else None)
-        )
+        with _stream_order(self.ctx, centers, inv_cov, attr):
+            self.ctx.check(
+                fn(self.ctx.handle, self.handle, int(K), int(D), float(tau), _ptr(centers), _ptr(inv_cov),
+                   _ptr(attr) if D > 0 else None)
+            )
         self.K, self.D, self.tau = int(K), int(D), float(tau)
         return self
 
@@ -353,8 +402,9 @@ def render_into(ctx: Context, dscene: DeviceScene, camera: Camera, cfg: Selectio
     ``shard=(r, n)`` renders only tiles with index % n == r (C4 tile sharding)."""
     out = _lib.GvrRenderOutputs(_ptr(image), _ptr(alpha), _ptr(depth), _ptr(topk_idx), _ptr(topk_w))
     cam_c, sel_c = _camera_c(camera), _selection_c(cfg)
-    ctx.check(ctx.lib.gvr_render_shard(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c),
-                                       tape.handle, ctypes.byref(out), int(shard[0]), int(shard[1])))
+    with _stream_order(ctx, image, alpha, depth, topk_idx, topk_w):
+        ctx.check(ctx.lib.gvr_render_shard(ctx.handle, dscene.handle, ctypes.byref(cam_c), ctypes.byref(sel_c),
+                                           tape.handle, ctypes.byref(out), int(shard[0]), int(shard[1])))
     tape.scene, tape.camera, tape.cfg = dscene, camera, cfg
 
 
@@ -390,9 +440,10 @@ def scalar_loss_into(tape: Tape, target_image, target_alpha, w_image: float = 1.
     """Low-level ``gvr_scalar_loss``: targets / outputs host or device; the
     upstream gradient is also kept in the tape for ``backward_into(tape, None, None)``."""
     ctx = tape.ctx
-    ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(target_image), _ptr(target_alpha),
-                                      float(w_image), float(w_alpha), _ptr(loss_out), _ptr(d_image_out),
-                                      _ptr(d_alpha_out)))
+    with _stream_order(ctx, target_image, target_alpha, loss_out, d_image_out, d_alpha_out):
+        ctx.check(ctx.lib.gvr_scalar_loss(ctx.handle, tape.handle, _ptr(target_image), _ptr(target_alpha),
+                                          float(w_image), float(w_alpha), _ptr(loss_out), _ptr(d_image_out),
+                                          _ptr(d_alpha_out)))
 
 
 def scalar_loss(tape: Tape, loss: ScalarLoss, *, want_grads: bool = True):
@@ -420,7 +471,8 @@ def backward_into(tape: Tape, d_image, d_alpha, flags: GradFlags = GradFlags(), 
     f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
     g = _lib.GvrGradients(_ptr(d_center), _ptr(d_inv_cov), _ptr(d_attr), _ptr(d_rotation), _ptr(d_translation))
     fn = ctx.lib.gvr_backward_accumulate if accumulate else ctx.lib.gvr_backward
-    ctx.check(fn(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f), ctypes.byref(g)))
+    with _stream_order(ctx, d_image, d_alpha, d_center, d_inv_cov, d_attr, d_rotation, d_translation):
+        ctx.check(fn(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f), ctypes.byref(g)))
 
 
 def backward_packed_into(tape: Tape, d_image, d_alpha, flags: GradFlags, packed, d_rt) -> None:
@@ -428,8 +480,9 @@ def backward_packed_into(tape: Tape, d_image, d_alpha, flags: GradFlags, packed,
     (device [K, 9 + D]) and d_rt = [d_rotation | d_translation] (device [12])."""
     ctx = tape.ctx
     f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
-    ctx.check(ctx.lib.gvr_backward_packed(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha), ctypes.byref(f),
-                                          _ptr(packed), _ptr(d_rt)))
+    with _stream_order(ctx, d_image, d_alpha, packed, d_rt):
+        ctx.check(ctx.lib.gvr_backward_packed(ctx.handle, tape.handle, _ptr(d_image), _ptr(d_alpha),
+                                              ctypes.byref(f), _ptr(packed), _ptr(d_rt)))
 
 
 def unpack_gradients(packed, d_rt, D: int):
@@ -624,7 +677,8 @@ def render_views_into(ctx: Context, dscene: DeviceScene, cameras, cfg: Selection
                               _ptr(pick(topk_idx, v)), _ptr(pick(topk_w, v))) for v in range(n)])
     th = _ptr_array(tapes)
     sel_c = _selection_c(cfg)
-    ctx.check(ctx.lib.gvr_render_views(ctx.handle, dscene.handle, n, cams, ctypes.byref(sel_c), th, outs))
+    with _stream_order(ctx, images, alphas, depths, topk_idx, topk_w):
+        ctx.check(ctx.lib.gvr_render_views(ctx.handle, dscene.handle, n, cams, ctypes.byref(sel_c), th, outs))
     for v, t in enumerate(tapes):
         t.scene, t.camera, t.cfg = dscene, cameras[v], cfg
 
@@ -633,9 +687,10 @@ def scalar_loss_views_into(ctx: Context, tapes, target_images, target_alphas, w_
                            w_alpha: float = 1.0, losses=None) -> None:
     """``gvr_scalar_loss_views``: per-view ScalarLoss; ``losses`` [V] host or device (nullable)."""
     n = len(tapes)
-    ctx.check(ctx.lib.gvr_scalar_loss_views(ctx.handle, n, _ptr_array(tapes), _ptr_array(target_images),
-                                            _ptr_array(target_alphas), float(w_image), float(w_alpha),
-                                            _ptr(losses)))
+    with _stream_order(ctx, target_images, target_alphas, losses):
+        ctx.check(ctx.lib.gvr_scalar_loss_views(ctx.handle, n, _ptr_array(tapes), _ptr_array(target_images),
+                                                _ptr_array(target_alphas), float(w_image), float(w_alpha),
+                                                _ptr(losses)))
 
 
 def backward_views_into(ctx: Context, tapes, flags: GradFlags = GradFlags(), outs=None, total=None) -> None:
@@ -652,5 +707,6 @@ def backward_views_into(ctx: Context, tapes, flags: GradFlags = GradFlags(), out
     f = _lib.GvrGradFlags(int(bool(flags.through_transmittance)), int(bool(flags.through_density)))
     o = (_lib.GvrGradients * max(n, 1))(*[bundle(outs[v]) for v in range(n)]) if outs is not None else None
     t = bundle(total) if total is not None else None
-    ctx.check(ctx.lib.gvr_backward_views(ctx.handle, n, _ptr_array(tapes), ctypes.byref(f), o,
-                                         ctypes.byref(t) if t is not None else None))
+    with _stream_order(ctx, outs, total):
+        ctx.check(ctx.lib.gvr_backward_views(ctx.handle, n, _ptr_array(tapes), ctypes.byref(f), o,
+                                             ctypes.byref(t) if t is not None else None))

@@ -353,3 +353,26 @@ def test_packed_backward_equals_the_gradient_bundle(ctx):
     c, s, a, r, t = gvr.unpack_gradients(packed.cpu().numpy(), d_rt.cpu().numpy(), 3)
     for got, want in ((c, g.d_center), (s, g.d_inv_cov), (a, g.d_attr), (r, g.d_rotation), (t, g.d_translation)):
         assert np.array_equal(got, want)
+
+
+def test_device_buffers_on_torchs_own_stream_are_ordered(ctx):
+    """Tensors made on torch's current stream (not the context's) are safe to pass:
+    the *_into calls order the two streams with events (no host sync needed)."""
+    import torch
+    assert torch.cuda.current_stream().cuda_stream != ctx.torch_stream().cuda_stream
+    scene = gvr.make_bench_scene(2000)
+    fr = gvr.render_with_tape(scene, gvr.make_bench_camera(96), ctx=ctx)
+    rng = np.random.default_rng(3)
+    di = rng.uniform(-1, 1, fr.buffers.image.shape)
+    da = rng.uniform(-1, 1, fr.buffers.alpha.shape)
+    want = gvr.backward(fr, di, da)
+    dev = torch.device("cuda:0")
+    for _ in range(3):
+        big = torch.empty(64 << 20, dtype=torch.float64, device=dev).fill_(1.0)  # keeps torch's stream busy
+        packed = torch.zeros((scene.size, 12), dtype=torch.float64, device=dev)
+        d_rt = torch.zeros(12, dtype=torch.float64, device=dev)
+        gvr.backward_packed_into(fr.tape, torch.tensor(di, device=dev), torch.tensor(da, device=dev),
+                                 gvr.GradFlags(), packed, d_rt)
+        c = packed[:, :3].cpu().numpy()  # torch's stream waits for the context's
+        assert np.array_equal(c, want.d_center)
+        del big
