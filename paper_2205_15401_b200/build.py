@@ -92,7 +92,7 @@ def build_cli(verbose: bool = False) -> str:
     return CLI
 
 
-REF_TESTS = ("test_scene", "test_tracer", "test_blender", "test_grad")
+REF_TESTS = ("test_scene", "test_tracer", "test_blender", "test_grad", "test_fit")
 CLI_DATA = os.path.join(ROOT, "tests", "cpp", "_build", "cli_data")
 
 
@@ -128,7 +128,7 @@ REF_TEST_DIR = os.path.join(ROOT, "tests", "cpp", "_build")
 
 def build_reference_suites(verbose: bool = False) -> list:
     """The reference's own hot-path test suites (/root/reference/proj/tests/
-    test_{scene,tracer,blender,grad}.cpp), compiled UNMODIFIED against the C++
+    test_{scene,tracer,blender,grad,fit}.cpp), compiled UNMODIFIED against the C++
     drop-in (include/gvr/*.hpp -> libgvr_cuda.so), with Eigen and doctest from
     the repo's test shims (oracle/shim). Only where /root/reference exists (this
     container); the binaries travel to the GPU box with the tree and are run by
@@ -141,7 +141,8 @@ def build_reference_suites(verbose: bool = False) -> list:
     for t in REF_TESTS:
         exe = os.path.join(REF_TEST_DIR, "ref_" + t)
         cpp = os.path.join(src, t + ".cpp")
-        deps = [cpp, os.path.join(ROOT, "include", "gvr", "gvr.hpp"), os.path.join(ROOT, "include", "gvr_cuda.h")]
+        deps = [cpp, os.path.join(ROOT, "include", "gvr_cuda.h")] + [
+            os.path.join(ROOT, "include", "gvr", f) for f in ("gvr.hpp", "fit.hpp", "shapes.hpp", "convert.hpp")]
         if _stale(exe, deps):
             cmd = ["g++", "-std=c++20", "-O2", "-DGVR_WITH_EIGEN", f"-I{ROOT}/include", f"-I{ROOT}/oracle/shim",
                    f"-I{src}", cpp, f"-L{HERE}", "-lgvr_cuda", "-Wl,-rpath,$ORIGIN/../../../paper_2205_15401_b200",

@@ -1,6 +1,7 @@
 """GPU: the reference's OWN hot-path test suites, compiled unmodified against the
-C++ drop-in (include/gvr/{types,tracer,blender,grad,scene,so3}.hpp over
-libgvr_cuda.so): /root/reference/proj/tests/test_{scene,tracer,blender,grad}.cpp.
+C++ drop-in (include/gvr/{types,tracer,blender,grad,scene,so3,fit,shapes,
+convert}.hpp over libgvr_cuda.so): /root/reference/proj/tests/
+test_{scene,tracer,blender,grad,fit}.cpp, and test_cli.cpp against the `gvr` tool.
 The binaries are built in the container by __graft_entry__.build()
 (paper_2205_15401_b200/build.py: build_reference_suites) and travel to the GPU
 box with the tree. Every case must pass except the ones listed in
@@ -37,7 +38,7 @@ CLI_OUT_OF_SCOPE = {
 }
 
 
-@pytest.mark.parametrize("suite", ["test_scene", "test_tracer", "test_blender", "test_grad", "test_cli"])
+@pytest.mark.parametrize("suite", ["test_scene", "test_tracer", "test_blender", "test_grad", "test_fit", "test_cli"])
 def test_reference_suite_against_the_drop_in(suite):
     exe = os.path.join(BUILD, "ref_" + suite)
     if not os.path.exists(exe):
