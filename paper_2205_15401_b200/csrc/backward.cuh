@@ -17,6 +17,7 @@ struct BwdParams {
     const int* count;  // [P]
     const double* tape_t;  // [P*kp] T(l_k) from the forward
     const EntryRec* ent;   // [P*kp] traced entries (l, e^q, 1/sigma) from the forward
+    const double* ent_a;   // [P*kp] a = d.Sd of the traced entries (FP64)
     const Rec64* rec64;
     const double* attr;     // [K*D]
     const double* d_image;  // [P*D]
@@ -24,7 +25,7 @@ struct BwdParams {
     const int4* kinfo;           // [K] mask rectangle of each kernel (project_kernel)
     const unsigned long long* masks;  // per (kernel, tile): pixels of the tile that selected the kernel
     const int* slot_off;              // per (kernel, tile): first record of its pixels (appearance_kernel)
-    double4* bent;                    // records {d_l, d_q, d_sigma, W}
+    double4* bent;                    // records {alpha, d_q, beta, W} (entry_coeffs)
     int2* bkey;                       // records' {pixel, kernel}
     double4* rays;                    // [P] the pixel's ray (pixel_ray), for the record pass
     // fallback for kernels without a mask rectangle (mask pool full): FP64 atomics
@@ -66,6 +67,26 @@ __device__ __forceinline__ void chain_entry(const Rec64& r, const double* d, dou
     }
 }
 
+// The chain of grad.cpp:140-170 regrouped so that the kernel's camera-space
+// centre m and inverse covariance S enter only through per-kernel sums: with
+// s = d_l / a, v = m - l d and d_a = -0.5 sigma^3 d_sigma,
+//   dm = S (s d - d_q v)                  = S (alpha d - d_q m)
+//   dS = s sym(v d^T) - d_q/2 v v^T + d_a d d^T
+//      = alpha sym(m d^T) + beta d d^T - d_q/2 m m^T,
+//   alpha = s + d_q l,   beta = -s l - d_q l^2 / 2 + d_a,
+// so a kernel needs A = sum alpha d, Q = sum d_q, B = sum beta d d^T over its
+// entries (finish_kernel then applies m and S once). Every entry input is the
+// traced (l, a) of the forward and the pixel's ray; the sums cancel at most
+// (|m| / sigma)^2 in FP64.
+__device__ __forceinline__ void entry_coeffs(double l, double a, double dl, double dq, double dsg, double* alpha,
+                                             double* beta) {
+    const double ia = 1.0 / a;
+    const double sc = dl * ia;
+    const double d_a = -0.5 * ia * sqrt(ia) * dsg;  // -0.5 sigma^3 d_sigma, sigma = a^-1/2
+    *alpha = fma(dq, l, sc);
+    *beta = fma(-0.5 * dq * l, l, fma(-sc, l, d_a));
+}
+
 // Entry of a kernel without a mask rectangle (the mask pool was full): FP64
 // atomics into camera-space accumulators, consumed by the gather (rare; kept
 // out of line so it costs the hot loop no registers).
@@ -88,10 +109,18 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]
     // pairs read together are packed: one 16-byte and one 8-byte load per pair
+#if GVR_BWD_F32
+    // {hi, lo of l_k - l_0, d_acc_k = -tau T_k d_w_k e^{q_k}, e^{q_k}} as floats, 1 / sigma_k
+    float4* b_q = reinterpret_cast<float4*>(smem);
+    double* b_dt = reinterpret_cast<double*>(b_q + KMAX * NP);  // density path d_w_k T_k (grad.cpp:120)
+    float* b_is = reinterpret_cast<float*>(b_dt + KMAX * NP);
+    int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
+#else
     double2* b_lda = reinterpret_cast<double2*>(smem);  // {l_k - l_0, d_acc_k = -tau T_k d_w_k e^{q_k}}
     double* b_dt = reinterpret_cast<double*>(b_lda + KMAX * NP);  // density path d_w_k T_k (grad.cpp:120)
     float2* b_pi = reinterpret_cast<float2*>(b_dt + KMAX * NP);   // {e^{q_k}, 1 / sigma_k}
     int* b_id = reinterpret_cast<int*>(b_pi + KMAX * NP);
+#endif
 
     if ((int)(blockIdx.x / GVR_BWD_SPLIT) >= *p.n_order) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
@@ -147,9 +176,17 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         } else {
             for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * k + c];
         }
-        b_lda[s * NP + g] = make_double2(er.l - l0, (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0);
-        b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
+        const double dacc = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
+#if GVR_BWD_F32
+        const double dl0 = er.l - l0;
+        const float hi = (float)dl0;
+        b_q[s * NP + g] = make_float4(hi, (float)(dl0 - (double)hi), (float)dacc, pkf);
+        b_is[s * NP + g] = er.is;
+#else
+        b_lda[s * NP + g] = make_double2(er.l - l0, dacc);
         b_pi[s * NP + g] = make_float2(pkf, er.is);
+#endif
+        b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
         b_id[s * NP + g] = k;
     }
     peak_part += __shfl_xor_sync(grp, peak_part, 1, 4);
@@ -160,6 +197,41 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
 
     // entry-major pair terms + chain to camera space (grad.cpp:121-173)
     for (int e = sub; e < n; e += 4) {
+#if GVR_BWD_F32
+        // FP32 pair terms with Kahan-compensated FP32 sums: no FP64 conversions
+        // in the loop (those share the XU pipe with the exp2 / reciprocal)
+        const float4 qe = b_q[e * NP + g];
+        const float ise = b_is[e * NP + g];
+        const float pkef = qe.w;
+        const double pke = (double)pkef;
+        const int kid = b_id[e * NP + g];
+        double dpk = d_total + b_dt[e * NP + g];  // density path (grad.cpp:120)
+        float s_pk = 0.0f, c_pk = 0.0f, s_l = 0.0f, c_l = 0.0f, s_sg = 0.0f, c_sg = 0.0f;
+        auto kahan = [](float& sum, float& comp, float term) {
+            const float y = term - comp;
+            const float t = sum + y;
+            comp = (t - sum) - y;
+            sum = t;
+        };
+#pragma unroll 2
+        for (int k = 0; k < n; ++k) {
+            const float4 qk = b_q[k * NP + g];
+            const float isk = b_is[k * NP + g];
+            // pair (k, m = e): z1 = (l_k - l_e) / sigma_e ; pair (k = e, m = k): z2 = (l_e - l_k) / sigma_k
+            const float dlf = (qk.x - qe.x) + (qk.y - qe.y);
+            const float z1 = dlf * ise;
+            const float phi1 = normal_pdf_fast(z1);
+            // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
+            const float phi2 = isk == ise ? phi1 : normal_pdf_fast(-dlf * isk);
+            kahan(s_pk, c_pk, qk.z * fast_normal_cdf(z1));
+            const float gg = k != e ? qk.z * (phi1 * ise) * pkef : 0.0f;
+            kahan(s_sg, c_sg, -gg * z1);
+            kahan(s_l, c_l, k != e ? fmaf(qe.z, qk.w * phi2 * isk, -gg) : 0.0f);
+        }
+        dpk += (double)s_pk - (double)c_pk;
+        const double dl = (double)s_l - (double)c_l;
+        const double dsg = (double)s_sg - (double)c_sg;
+#else
         const double2 lde = b_lda[e * NP + g];
         const double dle = lde.x, dae = lde.y;
         const float2 pie = b_pi[e * NP + g];
@@ -211,6 +283,7 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         dpk += dpk2;
         dl += dl2;
         dsg += dsg2;
+#endif
         const double dq = dpk * pke;
         const double w = p.tape_t[pix * p.kp + e] * pke;  // W_e (the forward's weight)
         const int4 ki = p.kinfo[kid];
@@ -220,7 +293,9 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
             const int slot = ki.x + (i / TILE - (ki.y >> 16)) * ki.z + (j / TILE - (ki.y & 0xffff));
             const int bit = (i % TILE) * TILE + j % TILE;
             const int rec = p.slot_off[slot] + __popcll(p.masks[slot] & ((1ull << bit) - 1ull));
-            p.bent[rec] = make_double4(dl, dq, dsg, w);
+            double alpha, beta;
+            entry_coeffs(p.ent[pix * p.kp + e].l, p.ent_a[pix * p.kp + e], dl, dq, dsg, &alpha, &beta);
+            p.bent[rec] = make_double4(alpha, dq, beta, w);
             p.bkey[rec] = make_int2((int)pix, kid);
             continue;
         }
@@ -238,27 +313,6 @@ __device__ __noinline__ void backward_fallback(const Rec64* rec, double* acc, do
     chain_entry(*rec, d, dl, dq, dsg, dmv, dsv);
     for (int t = 0; t < 3; ++t) atomicAdd(acc + t, dmv[t]);
     for (int t = 0; t < 6; ++t) atomicAdd(acc + 3 + t, dsv[t]);
-}
-
-// Position of the r-th (0-based) set bit of m (r < popc(m)): popc binary search.
-__device__ __forceinline__ int select_bit64(unsigned long long m, int r) {
-    unsigned w = (unsigned)m;
-    int pos = 0, c = __popc(w);
-    if (r >= c) {
-        r -= c;
-        w = (unsigned)(m >> 32);
-        pos = 32;
-    }
-#pragma unroll
-    for (int width = 16; width >= 1; width >>= 1) {
-        c = __popc(w & ((1u << width) - 1u));
-        if (r >= c) {
-            r -= c;
-            w >>= width;
-            pos += width;
-        }
-    }
-    return pos;
 }
 
 // Block-contiguous rows of `width` doubles staged through shared memory so the
@@ -285,25 +339,6 @@ __device__ __forceinline__ void stage_rows_out(double* __restrict__ dst, const d
     } else {
         for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[off + i] = src[i];
     }
-}
-
-__device__ __forceinline__ void prefetch_l1(const void* ptr, int offset = 0) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(ptr) + offset));
-}
-
-// Position of the j-th (0-based) set bit of m (j < popc(m)).
-__device__ __forceinline__ int select_bit32(unsigned m, int j) {
-    int pos = 0;
-#pragma unroll
-    for (int width = 16; width >= 1; width >>= 1) {
-        const int c = __popc(m & ((1u << width) - 1u));
-        if (j >= c) {
-            j -= c;
-            m >>= width;
-            pos += width;
-        }
-    }
-    return pos;
 }
 
 // ---------------------------------------------------------------- deterministic backward layout
@@ -403,18 +438,19 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
 constexpr int kRecThreads = 128;
 
 // K5a: one thread per record (grid-stride over 32-record windows, one warp per
-// window): the entry's chain to camera space (chain_entry) and its attribute
-// term, then a segmented reduction of the window by kernel (shfl_down over
-// equal keys: a fixed tree given the layout). The first lane of each kernel's
-// piece writes it to pieces[k + window] -- injective, because records are in
-// kernel order, so a kernel's pieces are consecutive in window order.
+// window): the entry's terms of the regrouped chain (entry_coeffs: alpha d,
+// d_q, beta d d^T) and its attribute term as a row in shared memory, then the
+// window's rows summed per kernel piece, (piece, value) tasks over the lanes,
+// each in record order (a fixed order given the layout). Piece j of the window
+// goes to pieces[k + window] -- injective, because records are in kernel order,
+// so a kernel's pieces are consecutive in window order.
 struct GatherParams {
-    int K, D, nv;           // nv = 9 + D values per piece
+    int K, D, nv;           // nv = 10 + D values per piece: A (3), Q, B upper (6), d_attr (D)
     CameraP cam;
     const int4* kinfo;
     const int2* app;        // [K] {first record, count}
     const int* total;       // records of the render
-    const double4* bent;    // records {d_l, d_q, d_sigma, W}
+    const double4* bent;    // records {alpha, d_q, beta, W}
     const int2* bkey;       // records' {pixel, kernel}
     const double4* rays;    // [P] pixel rays (K4)
     const Rec64* rec64;
@@ -427,31 +463,63 @@ struct GatherParams {
     double* d_center;       // [K*3]
     double* d_inv_cov;      // [K*9]
     double* d_attr;         // [K*D]
-    double* packed;         // nullable: instead of d_center / d_inv_cov / d_attr, rows of nv values
+    double* packed;         // nullable: instead of d_center / d_inv_cov / d_attr, rows of 9 + D values
                             // [d_center(3) | d_inv_cov upper (00 01 02 11 12 22) | d_attr(D)] (multi-GPU)
     double* rt_part;        // [gridDim.x * 12] then [groups * 12]
     unsigned* tickets;      // [1 + groups], zero between launches (reset by the last CTAs)
     double* d_rt;           // [12] d_rotation (9), d_translation (3)
 };
 
-__global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
+#ifndef GVR_REC_MINB  // resident records CTAs per SM (register budget)
+#define GVR_REC_MINB 1
+#endif
+#ifndef GVR_REC_PREFETCH  // the next window's record loads issued under the current window's work
+#define GVR_REC_PREFETCH 0
+#endif
+
+__global__ void __launch_bounds__(kRecThreads, GVR_REC_MINB) records_kernel(GatherParams p) {
     // per warp: the window's record values [32][nv], summed per kernel piece by
     // one lane each, rows in record order
     extern __shared__ __align__(16) double s_rows[];
     const int lane = threadIdx.x & 31;
     double* rows = s_rows + (threadIdx.x >> 5) * 32 * p.nv;
     __shared__ int s_keys[kRecThreads / 32][32];
+    __shared__ int s_start[kRecThreads / 32][33];  // first record of each piece of the window, then the end
     int* keys = s_keys[threadIdx.x >> 5];
+    int* starts = s_start[threadIdx.x >> 5];
     const int n_rec = *p.total;
     const int windows = (n_rec + 31) >> 5;
     const int wstride = (gridDim.x * blockDim.x) >> 5;
-    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < windows; w += wstride) {
+    const float inv_nv = 1.0f / (float)p.nv;
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#if GVR_REC_PREFETCH
+    int2 key_n = make_int2(0, -1);
+    double4 b_n = make_double4(0, 0, 0, 0);
+    if (32 * w + lane < n_rec) {
+        key_n = p.bkey[32 * w + lane];
+        b_n = p.bent[32 * w + lane];
+    }
+#endif
+    for (; w < windows; w += wstride) {
         const int r = 32 * w + lane;
         const bool valid = r < n_rec;
+#if GVR_REC_PREFETCH
+        const int2 key = key_n;
+        const double4 b = b_n;
+        {
+            const int rn = r + 32 * wstride;
+            if (rn < n_rec) {
+                key_n = p.bkey[rn];
+                b_n = p.bent[rn];
+            }
+        }
+#endif
         int k = -1;
         if (valid) {
+#if !GVR_REC_PREFETCH
             const int2 key = p.bkey[r];
             const double4 b = p.bent[r];
+#endif
             k = key.y;
             const long long pix = key.x;
             const double4 ray = p.rays[pix];
@@ -460,28 +528,36 @@ __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
             double di[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) di[c] = c < p.D ? p.d_image[pix * p.D + c] : 0.0;
-            double v[9];
-            const double d[3] = {ray.x, ray.y, ray.z};
-            chain_entry(p.rec64[k], d, b.x, b.y, b.z, v, v + 3);
-#pragma unroll
-            for (int u = 0; u < 9; ++u) row[u] = v[u];
+            // the entry's terms of A = sum alpha d, Q = sum d_q, B = sum beta d d^T (entry_coeffs)
+            row[0] = b.x * ray.x;
+            row[1] = b.x * ray.y;
+            row[2] = b.x * ray.z;
+            row[3] = b.y;
+            row[4] = b.z * (ray.x * ray.x);
+            row[5] = b.z * (ray.x * ray.y);
+            row[6] = b.z * (ray.x * ray.z);
+            row[7] = b.z * (ray.y * ray.y);
+            row[8] = b.z * (ray.y * ray.z);
+            row[9] = b.z * (ray.z * ray.z);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-                if (c < p.D) row[9 + c] = b.w * di[c];
-            for (int c = 4; c < p.D; ++c) row[9 + c] = b.w * p.d_image[pix * p.D + c];
+                if (c < p.D) row[10 + c] = b.w * di[c];
+            for (int c = 4; c < p.D; ++c) row[10 + c] = b.w * p.d_image[pix * p.D + c];
         }
         keys[lane] = k;
         const int kprev = __shfl_up_sync(0xffffffffu, k, 1);
-        const unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || kprev != k));
-        const int nvalid = min(32, n_rec - 32 * w);
+        const bool head = valid && (lane == 0 || kprev != k);
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        const int npieces = __popc(heads);
+        if (head) starts[__popc(heads & ((1u << lane) - 1u))] = lane;
+        if (lane == 0) starts[npieces] = min(32, n_rec - 32 * w);
         __syncwarp();
         // piece sums: (piece, value) tasks over the lanes, each summing its rows
         // in record order
-        const int npieces = __popc(heads);
         for (int task = lane; task < npieces * p.nv; task += 32) {
-            const int j = task / p.nv, u = task - j * p.nv;
-            const int start = select_bit32(heads, j);
-            const int end = j + 1 < npieces ? select_bit32(heads, j + 1) : nvalid;
+            const int j = __float2int_rd(((float)task + 0.5f) * inv_nv);  // task / nv (exact: task < 2^20)
+            const int u = task - j * p.nv;
+            const int start = starts[j], end = starts[j + 1];
             // four interleaved partial sums (records q = start + 4i + r), combined in a fixed order
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int q = start;
@@ -531,16 +607,34 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
         for (int u = 0; u < 9; ++u) c9[u] = 0.0;
         if (ap.y > 0) {
             const int w0 = ap.x >> 5, w1 = (ap.x + ap.y - 1) >> 5;
+            double c10[10];  // A (3), Q, B upper (00 01 02 11 12 22)
+#pragma unroll
+            for (int u = 0; u < 10; ++u) c10[u] = 0.0;
             for (int w = w0; w <= w1; ++w) {
                 const double* src = p.pieces + (long long)(k + w) * p.nv;
 #pragma unroll
-                for (int u = 0; u < 9; ++u) c9[u] += src[u];
+                for (int u = 0; u < 10; ++u) c10[u] += src[u];
             }
             for (int c = 0; c < p.D; ++c) {
                 double a = 0.0;
-                for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 9 + c];
-                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = a;
+                for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 10 + c];
+                if (p.packed) p.packed[(long long)k * (9 + p.D) + 9 + c] = a;
                 else p.d_attr[(long long)p.D * k + c] = a;
+            }
+            // camera-space chain (entry_coeffs): dm = S (A - Q m),
+            // dS = sym(m A^T) + B - Q/2 m m^T (upper triangle)
+            const Rec64& r = p.rec64[k];
+            const double m0 = r.m[0], m1 = r.m[1], m2 = r.m[2], Q = c10[3];
+            const double u0 = fma(-Q, m0, c10[0]), u1 = fma(-Q, m1, c10[1]), u2 = fma(-Q, m2, c10[2]);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) c9[t] = fma(r.s[3 * t], u0, fma(r.s[3 * t + 1], u1, r.s[3 * t + 2] * u2));
+            const double mm[3] = {m0, m1, m2};
+            const int rr[6] = {0, 0, 0, 1, 1, 2};
+            const int cc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+                const int a0 = rr[t], a1 = cc[t];
+                c9[3 + t] = 0.5 * (mm[a0] * c10[a1] + c10[a0] * mm[a1]) + c10[4 + t] - 0.5 * Q * (mm[a0] * mm[a1]);
             }
         } else if (ki.x < 0 && ki.w > 0) {  // fallback accumulators (no mask rectangle): consume, re-zero
 #pragma unroll
@@ -550,13 +644,13 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
             }
             for (int c = 0; c < p.D; ++c) {
                 const double a = p.attr_fb[(long long)p.D * k + c];
-                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = a;
+                if (p.packed) p.packed[(long long)k * (9 + p.D) + 9 + c] = a;
                 else p.d_attr[(long long)p.D * k + c] = a;
                 p.attr_fb[(long long)p.D * k + c] = 0.0;
             }
         } else {
             for (int c = 0; c < p.D; ++c) {
-                if (p.packed) p.packed[(long long)k * p.nv + 9 + c] = 0.0;
+                if (p.packed) p.packed[(long long)k * (9 + p.D) + 9 + c] = 0.0;
                 else p.d_attr[(long long)p.D * k + c] = 0.0;
             }
         }
@@ -597,7 +691,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
 #pragma unroll
         for (int t = 0; t < 9; ++t) s_cov[9 * threadIdx.x + t] = dcov[t];
         if (p.packed) {
-            double* row = p.packed + (long long)k * p.nv;
+            double* row = p.packed + (long long)k * (9 + p.D);
 #pragma unroll
             for (int t = 0; t < 3; ++t) row[t] = dc[t];
             row[3] = dcov[0];
@@ -666,18 +760,32 @@ __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const dou
                                    double* __restrict__ d_image, double* __restrict__ d_alpha,
                                    double* __restrict__ loss, double* __restrict__ part_out, unsigned* ticket) {
     double part = 0.0;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_img + n_alpha;
-         idx += (long long)gridDim.x * blockDim.x) {
-        if (idx < n_img) {
-            const double diff = image[idx] - t_image[idx];
-            part += 0.5 * w_image * diff * diff;
-            d_image[idx] = w_image * diff;
-        } else {
-            const long long a = idx - n_img;
-            const double diff = alpha[a] - t_alpha[a];
-            part += 0.5 * w_alpha * diff * diff;
-            d_alpha[a] = w_alpha * diff;
-        }
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+    // 16-byte accesses where the buffers allow (pairs of values), two pairs in flight per thread
+    const bool vec = ((reinterpret_cast<uintptr_t>(image) | reinterpret_cast<uintptr_t>(t_image) |
+                       reinterpret_cast<uintptr_t>(d_image)) & 15) == 0;
+    const long long n2 = vec ? n_img / 2 : 0;
+    const double2* im2 = reinterpret_cast<const double2*>(image);
+    const double2* ti2 = reinterpret_cast<const double2*>(t_image);
+    double2* di2 = reinterpret_cast<double2*>(d_image);
+#pragma unroll 2
+    for (long long i = tid; i < n2; i += nt) {
+        const double2 a = im2[i], b = ti2[i];
+        const double x = a.x - b.x, y = a.y - b.y;
+        part += 0.5 * w_image * x * x;
+        part += 0.5 * w_image * y * y;
+        di2[i] = make_double2(w_image * x, w_image * y);
+    }
+    for (long long idx = 2 * n2 + tid; idx < n_img; idx += nt) {
+        const double diff = image[idx] - t_image[idx];
+        part += 0.5 * w_image * diff * diff;
+        d_image[idx] = w_image * diff;
+    }
+#pragma unroll 2
+    for (long long a = tid; a < n_alpha; a += nt) {
+        const double diff = alpha[a] - t_alpha[a];
+        part += 0.5 * w_alpha * diff * diff;
+        d_alpha[a] = w_alpha * diff;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);

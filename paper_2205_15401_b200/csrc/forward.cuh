@@ -5,6 +5,13 @@
 
 namespace gvrk {
 
+// FP32 constants of the q classification (classify_key), set on the host.
+struct QClass {
+    float c_rej, c_acc;   // 2(-ln eta + g), 2(-ln eta - g)
+    float slack_lo, slack_hi;  // 1 -/+ relative slack
+    float f, inv_f;       // F, 1 / F
+};
+
 struct FwdParams {
     CameraP cam;
     SelP sel;
@@ -12,6 +19,7 @@ struct FwdParams {
     double tau;
     float guard_abs;     // FP32 guard band on q (absolute)
     float prefilter_c1;  // 1 - relative slack on delta.S.delta
+    QClass qc;           // classification constants (from guard_abs, prefilter_c1, ln eta, F)
     int exact_only;      // test hook: every candidate through the exact FP64 trace
     int tiles_x;
     const int* tile_order;  // tiles by list length, longest first (LPT); first *n_order valid
@@ -38,6 +46,7 @@ struct FwdParams {
     double* topk_w; // [P*kp] or null
     double* tape_t; // [P*kp] T(l_k) of the selected entries (backward input)
     EntryRec* ent;  // [P*kp] traced selected entries (written by the blend)
+    double* ent_a;  // [P*kp] a = d.Sd of each selected entry (FP64, the backward's chain)
     float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
     int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
     unsigned* tile_done;     // [tiles] set (release) when the tile's selection is written; the blend,
@@ -68,11 +77,6 @@ struct FwdParams {
 // 6 units of 2^-24 |l| of the exact l (z: 1, c: <= 2 by the checked bound
 // below, fma + product: 2, nrm: 1), so keys more than kKeyClose apart order
 // like the exact keys and closer ones are decided on the exact trace.
-struct QClass {
-    float c_rej, c_acc;   // 2(-ln eta + g), 2(-ln eta - g)
-    float slack_lo, slack_hi;  // 1 -/+ relative slack
-    float f, inv_f;       // F, 1 / F
-};
 
 __device__ __forceinline__ int classify_key(const Rec32& r, int i, int j, float u, float v, float nrm,
                                             const QClass& qc, float* key) {
@@ -311,14 +315,7 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
     const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
     const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
     const float fi = (float)i, fj = (float)j;
-    const float neg_log_eta = -(float)p.sel.log_eta;
-    QClass qc;
-    qc.c_rej = 2.0f * (neg_log_eta + p.guard_abs);
-    qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
-    qc.slack_lo = p.prefilter_c1;
-    qc.slack_hi = 2.0f - p.prefilter_c1;
-    qc.f = (float)p.cam.focal;
-    qc.inv_f = (float)(1.0 / p.cam.focal);
+    const QClass& qc = p.qc;  // kernel parameter space: no registers
     const bool exact_only = p.exact_only != 0;
     const double log_eta = p.sel.log_eta;
     const Rec64* rec64 = p.rec64;
@@ -517,6 +514,134 @@ __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int
     return !__any_sync(FULL, bad);
 }
 
+// One pixel's K'-nearest selection (warp-wide) over a depth-ordered candidate
+// list (or, overflow, every kernel): lanes stride the list 32 candidates at a
+// time; box test (one 16-byte load), FP32 q classification and depth key for
+// the eligible lanes; the K' nearest kept warp-distributed and sorted (lane s
+// holds the s-th nearest) as FP32 rank keys + kernel ids; eligible candidates
+// merged per batch (merge_batch, or ranks from ballots with exact-trace
+// tie-breaks). Writes topk / count of the pixel; returns the count.
+__device__ __forceinline__ int select_pixel(const FwdParams& p, const unsigned long long* list, int end, bool overflow,
+                                            const double* d, float u, float v, float nrm, int i, int j,
+                                            const QClass& qc, bool exact_only, float* sl, int* si, int lane) {
+    const unsigned FULL = 0xffffffffu;
+    const int kp = p.sel.kp;
+    const Rec64* rec64 = p.rec64;
+    const double log_eta = p.sel.log_eta;
+    const bool early = !overflow;  // the list is ordered by its depth bound
+    const int start = 0;
+    const long long pix = (long long)i * p.cam.W + j;
+    const float fi = (float)i, fj = (float)j;
+
+    float L = INFINITY;  // lane s < n: rank key of the s-th nearest
+    int I = 0x7fffffff;
+    int n = 0;
+    float worst = INFINITY;  // key of lane kp-1 once full (warp-uniform)
+
+    for (int base = start; base < end; base += 32) {
+        const int e = base + lane;
+        const bool valid = e < end;
+        const int k = overflow ? (valid ? e : 0) : (int)(list[valid ? e : 0] & 0xffffffffu);
+        // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
+        if (early) {
+            const float zmin0 = float_from_order_bits((uint32_t)(list[base] >> 32));
+            if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
+        }
+        const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
+        const float4 box = __ldg(rp);        // top, bottom, left, right
+        const float4 zrec = __ldg(rp + 1);   // zmin, z, ci_frac, cj_frac
+        // zmin <= l for any kernel that can pass eta: a candidate whose bound is
+        // past the worst kept key cannot enter the full list (skip the tests)
+        const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w &&
+                            !(zrec.x > worst + 2.0f * kKeyClose * fabsf(worst));
+        int cls = 0;
+        float lk = INFINITY;
+        if (in_box) {
+            Rec32 r;
+            r.zmin = zrec.x;
+            r.z = zrec.y;
+            r.ci_frac = zrec.z;
+            r.cj_frac = zrec.w;
+            const float4 c2 = __ldg(rp + 2), c3 = __ldg(rp + 3);
+            r.ci_int = __float_as_int(c2.x);
+            r.cj_int = __float_as_int(c2.y);
+            r.s00 = c2.z;
+            r.s01 = c2.w;
+            r.s02 = c3.x;
+            r.s11 = c3.y;
+            r.s12 = c3.z;
+            r.s22 = c3.w;
+            cls = classify_key(r, i, j, u, v, nrm, qc, &lk);
+        }
+        if (cls != 0) {
+            if (exact_only || cls == 1) {
+                const double dr[3] = {d[0], d[1], d[2]};
+                const Traced64 t = trace_exact(dr, rec64[k]);
+                if (t.q > log_eta) {  // fine_select threshold (tracer.cpp:117-118)
+                    lk = (float)t.l;
+                } else {
+                    cls = 0;
+                }
+            }
+            // cannot enter a full list
+            if (cls != 0 && lk > worst + 2.0f * kKeyClose * fabsf(worst)) cls = 0;
+        }
+        const unsigned elig = __ballot_sync(FULL, cls != 0);
+#ifdef GVR_SEL_STATS  // experiment: histogram of eligible candidates per batch (n == 0 / n > 0) into tile_cycles
+        if (p.tile_cycles && lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles) + (n > 0 ? 33 : 0) + __popc(elig), 1ull);
+#endif
+        if (elig == 0) continue;
+        const bool me = (elig >> lane) & 1u;
+        const int m = __popc(elig);
+        bool merged = false;
+        if (m >= GVR_SEL_BATCH_MIN) merged = merge_batch(L, I, n, lk, k, me, m, kp, lane, sl, si);
+        if (!merged) {
+        // ranks: for each eligible candidate (broadcast), the kept keys and the
+        // other candidates smaller than it; kept entries count the candidates
+        // that precede them.
+        int shift = 0, mypos = 0;
+        unsigned pend = elig;
+        while (pend) {
+            const int src = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const float bl = __shfl_sync(FULL, lk, src);
+            const int bi = __shfl_sync(FULL, k, src);
+            const bool in_ex = lane < n, in_c = me && lane != src;
+            bool ex_lt = in_ex && L < bl;
+            bool c_lt = in_c && lk < bl;
+            const bool ex_close = in_ex && keyf_close(L, bl);
+            const bool c_close = in_c && keyf_close(lk, bl);
+            if (__any_sync(FULL, ex_close || c_close)) {  // rare: decide on the exact trace
+                if (ex_close) ex_lt = exact_less(I, bi, d, rec64);
+                if (c_close) c_lt = exact_less(k, bi, d, rec64);
+            }
+            const int pos = __popc(__ballot_sync(FULL, ex_lt)) + __popc(__ballot_sync(FULL, c_lt));
+            if (lane == src) mypos = pos;
+            if (in_ex && !ex_lt) ++shift;
+        }
+        // scatter into the merged order, keep the first kp
+        if (lane < n && lane + shift < kp) {
+            sl[lane + shift] = L;
+            si[lane + shift] = I;
+        }
+        if (me && mypos < kp) {
+            sl[mypos] = lk;
+            si[mypos] = k;
+        }
+        }
+        __syncwarp();
+        n = min(n + m, kp);
+        L = lane < n ? sl[lane] : INFINITY;
+        I = lane < n ? (si[lane] & 0x7fffffff) : 0x7fffffff;
+        __syncwarp();
+        if (n == kp) worst = __shfl_sync(FULL, L, kp - 1);
+    }
+    if (lane < n) p.topk[pix * kp + lane] = I;  // exact (l, idx) order
+    if (lane == 0) p.count[pix] = n;
+    return n;
+}
+
 // K3a selection, warp-per-pixel form (K' <= 32). CTA = one 8x8 tile, 8 warps;
 // warp w handles pixels w, w+8, ... of the tile. Lanes stride the tile's list
 // 32 candidates at a time: box test (one 16-byte load), FP32 q classification
@@ -546,8 +671,6 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     const unsigned long long* tl = keys;
     const int listed = load_sorted_list(p, tile, keys, p.list_smem, &tl);
     const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
-    const bool early = !overflow;  // the list is ordered by its depth bound
-    const int start = 0;
     // Each warp owns a 2x4-pixel sub-block of the tile and first compacts the
     // tile list to the entries whose screen box meets the sub-block (stable, so
     // the depth order survives): its pixels then scan ~half the list. Lists
@@ -596,6 +719,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     // with its slowest warp)
     constexpr int NSB = 8 / GVR_SEL_SPLIT;  // sub-blocks (= warps) of this CTA
     __shared__ int sh_end[NSB], sh_sbo[NSB], sh_next;
+    __shared__ int2 sh_tile_rc;  // the tile's first pixel row / column
+    if (threadIdx.x == 0) sh_tile_rc = make_int2(sr0 - (sb >> 1) * 2, sc0 - (sb & 1) * 4);
     if (lane == 0) sh_end[warp] = list == wlist ? end : -1;
     if (threadIdx.x == 0) sh_next = 0;
     __syncthreads();
@@ -631,17 +756,7 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     }
     __syncthreads();
 #endif
-    const int kp = p.sel.kp;
-    const Rec64* rec64 = p.rec64;
-    const double log_eta = p.sel.log_eta;
-    const float neg_log_eta = -(float)p.sel.log_eta;
-    QClass qc;
-    qc.c_rej = 2.0f * (neg_log_eta + p.guard_abs);
-    qc.c_acc = 2.0f * (neg_log_eta - p.guard_abs);
-    qc.slack_lo = p.prefilter_c1;
-    qc.slack_hi = 2.0f - p.prefilter_c1;
-    qc.f = (float)p.cam.focal;
-    qc.inv_f = (float)(1.0 / p.cam.focal);
+    const QClass& qc = p.qc;  // kernel parameter space: no registers
     const bool exact_only = p.exact_only != 0;
     float cost = 0.0f;
 
@@ -653,8 +768,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         if (item >= NSB * 8) break;
         const int pw = sh_sbo[item >> 3], px = item & 7;  // owning warp, pixel of its sub-block
         const int psb = (blockIdx.x % GVR_SEL_SPLIT) * NSB + pw;
-        const int psr = (tile / p.tiles_x) * TILE + (psb >> 1) * 2;
-        const int psc = (tile % p.tiles_x) * TILE + (psb & 1) * 4;
+        const int psr = sh_tile_rc.x + (psb >> 1) * 2;  // (no per-item division)
+        const int psc = sh_tile_rc.y + (psb & 1) * 4;
         const int i = psr + (px >> 2);
         const int j = psc + (px & 3);
         const int pe = sh_end[pw];
@@ -676,115 +791,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
         const float nrm = (float)sqrt((double)u * u + (double)v * v + 1.0);
 #endif
-        const long long pix = (long long)i * p.cam.W + j;
-        const float fi = (float)i, fj = (float)j;
-
-        float L = INFINITY;  // lane s < n: rank key of the s-th nearest
-        int I = 0x7fffffff;
-        int n = 0;
-        float worst = INFINITY;  // key of lane kp-1 once full (warp-uniform)
-
-        for (int base = start; base < end; base += 32) {
-            const int e = base + lane;
-            const bool valid = e < end;
-            const int k = overflow ? (valid ? e : 0) : (int)(list[valid ? e : 0] & 0xffffffffu);
-            // early exit: lists are sorted by zmin <= l; the batch's first zmin bounds the rest
-            if (early) {
-                const float zmin0 = float_from_order_bits((uint32_t)(list[base] >> 32));
-                if (zmin0 > worst + 2.0f * kKeyClose * fabsf(worst)) break;
-            }
-            const float4* rp = reinterpret_cast<const float4*>(p.rec32 + k);
-            const float4 box = __ldg(rp);        // top, bottom, left, right
-            const float4 zrec = __ldg(rp + 1);   // zmin, z, ci_frac, cj_frac
-            // zmin <= l for any kernel that can pass eta: a candidate whose bound is
-            // past the worst kept key cannot enter the full list (skip the tests)
-            const bool in_box = valid && fi >= box.x && fi <= box.y && fj >= box.z && fj <= box.w &&
-                                !(zrec.x > worst + 2.0f * kKeyClose * fabsf(worst));
-            int cls = 0;
-            float lk = INFINITY;
-            if (in_box) {
-                Rec32 r;
-                r.zmin = zrec.x;
-                r.z = zrec.y;
-                r.ci_frac = zrec.z;
-                r.cj_frac = zrec.w;
-                const float4 c2 = __ldg(rp + 2), c3 = __ldg(rp + 3);
-                r.ci_int = __float_as_int(c2.x);
-                r.cj_int = __float_as_int(c2.y);
-                r.s00 = c2.z;
-                r.s01 = c2.w;
-                r.s02 = c3.x;
-                r.s11 = c3.y;
-                r.s12 = c3.z;
-                r.s22 = c3.w;
-                cls = classify_key(r, i, j, u, v, nrm, qc, &lk);
-            }
-            if (cls != 0) {
-                if (exact_only || cls == 1) {
-                    const double dr[3] = {d[0], d[1], d[2]};
-                    const Traced64 t = trace_exact(dr, rec64[k]);
-                    if (t.q > log_eta) {  // fine_select threshold (tracer.cpp:117-118)
-                        lk = (float)t.l;
-                    } else {
-                        cls = 0;
-                    }
-                }
-                // cannot enter a full list
-                if (cls != 0 && lk > worst + 2.0f * kKeyClose * fabsf(worst)) cls = 0;
-            }
-            const unsigned elig = __ballot_sync(FULL, cls != 0);
-#ifdef GVR_SEL_STATS  // experiment: histogram of eligible candidates per batch (n == 0 / n > 0) into tile_cycles
-            if (p.tile_cycles && lane == 0)
-                atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles) + (n > 0 ? 33 : 0) + __popc(elig), 1ull);
-#endif
-            if (elig == 0) continue;
-            const bool me = (elig >> lane) & 1u;
-            const int m = __popc(elig);
-            bool merged = false;
-            if (m >= GVR_SEL_BATCH_MIN) merged = merge_batch(L, I, n, lk, k, me, m, kp, lane, sh_l[warp], sh_i[warp]);
-            if (!merged) {
-            // ranks: for each eligible candidate (broadcast), the kept keys and the
-            // other candidates smaller than it; kept entries count the candidates
-            // that precede them.
-            int shift = 0, mypos = 0;
-            unsigned pend = elig;
-            while (pend) {
-                const int src = __ffs(pend) - 1;
-                pend &= pend - 1;
-                const float bl = __shfl_sync(FULL, lk, src);
-                const int bi = __shfl_sync(FULL, k, src);
-                const bool in_ex = lane < n, in_c = me && lane != src;
-                bool ex_lt = in_ex && L < bl;
-                bool c_lt = in_c && lk < bl;
-                const bool ex_close = in_ex && keyf_close(L, bl);
-                const bool c_close = in_c && keyf_close(lk, bl);
-                if (__any_sync(FULL, ex_close || c_close)) {  // rare: decide on the exact trace
-                    if (ex_close) ex_lt = exact_less(I, bi, d, rec64);
-                    if (c_close) c_lt = exact_less(k, bi, d, rec64);
-                }
-                const int pos = __popc(__ballot_sync(FULL, ex_lt)) + __popc(__ballot_sync(FULL, c_lt));
-                if (lane == src) mypos = pos;
-                if (in_ex && !ex_lt) ++shift;
-            }
-            // scatter into the merged order, keep the first kp
-            if (lane < n && lane + shift < kp) {
-                sh_l[warp][lane + shift] = L;
-                sh_i[warp][lane + shift] = I;
-            }
-            if (me && mypos < kp) {
-                sh_l[warp][mypos] = lk;
-                sh_i[warp][mypos] = k;
-            }
-            }
-            __syncwarp();
-            n = min(n + m, kp);
-            L = lane < n ? sh_l[warp][lane] : INFINITY;
-            I = lane < n ? (sh_i[warp][lane] & 0x7fffffff) : 0x7fffffff;
-            __syncwarp();
-            if (n == kp) worst = __shfl_sync(FULL, L, kp - 1);
-        }
-        if (lane < n) p.topk[pix * kp + lane] = I;  // exact (l, idx) order
-        if (lane == 0) p.count[pix] = n;
+        const int n = select_pixel(p, list, end, overflow, d, u, v, nrm, i, j, qc, exact_only, sh_l[warp], sh_i[warp],
+                                   lane);
         cost += (float)(n * n);
     }
     if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
@@ -893,6 +901,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
                 const double pk = exp(t.q);
                 const float pkf = (float)pk;
                 b_w[s * NP + g] = pk;  // FP64 peak until W overwrites it (alpha sum, after the sort)
+                if (p.presorted) p.ent_a[pix * kp + s] = t.a;
                 BlendSlot v;
                 v.l = t.l;  // l for now; relative to the nearest after the sort
                 v.pk = pkf;
@@ -952,6 +961,7 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         if (!p.presorted) {
             b_id[s * NP + g] &= ~kExact;
             p.topk[pix * kp + s] = b_id[s * NP + g];
+            p.ent_a[pix * kp + s] = trace_fast(d, p.rec64[b_id[s * NP + g]]).a;  // the same a, sorted order
         }
         // tape the traced entry for the backward and the sampler
         EntryRec er;

@@ -32,6 +32,9 @@
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
 #endif
+#ifndef GVR_BWD_F32  // backward pair loop in FP32 with Kahan-compensated sums
+#define GVR_BWD_F32 1
+#endif
 #ifndef GVR_BWD_IDS_FIRST  // backward staging loop: entry ids loaded before the records
 #define GVR_BWD_IDS_FIRST 1
 #endif

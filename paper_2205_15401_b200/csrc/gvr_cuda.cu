@@ -147,9 +147,10 @@ struct gvr_tape {
     Buf tile_count, tile_off, tile_fill, pool, sorted_pool, tile_cycles;
     long long pool_hint = 0;  // entries the last observed render listed (grow-only sizing)
     bool profiled = false;    // the last render recorded tile cycles
-    Buf sched;  // [0] n_fwd, [1] n_bwd, then order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float)
+    Buf sched;  // [0] n_fwd, [1] n_bwd, order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float), n_all,
+                // tile_done[tiles]
     // per pixel
-    Buf topk, count, image, alpha, depth, topk_w, tape_t, ent;
+    Buf topk, count, image, alpha, depth, topk_w, tape_t, ent, ent_a;
     Buf d_image, d_alpha;
     // gradients
     Buf acc, attr_fb, d_attr, d_center, d_inv_cov, d_rt;
@@ -812,7 +813,7 @@ void gvr_tape_destroy(gvr_tape* t) {
     cudaStreamSynchronize(t->ctx->stream);
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_off, &t->tile_fill, &t->pool, &t->sorted_pool,
                    &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
-                   &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
+                   &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->ent_a, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags, &t->attr_fb, &t->kinfo,
                    &t->masks, &t->slot_off, &t->app, &t->bent, &t->bkey, &t->rays, &t->pieces, &t->kcount, &t->rt_part, &t->tickets,
                    &t->loss_part};
@@ -932,6 +933,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
     CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->ent.ensure(sizeof(EntryRec) * (size_t)P * kp));
+    CUDA_TRY(ctx, tape->ent_a.ensure(sizeof(double) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->image.ensure(sizeof(double) * (size_t)P * Dc));
     CUDA_TRY(ctx, tape->alpha.ensure(sizeof(double) * (size_t)P));
     CUDA_TRY(ctx, tape->depth.ensure(sizeof(double) * (size_t)P));
@@ -1018,6 +1020,15 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.tau = scene->tau;
     fp.guard_abs = (float)ctx->guard;
     fp.prefilter_c1 = 1.0f - 1e-4f;
+    {
+        const float neg_log_eta = -(float)sp.log_eta;
+        fp.qc.c_rej = 2.0f * (neg_log_eta + fp.guard_abs);
+        fp.qc.c_acc = 2.0f * (neg_log_eta - fp.guard_abs);
+        fp.qc.slack_lo = fp.prefilter_c1;
+        fp.qc.slack_hi = 2.0f - fp.prefilter_c1;
+        fp.qc.f = (float)cp.focal;
+        fp.qc.inv_f = (float)(1.0 / cp.focal);
+    }
     fp.exact_only = ctx->guard > 1e3 ? 1 : 0;
     fp.tiles_x = tiles_x;
     fp.tile_order = order_f;
@@ -1047,6 +1058,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.topk_w = want_w ? tape->topk_w.as<double>() : nullptr;
     fp.tape_t = tape->tape_t.as<double>();
     fp.ent = tape->ent.as<EntryRec>();
+    fp.ent_a = tape->ent_a.as<double>();
     fp.nonfinite = dflags + 1;
     fp.kinfo = tape->kinfo.as<int4>();
     fp.masks = tape->masks.as<unsigned long long>();
@@ -1311,7 +1323,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     if (int rc = ensure_zeroed(ctx, t->attr_fb, sizeof(double) * (size_t)(D > 0 ? D : 1) * (K > 0 ? K : 1))) return rc;
     if (int rc = ensure_zeroed(ctx, t->tickets, sizeof(unsigned) * (2 + (size_t)rt_groups))) return rc;
     CUDA_TRY(ctx, t->rt_part.ensure(sizeof(double) * 12 * ((size_t)finish_grid + rt_groups)));
-    CUDA_TRY(ctx, t->pieces.ensure(sizeof(double) * (9 + (size_t)D) * ((size_t)K + windows + 1)));
+    CUDA_TRY(ctx, t->pieces.ensure(sizeof(double) * (10 + (size_t)D) * ((size_t)K + windows + 1)));
 
     CUDA_TRY(ctx, t->bent.ensure(sizeof(double4) * (size_t)(P_kp > 0 ? P_kp : 1)));
     CUDA_TRY(ctx, t->bkey.ensure(sizeof(int2) * (size_t)(P_kp > 0 ? P_kp : 1)));
@@ -1348,6 +1360,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.count = t->count.as<int>();
         bp.tape_t = t->tape_t.as<double>();
         bp.ent = t->ent.as<EntryRec>();
+        bp.ent_a = t->ent_a.as<double>();
         bp.rec64 = t->rec64.as<Rec64>();
         bp.attr = scene->attr.as<double>();
         bp.d_image = di;
@@ -1395,7 +1408,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         GatherParams gp{};
         gp.K = K;
         gp.D = D;
-        gp.nv = 9 + D;
+        gp.nv = 10 + D;
         gp.cam = t->camp;
         gp.kinfo = t->kinfo.as<int4>();
         gp.app = t->app.as<int2>();

@@ -118,7 +118,9 @@ def test_two_ranks_match_one_rank():
     assert np.array_equal(np.where(own0, r0["image"], r1["image"]), one["image"])
     for a, b, c in zip(r0["grads"], r1["grads"], one["grads"]):
         assert np.array_equal(a, b)  # every rank holds the same reduced gradient
-        np.testing.assert_allclose(a, c, rtol=1e-9, atol=1e-12 * np.abs(c).max())
+        # the same sums in another grouping (per shard, then NCCL): FP64 rounding of the
+        # per-kernel chain, which cancels up to (|m| / sigma)^2 (backward.cuh: entry_coeffs)
+        np.testing.assert_allclose(a, c, rtol=1e-9, atol=1e-10 * np.abs(c).max())
     # C5: identical parameters on both ranks, the 1-rank trajectory
     assert np.array_equal(r0["params"], r1["params"])
     np.testing.assert_allclose(r0["params"], one["params"], rtol=1e-9, atol=1e-12)
