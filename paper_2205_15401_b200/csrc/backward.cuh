@@ -221,8 +221,7 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
             const float dlf = (qk.x - qe.x) + (qk.y - qe.y);
             const float z1 = dlf * ise;
             const float phi1 = normal_pdf_fast(z1);
-            // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
-            const float phi2 = isk == ise ? phi1 : normal_pdf_fast(-dlf * isk);
+            const float phi2 = normal_pdf_fast(-dlf * isk);  // branch-free (equals phi1 when sigma_k == sigma_e)
             kahan(s_pk, c_pk, qk.z * fast_normal_cdf(z1));
             const float gg = k != e ? qk.z * (phi1 * ise) * pkef : 0.0f;
             kahan(s_sg, c_sg, -gg * z1);

@@ -221,9 +221,23 @@ __device__ __forceinline__ float normal_pdf_f(float x) { return 0.39894228040143
 // Branch-free Phi for the forward blend: erfc(x) = t exp(-x^2 + P(t)),
 // t = 1 / (1 + x/2) (Chebyshev-fitted erfc, fractional error < 1.2e-7 for all
 // x >= 0), so |Phi - Phi_exact| < 6e-8 absolute: one reciprocal, one exp2, 10 FMA.
+// The SFU instructions without the denormal-range fix-ups of exp2f / __fdividef
+// (equal results outside that range: the reciprocal's argument is >= 1 here,
+// and exp2 results below 2^-126 flush to zero).
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float fast_normal_cdf(float z) {
     const float x = fabsf(z) * 0.70710678118654752f;
-    const float t = __fdividef(1.0f, fmaf(0.5f, x, 1.0f));
+    const float t = rcp_ftz(fmaf(0.5f, x, 1.0f));
     float p = 0.17087277f;
     p = fmaf(p, t, -0.82215223f);
     p = fmaf(p, t, 1.48851587f);
@@ -234,14 +248,14 @@ __device__ __forceinline__ float fast_normal_cdf(float z) {
     p = fmaf(p, t, 0.37409196f);
     p = fmaf(p, t, 1.00002368f);
     p = fmaf(p, t, -1.26551223f);
-    const float e = exp2f(fmaf(-x, x, p) * 1.4426950408889634f);
+    const float e = ex2_ftz(fmaf(-x, x, p) * 1.4426950408889634f);
     const float half_erfc = 0.5f * t * e;
     return z >= 0.0f ? 1.0f - half_erfc : half_erfc;
 }
 
 // phi(z) with the hardware exp2 (relative error ~2^-22 + |z^2/2| 2^-24).
 __device__ __forceinline__ float normal_pdf_fast(float z) {
-    return 0.398942280401432678f * exp2f(-0.72134752044448170f * z * z);
+    return 0.398942280401432678f * ex2_ftz(-0.72134752044448170f * z * z);
 }
 
 // Order-preserving float <-> uint32 map (sort keys of the depth bound).
