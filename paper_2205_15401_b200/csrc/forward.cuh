@@ -52,6 +52,7 @@ struct FwdParams {
     unsigned* tile_done;     // [tiles] set (release) when the tile's selection is written; the blend,
                              // launched as a programmatic dependent, waits per tile (nullable)
     long long* tile_cycles;  // profiling hook: [tiles] SM cycles of the tile's selection CTA (nullable)
+    unsigned* tile_hint;     // [tiles] out: the same cycles, the LPT costs of the next render of this view
     int precise;     // verification mode: FP64 exact traces and erfc in the blend sums (gradcheck)
     int* nonfinite; // flag
     const int4* kinfo;          // [K] mask rectangles (project_kernel)
@@ -661,8 +662,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     // GVR_SEL_SPLIT CTAs per tile, each 8 / GVR_SEL_SPLIT warps (2x4 sub-blocks)
     launch_dependents();  // the blend may fill the SMs this grid's tail leaves idle
     if ((int)(blockIdx.x / GVR_SEL_SPLIT) >= *p.n_order) return;
-    __shared__ long long sh_t0;  // profiling hook (kept out of registers)
-    if (p.tile_cycles && threadIdx.x == 0) sh_t0 = clock64();
+    __shared__ long long sh_t0;  // the CTA's start (cost hint, profiling hook; kept out of registers)
+    if (threadIdx.x == 0) sh_t0 = clock64();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sb = (blockIdx.x % GVR_SEL_SPLIT) * (8 / GVR_SEL_SPLIT) + warp;  // sub-block of the tile
     const unsigned FULL = 0xffffffffu;
@@ -796,15 +797,16 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         cost += (float)(n * n);
     }
     if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
-    if (p.tile_done || p.tile_cycles) {
+    if (p.tile_done || p.tile_cycles || p.tile_hint) {
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
+            const long long dt = clock64() - sh_t0;  // the CTA's duration (its slowest warp)
 #ifndef GVR_SEL_STATS
-            if (p.tile_cycles)  // profiling hook: the CTA's duration (its slowest warp)
-                atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles + tile),
-                          (unsigned long long)(clock64() - sh_t0));
+            if (p.tile_cycles)  // profiling hook
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles + tile), (unsigned long long)dt);
 #endif
+            if (p.tile_hint) p.tile_hint[tile] = (unsigned)min(max(dt, 1ll), 0xffffffffll);
             if (p.tile_done) red_add_release_gpu(p.tile_done + tile, 1u);  // one count per split CTA
         }
     }
@@ -1147,14 +1149,17 @@ __device__ void list_offsets(int tiles, const int* __restrict__ count, int* __re
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
 // log-spaced cost buckets, descending). Zero-cost tiles and tiles of other
 // shards (t % nshards != shard) are dropped; *n_out receives the number kept.
-// Cost = icost[t] (list length) or fcost[t]. With tile_off, the tile-list
-// offsets are laid out first (list_offsets; icost = the list lengths).
+// Cost = icost[t] (list length) or fcost[t]; with a hint (the selection cycles
+// of the previous render of the same view, tile_hint) the listed tiles are
+// ordered by it instead. With tile_off, the tile-list offsets are laid out
+// first (list_offsets; icost = the list lengths).
 __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
                                                            const float* __restrict__ fcost, int* __restrict__ order,
                                                            int* __restrict__ n_out, int shard, int nshards,
                                                            int* __restrict__ n_all_out, int* __restrict__ tile_off = nullptr,
                                                            int pool_cap = 0, int smem_cap = 0,
-                                                           int* __restrict__ stats = nullptr) {
+                                                           int* __restrict__ stats = nullptr,
+                                                           const unsigned* __restrict__ hint = nullptr) {
     __shared__ int hist[256];
     __shared__ int offs[256];
     __shared__ int s_tail;
@@ -1163,8 +1168,9 @@ __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int*
     __syncthreads();
     auto bucket_of = [&](int t) -> int {
         if (t % nshards != shard) return -1;  // tile owned by another rank (C4 tile sharding)
-        const float c = fcost ? fcost[t] : (float)icost[t];
+        float c = fcost ? fcost[t] : (float)icost[t];
         if (!(c > 0.0f)) return -1;
+        if (hint) c = hint[t] > 0u ? (float)hint[t] : 100.0f * c;  // cycles (a tile new to the view: ~100 / entry)
         const int b = (int)(__log2f(c + 1.0f) * 8.0f);
         return 255 - min(b, 255);  // descending cost
     };

@@ -21,7 +21,7 @@
 #define GVR_SEL_MINB 3
 #endif
 #ifndef GVR_BLEND_MINB
-#define GVR_BLEND_MINB 12
+#define GVR_BLEND_MINB 10
 #endif
 #ifndef GVR_ONE_ORDER
 #define GVR_ONE_ORDER 1

@@ -145,6 +145,12 @@ struct gvr_tape {
     Buf rec32, rec64;
     // per-tile candidate lists
     Buf tile_count, tile_off, tile_fill, pool, sorted_pool, tile_cycles;
+    // LPT cost hint: the selection cycles per tile of the last render, valid for the
+    // same camera and tile layout (hint_cam, hint_shard) -- repeated renders of a view
+    Buf tile_hint;
+    bool hint_valid = false;
+    CameraP hint_cam{};
+    int hint_tiles = 0, hint_shard = -1, hint_nshards = 0;
     long long pool_hint = 0;  // entries the last observed render listed (grow-only sizing)
     bool profiled = false;    // the last render recorded tile cycles
     Buf sched;  // [0] n_fwd, [1] n_bwd, order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float), n_all,
@@ -812,7 +818,7 @@ void gvr_tape_destroy(gvr_tape* t) {
     if (!t) return;
     cudaStreamSynchronize(t->ctx->stream);
     Buf* bufs[] = {&t->rec32, &t->rec64, &t->tile_count, &t->tile_off, &t->tile_fill, &t->pool, &t->sorted_pool,
-                   &t->tile_cycles, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
+                   &t->tile_cycles, &t->tile_hint, &t->sched, &t->topk, &t->count, &t->image, &t->alpha,
                    &t->depth, &t->topk_w, &t->tape_t, &t->ent, &t->ent_a, &t->d_image, &t->d_alpha, &t->acc, &t->d_attr, &t->d_center,
                    &t->d_inv_cov, &t->d_rt, &t->stage_i, &t->stage_w, &t->flags, &t->attr_fb, &t->kinfo,
                    &t->masks, &t->slot_off, &t->app, &t->bent, &t->bkey, &t->rays, &t->pieces, &t->kcount, &t->rt_part, &t->tickets,
@@ -980,13 +986,19 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         LAUNCH_CHECK(ctx);
     }
 
-    // K3 over the non-empty tiles, longest list first
+    // K3 over the non-empty tiles, longest first: by the last render's selection
+    // cycles when this tape rendered the same view before, else by list length
+    const bool use_hint = tape->hint_valid && tape->hint_tiles == tiles && tape->hint_shard == shard &&
+                          tape->hint_nshards == nshards && std::memcmp(&tape->hint_cam, &cp, sizeof cp) == 0;
+    const bool want_hint = kp <= 32;  // the warp selection measures it
+    if (want_hint) CUDA_TRY(ctx, tape->tile_hint.ensure(sizeof(unsigned) * (size_t)tiles));
     {
         StageTimer st(ctx, ST_RANGES);
 #if GVR_ONE_ORDER  // one order (list length) for selection, blend and backward; then every other tile
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
                                                         sched + 2 + 3 * (size_t)tiles, tape->tile_off.as<int>(),
-                                                        (int)pool_cap, ctx->list_smem, dflags + kListStats);
+                                                        (int)pool_cap, ctx->list_smem, dflags + kListStats,
+                                                        use_hint ? tape->tile_hint.as<unsigned>() : nullptr);
 #else
         order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
                                                         nullptr, tape->tile_off.as<int>(), (int)pool_cap, ctx->list_smem,
@@ -1067,6 +1079,12 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.precise = ctx->precise ? 1 : 0;
     fp.tile_cycles = nullptr;
     fp.tile_done = GVR_PDL ? reinterpret_cast<unsigned*>(sched + 3 + 3 * (size_t)tiles) : nullptr;
+    fp.tile_hint = want_hint ? tape->tile_hint.as<unsigned>() : nullptr;
+    tape->hint_valid = want_hint;
+    tape->hint_cam = cp;
+    tape->hint_tiles = tiles;
+    tape->hint_shard = shard;
+    tape->hint_nshards = nshards;
     tape->profiled = ctx->tile_profile;
     if (ctx->tile_profile) {
         CUDA_TRY(ctx, tape->tile_cycles.ensure(sizeof(long long) * (size_t)tiles));
