@@ -109,6 +109,10 @@ struct gvr_context {
     cudaEvent_t fork_ev = nullptr;
     Buf ptr_table;
     gvr_tape* aux_tape = nullptr;  // render behind gvr_sample_attributes
+    // async host-buffer mode: device->host copies of a call's outputs drain on this
+    // stream while the context stream runs the next call (out_begin / out_end)
+    cudaStream_t out_stream = nullptr;
+    cudaEvent_t out_fork = nullptr;
 };
 
 struct gvr_graph {
@@ -145,6 +149,10 @@ struct gvr_tape {
     Buf rec32, rec64;
     // per-tile candidate lists
     Buf tile_count, tile_off, tile_fill, pool, sorted_pool, tile_cycles;
+    // pending device->host output copies on the context's out_stream, per call kind
+    // (0 render, 1 loss, 2 backward): the next call of that kind rewrites their sources
+    cudaEvent_t out_ev[3] = {nullptr, nullptr, nullptr};
+    bool out_pending[3] = {false, false, false};
     // LPT cost hint: the selection cycles per tile of the last render, valid for the
     // same camera and tile layout (hint_cam, hint_shard) -- repeated renders of a view
     Buf tile_hint;
@@ -254,11 +262,46 @@ int copy_in(gvr_context* ctx, void* dst, const void* src, size_t bytes) {
 }
 
 // Returns true in *host if a D2H copy was enqueued (caller must synchronise).
-int copy_out(gvr_context* ctx, void* dst, const void* src, size_t bytes, bool* host) {
+// Host destinations go on `hs` (the out stream of an async call, else the context stream).
+int copy_out(gvr_context* ctx, void* dst, const void* src, size_t bytes, bool* host, cudaStream_t hs = nullptr) {
     if (!dst || bytes == 0) return GVR_OK;
     const bool dev = is_device_ptr(dst);
-    CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                  dev || !hs ? ctx->stream : hs));
     if (!dev) *host = true;
+    return GVR_OK;
+}
+
+// Async host-buffer mode: the host copies of a call's outputs are forked onto the
+// context's out stream (after everything the context stream has enqueued), so the
+// next call of the step does not queue behind them; out_end records their event on
+// the tape and out_wait makes the next call of the same kind (which rewrites the
+// copied buffers) wait for it. Synchronous mode and graph capture: the context stream.
+int out_begin(gvr_context* ctx, cudaStream_t* hs) {
+    *hs = ctx->stream;
+    if (!ctx->async || ctx->capturing) return GVR_OK;
+    if (!ctx->out_stream) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->out_fork, cudaEventDisableTiming));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->out_fork, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->out_stream, ctx->out_fork, 0));
+    *hs = ctx->out_stream;
+    return GVR_OK;
+}
+
+int out_end(gvr_context* ctx, gvr_tape* t, int kind, cudaStream_t hs) {
+    if (hs == ctx->stream) return GVR_OK;
+    if (!t->out_ev[kind]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&t->out_ev[kind], cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventRecord(t->out_ev[kind], hs));
+    t->out_pending[kind] = true;
+    return GVR_OK;
+}
+
+int out_wait(gvr_context* ctx, gvr_tape* t, int kind) {
+    if (!t->out_pending[kind]) return GVR_OK;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, t->out_ev[kind], 0));
+    t->out_pending[kind] = false;
     return GVR_OK;
 }
 
@@ -390,6 +433,7 @@ int sync_and_check(gvr_context* ctx) {
     if (ctx->capturing)
         return set_err(ctx, GVR_ERR_RUNTIME, "operation needs a host synchronisation; not allowed while capturing a graph");
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->out_stream) CUDA_TRY(ctx, cudaStreamSynchronize(ctx->out_stream));
     if (!ctx->ev_pending.empty()) harvest_timings(ctx);
     return GVR_OK;
 }
@@ -489,6 +533,11 @@ void gvr_context_destroy(gvr_context* ctx) {
     for (cudaStream_t w : ctx->workers) cudaStreamDestroy(w);
     for (cudaEvent_t e : ctx->join_ev) cudaEventDestroy(e);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->out_stream) {
+        cudaStreamSynchronize(ctx->out_stream);
+        cudaStreamDestroy(ctx->out_stream);
+    }
+    if (ctx->out_fork) cudaEventDestroy(ctx->out_fork);
     if (ctx->aux_tape) gvr_tape_destroy(ctx->aux_tape);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -825,6 +874,9 @@ void gvr_tape_destroy(gvr_tape* t) {
                    &t->loss_part};
     for (Buf* b : bufs) b->release();
     if (t->h_flags) cudaFreeHost(t->h_flags);
+    if (t->ctx->out_stream) cudaStreamSynchronize(t->ctx->out_stream);
+    for (cudaEvent_t e : t->out_ev)
+        if (e) cudaEventDestroy(e);
     delete t;
 }
 
@@ -857,6 +909,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     if (!scene->valid) return set_err(ctx, GVR_ERR_VALIDATION, "scene has not been validated");
     if (int rc = validate_camera(ctx, camera)) return rc;
     if (int rc = validate_cfg(ctx, cfg)) return rc;
+    if (int rc = out_wait(ctx, tape, 0)) return rc;  // the last render's host copies read image / alpha / depth
     tape->valid = false;
     tape->has_upstream = false;
 
@@ -1111,9 +1164,11 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
 
     if (out) {
         bool host = false;
-        if ((rc = copy_out(ctx, out->image, tape->image.p, sizeof(double) * P * Dc, &host))) return rc;
-        if ((rc = copy_out(ctx, out->alpha, tape->alpha.p, sizeof(double) * P, &host))) return rc;
-        if ((rc = copy_out(ctx, out->depth, tape->depth.p, sizeof(double) * P, &host))) return rc;
+        cudaStream_t hs;
+        if ((rc = out_begin(ctx, &hs))) return rc;
+        if ((rc = copy_out(ctx, out->image, tape->image.p, sizeof(double) * P * Dc, &host, hs))) return rc;
+        if ((rc = copy_out(ctx, out->alpha, tape->alpha.p, sizeof(double) * P, &host, hs))) return rc;
+        if ((rc = copy_out(ctx, out->depth, tape->depth.p, sizeof(double) * P, &host, hs))) return rc;
         if (out->topk_idx || out->topk_w) {
             const bool dev_i = !out->topk_idx || is_device_ptr(out->topk_idx);
             const bool dev_w = !out->topk_w || is_device_ptr(out->topk_w);
@@ -1136,6 +1191,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
                                                       cudaMemcpyDeviceToHost, ctx->stream));
             host = host || !dev_i || !dev_w;
         }
+        if ((rc = out_end(ctx, tape, 0, hs))) return rc;
         if (host) {
             CUDA_TRY(ctx, cudaMemcpyAsync(tape->h_flags + 1, dflags + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
             *host_out = true;
@@ -1218,6 +1274,7 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
     if (!ctx || !t || !t->valid) return set_err(ctx, GVR_ERR_RUNTIME, "tape is not valid");
     if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!target_image || !target_alpha) return set_err(ctx, GVR_ERR_RUNTIME, "targets must not be null");
+    if (int rc = out_wait(ctx, t, 1)) return rc;  // the last loss's host copies read d_image / d_alpha
     const long long P = (long long)t->H * t->W;
     const int Dc = t->D > 1 ? t->D : 1;
     const long long n_img = P * Dc;
@@ -1254,9 +1311,12 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
     t->has_upstream = true;
     bool host = false;
     int rc;
-    if ((rc = copy_out(ctx, d_image_out, t->d_image.p, sizeof(double) * n_img, &host))) return rc;
-    if ((rc = copy_out(ctx, d_alpha_out, t->d_alpha.p, sizeof(double) * P, &host))) return rc;
-    if ((rc = copy_out(ctx, loss_out, dloss, sizeof(double), &host))) return rc;
+    cudaStream_t hs;
+    if ((rc = out_begin(ctx, &hs))) return rc;
+    if ((rc = copy_out(ctx, d_image_out, t->d_image.p, sizeof(double) * n_img, &host, hs))) return rc;
+    if ((rc = copy_out(ctx, d_alpha_out, t->d_alpha.p, sizeof(double) * P, &host, hs))) return rc;
+    if ((rc = copy_out(ctx, loss_out, dloss, sizeof(double), &host, hs))) return rc;
+    if ((rc = out_end(ctx, t, 1, hs))) return rc;
     *host_out = host;
     return GVR_OK;
 }
@@ -1300,6 +1360,9 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     if (t->ctx != ctx) return set_err(ctx, GVR_ERR_RUNTIME, "objects belong to another context");
     if (!t->scene || t->scene->version != t->scene_version || !t->scene->valid)
         return set_err(ctx, GVR_ERR_RUNTIME, "the scene changed after the forward render");
+    if (int rc = out_wait(ctx, t, 2)) return rc;  // the last backward's host copies read the gradients
+    if (d_image || d_alpha)
+        if (int rc = out_wait(ctx, t, 1)) return rc;  // the upstream is staged into d_image / d_alpha
     const gvr_scene* scene = t->scene;
     const int K = t->K, D = t->D;
     const long long P = (long long)t->H * t->W;
@@ -1475,11 +1538,16 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
     if (out) {
         bool host = false;
         int rc;
-        if ((rc = copy_out(ctx, out->d_center, t->d_center.p, sizeof(double) * 3 * (size_t)K, &host))) return rc;
-        if ((rc = copy_out(ctx, out->d_inv_cov, t->d_inv_cov.p, sizeof(double) * 9 * (size_t)K, &host))) return rc;
-        if ((rc = copy_out(ctx, out->d_attr, t->d_attr.p, sizeof(double) * (size_t)D * K, &host))) return rc;
-        if ((rc = copy_out(ctx, out->d_rotation, t->d_rt.p, sizeof(double) * 9, &host))) return rc;
-        if ((rc = copy_out(ctx, out->d_translation, t->d_rt.as<double>() + 9, sizeof(double) * 3, &host))) return rc;
+        cudaStream_t hs;
+        if ((rc = out_begin(ctx, &hs))) return rc;
+        if ((rc = copy_out(ctx, out->d_center, t->d_center.p, sizeof(double) * 3 * (size_t)K, &host, hs))) return rc;
+        if ((rc = copy_out(ctx, out->d_inv_cov, t->d_inv_cov.p, sizeof(double) * 9 * (size_t)K, &host, hs)))
+            return rc;
+        if ((rc = copy_out(ctx, out->d_attr, t->d_attr.p, sizeof(double) * (size_t)D * K, &host, hs))) return rc;
+        if ((rc = copy_out(ctx, out->d_rotation, t->d_rt.p, sizeof(double) * 9, &host, hs))) return rc;
+        if ((rc = copy_out(ctx, out->d_translation, t->d_rt.as<double>() + 9, sizeof(double) * 3, &host, hs)))
+            return rc;
+        if ((rc = out_end(ctx, t, 2, hs))) return rc;
         if (host && !ctx->async) return sync_and_check(ctx);
     }
     return GVR_OK;
