@@ -57,7 +57,6 @@ struct FwdParams {
     int* nonfinite; // flag
     const int4* kinfo;          // [K] mask rectangles (project_kernel)
     unsigned long long* masks;  // (kernel, tile) pixel masks for the backward
-    int* kcount;                // [K] selected pixels per kernel (zeroed by project_kernel)
 };
 
 // FP32 centre-relative classification of q against ln(eta), and the FP32

@@ -1030,7 +1030,6 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         pp.masks = tape->masks.as<unsigned long long>();
         pp.mask_total = dflags + kMaskTotal;
         pp.mask_cap = (int)mask_cap;
-        pp.kcount = tape->kcount.as<int>();
         pp.dropped_behind = dflags;
         {
             StageTimer st(ctx, ST_PROJECT);
@@ -1127,7 +1126,6 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.nonfinite = dflags + 1;
     fp.kinfo = tape->kinfo.as<int4>();
     fp.masks = tape->masks.as<unsigned long long>();
-    fp.kcount = tape->kcount.as<int>();
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     fp.precise = ctx->precise ? 1 : 0;
     fp.tile_cycles = nullptr;

@@ -142,7 +142,6 @@ struct ProjectParams {
     int4* kinfo;                 // [K] {mask base (-1: no room), tr0 << 16 | tc0, tiles per row, tiles}
     unsigned long long* masks;   // [mask_cap], zeroed here for every allocated rectangle
     int* mask_total;             // rectangle tiles requested (bump allocator, zeroed before the launch)
-    int* kcount;                 // [K] zeroed here (the blend counts each kernel's selected pixels)
     int4* ref_box;               // nullable: the reference's pushed pixel box {row_lo, row_hi, col_lo, col_hi}
                                  // (tracer.cpp:100-103), {1, 0, 1, 0} when not pushed (coarse_select API)
     int mask_cap;
@@ -358,7 +357,6 @@ __global__ void project_kernel(ProjectParams p) {
         if (k < p.K) {
             const bool fits = base >= 0 && (long long)base + job.nt <= (long long)p.mask_cap;
             p.kinfo[k] = make_int4(job.nt > 0 && fits ? base : -1, (job.tr0 << 16) | job.tc0, job.ntc, job.nt);
-            p.kcount[k] = 0;
             if (fits)
                 for (int t = 0; t < job.nt; ++t) p.masks[base + t] = 0ull;
         }
