@@ -606,28 +606,45 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
         for (int u = 0; u < 9; ++u) c9[u] = 0.0;
         if (ap.y > 0) {
             const int w0 = ap.x >> 5, w1 = (ap.x + ap.y - 1) >> 5;
-            double c10[10];  // A (3), Q, B upper (00 01 02 11 12 22)
+            double c10[10], ca[4] = {0.0, 0.0, 0.0, 0.0};  // A (3), Q, B upper (00 01 02 11 12 22); d_attr
 #pragma unroll
             for (int u = 0; u < 10; ++u) c10[u] = 0.0;
             for (int w = w0; w <= w1; ++w) {
                 const double* src = p.pieces + (long long)(k + w) * p.nv;
 #pragma unroll
                 for (int u = 0; u < 10; ++u) c10[u] += src[u];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < p.D) ca[c] += src[10 + c];
             }
             for (int c = 0; c < p.D; ++c) {
                 double a = 0.0;
-                for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 10 + c];
+                if (c < 4) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (q == c) a = ca[q];
+                } else {
+                    for (int w = w0; w <= w1; ++w) a += p.pieces[(long long)(k + w) * p.nv + 10 + c];
+                }
                 if (p.packed) p.packed[(long long)k * (9 + p.D) + 9 + c] = a;
                 else p.d_attr[(long long)p.D * k + c] = a;
             }
             // camera-space chain (entry_coeffs): dm = S (A - Q m),
-            // dS = sym(m A^T) + B - Q/2 m m^T (upper triangle)
-            const Rec64& r = p.rec64[k];
-            const double m0 = r.m[0], m1 = r.m[1], m2 = r.m[2], Q = c10[3];
-            const double u0 = fma(-Q, m0, c10[0]), u1 = fma(-Q, m1, c10[1]), u2 = fma(-Q, m2, c10[2]);
+            // dS = sym(m A^T) + B - Q/2 m m^T (upper triangle), with the kernel's
+            // camera-space m, S from its staged object-space rows (project_kernel's arithmetic)
+            double mm[3], ss[9];
+            {
+                double mo[3], so[9];
 #pragma unroll
-            for (int t = 0; t < 3; ++t) c9[t] = fma(r.s[3 * t], u0, fma(r.s[3 * t + 1], u1, r.s[3 * t + 2] * u2));
-            const double mm[3] = {m0, m1, m2};
+                for (int t = 0; t < 3; ++t) mo[t] = s_ctr[3 * threadIdx.x + t];
+#pragma unroll
+                for (int t = 0; t < 9; ++t) so[t] = s_cov[9 * threadIdx.x + t];
+                view_transform_one(p.cam, mo, so, mm, ss);
+            }
+            const double Q = c10[3];
+            const double u0 = fma(-Q, mm[0], c10[0]), u1 = fma(-Q, mm[1], c10[1]), u2 = fma(-Q, mm[2], c10[2]);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) c9[t] = fma(ss[3 * t], u0, fma(ss[3 * t + 1], u1, ss[3 * t + 2] * u2));
             const int rr[6] = {0, 0, 0, 1, 1, 2};
             const int cc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll

@@ -145,6 +145,22 @@ __device__ __forceinline__ double xdot(const double* a, const double* b) {
     return xadd(acc, xmul(a[2], b[2]));
 }
 
+// view_transform (scene.cpp:5-17) of one kernel, in Eigen's evaluation order:
+// M' = R M + T ; S' = (R S) R^T.
+__device__ __forceinline__ void view_transform_one(const CameraP& c, const double* mo, const double* so, double* m,
+                                                   double* s) {
+    xmatvec(c.R, mo, m);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) m[i] = xadd(m[i], c.T[i]);
+    double rt[9], rs[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) rt[3 * j + i] = c.R[3 * i + j];
+    xmatmul(c.R, so, rs);
+    xmatmul(rs, rt, s);
+}
+
 // pixel_ray (scene.cpp:19-22): normalize(((i - Oy)/F, (j - Ox)/F, 1))
 __device__ __forceinline__ void pixel_ray(const CameraP& c, int row, int col, double* d) {
     d[0] = xdiv(xsub((double)row, c.oy), c.focal);

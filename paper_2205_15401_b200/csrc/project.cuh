@@ -169,22 +169,6 @@ __device__ __forceinline__ BinJob job_from_record(const Rec32& q, int k, int H, 
     return job;
 }
 
-// view_transform (scene.cpp:5-17) of one kernel, in Eigen's evaluation order:
-// M' = R M + T ; S' = (R S) R^T.
-__device__ __forceinline__ void view_transform_one(const CameraP& c, const double* mo, const double* so, double* m,
-                                                   double* s) {
-    xmatvec(c.R, mo, m);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) m[i] = xadd(m[i], c.T[i]);
-    double rt[9], rs[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) rt[3 * j + i] = c.R[3 * i + j];
-    xmatmul(c.R, so, rs);
-    xmatmul(rs, rt, s);
-}
-
 __device__ __forceinline__ BinJob project_one(const ProjectParams& p, int k) {
     BinJob job;
     const CameraP& c = p.cam;
