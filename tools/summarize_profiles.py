@@ -53,7 +53,10 @@ def launch_list(tag):
 
 
 def ncu_metrics(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".raw.csv"):  # exported on the GPU box (tools/profile_round.sh)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units, row = rows[0], rows[1], rows[2]
     res = {"kernel": row[hdr.index("Kernel Name")]}
@@ -79,7 +82,7 @@ def main():
     traffic = {}
     issue = {}
     for f in sorted(os.listdir(OUT)):
-        if f.startswith("full_") and f.endswith(".ncu-rep"):
+        if f.startswith("full_") and (f.endswith(".ncu-rep") or f.endswith(".raw.csv")):
             m = ncu_metrics(os.path.join(OUT, f))
             name = m["kernel"].split("(")[0].split("<")[0].replace("void ", "").replace("gvrk::", "")
             rb = to_bytes(*m["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in m else 0.0
