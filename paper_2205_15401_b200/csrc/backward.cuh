@@ -109,18 +109,11 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     extern __shared__ __align__(16) unsigned char smem[];
     // per-entry staging, [slot][pixel]
     // pairs read together are packed: one 16-byte and one 8-byte load per pair
-#if GVR_BWD_F32
     // {hi, lo of l_k - l_0, d_acc_k = -tau T_k d_w_k e^{q_k}, e^{q_k}} as floats, 1 / sigma_k
     float4* b_q = reinterpret_cast<float4*>(smem);
     double* b_dt = reinterpret_cast<double*>(b_q + KMAX * NP);  // density path d_w_k T_k (grad.cpp:120)
     float* b_is = reinterpret_cast<float*>(b_dt + KMAX * NP);
     int* b_id = reinterpret_cast<int*>(b_is + KMAX * NP);
-#else
-    double2* b_lda = reinterpret_cast<double2*>(smem);  // {l_k - l_0, d_acc_k = -tau T_k d_w_k e^{q_k}}
-    double* b_dt = reinterpret_cast<double*>(b_lda + KMAX * NP);  // density path d_w_k T_k (grad.cpp:120)
-    float2* b_pi = reinterpret_cast<float2*>(b_dt + KMAX * NP);   // {e^{q_k}, 1 / sigma_k}
-    int* b_id = reinterpret_cast<int*>(b_pi + KMAX * NP);
-#endif
 
     if ((int)(blockIdx.x / GVR_BWD_SPLIT) >= *p.n_order) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
@@ -149,7 +142,6 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
     // re-trace the taped selection in exact FP64 (bit-identical to the forward),
     // d_weight, attribute gradient, d_acc (grad.cpp:79-120)
     double peak_part = 0.0;
-#if GVR_BWD_IDS_FIRST
     // ids first: the thread's id loads are independent, the record loads behind them overlap
     int kq[PER];
 #pragma unroll
@@ -159,10 +151,6 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         const int s = sub + 4 * q;
         if (s >= n) break;
         const int k = kq[q];
-#else
-    for (int s = sub; s < n; s += 4) {
-        const int k = p.topk[pix * p.kp + s];
-#endif
         const EntryRec er = p.ent[pix * p.kp + s];  // traced by the forward
         const float pkf = er.pk;
         const double pk = (double)pkf;
@@ -177,15 +165,10 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
             for (int c = 0; c < p.D; ++c) dw += p.d_image[pix * p.D + c] * p.attr[(long long)p.D * k + c];
         }
         const double dacc = (p.through_t && dw != 0.0) ? -tau * trans * (dw * pk) : 0.0;
-#if GVR_BWD_F32
         const double dl0 = er.l - l0;
         const float hi = (float)dl0;
         b_q[s * NP + g] = make_float4(hi, (float)(dl0 - (double)hi), (float)dacc, pkf);
         b_is[s * NP + g] = er.is;
-#else
-        b_lda[s * NP + g] = make_double2(er.l - l0, dacc);
-        b_pi[s * NP + g] = make_float2(pkf, er.is);
-#endif
         b_dt[s * NP + g] = (p.through_rho && dw != 0.0) ? dw * trans : 0.0;
         b_id[s * NP + g] = k;
     }
@@ -197,7 +180,6 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
 
     // entry-major pair terms + chain to camera space (grad.cpp:121-173)
     for (int e = sub; e < n; e += 4) {
-#if GVR_BWD_F32
         // FP32 pair terms with Kahan-compensated FP32 sums: no FP64 conversions
         // in the loop (those share the XU pipe with the exp2 / reciprocal)
         const float4 qe = b_q[e * NP + g];
@@ -230,59 +212,6 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         dpk += (double)s_pk - (double)c_pk;
         const double dl = (double)s_l - (double)c_l;
         const double dsg = (double)s_sg - (double)c_sg;
-#else
-        const double2 lde = b_lda[e * NP + g];
-        const double dle = lde.x, dae = lde.y;
-        const float2 pie = b_pi[e * NP + g];
-        const float ise = pie.y;
-        const double pke = (double)pie.x;
-        const int kid = b_id[e * NP + g];
-        double dpk = d_total + b_dt[e * NP + g];  // density path (grad.cpp:120)
-        // branch-free pair terms, two independent accumulator sets (even / odd k)
-        // so that consecutive pairs overlap instead of serialising on one chain
-        double dpk2 = 0.0, dl = 0.0, dl2 = 0.0, dsg = 0.0, dsg2 = 0.0;
-        auto pair = [&](int k, double& a_pk, double& a_l, double& a_sg) {
-            const double2 ldk = b_lda[k * NP + g];
-            const double dak = ldk.y, dlk = ldk.x;
-            const float2 pik = b_pi[k * NP + g];
-            const float isk = pik.y;
-            // pair (k, m = e): z1 = (l_k - l_e) / sigma_e ; pair (k = e, m = k): z2 = (l_e - l_k) / sigma_k
-            const float dlf = (float)(dlk - dle);
-            const float z1 = dlf * ise;
-            const float phi1 = normal_pdf_fast(z1);
-            // sigma_k == sigma_e (exactly): z2 = -z1 and phi(z2) = phi(z1)
-            const float phi2 = isk == ise ? phi1 : normal_pdf_fast(-dlf * isk);
-            a_pk = fma(dak, (double)fast_normal_cdf(z1), a_pk);
-            const double gg = k != e ? dak * (double)(phi1 * ise) * pke : 0.0;
-            a_l -= gg;
-            a_sg -= gg * (double)z1;
-            if (k != e) a_l = fma(dae, (double)(pik.x * phi2 * isk), a_l);
-        };
-        int k = 0;
-#if GVR_BWD_WAYS == 4
-        double dpk3 = 0.0, dpk4 = 0.0, dl3 = 0.0, dl4 = 0.0, dsg3 = 0.0, dsg4 = 0.0;
-        for (; k + 4 <= n; k += 4) {
-            pair(k, dpk, dl, dsg);
-            pair(k + 1, dpk2, dl2, dsg2);
-            pair(k + 2, dpk3, dl3, dsg3);
-            pair(k + 3, dpk4, dl4, dsg4);
-        }
-        dpk2 += dpk4;
-        dpk += dpk3;
-        dl += dl3;
-        dl2 += dl4;
-        dsg += dsg3;
-        dsg2 += dsg4;
-#endif
-        for (; k + 2 <= n; k += 2) {
-            pair(k, dpk, dl, dsg);
-            pair(k + 1, dpk2, dl2, dsg2);
-        }
-        if (k < n) pair(k, dpk, dl, dsg);
-        dpk += dpk2;
-        dl += dl2;
-        dsg += dsg2;
-#endif
         const double dq = dpk * pke;
         const double w = p.tape_t[pix * p.kp + e] * pke;  // W_e (the forward's weight)
         const int4 ki = p.kinfo[kid];
@@ -469,14 +398,7 @@ struct GatherParams {
     double* d_rt;           // [12] d_rotation (9), d_translation (3)
 };
 
-#ifndef GVR_REC_MINB  // resident records CTAs per SM (register budget)
-#define GVR_REC_MINB 1
-#endif
-#ifndef GVR_REC_PREFETCH  // the next window's record loads issued under the current window's work
-#define GVR_REC_PREFETCH 0
-#endif
-
-__global__ void __launch_bounds__(kRecThreads, GVR_REC_MINB) records_kernel(GatherParams p) {
+__global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
     // per warp: the window's record values [32][nv], summed per kernel piece by
     // one lane each, rows in record order
     extern __shared__ __align__(16) double s_rows[];
@@ -491,34 +413,13 @@ __global__ void __launch_bounds__(kRecThreads, GVR_REC_MINB) records_kernel(Gath
     const int wstride = (gridDim.x * blockDim.x) >> 5;
     const float inv_nv = 1.0f / (float)p.nv;
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-#if GVR_REC_PREFETCH
-    int2 key_n = make_int2(0, -1);
-    double4 b_n = make_double4(0, 0, 0, 0);
-    if (32 * w + lane < n_rec) {
-        key_n = p.bkey[32 * w + lane];
-        b_n = p.bent[32 * w + lane];
-    }
-#endif
     for (; w < windows; w += wstride) {
         const int r = 32 * w + lane;
         const bool valid = r < n_rec;
-#if GVR_REC_PREFETCH
-        const int2 key = key_n;
-        const double4 b = b_n;
-        {
-            const int rn = r + 32 * wstride;
-            if (rn < n_rec) {
-                key_n = p.bkey[rn];
-                b_n = p.bent[rn];
-            }
-        }
-#endif
         int k = -1;
         if (valid) {
-#if !GVR_REC_PREFETCH
             const int2 key = p.bkey[r];
             const double4 b = p.bent[r];
-#endif
             k = key.y;
             const long long pix = key.x;
             const double4 ray = p.rays[pix];

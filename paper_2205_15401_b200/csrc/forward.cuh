@@ -33,7 +33,6 @@ struct FwdParams {
     int K;
     const int* tile_order_blend;  // tiles by sum_p n_p^2 (from the selection), then the tiles with no
     const int* n_order_blend;     // selection (cleared by the blend); first *n_order_blend valid
-    int* n_order_blend_all;       // written by the ordering kernel
     const Rec32* rec32;
     const Rec64* rec64;
     const double* attr;  // [K*D] object attributes (FP64)
@@ -47,7 +46,6 @@ struct FwdParams {
     double* tape_t; // [P*kp] T(l_k) of the selected entries (backward input)
     EntryRec* ent;  // [P*kp] traced selected entries (written by the blend)
     double* ent_a;  // [P*kp] a = d.Sd of each selected entry (FP64, the backward's chain)
-    float* bwd_cost; // [tiles] sum_p n_p^2 of each tile (backward scheduling)
     int presorted;   // topk already in exact (l, idx) order (warp selection); else the blend sorts
     unsigned* tile_done;     // [tiles] set (release) when the tile's selection is written; the blend,
                              // launched as a programmatic dependent, waits per tile (nullable)
@@ -383,12 +381,6 @@ __global__ void __launch_bounds__(64) select_kernel(FwdParams p) {
         __syncwarp();
     }
 
-    // tile cost for the blend / backward schedulers
-    const int n_eff = inside ? n : 0;
-    float cost = (float)(n_eff * n_eff);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
-    if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
     if (!inside) return;
     for (int s = 0; s < n; ++s) p.topk[pix * kp + s] = s_id[s * NT + tid] & ~kExact;  // unsorted; the blend sorts
     p.count[pix] = n;
@@ -414,9 +406,6 @@ __device__ __forceinline__ bool keyf_close(float a, float b) { return fabsf(a - 
 
 #ifndef GVR_SEL_CUNROLL  // list batches per compaction step (loads in flight together)
 #define GVR_SEL_CUNROLL 4
-#endif
-#ifndef GVR_SEL_FIRST_FAST  // a pixel's first batch merge skips the kept-list ranks
-#define GVR_SEL_FIRST_FAST 1
 #endif
 #ifndef GVR_SEL_BATCH_MIN  // eligible candidates per batch from which the batch merge is used (33: never)
 #define GVR_SEL_BATCH_MIN 10
@@ -470,7 +459,6 @@ __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int
         ck = bitonic_lanes<32>(ck, lane);
     }
     const unsigned cu = (unsigned)(ck >> 32);  // lane r < m: key of the r-th smallest candidate
-#if GVR_SEL_FIRST_FAST
     if (n == 0) {
         // nothing kept yet (a pixel's first eligible batch): the sorted
         // candidates are the merged order; only their adjacency is checked
@@ -484,7 +472,6 @@ __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int
         __syncwarp();
         return true;
     }
-#endif
     const unsigned ku = float_order_bits(L);   // lane s < n: key of kept entry s (non-decreasing)
     // below: kept entries at or before the candidate (ties: kept first); above: candidates before the kept entry
     int below = 0, above = 0;
@@ -587,10 +574,6 @@ __device__ __forceinline__ int select_pixel(const FwdParams& p, const unsigned l
             if (cls != 0 && lk > worst + 2.0f * kKeyClose * fabsf(worst)) cls = 0;
         }
         const unsigned elig = __ballot_sync(FULL, cls != 0);
-#ifdef GVR_SEL_STATS  // experiment: histogram of eligible candidates per batch (n == 0 / n > 0) into tile_cycles
-        if (p.tile_cycles && lane == 0)
-            atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles) + (n > 0 ? 33 : 0) + __popc(elig), 1ull);
-#endif
         if (elig == 0) continue;
         const bool me = (elig >> lane) & 1u;
         const int m = __popc(elig);
@@ -713,7 +696,6 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
             end = cnt;
         }
     }
-#if GVR_SEL_DYN
     // dynamic pixel queue: the CTA's 64 pixels, heaviest sub-blocks first, are
     // pulled by whichever warp is free (the CTA ends with its last pixel, not
     // with its slowest warp)
@@ -755,12 +737,9 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         }
     }
     __syncthreads();
-#endif
     const QClass& qc = p.qc;  // kernel parameter space: no registers
     const bool exact_only = p.exact_only != 0;
-    float cost = 0.0f;
 
-#if GVR_SEL_DYN
     for (;;) {
         int item = 0;
         if (lane == 0) item = atomicAdd(&sh_next, 1);
@@ -780,31 +759,15 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
         const double* d = sh_ray[q];  // read only on the exact path
         const float4 uvn = sh_uvn[q];
         const float u = uvn.x, v = uvn.y, nrm = uvn.z;
-#else
-    for (int px = 0; px < 8; ++px) {
-        const int i = sr0 + (px >> 2);
-        const int j = sc0 + (px & 3);
-        if (i >= p.cam.H || j >= p.cam.W) continue;  // warp-uniform
-        double d[3];
-        pixel_ray(p.cam, i, j, d);
-        const float u = (float)xdiv(xsub((double)i, p.cam.oy), p.cam.focal);
-        const float v = (float)xdiv(xsub((double)j, p.cam.ox), p.cam.focal);
-        const float nrm = (float)sqrt((double)u * u + (double)v * v + 1.0);
-#endif
-        const int n = select_pixel(p, list, end, overflow, d, u, v, nrm, i, j, qc, exact_only, sh_l[warp], sh_i[warp],
-                                   lane);
-        cost += (float)(n * n);
+        select_pixel(p, list, end, overflow, d, u, v, nrm, i, j, qc, exact_only, sh_l[warp], sh_i[warp], lane);
     }
-    if (lane == 0 && cost > 0.0f) atomicAdd(p.bwd_cost + tile, cost);
     if (p.tile_done || p.tile_cycles || p.tile_hint) {
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
             const long long dt = clock64() - sh_t0;  // the CTA's duration (its slowest warp)
-#ifndef GVR_SEL_STATS
             if (p.tile_cycles)  // profiling hook
                 atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_cycles + tile), (unsigned long long)dt);
-#endif
             if (p.tile_hint) p.tile_hint[tile] = (unsigned)min(max(dt, 1ll), 0xffffffffll);
             if (p.tile_done) red_add_release_gpu(p.tile_done + tile, 1u);  // one count per split CTA
         }
@@ -1148,12 +1111,12 @@ __device__ void list_offsets(int tiles, const int* __restrict__ count, int* __re
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
 // log-spaced cost buckets, descending). Zero-cost tiles and tiles of other
 // shards (t % nshards != shard) are dropped; *n_out receives the number kept.
-// Cost = icost[t] (list length) or fcost[t]; with a hint (the selection cycles
+// Cost = icost[t] (list length); with a hint (the selection cycles
 // of the previous render of the same view, tile_hint) the listed tiles are
 // ordered by it instead. With tile_off, the tile-list offsets are laid out
 // first (list_offsets; icost = the list lengths).
 __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int* __restrict__ icost,
-                                                           const float* __restrict__ fcost, int* __restrict__ order,
+                                                           int* __restrict__ order,
                                                            int* __restrict__ n_out, int shard, int nshards,
                                                            int* __restrict__ n_all_out, int* __restrict__ tile_off = nullptr,
                                                            int pool_cap = 0, int smem_cap = 0,
@@ -1167,7 +1130,7 @@ __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int*
     __syncthreads();
     auto bucket_of = [&](int t) -> int {
         if (t % nshards != shard) return -1;  // tile owned by another rank (C4 tile sharding)
-        float c = fcost ? fcost[t] : (float)icost[t];
+        float c = (float)icost[t];
         if (!(c > 0.0f)) return -1;
         if (hint) c = hint[t] > 0u ? (float)hint[t] : 100.0f * c;  // cycles (a tile new to the view: ~100 / entry)
         const int b = (int)(__log2f(c + 1.0f) * 8.0f);

@@ -23,20 +23,11 @@
 #ifndef GVR_BLEND_MINB
 #define GVR_BLEND_MINB 10
 #endif
-#ifndef GVR_ONE_ORDER
-#define GVR_ONE_ORDER 1
-#endif
 #ifndef GVR_BLEND_SPLIT
 #define GVR_BLEND_SPLIT 4
 #endif
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
-#endif
-#ifndef GVR_BWD_F32  // backward pair loop in FP32 with Kahan-compensated sums
-#define GVR_BWD_F32 1
-#endif
-#ifndef GVR_BWD_IDS_FIRST  // backward staging loop: entry ids loaded before the records
-#define GVR_BWD_IDS_FIRST 1
 #endif
 #ifndef GVR_PDL_SLEEP_NS  // back-off of a blend CTA waiting for its tile's selection
 #define GVR_PDL_SLEEP_NS 100
@@ -46,12 +37,6 @@
 #endif
 #ifndef GVR_SEL_SPLIT
 #define GVR_SEL_SPLIT 1
-#endif
-#ifndef GVR_SEL_DYN
-#define GVR_SEL_DYN 1
-#endif
-#ifndef GVR_BWD_WAYS
-#define GVR_BWD_WAYS 2
 #endif
 #ifndef GVR_BWD_MINB
 #define GVR_BWD_MINB 16

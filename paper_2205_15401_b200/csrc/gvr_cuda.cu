@@ -161,8 +161,7 @@ struct gvr_tape {
     int hint_tiles = 0, hint_shard = -1, hint_nshards = 0;
     long long pool_hint = 0;  // entries the last observed render listed (grow-only sizing)
     bool profiled = false;    // the last render recorded tile cycles
-    Buf sched;  // [0] n_fwd, [1] n_bwd, order_fwd[tiles], order_bwd[tiles], bwd_cost[tiles] (float), n_all,
-                // tile_done[tiles]
+    Buf sched;  // [0] n_order (selected tiles), [1] n_all, order[tiles], tile_done[tiles]
     // per pixel
     Buf topk, count, image, alpha, depth, topk_w, tape_t, ent, ent_a;
     Buf d_image, d_alpha;
@@ -353,7 +352,7 @@ void harvest_timings(gvr_context* ctx) {
 unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 template <int KMAX>
-int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_b, int* n_b, const float* cost) {
+int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
     const size_t list_smem = sizeof(unsigned long long) * (size_t)kSelListSmem;
     if (KMAX <= 32) {
         auto kern = select_warp_kernel<KMAX>;
@@ -371,18 +370,6 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles, int* order_
         kern<<<tiles, NT, smem, ctx->stream>>>(fp);
     }
     LAUNCH_CHECK(ctx);
-#if !GVR_ONE_ORDER
-    {
-        StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, nullptr, cost, order_b, n_b, 0, 1,
-                                                        fp.n_order_blend_all);
-    }
-    LAUNCH_CHECK(ctx);
-#else
-    (void)order_b;
-    (void)n_b;
-    (void)cost;
-#endif
     {
         const size_t smem = 32ull * KMAX * (64 / GVR_BLEND_SPLIT);
         auto kern = blend_kernel<KMAX>;
@@ -987,7 +974,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
                                                     ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL});
     CUDA_TRY(ctx, tape->tile_count.ensure(sizeof(int) * 2 * (size_t)tiles));
     CUDA_TRY(ctx, tape->tile_off.ensure(sizeof(int) * (size_t)tiles));
-    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (3 + 4 * (size_t)tiles)));
+    CUDA_TRY(ctx, tape->sched.ensure(sizeof(int) * (2 + 2 * (size_t)tiles)));
     CUDA_TRY(ctx, tape->topk.ensure(sizeof(int) * (size_t)P * kp));
     CUDA_TRY(ctx, tape->count.ensure(sizeof(int) * (size_t)P));
     CUDA_TRY(ctx, tape->tape_t.ensure(sizeof(double) * (size_t)P * kp));
@@ -1003,12 +990,11 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     int* tile_count = tape->tile_count.as<int>();
     int* sched = tape->sched.as<int>();
     int* order_f = sched + 2;
-    float* bwd_cost = reinterpret_cast<float*>(sched + 2 + 2 * (size_t)tiles);
     CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 16 * sizeof(int), ctx->stream));
     int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts: one memset
     CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
-    // bwd_cost[tiles], n_all, tile_done[tiles] (contiguous)
-    CUDA_TRY(ctx, cudaMemsetAsync(bwd_cost, 0, sizeof(float) * (2 * (size_t)tiles + 1), ctx->stream));
+    // the per-tile selection hand-off flags
+    CUDA_TRY(ctx, cudaMemsetAsync(sched + 2 + (size_t)tiles, 0, sizeof(int) * (size_t)tiles, ctx->stream));
 
     if (K > 0) {
         // K1 projection + culling + binning into per-tile lists
@@ -1046,16 +1032,10 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     if (want_hint) CUDA_TRY(ctx, tape->tile_hint.ensure(sizeof(unsigned) * (size_t)tiles));
     {
         StageTimer st(ctx, ST_RANGES);
-#if GVR_ONE_ORDER  // one order (list length) for selection, blend and backward; then every other tile
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
-                                                        sched + 2 + 3 * (size_t)tiles, tape->tile_off.as<int>(),
+        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, order_f, sched, shard, nshards,
+                                                        sched + 1, tape->tile_off.as<int>(),
                                                         (int)pool_cap, ctx->list_smem, dflags + kListStats,
                                                         use_hint ? tape->tile_hint.as<unsigned>() : nullptr);
-#else
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, nullptr, order_f, sched, shard, nshards,
-                                                        nullptr, tape->tile_off.as<int>(), (int)pool_cap, ctx->list_smem,
-                                                        dflags + kListStats);
-#endif
     }
     LAUNCH_CHECK(ctx);
     if (K > 0) {
@@ -1097,14 +1077,8 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.tiles_x = tiles_x;
     fp.tile_order = order_f;
     fp.n_order = sched;
-#if GVR_ONE_ORDER
     fp.tile_order_blend = order_f;
-#else
-    fp.tile_order_blend = sched + 2 + tiles;
-#endif
-    fp.n_order_blend = sched + 2 + 3 * (size_t)tiles;  // all tiles: selected first, then cleared ones
-    fp.n_order_blend_all = sched + 2 + 3 * (size_t)tiles;
-    fp.bwd_cost = bwd_cost;
+    fp.n_order_blend = sched + 1;  // all tiles: selected first, then cleared ones
     fp.tile_count = tile_count;
     fp.tile_off = tape->tile_off.as<int>();
     fp.pool = tape->pool.as<unsigned long long>();
@@ -1129,7 +1103,7 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     fp.presorted = kp <= 32 ? 1 : 0;  // select_warp_kernel emits the exact (l, idx) order
     fp.precise = ctx->precise ? 1 : 0;
     fp.tile_cycles = nullptr;
-    fp.tile_done = GVR_PDL ? reinterpret_cast<unsigned*>(sched + 3 + 3 * (size_t)tiles) : nullptr;
+    fp.tile_done = GVR_PDL ? reinterpret_cast<unsigned*>(sched + 2 + (size_t)tiles) : nullptr;
     fp.tile_hint = want_hint ? tape->tile_hint.as<unsigned>() : nullptr;
     tape->hint_valid = want_hint;
     tape->hint_cam = cp;
@@ -1143,16 +1117,15 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         fp.tile_cycles = tape->tile_cycles.as<long long>();
     }
     int rc = GVR_OK;
-    int* order_b = sched + 2 + tiles;
-    if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 16) rc = launch_forward<16>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 20) rc = launch_forward<20>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 24) rc = launch_forward<24>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 32) rc = launch_forward<32>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 48) rc = launch_forward<48>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 64) rc = launch_forward<64>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else if (kp <= 96) rc = launch_forward<96>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
-    else rc = launch_forward<128>(ctx, fp, tiles, order_b, sched + 1, bwd_cost);
+    if (kp <= 8) rc = launch_forward<8>(ctx, fp, tiles);
+    else if (kp <= 16) rc = launch_forward<16>(ctx, fp, tiles);
+    else if (kp <= 20) rc = launch_forward<20>(ctx, fp, tiles);
+    else if (kp <= 24) rc = launch_forward<24>(ctx, fp, tiles);
+    else if (kp <= 32) rc = launch_forward<32>(ctx, fp, tiles);
+    else if (kp <= 48) rc = launch_forward<48>(ctx, fp, tiles);
+    else if (kp <= 64) rc = launch_forward<64>(ctx, fp, tiles);
+    else if (kp <= 96) rc = launch_forward<96>(ctx, fp, tiles);
+    else rc = launch_forward<128>(ctx, fp, tiles);
     if (rc) return rc;
 
     tape->valid = true;
@@ -1426,13 +1399,8 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
         bp.through_rho = through_rho;
         const int btx = t->tiles_x, bty = t->tiles_y;
         int* sched = t->sched.as<int>();
-#if GVR_ONE_ORDER
         int* order_b = sched + 2;  // the selection's order
         bp.n_order = sched;
-#else
-        int* order_b = sched + 2 + btx * bty;  // tiles by sum_p n_p^2, from the forward
-        bp.n_order = sched + 1;
-#endif
         bp.tiles_x = btx;
         bp.tile_order = order_b;
         bp.topk = t->topk.as<int>();
