@@ -453,7 +453,7 @@ def measure_e2e(args, ctx, stream, dev, scene, cam, cfg, ti_h, ta_h, flush, worl
     for i in range(2 * ns):  # warm-up (sizes every buffer)
         enqueue(slots[i % ns])
         consume(slots[i % ns])
-    e_steps = max(6, min(args.steps, 40))
+    e_steps = max(40, min(4 * args.steps, 200))  # steady state: the 4-deep pipeline fills and drains once
     torch.cuda.synchronize(dev)
     flush.zero_()
     torch.cuda.synchronize(dev)
