@@ -125,12 +125,15 @@ int gvr_context_create(int device, gvr_context** out);
 void gvr_context_destroy(gvr_context* ctx);
 const char* gvr_last_error(const gvr_context* ctx);
 /* Asynchronous host buffers (on != 0): gvr_scene_set, gvr_render, gvr_scalar_loss
- * and gvr_backward with HOST pointers enqueue their copies on the context stream
- * and return without synchronising (host buffers should be pinned). Results are
- * valid after gvr_context_synchronize; the checks that need the host then are
- * deferred: scene validation -> gvr_scene_check, non-finite outputs ->
- * gvr_tape_check_finite. Lets a caller pipeline steps over two contexts (one
- * step's copies under the other's kernels). Synchronises when switched. */
+ * and gvr_backward with HOST pointers enqueue their copies and return without
+ * synchronising (host buffers should be pinned). Inputs are copied on the context
+ * stream; device->host copies of a call's outputs drain on a second stream of the
+ * context while the context stream runs the next call (the next call of the same
+ * kind on the tape waits for them). Results are valid after gvr_context_synchronize
+ * (both streams); the checks that need the host then are deferred: scene
+ * validation -> gvr_scene_check, non-finite outputs -> gvr_tape_check_finite. Lets
+ * a caller pipeline steps over several contexts (one step's copies under the
+ * others' kernels). Synchronises when switched. */
 int gvr_context_set_async(gvr_context* ctx, int on);
 /* Use an external cudaStream_t (NULL = the context's own stream). */
 int gvr_context_set_stream(gvr_context* ctx, void* cuda_stream);

@@ -376,3 +376,91 @@ def test_device_buffers_on_torchs_own_stream_are_ordered(ctx):
         c = packed[:, :3].cpu().numpy()  # torch's stream waits for the context's
         assert np.array_equal(c, want.d_center)
         del big
+
+
+def test_pipelined_async_steps_with_side_stream_copies_match_synchronous():
+    """Async host-buffer mode copies a call's host outputs on a side stream while
+    the context stream runs the next call; the next call of the same kind waits
+    for them. Steps pipelined over two contexts (as in bench.py's e2e loop), with
+    changing targets, give the synchronous results bit for bit."""
+    scene = gvr.make_bench_scene(3000)
+    cam = gvr.make_bench_camera(64)
+    rng = np.random.default_rng(5)
+    targets = [(torch.tensor(rng.uniform(0, 1, (64, 64, 3))).pin_memory(),
+                torch.tensor(rng.uniform(0, 1, (64, 64, 1))).pin_memory()) for _ in range(6)]
+    pin = lambda a: torch.tensor(a).pin_memory()  # noqa: E731
+    hc, hs, ha = pin(scene.centers), pin(scene.inv_cov), pin(scene.attr)
+
+    def make_slot(async_mode):
+        c = gvr.Context(0)
+        c.set_async(async_mode)
+        out = dict(img=torch.empty((64, 64, 3), dtype=torch.float64).pin_memory(),
+                   loss=torch.zeros(1, dtype=torch.float64).pin_memory(),
+                   gc=torch.empty((scene.size, 3), dtype=torch.float64).pin_memory(),
+                   gs=torch.empty((scene.size, 3, 3), dtype=torch.float64).pin_memory())
+        return c, gvr.DeviceScene(c), gvr.Tape(c), out
+
+    def enqueue(slot, t):
+        c, ds, tp, o = slot
+        ds.set_raw(scene.size, 3, scene.tau, hc, hs, ha)
+        gvr.render_into(c, ds, cam, SelectionConfig(), tp, o["img"])
+        gvr.scalar_loss_into(tp, targets[t][0], targets[t][1], 1.0, 1.0, o["loss"])
+        gvr.backward_into(tp, None, None, gvr.GradFlags(), o["gc"], o["gs"])
+
+    def take(slot):
+        c, ds, tp, o = slot
+        c.synchronize()
+        ds.check()
+        tp.check_finite()
+        return {k: v.clone() for k, v in o.items()}
+
+    ref = []
+    sync = make_slot(False)
+    for t in range(len(targets)):
+        enqueue(sync, t)
+        ref.append(take(sync))
+    slots = [make_slot(True), make_slot(True)]
+    got = [None] * len(targets)
+    for t in range(len(targets)):
+        if t >= 2:
+            got[t - 2] = take(slots[t % 2])
+        enqueue(slots[t % 2], t)
+    for t in range(len(targets) - 2, len(targets)):
+        got[t] = take(slots[t % 2])
+    for a, b in zip(ref, got):
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
+    assert len({float(r["loss"][0]) for r in ref}) == len(targets)  # the targets did change
+
+
+def test_schedule_from_the_last_render_of_the_view_keeps_outputs():
+    """The tile order of a render may come from the selection cycles of the last
+    render of the same view on the tape (LPT costs); it only reorders work: a
+    repeated view, a view after a different camera, and a fresh tape agree bit
+    for bit (topk, image, gradients)."""
+    scene = gvr.make_bench_scene(20000)
+    cam_a = gvr.make_bench_camera(128)
+    cam_b = gvr.make_orbit_camera(0.7, 0.2, 4.0, (0, 0, 4), 128, 128, 1.6 * 128)
+
+    kp = SelectionConfig().k_prime
+
+    def run(tape, cam):
+        img = np.empty((128, 128, 3))
+        tidx = np.empty((128, 128, kp), dtype=np.int32)
+        gvr.render_into(c, ds, cam, SelectionConfig(), tape, img, None, None, tidx)
+        dc = np.empty((scene.size, 3))
+        ds_ = np.empty((scene.size, 3, 3))
+        gvr.backward_into(tape, np.ones((128, 128, 3)), np.ones((128, 128, 1)), gvr.GradFlags(), dc, ds_)
+        return tidx, img, dc, ds_
+
+    c = gvr.Context(0)
+    ds = gvr.DeviceScene(c).set(scene)
+    fresh = run(gvr.Tape(c), cam_a)
+    tape = gvr.Tape(c)
+    seq = [run(tape, cam_a), run(tape, cam_a), run(tape, cam_b), run(tape, cam_a), run(tape, cam_a)]
+    for r in (seq[0], seq[1], seq[3], seq[4]):
+        for a, b in zip(fresh, r):
+            assert np.array_equal(a, b)
+    other = run(gvr.Tape(c), cam_b)
+    for a, b in zip(other, seq[2]):
+        assert np.array_equal(a, b)
