@@ -125,8 +125,12 @@ __device__ __forceinline__ int classify_q(const Rec32& r, int i, int j, float u,
 // caller then streams every kernel, unsorted, with the same exact tests).
 // Lists longer than smem_cap are sorted into the tile's slot of the global
 // sorted pool instead of shared memory; *list points at the sorted list.
+// With `stage` (>= smem_cap + 2 entries of shared memory), a list that fits is
+// first brought into shared memory with one TMA bulk copy (cp.async.bulk,
+// completing on an mbarrier), and the three sort passes read it there.
 __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, unsigned long long* keys,
-                                                int smem_cap, const unsigned long long** list) {
+                                                int smem_cap, const unsigned long long** list,
+                                                unsigned long long* stage = nullptr) {
     constexpr int NB = 256;
     __shared__ unsigned s_lo, s_hi;
     __shared__ int s_hist[NB];
@@ -136,12 +140,25 @@ __device__ __forceinline__ int load_sorted_list(const FwdParams& p, int tile, un
     const unsigned long long* src = p.pool + off;
     if (count > smem_cap) keys = p.sorted_pool + off;
     *list = keys;
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const bool bulk = stage && count > 0 && count <= smem_cap;
+    const int a0 = off & ~1;  // 16-byte aligned source (the pool keeps 2 entries of slack at its end)
     if (threadIdx.x == 0) {
         s_lo = 0xffffffffu;
         s_hi = 0u;
+        if (bulk) {
+            const unsigned bytes = (unsigned)(((off + count - a0) * 8 + 15) & ~15);
+            mbar_init(&s_mbar, 1);
+            mbar_expect_tx(&s_mbar, bytes);
+            bulk_copy_g2s(stage, p.pool + a0, bytes, &s_mbar);
+        }
     }
     for (int b = threadIdx.x; b < NB; b += blockDim.x) s_hist[b] = 0;
     __syncthreads();
+    if (bulk) {
+        mbar_wait(&s_mbar, 0);
+        src = stage + (off - a0);
+    }
     unsigned lo = 0xffffffffu, hi = 0u;
     for (int e = threadIdx.x; e < count; e += blockDim.x) {
         const unsigned z = (unsigned)(src[e] >> 32);
@@ -652,7 +669,8 @@ __global__ void __launch_bounds__(256 / GVR_SEL_SPLIT, GVR_SEL_MINB) select_warp
     const int tile = p.tile_order[blockIdx.x / GVR_SEL_SPLIT];
     const int smem_cap = kSelListSmem;  // shared-memory layout; p.list_smem decides where a list is sorted
     const unsigned long long* tl = keys;
-    const int listed = load_sorted_list(p, tile, keys, p.list_smem, &tl);
+    // staged through the per-warp list area (free until the compaction below)
+    const int listed = load_sorted_list(p, tile, keys, p.list_smem, &tl, keys + smem_cap);
     const bool overflow = listed < 0;  // stream every kernel, unsorted, no early exit
     // Each warp owns a 2x4-pixel sub-block of the tile and first compacts the
     // tile list to the entries whose screen box meets the sub-block (stable, so

@@ -955,8 +955,9 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
         if (!ctx->capturing || tape->sorted_pool.cap == 0)
             CUDA_TRY(ctx, tape->sorted_pool.ensure(sizeof(unsigned long long) * (size_t)want));
     }
+    // (2 entries of slack at the end: the selection's bulk copies read 16-byte aligned spans)
     const long long pool_cap = std::min<long long>(
-        {(long long)(tape->pool.cap / sizeof(unsigned long long)), (long long)(tape->sorted_pool.cap / sizeof(unsigned long long)),
+        {(long long)(tape->pool.cap / sizeof(unsigned long long)) - 2, (long long)(tape->sorted_pool.cap / sizeof(unsigned long long)),
          0x7fffffffLL, ctx->pool_override > 0 ? ctx->pool_override : 0x7fffffffLL});
     // mask rectangles of the deterministic backward: one 8-byte pixel mask per
     // (kernel, tile of its box), sized like the pool (estimate / earlier totals)
