@@ -144,9 +144,9 @@ int gvr_context_synchronize(gvr_context* ctx);
 int64_t gvr_context_launch_count(const gvr_context* ctx);
 int64_t gvr_context_library_call_count(const gvr_context* ctx);
 /* Per-stage device time via CUDA events around each launch (off by default).
- * Stages: 0 project + bin count, 1 (unused), 2 bin emit, 3 (unused), 4 tile
- * order + list layout, 5 select, 6 blend, 7 loss, 8 backward, 9 object-space. Enabling resets the
- * accumulators. */
+ * Stages: 0 project + bin count, 1 bin emit, 2 tile order + list layout,
+ * 3 select, 4 blend, 5 loss, 6 backward pixels, 7 record layout + records +
+ * finish (object space). Enabling resets the accumulators. */
 int gvr_context_enable_timing(gvr_context* ctx, int on);
 int gvr_context_stage_times(gvr_context* ctx, double* ms, int64_t* count, int n);
 /* Calibration for the roofline: FMA-chain peak of the FP32 (kind 0) or FP64

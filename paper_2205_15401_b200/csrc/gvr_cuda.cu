@@ -76,7 +76,7 @@ bool is_device_ptr(const void* ptr) {
 constexpr int kListStats = 8, kMaskTotal = 12;
 
 enum Stage {
-    ST_PROJECT, ST_SCAN, ST_EMIT, ST_SORT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
+    ST_PROJECT, ST_EMIT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
 };
 
 struct gvr_context {

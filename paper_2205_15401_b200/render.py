@@ -128,7 +128,7 @@ class Context:
     def library_call_count(self) -> int:
         return int(self.lib.gvr_context_library_call_count(self.handle))
 
-    STAGES = ("project", "scan", "emit", "sort", "ranges", "select", "blend", "loss", "backward", "object_space")
+    STAGES = ("project", "emit", "ranges", "select", "blend", "loss", "backward", "object_space")
 
     def enable_timing(self, on: bool = True) -> None:
         self.check(self.lib.gvr_context_enable_timing(self.handle, int(on)))
