@@ -74,6 +74,7 @@ bool is_device_ptr(const void* ptr) {
 // [kListStats .. +3] tile-list stats of the last render (list_offsets),
 // [kMaskTotal] mask-rectangle tiles requested by the last render (project_kernel).
 constexpr int kListStats = 8, kMaskTotal = 12;
+constexpr unsigned kLossBlocks = 148u * 4u;  // loss kernel grid (grid-stride; 2 / 8 / 16 per SM: slower)
 
 enum Stage {
     ST_PROJECT, ST_EMIT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
@@ -1266,18 +1267,18 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
         ta = talpha;
     }
     double* dloss = reinterpret_cast<double*>(t->flags.as<int>() + 2);
-    // block partials (<= 148 * 8) + the last-block ticket (zero between launches)
-    if (int rc = ensure_zeroed(ctx, t->loss_part, sizeof(double) * 148 * 8 + 16)) return rc;
+    // block partials (<= kLossBlocks) + the last-block ticket (zero between launches)
+    if (int rc = ensure_zeroed(ctx, t->loss_part, sizeof(double) * kLossBlocks + 16)) return rc;
     CUDA_TRY(ctx, cudaMemsetAsync(dloss, 0, sizeof(double), ctx->stream));
     const int threads = 256;
-    const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), 148 * 8);
+    const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), kLossBlocks);
     {
         StageTimer st(ctx, ST_LOSS);
         scalar_loss_kernel<<<blocks, threads, 0, ctx->stream>>>(n_img, P, t->image.as<double>(), ti,
                                                                 t->alpha.as<double>(), ta, w_image, w_alpha,
                                                                 t->d_image.as<double>(), t->d_alpha.as<double>(),
                                                                 dloss, t->loss_part.as<double>(),
-                                                                t->loss_part.as<unsigned>() + 2 * 148 * 8);
+                                                                t->loss_part.as<unsigned>() + 2 * kLossBlocks);
     }
     LAUNCH_CHECK(ctx);
     t->has_upstream = true;
