@@ -299,7 +299,8 @@ int out_end(gvr_context* ctx, gvr_tape* t, int kind, cudaStream_t hs) {
 }
 
 int out_wait(gvr_context* ctx, gvr_tape* t, int kind) {
-    if (!t->out_pending[kind]) return GVR_OK;
+    // (a capture cannot wait on work recorded before it: the caller synchronises first)
+    if (!t->out_pending[kind] || ctx->capturing) return GVR_OK;
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, t->out_ev[kind], 0));
     t->out_pending[kind] = false;
     return GVR_OK;
