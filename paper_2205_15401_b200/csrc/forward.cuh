@@ -515,7 +515,9 @@ __device__ __forceinline__ bool merge_batch(float L, int I, int n, float lk, int
         const unsigned a = float_order_bits(sl[lane]), b = float_order_bits(sl[lane + 1]);
         bad = (si[lane] | si[lane + 1]) < 0 && b - a + kKeyUlps <= 2u * kKeyUlps;
     }
-    return !__any_sync(FULL, bad);
+    const bool ok = !__any_sync(FULL, bad);
+    __syncwarp();  // the reads above before any lane's next write of sl / si (memory order, not just a vote)
+    return ok;
 }
 
 // One pixel's K'-nearest selection (warp-wide) over a depth-ordered candidate

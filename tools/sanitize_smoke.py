@@ -18,4 +18,23 @@ for size, kp in ((40, 20), (33, 40)):
 ctx.set_tile_capacity(8)  # overflow path
 fr = gvr.render_with_tape(scene, gvr.make_bench_camera(48), SelectionConfig(), ctx=ctx)
 print("overflow", float(fr.buffers.image.sum()))
+ctx.set_tile_capacity(0)
+# repeated view on one tape (the last render's cycles order the tiles), async host buffers
+import torch  # noqa: E402
+c2 = gvr.Context()
+c2.set_async(True)
+ds = gvr.DeviceScene(c2).set(scene)
+tp = gvr.Tape(c2)
+cam = gvr.make_bench_camera(48)
+img = torch.empty((48, 48, 3), dtype=torch.float64).pin_memory()
+gc = torch.empty((scene.size, 3), dtype=torch.float64).pin_memory()
+ti = torch.rand((48, 48, 3), dtype=torch.float64).pin_memory()
+ta = torch.rand((48, 48, 1), dtype=torch.float64).pin_memory()
+loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+for _ in range(3):
+    gvr.render_into(c2, ds, cam, SelectionConfig(), tp, img)
+    gvr.scalar_loss_into(tp, ti, ta, 1.0, 1.0, loss)
+    gvr.backward_into(tp, None, None, gvr.GradFlags(), gc)
+c2.synchronize()
+print("async repeated view", float(loss[0]), float(gc.abs().sum()))
 print("sanitize smoke ok")
