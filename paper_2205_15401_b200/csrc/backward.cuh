@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
 }
 
 constexpr int kRecThreads = 128;
+constexpr int kRecCtasPerSm = 8;  // records grid: 8 CTAs per SM walking the windows (16: slower)
 
 // K5a: one thread per record (grid-stride over 32-record windows, one warp per
 // window): the entry's terms of the regrouped chain (entry_coeffs: alpha d,
@@ -413,13 +414,24 @@ __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
     const int wstride = (gridDim.x * blockDim.x) >> 5;
     const float inv_nv = 1.0f / (float)p.nv;
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // the next window's record and key loaded under the current window's work
+    int2 key_n = make_int2(0, -1);
+    double4 b_n = make_double4(0, 0, 0, 0);
+    if (32 * w + lane < n_rec) {
+        key_n = p.bkey[32 * w + lane];
+        b_n = p.bent[32 * w + lane];
+    }
     for (; w < windows; w += wstride) {
         const int r = 32 * w + lane;
         const bool valid = r < n_rec;
         int k = -1;
+        const int2 key = key_n;
+        const double4 b = b_n;
+        if (r + 32 * wstride < n_rec) {
+            key_n = p.bkey[r + 32 * wstride];
+            b_n = p.bent[r + 32 * wstride];
+        }
         if (valid) {
-            const int2 key = p.bkey[r];
-            const double4 b = p.bent[r];
             k = key.y;
             const long long pix = key.x;
             const double4 ray = p.rays[pix];

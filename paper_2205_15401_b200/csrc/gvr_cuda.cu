@@ -1484,7 +1484,7 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
             StageTimer st(ctx, ST_OBJECT);
             const size_t rsmem = sizeof(double) * kRecThreads * (size_t)gp.nv;
             CUDA_TRY(ctx, cudaFuncSetAttribute(records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-            records_kernel<<<148 * 16, kRecThreads, rsmem, ctx->stream>>>(gp);
+            records_kernel<<<148 * kRecCtasPerSm, kRecThreads, rsmem, ctx->stream>>>(gp);
             finish_kernel<<<finish_grid, kFinishThreads, 0, ctx->stream>>>(gp);
         }
         ++ctx->launches;
