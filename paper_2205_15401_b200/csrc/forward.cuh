@@ -1128,6 +1128,8 @@ __device__ void list_offsets(int tiles, const int* __restrict__ count, int* __re
     }
 }
 
+constexpr int kOrderSmemTiles = 16384;  // 6 B of shared memory per tile (96 KB)
+
 // Longest-processing-time-first order of tiles (single-CTA counting sort over
 // log-spaced cost buckets, descending). Zero-cost tiles and tiles of other
 // shards (t % nshards != shard) are dropped; *n_out receives the number kept.
@@ -1145,17 +1147,36 @@ __global__ void __launch_bounds__(1024) order_tiles_kernel(int tiles, const int*
     __shared__ int hist[256];
     __shared__ int offs[256];
     __shared__ int s_tail;
-    if (tile_off) list_offsets(tiles, icost, tile_off, pool_cap, smem_cap, stats);
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    auto bucket_of = [&](int t) -> int {
+    // up to kOrderSmemTiles tiles: counts and buckets read from global memory once
+    // (all loads of a thread in flight together) into shared memory for every pass
+    extern __shared__ int s_dyn[];
+    const bool staged = tiles <= kOrderSmemTiles;
+    int* s_cnt = s_dyn;
+    short* s_bkt = reinterpret_cast<short*>(s_dyn + (staged ? tiles : 0));
+    auto bucket_from = [&](int t, int cnt, unsigned h) -> int {
         if (t % nshards != shard) return -1;  // tile owned by another rank (C4 tile sharding)
-        float c = (float)icost[t];
+        float c = (float)cnt;
         if (!(c > 0.0f)) return -1;
-        if (hint) c = hint[t] > 0u ? (float)hint[t] : 100.0f * c;  // cycles (a tile new to the view: ~100 / entry)
+        if (hint) c = h > 0u ? (float)h : 100.0f * c;  // cycles (a tile new to the view: ~100 / entry)
         const int b = (int)(__log2f(c + 1.0f) * 8.0f);
         return 255 - min(b, 255);  // descending cost
     };
+    if (staged) {
+#pragma unroll 4
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+            const int c = icost[t];
+            const unsigned h = hint ? hint[t] : 0u;
+            s_cnt[t] = c;
+            s_bkt[t] = (short)bucket_from(t, c, h);
+        }
+        __syncthreads();
+    }
+    auto bucket_of = [&](int t) -> int {
+        return staged ? (int)s_bkt[t] : bucket_from(t, icost[t], hint ? hint[t] : 0u);
+    };
+    if (tile_off) list_offsets(tiles, staged ? s_cnt : icost, tile_off, pool_cap, smem_cap, stats);
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
     for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
         const int b = bucket_of(t);
         if (b >= 0) atomicAdd(&hist[b], 1);

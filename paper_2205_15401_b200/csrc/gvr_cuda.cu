@@ -1035,7 +1035,10 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     if (want_hint) CUDA_TRY(ctx, tape->tile_hint.ensure(sizeof(unsigned) * (size_t)tiles));
     {
         StageTimer st(ctx, ST_RANGES);
-        order_tiles_kernel<<<1, 1024, 0, ctx->stream>>>(tiles, tile_count, order_f, sched, shard, nshards,
+        const size_t osmem = tiles <= kOrderSmemTiles ? 6ull * (size_t)tiles : 0;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(order_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(6ull * kOrderSmemTiles)));
+        order_tiles_kernel<<<1, 1024, osmem, ctx->stream>>>(tiles, tile_count, order_f, sched, shard, nshards,
                                                         sched + 1, tape->tile_off.as<int>(),
                                                         (int)pool_cap, ctx->list_smem, dflags + kListStats,
                                                         use_hint ? tape->tile_hint.as<unsigned>() : nullptr);
