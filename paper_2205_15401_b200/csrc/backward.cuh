@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(256 / GVR_BWD_SPLIT, GVR_BWD_MINB) backward_pi
         const double dsg = (double)s_sg - (double)c_sg;
         const double dq = dpk * pke;
         const double w = p.tape_t[pix * p.kp + e] * pke;  // W_e (the forward's weight)
+        // (programmatic dependent of offsets_kernel: the record offsets are complete from here)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int4 ki = p.kinfo[kid];
         if (ki.x >= 0) {
             // deterministic path: the entry's adjoints go to its record in the
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(1024) cta_scan_kernel(AppParams p, int n) {
 }
 
 __global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
+    launch_dependents();  // K4 may start its pair terms while the offsets are written
     const int k = blockIdx.x * kScanThreads + threadIdx.x;
     const int c = k < p.K ? p.count[k] : 0;
     const int off = p.cta_sum[blockIdx.x] + block_exclusive_scan(c, nullptr);

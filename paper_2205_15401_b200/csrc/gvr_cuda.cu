@@ -404,7 +404,17 @@ int launch_backward(gvr_context* ctx, const BwdParams& bp, int tiles) {
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
         StageTimer st(ctx, ST_BACKWARD);
-        kern<<<tiles * GVR_BWD_SPLIT, 256 / GVR_BWD_SPLIT, smem, ctx->stream>>>(bp);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(tiles * GVR_BWD_SPLIT);
+        cfg.blockDim = dim3(256 / GVR_BWD_SPLIT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;  // programmatic dependent of offsets_kernel (griddepcontrol.wait before the records)
+        CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, bp));
     }
     LAUNCH_CHECK(ctx);
     return GVR_OK;
