@@ -402,7 +402,9 @@ struct GatherParams {
     double* d_rt;           // [12] d_rotation (9), d_translation (3)
 };
 
+
 __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
+    launch_dependents();  // the finish may stage its object-space rows meanwhile
     // per warp: the window's record values [32][nv], summed per kernel piece by
     // one lane each, rows in record order
     extern __shared__ __align__(16) double s_rows[];
@@ -508,6 +510,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) 
     const int count = min(kFinishThreads, p.K - k0);
     stage_rows_in(s_cov, p.inv_cov, k0, count, 9);
     stage_rows_in(s_ctr, p.centers, k0, count, 3);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the records' pieces are complete from here
     __syncthreads();
     const int k = k0 + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

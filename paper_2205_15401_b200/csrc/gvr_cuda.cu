@@ -1498,7 +1498,17 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
             const size_t rsmem = sizeof(double) * kRecThreads * (size_t)gp.nv;
             CUDA_TRY(ctx, cudaFuncSetAttribute(records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
             records_kernel<<<148 * kRecCtasPerSm, kRecThreads, rsmem, ctx->stream>>>(gp);
-            finish_kernel<<<finish_grid, kFinishThreads, 0, ctx->stream>>>(gp);
+            // programmatic dependent of the records: stages its object-space rows first
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)finish_grid);
+            cfg.blockDim = dim3(kFinishThreads);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, finish_kernel, gp));
         }
         ++ctx->launches;
         LAUNCH_CHECK(ctx);
