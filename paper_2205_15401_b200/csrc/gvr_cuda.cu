@@ -1283,7 +1283,7 @@ static int scalar_loss_impl(gvr_context* ctx, gvr_tape* t, const double* target_
     double* dloss = reinterpret_cast<double*>(t->flags.as<int>() + 2);
     // block partials (<= kLossBlocks) + the last-block ticket (zero between launches)
     if (int rc = ensure_zeroed(ctx, t->loss_part, sizeof(double) * kLossBlocks + 16)) return rc;
-    CUDA_TRY(ctx, cudaMemsetAsync(dloss, 0, sizeof(double), ctx->stream));
+    // (*dloss is written by the loss kernel's last block: no clearing needed)
     const int threads = 256;
     const unsigned blocks = std::min<unsigned>(blocks_for(n_img + P, threads), kLossBlocks);
     {
