@@ -1003,11 +1003,12 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     int* tile_count = tape->tile_count.as<int>();
     int* sched = tape->sched.as<int>();
     int* order_f = sched + 2;
-    CUDA_TRY(ctx, cudaMemsetAsync(dflags, 0, 16 * sizeof(int), ctx->stream));
-    int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts: one memset
-    CUDA_TRY(ctx, cudaMemsetAsync(tile_count, 0, sizeof(int) * 2 * (size_t)tiles, ctx->stream));
-    // the per-tile selection hand-off flags
-    CUDA_TRY(ctx, cudaMemsetAsync(sched + 2 + (size_t)tiles, 0, sizeof(int) * (size_t)tiles, ctx->stream));
+    int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts
+    // flags, tile counts + emit cursors, the per-tile selection hand-off flags:
+    // cleared by one launch (instead of three memset nodes)
+    clear3_kernel<<<std::min<unsigned>(blocks_for(2 * (long long)tiles, 256), 148 * 4), 256, 0, ctx->stream>>>(
+        dflags, 16, tile_count, 2 * tiles, sched + 2 + (size_t)tiles, tiles);
+    LAUNCH_CHECK(ctx);
 
     if (K > 0) {
         // K1 projection + culling + binning into per-tile lists

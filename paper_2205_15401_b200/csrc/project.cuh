@@ -357,6 +357,16 @@ __global__ void project_kernel(ProjectParams p) {
     }
 }
 
+// Zero three int arrays in one launch (the render's per-call counters and flags).
+__global__ void clear3_kernel(int* __restrict__ a, int na, int* __restrict__ b, int nb, int* __restrict__ c, int nc) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na + nb + nc; i += stride) {
+        if (i < na) a[i] = 0;
+        else if (i < na + nb) b[i - na] = 0;
+        else c[i - na - nb] = 0;
+    }
+}
+
 struct EmitParams {
     int K;
     const Rec32* rec32;
