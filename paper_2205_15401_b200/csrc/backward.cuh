@@ -275,7 +275,7 @@ __device__ __forceinline__ void stage_rows_out(double* __restrict__ dst, const d
 // Kernel k's selected (pixel, entry) pairs are the set bits of its mask
 // rectangle (set by the blend). Records are laid out in kernel order, and
 // inside a kernel in (tile row-major, pixel) order: an exclusive scan of the
-// per-kernel counts (K4a/b/c: counts + CTA sums, CTA-sum scan, offsets), so
+// per-kernel counts (K4a/b: counts + CTA sums, offsets), so
 // the layout is a pure function of the selection.
 constexpr int kScanThreads = 256;
 
@@ -284,7 +284,7 @@ struct AppParams {
     const int4* kinfo;
     const unsigned long long* masks;
     int* count;      // [K] records of each kernel (count_kernel)
-    int* cta_sum;    // [ceil(K / kScanThreads)] then exclusive offsets (in place)
+    int* cta_sum;    // [ceil(K / kScanThreads)] record totals of each count_kernel CTA
     int* slot_off;   // [mask slots] first record of each (kernel, tile)
     int2* app;       // [K] {first record, count}
     int* total;      // records of the render
@@ -333,27 +333,20 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(AppParams p) {
     if (threadIdx.x == 0) p.cta_sum[blockIdx.x] = tot;
 }
 
-// exclusive scan of the CTA sums in place (one CTA of 1024 threads, chunks per thread)
-__global__ void __launch_bounds__(1024) cta_scan_kernel(AppParams p, int n) {
-    const int chunk = (n + 1023) / 1024;
-    const int t0 = min(n, (int)threadIdx.x * chunk), t1 = min(n, t0 + chunk);
-    int run = 0;
-    for (int t = t0; t < t1; ++t) run += p.cta_sum[t];
-    int tot;
-    int off = block_exclusive_scan(run, &tot);
-    for (int t = t0; t < t1; ++t) {
-        const int v = p.cta_sum[t];
-        p.cta_sum[t] = off;
-        off += v;
-    }
-    if (threadIdx.x == 0) *p.total = tot;
-}
-
+// Record offsets: this CTA's prefix = the sum of the earlier CTAs' totals (read
+// and reduced by the CTA itself: no separate scan launch), then the exclusive
+// scan of its kernels' counts. The last CTA writes the render's record total.
 __global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
     launch_dependents();  // K4 may start its pair terms while the offsets are written
     const int k = blockIdx.x * kScanThreads + threadIdx.x;
     const int c = k < p.K ? p.count[k] : 0;
-    const int off = p.cta_sum[blockIdx.x] + block_exclusive_scan(c, nullptr);
+    int before = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += blockDim.x) before += p.cta_sum[b];
+    int prefix;
+    block_exclusive_scan(before, &prefix);  // (the block total of the partial sums)
+    int tot;
+    const int off = prefix + block_exclusive_scan(c, &tot);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *p.total = prefix + tot;
     if (k >= p.K) return;
     p.app[k] = make_int2(off, c);
     if (c > 0) {

@@ -1452,10 +1452,9 @@ static int backward_impl(gvr_context* ctx, gvr_tape* t, const double* d_image, c
             // K4a-c: record layout (per-kernel counts from the blend's masks, scan, offsets)
             StageTimer st(ctx, ST_OBJECT);
             count_kernel<<<(unsigned)scan_ctas, kScanThreads, 0, ctx->stream>>>(ap);
-            cta_scan_kernel<<<1, 1024, 0, ctx->stream>>>(ap, (int)scan_ctas);
             offsets_kernel<<<(unsigned)scan_ctas, kScanThreads, 0, ctx->stream>>>(ap);
         }
-        ctx->launches += 2;
+        ctx->launches += 1;
         LAUNCH_CHECK(ctx);
         int rc;
         if (kp <= 8) rc = launch_backward<8>(ctx, bp, btx * bty);
