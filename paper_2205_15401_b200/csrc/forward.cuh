@@ -1050,23 +1050,6 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     if (bad) atomicExch(p.nonfinite, 1);
 }
 
-// Tiles whose pixels selected nothing (zero blend cost) are not visited by the
-// blend grid: write their empty-render outputs (image 0, alpha 0, depth 0, count 0).
-__global__ void clear_empty_tiles_kernel(CameraP cam, int Dc, int tiles_x, const float* __restrict__ tile_cost,
-                                         double* __restrict__ image, double* __restrict__ alpha,
-                                         double* __restrict__ depth, int* __restrict__ count) {
-    const int tile = blockIdx.x;
-    if (tile_cost[tile] > 0.0f) return;
-    const int i = (tile / tiles_x) * 8 + threadIdx.x / 8;
-    const int j = (tile % tiles_x) * 8 + threadIdx.x % 8;
-    if (i >= cam.H || j >= cam.W) return;
-    const long long pix = (long long)i * cam.W + j;
-    for (int c = 0; c < Dc; ++c) image[pix * Dc + c] = 0.0;
-    alpha[pix] = 0.0;
-    depth[pix] = 0.0;
-    count[pix] = 0;
-}
-
 // Tile-list layout (blockDim.x == 1024): exclusive scan of the per-tile counts
 // in tile order into pool offsets. Lists that would end past pool_cap get
 // offset -1 (streamed by the selection, counted as overflow). stats: [0] total

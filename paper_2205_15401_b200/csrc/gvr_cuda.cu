@@ -74,6 +74,7 @@ bool is_device_ptr(const void* ptr) {
 // [kListStats .. +3] tile-list stats of the last render (list_offsets),
 // [kMaskTotal] mask-rectangle tiles requested by the last render (project_kernel).
 constexpr int kListStats = 8, kMaskTotal = 12;
+
 constexpr unsigned kLossBlocks = 148u * 4u;  // loss kernel grid (grid-stride; 2 / 8 / 16 per SM: slower)
 
 enum Stage {
@@ -1005,9 +1006,21 @@ static int render_impl(gvr_context* ctx, const gvr_scene* scene, const gvr_camer
     int* order_f = sched + 2;
     int* tile_fill = tile_count + tiles;  // emit cursors, contiguous with the counts
     // flags, tile counts + emit cursors, the per-tile selection hand-off flags:
-    // cleared by one launch (instead of three memset nodes)
-    clear3_kernel<<<std::min<unsigned>(blocks_for(2 * (long long)tiles, 256), 148 * 4), 256, 0, ctx->stream>>>(
-        dflags, 16, tile_count, 2 * tiles, sched + 2 + (size_t)tiles, tiles);
+    // cleared by one launch (instead of memset nodes). (Clearing the outputs here
+    // too, so that the blend visits only the selected tiles: C2 +4 µs, C4 -4 µs.)
+    {
+        ClearList cl{};
+        long long words = 0;
+        auto add = [&](void* ptr, long long n) {
+            cl.ptr[cl.m] = static_cast<int*>(ptr);
+            cl.n[cl.m++] = n;
+            words += n;
+        };
+        add(dflags, 16);
+        add(tile_count, 2LL * tiles);
+        add(sched + 2 + (size_t)tiles, tiles);
+        clear_kernel<<<std::min<unsigned>(blocks_for(words, 256), 148 * 8), 256, 0, ctx->stream>>>(cl);
+    }
     LAUNCH_CHECK(ctx);
 
     if (K > 0) {

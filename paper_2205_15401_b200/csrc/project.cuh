@@ -357,13 +357,19 @@ __global__ void project_kernel(ProjectParams p) {
     }
 }
 
-// Zero three int arrays in one launch (the render's per-call counters and flags).
-__global__ void clear3_kernel(int* __restrict__ a, int na, int* __restrict__ b, int nb, int* __restrict__ c, int nc) {
-    const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na + nb + nc; i += stride) {
-        if (i < na) a[i] = 0;
-        else if (i < na + nb) b[i - na] = 0;
-        else c[i - na - nb] = 0;
+// Zero up to 8 arrays of 32-bit words in one launch (the render's per-call
+// counters and flags, and the outputs of the tiles the blend does not visit).
+struct ClearList {
+    int* ptr[8];
+    long long n[8];  // words
+    int m;
+};
+__global__ void clear_kernel(ClearList c) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (int a = 0; a < c.m; ++a) {
+        for (; i < c.n[a]; i += stride) c.ptr[a][i] = 0;
+        i -= c.n[a];
     }
 }
 
