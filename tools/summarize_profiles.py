@@ -43,6 +43,8 @@ def launch_list(tag):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     ks = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[h + 1:] if len(r) > vi]
     last = max(i for i, (k, _) in enumerate(ks) if "project_kernel" in k)
+    if last > 0 and "clear_kernel" in ks[last - 1][0]:  # the render's first launch
+        last -= 1
     step = [kv for kv in ks[last:] if "fma_peak" not in kv[0]]
     total = sum(v for _, v in step)
     lines = ["kernel,ns,share"]
