@@ -1823,7 +1823,15 @@ __global__ void view_sum_kernel(ViewSumParams p) {
         for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n[b];
              i += (long long)gridDim.x * blockDim.x) {
             double acc = p.dst[b][i];
-            for (int v = 0; v < p.V; ++v) acc += p.src[v][b][i];
+            int v = 0;
+            for (; v + 8 <= p.V; v += 8) {  // 8 loads in flight, added in view order
+                double a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = p.src[v + u][b][i];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += a[u];
+            }
+            for (; v < p.V; ++v) acc += p.src[v][b][i];
             p.dst[b][i] = acc;
         }
     }
