@@ -829,10 +829,14 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     int* b_id = reinterpret_cast<int*>(b_w + KMAX * NP);
     int* b_slot = b_id + KMAX * NP;  // the entry's (kernel, tile) mask slot, -1: none (selection order)
 
-    if ((int)(blockIdx.x / GVR_BLEND_SPLIT) >= *p.n_order_blend) return;
+    // the order counts and this CTA's tile are loaded together (the order array
+    // holds every tile, so the read is in bounds before the count check)
+    const int bt = (int)(blockIdx.x / GVR_BLEND_SPLIT);
+    const int n_blend = *p.n_order_blend, n_sel = *p.n_order;
+    const int tile = p.tile_order_blend[bt];
+    if (bt >= n_blend) return;
     const int g = threadIdx.x >> 2, sub = threadIdx.x & 3;
-    const int tile = p.tile_order_blend[blockIdx.x / GVR_BLEND_SPLIT];
-    if (p.tile_done && (int)(blockIdx.x / GVR_BLEND_SPLIT) < *p.n_order) {
+    if (p.tile_done && bt < n_sel) {
         // started early (programmatic dependent of the selection): wait for this tile only
         if (threadIdx.x == 0) {
             // bounded: a selection that never publishes (a bug) must fail the launch, not hang the device
@@ -851,7 +855,15 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     const int kp = p.sel.kp;
     // tiles after the selected ones in the order (other shards, empty lists) are
     // cleared; a selected tile has a count for every pixel
-    const bool visited = (int)(blockIdx.x / GVR_BLEND_SPLIT) < *p.n_order;
+    const bool visited = bt < n_sel;
+    // the pixel's whole top-K row is loaded with its count (one dependent hop
+    // fewer before the record loads; slots past the count are never used)
+    int ids[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int s = sub + 4 * q;
+        ids[q] = inside && visited && s < kp ? __ldcg(p.topk + pix * kp + s) : 0;
+    }
     const int n = inside && visited ? p.count[pix] : 0;
     if (n == 0) {
         if (inside && sub == 0) {
@@ -870,12 +882,6 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
     // ids first (independent loads), then the traces: the id -> record load
     // chains of a thread's entries overlap instead of running back to back
     {
-        int ids[PER];
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int s = sub + 4 * q;
-            ids[q] = s < n ? p.topk[pix * kp + s] : 0;
-        }
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const int s = sub + 4 * q;
