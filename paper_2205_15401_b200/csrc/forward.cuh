@@ -814,6 +814,13 @@ __device__ __forceinline__ void mark_selection(const FwdParams& p, const int* b_
 // Blend staging slot: the traced l with the FP32 peak and 1/sigma; after the
 // sort the first 8 bytes become the float pair (hi, lo) of l - l_0, so the pair
 // loop reads everything it needs about entry m with one 16-byte load.
+#ifndef GVR_BLEND_STAGE
+#define GVR_BLEND_STAGE 1
+#endif
+// per-warp record stage of the blend: 32 records at a 144-byte stride (9 x 16 B:
+// the 8 lanes of a quarter-warp reading 16 bytes each hit distinct banks)
+constexpr int kStageRecU4 = 9;
+constexpr size_t kBlendStageBytes = GVR_BLEND_STAGE ? (256 / GVR_BLEND_SPLIT) * 16 * kStageRecU4 : 0;
 struct __align__(16) BlendSlot {
     double l;
     float pk, is;
@@ -865,6 +872,55 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         ids[q] = inside && visited && s < kp ? __ldcg(p.topk + pix * kp + s) : 0;
     }
     const int n = inside && visited ? p.count[pix] : 0;
+    double d[3];
+    double peak_part = 0.0;
+    // one traced entry: FP64 peak, taped l / 1/sigma, id and the kernel's mask
+    // slot for this tile
+    auto trace_entry = [&](int s, int k, const Rec64& r) {
+        const Traced64 t = trace_fast(d, r);
+        const double pk = exp(t.q);
+        b_w[s * NP + g] = pk;  // FP64 peak until W overwrites it (alpha sum, after the sort)
+        if (p.presorted) p.ent_a[pix * kp + s] = t.a;
+        BlendSlot v;
+        v.l = t.l;  // l for now; relative to the nearest after the sort
+        v.pk = (float)pk;
+        v.is = (float)sqrt(t.a);  // 1/sigma
+        b_s[s * NP + g] = v;
+        b_id[s * NP + g] = k;
+        const int4 ki = p.kinfo[k];
+        b_slot[s * NP + g] = ki.x >= 0 ? ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff)) : -1;
+    };
+#if GVR_BLEND_STAGE
+    {
+        // The records are staged per warp through shared memory, one round per
+        // entry slot sub + 4q: the warp copies its lanes' 32 records with
+        // coalesced 16-byte loads (8 lanes per 128-byte record, 4 records per
+        // instruction) instead of each lane reading its own record (32 lines
+        // per load instruction: the L1 wavefronts were the blend's busiest
+        // unit). All lanes of the CTA are present here (empty pixels included).
+        const unsigned FULL = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        uint4* st = reinterpret_cast<uint4*>(smem + 32 * KMAX * NP) + (threadIdx.x >> 5) * (32 * kStageRecU4);
+        const int qmax = (int)__reduce_max_sync(FULL, (unsigned)((n + 3) >> 2));
+        if (n > 0) pixel_ray(p.cam, i, j, d);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            if (q >= qmax) break;  // warp-uniform
+            const int s = sub + 4 * q;
+            const int myid = s < n ? ids[q] : -1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int src = (lane >> 3) + 4 * c;
+                const int kid = __shfl_sync(FULL, myid, src);
+                if (kid >= 0)
+                    st[src * kStageRecU4 + (lane & 7)] = __ldg(reinterpret_cast<const uint4*>(p.rec64 + kid) + (lane & 7));
+            }
+            __syncwarp();
+            if (s < n) trace_entry(s, ids[q], *reinterpret_cast<const Rec64*>(st + lane * kStageRecU4));
+            __syncwarp();  // the stage is rewritten by the next round
+        }
+    }
+#endif
     if (n == 0) {
         if (inside && sub == 0) {
             for (int c = 0; c < p.Dc; ++c) p.image[pix * p.Dc + c] = 0.0;
@@ -875,36 +931,12 @@ __global__ void __launch_bounds__(256 / GVR_BLEND_SPLIT, GVR_BLEND_MINB) blend_k
         return;  // the 4 threads of a pixel leave together
     }
     const unsigned grp = 0xfu << (threadIdx.x & 28);  // the pixel's 4 lanes
-
-    double d[3];
+#if !GVR_BLEND_STAGE
     pixel_ray(p.cam, i, j, d);
-    double peak_part = 0.0;
-    // ids first (independent loads), then the traces: the id -> record load
-    // chains of a thread's entries overlap instead of running back to back
-    {
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int s = sub + 4 * q;
-            if (s < n) {
-                const int k = ids[q];
-                const Traced64 t = trace_fast(d, p.rec64[k]);
-                const double pk = exp(t.q);
-                const float pkf = (float)pk;
-                b_w[s * NP + g] = pk;  // FP64 peak until W overwrites it (alpha sum, after the sort)
-                if (p.presorted) p.ent_a[pix * kp + s] = t.a;
-                BlendSlot v;
-                v.l = t.l;  // l for now; relative to the nearest after the sort
-                v.pk = pkf;
-                v.is = (float)sqrt(t.a);  // 1/sigma
-                b_s[s * NP + g] = v;
-                b_id[s * NP + g] = k;
-                // the kernel's mask slot for this tile (its record was loaded with the trace's)
-                const int4 ki = p.kinfo[k];
-                b_slot[s * NP + g] =
-                    ki.x >= 0 ? ki.x + (i / 8 - (ki.y >> 16)) * ki.z + (j / 8 - (ki.y & 0xffff)) : -1;
-            }
-        }
-    }
+    for (int q = 0; q < PER; ++q)
+        if (sub + 4 * q < n) trace_entry(sub + 4 * q, ids[q], p.rec64[ids[q]]);
+#endif
     __syncwarp(grp);
     if (sub == 0 && !p.presorted) {
         // ascending (l, idx) of fine_select (tracer.cpp:119-122): insertion sort;

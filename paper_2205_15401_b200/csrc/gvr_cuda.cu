@@ -374,7 +374,7 @@ int launch_forward(gvr_context* ctx, const FwdParams& fp, int tiles) {
     }
     LAUNCH_CHECK(ctx);
     {
-        const size_t smem = 32ull * KMAX * (64 / GVR_BLEND_SPLIT);
+        const size_t smem = 32ull * KMAX * (64 / GVR_BLEND_SPLIT) + kBlendStageBytes;
         auto kern = blend_kernel<KMAX>;
         CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         StageTimer st(ctx, ST_BLEND);
