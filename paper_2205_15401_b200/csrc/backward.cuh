@@ -696,8 +696,55 @@ __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const dou
     const double2* im2 = reinterpret_cast<const double2*>(image);
     const double2* ti2 = reinterpret_cast<const double2*>(t_image);
     double2* di2 = reinterpret_cast<double2*>(d_image);
+#ifndef GVR_LOSS_BATCH
+#define GVR_LOSS_BATCH 1
+#endif
+#if GVR_LOSS_BATCH
+    // the thread's first 3 image pairs and 2 alpha values are loaded before any
+    // is used (one memory round trip for the common grid; the rest below)
+    double2 ia[3], ib[3];
+    double aa[2], ab[2];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const long long i = tid + u * nt;
+        if (i < n2) {
+            ia[u] = im2[i];
+            ib[u] = ti2[i];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const long long a = tid + u * nt;
+        if (a < n_alpha) {
+            aa[u] = alpha[a];
+            ab[u] = t_alpha[a];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const long long i = tid + u * nt;
+        if (i < n2) {
+            const double x = ia[u].x - ib[u].x, y = ia[u].y - ib[u].y;
+            part += 0.5 * w_image * x * x;
+            part += 0.5 * w_image * y * y;
+            di2[i] = make_double2(w_image * x, w_image * y);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const long long a = tid + u * nt;
+        if (a < n_alpha) {
+            const double diff = aa[u] - ab[u];
+            part += 0.5 * w_alpha * diff * diff;
+            d_alpha[a] = w_alpha * diff;
+        }
+    }
+    const long long i0 = tid + 3 * nt, a0 = tid + 2 * nt;
+#else
+    const long long i0 = tid, a0 = tid;
+#endif
 #pragma unroll 2
-    for (long long i = tid; i < n2; i += nt) {
+    for (long long i = i0; i < n2; i += nt) {
         const double2 a = im2[i], b = ti2[i];
         const double x = a.x - b.x, y = a.y - b.y;
         part += 0.5 * w_image * x * x;
@@ -710,7 +757,7 @@ __global__ void scalar_loss_kernel(long long n_img, long long n_alpha, const dou
         d_image[idx] = w_image * diff;
     }
 #pragma unroll 2
-    for (long long a = tid; a < n_alpha; a += nt) {
+    for (long long a = a0; a < n_alpha; a += nt) {
         const double diff = alpha[a] - t_alpha[a];
         part += 0.5 * w_alpha * diff * diff;
         d_alpha[a] = w_alpha * diff;

@@ -75,7 +75,10 @@ bool is_device_ptr(const void* ptr) {
 // [kMaskTotal] mask-rectangle tiles requested by the last render (project_kernel).
 constexpr int kListStats = 8, kMaskTotal = 12;
 
-constexpr unsigned kLossBlocks = 148u * 4u;  // loss kernel grid (grid-stride; 2 / 8 / 16 per SM: slower)
+#ifndef GVR_LOSS_CTAS_PER_SM
+#define GVR_LOSS_CTAS_PER_SM 4
+#endif
+constexpr unsigned kLossBlocks = 148u * GVR_LOSS_CTAS_PER_SM;  // loss kernel grid (grid-stride; 2 / 8 / 16 per SM: slower)
 
 enum Stage {
     ST_PROJECT, ST_EMIT, ST_RANGES, ST_SELECT, ST_BLEND, ST_LOSS, ST_BACKWARD, ST_OBJECT, ST_COUNT
