@@ -39,7 +39,7 @@
 #define GVR_SEL_SPLIT 1
 #endif
 #ifndef GVR_BWD_MINB
-#define GVR_BWD_MINB 16
+#define GVR_BWD_MINB 12
 #endif
 
 namespace gvrk {
