@@ -491,7 +491,10 @@ __global__ void __launch_bounds__(kRecThreads) records_kernel(GatherParams p) {
 //   d_center = R^T dm, d_inv_cov = R^T dS R, d_T = sum dm, d_R = sum dm m^T + 2 dS R S.
 // d_R, d_T: CTA partial in kernel order -> group of kRtGroup CTAs -> total,
 // each in a fixed order (tickets: the last CTA of a level reduces it).
-constexpr int kFinishThreads = 128, kRtGroup = 32;
+#ifndef GVR_FINISH_THREADS
+#define GVR_FINISH_THREADS 128
+#endif
+constexpr int kFinishThreads = GVR_FINISH_THREADS, kRtGroup = 32;
 
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(GatherParams p) {
     __shared__ double s_part[kFinishThreads / 32][12];
