@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(AppParams p) {
 }
 
 constexpr int kRecThreads = 128;
-constexpr int kRecCtasPerSm = 8;  // records grid: 8 CTAs per SM walking the windows (16: slower)
+#ifndef GVR_REC_CTAS_PER_SM
+#define GVR_REC_CTAS_PER_SM 8
+#endif
+constexpr int kRecCtasPerSm = GVR_REC_CTAS_PER_SM;  // records grid: CTAs per SM walking the windows (16: slower)
 
 // K5a: one thread per record (grid-stride over 32-record windows, one warp per
 // window): the entry's terms of the regrouped chain (entry_coeffs: alpha d,
