@@ -21,10 +21,10 @@
 #define GVR_SEL_MINB 3
 #endif
 #ifndef GVR_BLEND_MINB
-#define GVR_BLEND_MINB 10
+#define GVR_BLEND_MINB 5
 #endif
 #ifndef GVR_BLEND_SPLIT
-#define GVR_BLEND_SPLIT 4
+#define GVR_BLEND_SPLIT 2
 #endif
 #ifndef GVR_BWD_SPLIT
 #define GVR_BWD_SPLIT 4
